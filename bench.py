@@ -1,0 +1,308 @@
+#!/usr/bin/env python
+"""Benchmark: site updates/ns of the bit-vectorized octahedron SCA on B200.
+
+Workload (default, BASELINE.json configs[1]): a 2^16 x 2^16 lattice from the
+flat start, KPZ p=1 q=0, one MCS per step, W^2(t) measured on the device at
+the points of log_schedule(10^4, 8) that fall inside the K timed steps (the
+first K MCS of the configs[1] job; K = 10^4 runs it whole). Inputs: the slope
+planes are 1 GiB, far larger than the 126 MB L2, so no L2 flush is needed.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c2h|c3|c4|c5] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0). --impl reference times the reference's own
+multi-threaded CPU VecEngine (oracle/_ref, built from /root/reference) on
+this host's cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c2": dict(X=1 << 16, Y=1 << 16, p=1.0, q=0.0,
+               workload="2^16x2^16 KPZ p=1 q=0, W^2(t) log-sampled (BASELINE configs[1])"),
+    "c2h": dict(X=1 << 16, Y=1 << 16, p=0.5, q=0.0,
+                workload="2^16x2^16 KPZ p=0.5 q=0 (half mode; paper's benchmark case), W^2(t) log-sampled"),
+    "c3": dict(X=1 << 16, Y=1 << 16, p=0.5, q=0.5, workload="2^16x2^16 EW-like p=q=1/2 (BASELINE configs[2])"),
+    "c4": dict(X=1 << 16, Y=1 << 16, p=0.98, q=0.02,
+               workload="2^16x2^16 arbitrary p=0.98 q=0.02 (BASELINE configs[3])"),
+    "c5": dict(X=1 << 17, Y=1 << 17, p=1.0, q=0.0, workload="2^17x2^17 KPZ p=1 q=0 (BASELINE configs[4])"),
+}
+METRIC = "site updates/ns"
+SCHEDULE_TMAX, SCHEDULE_PPD = 10000, 8
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons via NVML during the timed region."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting",
+               0x10: "sync_boost"}
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.stop_ev = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self.stop_ev.wait(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop_ev.set()
+        if self.nv:
+            self.th.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference_run(cfg: dict, steps: int, warmup: int, budget_s: float):
+    """Time the reference's VecEngine<uint64_t> (oracle/_ref) on this host."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import RefEngine, RefLib
+
+    lib = RefLib()
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    X, Y = cfg["X"], cfg["Y"]
+    eng = RefEngine(lib, X, Y, 1, workers=cores)
+    for _ in range(max(0, min(warmup, 1))):
+        eng.step(cfg["p"], cfg["q"], 1)
+    done, t0 = 0, time.perf_counter()
+    while done < max(1, steps):
+        eng.step(cfg["p"], cfg["q"], 1)
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    el = time.perf_counter() - t0
+    return X * Y * done / (el * 1e9), cores, done, el
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=SCHEDULE_TMAX)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU reference work")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    ws, rank, local = _dist()
+    K, W = args.steps, max(3, args.warmup)
+
+    config_key = {"workload": cfg["workload"], "X": cfg["X"], "Y": cfg["Y"], "p": cfg["p"], "q": cfg["q"],
+                  "w": 64, "seed": 1, "schedule": f"log_schedule({SCHEDULE_TMAX},{SCHEDULE_PPD}) within steps",
+                  "l2": "planes (>=1 GiB) exceed L2 (126 MB); no flush needed", "parallelism": f"rows/{ws}"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        v, cores, done, el = cpu_reference_run(cfg, K, W, args.cpu_budget)
+        sample = f"{done} MCS of {cfg['X']}x{cfg['Y']} (steps only, no W2), {el:.1f} s"
+        print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": "updates/ns",
+                          "n_gpus": 0, "steps": done, "warmup": min(W, 1), "ms_per_step": el * 1e3 / done,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+                          "data": "synthetic (flat start, seed 1)", "config": config_key,
+                          "cpu_baseline": {"value": v, "unit": "updates/ns", "cores": cores, "kind": "reference",
+                                           "sample": sample},
+                          "e2e": {"value": v, "unit": "updates/ns", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}))
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_1606_00310_b200 as octgpu
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    X, Y = cfg["X"], cfg["Y"]
+    lat = octgpu.LatticeConfig(X, Y, 64)
+    prm = octgpu.UpdateParams.make(cfg["p"], cfg["q"])
+    sched = [t for t in octgpu.log_schedule(SCHEDULE_TMAX, SCHEDULE_PPD) if t <= K]
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    # ---- warm-up (separate engine; the timed run starts from the flat state) ----
+    eng = octgpu.GpuEngine(lat, 1, device=local)
+    eng.set_stream(stream.cuda_stream)
+    eng.step(prm, W)
+    eng.measure()
+    eng.sync()
+    eng.close()
+    torch.cuda.synchronize()
+
+    # ---- timed region, device-resident ----
+    eng = octgpu.GpuEngine(lat, 1, device=local)
+    eng.set_stream(stream.cuda_stream)
+    torch.cuda.synchronize()
+    seg_events = []
+    records = []
+    launches0 = eng.launches
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        t = 0
+        for target in sched + ([K] if not sched or sched[-1] != K else []):
+            if target > t:
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                eng.step(prm, target - t)
+                b.record(stream)
+                seg_events.append((a, b))
+                t = target
+            if target in sched:
+                records.append(eng.measure())
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    step_ms = sum(a.elapsed_time(b) for a, b in seg_events)
+    launches = eng.launches - launches0
+    if ws > 1:
+        tt = torch.tensor([ms, step_ms], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms, step_ms = float(tt[0]), float(tt[1])
+    value = ws * X * Y * K / (ms * 1e6)
+    kernel_ms = step_ms / K
+    peak, peak_src = _peaks()
+    alg_bytes = X * Y  # paper identity: 1 byte of slope traffic per site update
+    achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
+    final_checksum = eng.checksum() if X * Y <= (1 << 32) else None
+    eng.close()
+
+    # ---- e2e through the C-ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        flat = octgpu.new_flat(lat)
+        host_planes = torch.from_numpy(flat.planes.view(np.int64)).pin_memory()
+        host_states = torch.from_numpy(octgpu.RngStreamSet.derive(1, Y).states.view(np.int64)).pin_memory()
+        out_planes = torch.empty_like(host_planes).pin_memory()
+        out_states = torch.empty_like(host_states).pin_memory()
+        import ctypes as C
+        L = octgpu._lib.lib()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h = C.c_void_p()
+        octgpu._lib.check(L.octgpu_create_from(X, Y, 64, 0, 0, C.c_void_p(host_planes.data_ptr()),
+                                               C.c_void_p(host_states.data_ptr()), Y, 1, local, C.byref(h)))
+        cp = prm.to_c()
+        m = octgpu._lib.OctMoments()
+        t = 0
+        n_meas = 0
+        for target in sched + ([K] if not sched or sched[-1] != K else []):
+            if target > t:
+                octgpu._lib.check(L.octgpu_step(h, C.byref(cp), target - t))
+                t = target
+            if target in sched:
+                octgpu._lib.check(L.octgpu_measure(h, C.byref(m)))
+                n_meas += 1
+        octgpu._lib.check(L.octgpu_get_planes(h, C.c_void_p(out_planes.data_ptr())))
+        octgpu._lib.check(L.octgpu_get_states(h, C.c_void_p(out_states.data_ptr())))
+        el = time.perf_counter() - t0
+        L.octgpu_destroy(h)
+        if ws > 1:
+            tt = torch.tensor([el], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            el = float(tt[0])
+        e2e = {"value": ws * X * Y * K / (el * 1e9), "unit": "updates/ns",
+               "h2d_bytes_per_step": (host_planes.numel() * 8 + host_states.numel() * 8) / K,
+               "d2h_bytes_per_step": (out_planes.numel() * 8 + out_states.numel() * 8
+                                      + n_meas * C.sizeof(octgpu._lib.OctMoments)) / K,
+               "wall_s": el, "note": "create_from(host planes+states) + K MCS + measurements + planes/states D2H"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            v, cores, done, el = cpu_reference_run(cfg, 1000, 1, args.cpu_budget)
+            cpu = {"value": v, "unit": "updates/ns", "cores": cores, "kind": "reference",
+                   "sample": f"{done} MCS of {X}x{Y} p={cfg['p']} q={cfg['q']} after 1 warm-up MCS, "
+                             f"steps only (no W2), {el:.1f} s, VecEngine<uint64_t> workers={cores}"}
+        except Exception as ex:  # reported, never fatal
+            cpu = {"value": None, "unit": "updates/ns", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "updates/ns", "n_gpus": ws, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u64", "data": "synthetic (flat start h=(x+y) mod 2, seed 1)", "config": config_key,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "kernel": "k_mcs (fused even+odd MCS)",
+                         "alg_bytes_per_launch": alg_bytes, "kernel_ms": kernel_ms, "peak_source": peak_src},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+            "measurements": len(records),
+            "W2_last": records[-1].W2 if records else None,
+            "final_checksum": hex(final_checksum) if final_checksum is not None else None,
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

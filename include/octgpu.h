@@ -1,0 +1,150 @@
+/*
+ * octgpu — C-ABI of the B200-native bit-vectorized octahedron-model SCA.
+ *
+ * This is the drop-in boundary for the reference engine
+ * `octsca::VecEngine<Word>` (/root/reference/proj/include/octsca/engine_vec.hpp:184-213)
+ * as consumed by `octsca::run` (run.hpp:18-38) and `run_session`'s `drive`
+ * (session.cpp:37-85). Plain pointers and sizes only; no C++ or torch types.
+ * Every entry point names the reference interface it replaces.
+ *
+ * Conventions
+ *  - Plane buffers on the host side use the reference SlopeField layout
+ *    (slope_field.hpp:15-53, 207-210): 4 planes in order x/even, x/odd,
+ *    y/even, y/odd; each Y rows x n words, row-major; n = X / (2w); words
+ *    are uint64_t for w = 64 and uint32_t for w = 32, LSB-first, bit 1 =
+ *    slope +1.
+ *  - RNG states: one xoshiro256++ state (4 x uint64_t) per lattice row, in
+ *    row order (RngStreamSet::states(), rng.hpp:102-108).
+ *  - Errors: every function returning int returns an octgpu_status; the
+ *    message of the last failure on the calling thread is available from
+ *    octgpu_last_error(). The codes map 1:1 to the reference exceptions
+ *    (errors.hpp:8-25; CLI exit codes SPEC.md:475). There is NO CPU
+ *    fallback: if CUDA is unavailable the call fails with OCTGPU_ERR_CUDA.
+ *  - Engines are not thread-safe (same as VecEngine). All work is enqueued
+ *    on the engine's CUDA stream; calls that return data synchronise.
+ */
+#ifndef OCTGPU_H
+#define OCTGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    OCTGPU_OK = 0,
+    OCTGPU_ERR_CONFIG = 1,    /* octsca::ConfigError    (errors.hpp:8-12)  */
+    OCTGPU_ERR_INVARIANT = 2, /* octsca::InvariantError (errors.hpp:14-19) */
+    OCTGPU_ERR_IO = 3,        /* octsca::IoError        (errors.hpp:21-25) */
+    OCTGPU_ERR_CUDA = 4       /* device/runtime failure (no reference analogue) */
+} octgpu_status;
+
+/* octsca::ProbMode (params.hpp:13) */
+typedef enum { OCTGPU_ZERO = 0, OCTGPU_HALF = 1, OCTGPU_DYADIC = 2, OCTGPU_ARBITRARY = 3 } octgpu_mode;
+
+/* octsca::ProbSpec (params.hpp:28-44): value + generation mode (+ DyadicPlan
+ * rng.hpp:142-151 as r = m / 2^k with m odd; ops follow the bits of m). */
+typedef struct {
+    double value;
+    int32_t mode;
+    uint32_t k;
+    uint64_t m;
+} octgpu_prob;
+
+/* octsca::UpdateParams (params.hpp:95-102) */
+typedef struct {
+    octgpu_prob p;
+    octgpu_prob q;
+} octgpu_params;
+
+/* MeasurementRecord (measure.hpp:11-17) plus the exact integer sufficient
+ * statistics it is derived from: S_k = sum_{x,y} h(x,y)^k with the
+ * reference's gauge h(0,0) = 0 (slope_field.hpp:214), as two's-complement
+ * int128 split into (lo, hi). */
+typedef struct {
+    uint64_t t;
+    uint64_t n_sites;
+    uint64_t s_lo[4];
+    int64_t s_hi[4];
+    double W2;
+    double mean_h;
+    double skew;
+    double kurt;
+} octgpu_moments;
+
+typedef struct octgpu_engine octgpu_engine;
+
+/* ---- host-side parameter plumbing (no GPU needed) ---- */
+
+/* ProbSpec::resolve(r) when forced_mode < 0, else ProbSpec::resolve(r, forced)
+ * (params.hpp:34-69, dyadic_plan rng.cpp:7-30). */
+int octgpu_resolve(double r, int forced_mode, octgpu_prob* out);
+/* ProbSpec::draws_per_word (params.hpp:72-80) */
+uint32_t octgpu_draws_per_word(const octgpu_prob* p, uint32_t w);
+/* LatticeConfig::validate (lattice.hpp:31-39) */
+int octgpu_validate_lattice(uint32_t X, uint32_t Y, uint32_t w);
+/* RngStreamSet(master_seed, n).states() (rng.hpp:84-94, 102-108) into out[n*4] */
+int octgpu_stream_states(uint64_t master_seed, uint32_t n, uint64_t* out);
+/* log_schedule (measure.cpp:143-165); returns the number of points, writes up to cap */
+uint32_t octgpu_log_schedule(uint64_t t_max, uint32_t points_per_decade, uint64_t* out, uint32_t cap);
+
+/* ---- engine lifecycle ---- */
+
+/* VecEngine(LatticeConfig{X,Y,w}, seed, workers) (engine_vec.hpp:187-189):
+ * new_flat field (slope_field.hpp:110-118), RngStreamSet(seed, Y). */
+int octgpu_create(uint32_t X, uint32_t Y, uint32_t w, uint64_t seed, int device, octgpu_engine** out);
+/* VecEngine(SlopeField, RngStreamSet, workers) (engine_vec.hpp:191-193) —
+ * resume from any state, including phase = 1 (mid-MCS). planes: host,
+ * reference layout; states: host, n_states >= Y rows of 4 words. */
+int octgpu_create_from(uint32_t X, uint32_t Y, uint32_t w, uint64_t t_mcs, int phase, const void* planes,
+                       const uint64_t* states, uint32_t n_states, uint64_t master_seed, int device,
+                       octgpu_engine** out);
+void octgpu_destroy(octgpu_engine* e);
+/* Use an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL restores the engine's own. */
+int octgpu_set_stream(octgpu_engine* e, void* cuda_stream);
+/* Block until all enqueued work finished; surfaces asynchronous CUDA errors. */
+int octgpu_sync(octgpu_engine* e);
+
+/* ---- the hot path ---- */
+
+/* n_mcs x VecEngine::step(prm) = mcs_step (engine_vec.hpp:171-177, 197). */
+int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs);
+/* sublattice_sweep(field, parity, prm, plan, streams, mask_log)
+ * (engine_vec.hpp:145-168). mask_log: NULL or host buffer of Y*n words
+ * (reference row-major), receives the applied mask of every (row, word). */
+int octgpu_sweep(octgpu_engine* e, int parity, const octgpu_params* prm, void* mask_log);
+
+/* ---- state access ---- */
+
+uint64_t octgpu_t(const octgpu_engine* e);         /* VecEngine::t (engine_vec.hpp:199) */
+int octgpu_phase(const octgpu_engine* e);          /* SlopeField::phase (slope_field.hpp:44) */
+uint64_t octgpu_master_seed(const octgpu_engine* e); /* RngStreamSet::master_seed (rng.hpp:97) */
+/* VecEngine::field() planes (engine_vec.hpp:200-201), reference layout, 4*Y*n words */
+int octgpu_get_planes(octgpu_engine* e, void* out);
+/* VecEngine::streams().states() (rng.hpp:102-108), Y*4 words */
+int octgpu_get_states(octgpu_engine* e, uint64_t* out);
+/* field_checksum(field()) (slope_field.hpp:232-246) */
+int octgpu_field_checksum(octgpu_engine* e, uint64_t* out);
+
+/* ---- measurement ---- */
+
+/* measure_heights(t(), heights()) (run.hpp:28, measure.cpp:53-56) computed on
+ * the device without materialising the HeightMap: curl_check + closure checks
+ * as reconstruct_heights (slope_field.hpp:206-229, same InvariantError
+ * messages), exact int128 power sums, doubles derived from them. */
+int octgpu_measure(octgpu_engine* e, octgpu_moments* out);
+/* VecEngine::heights() = reconstruct_heights(field) (engine_vec.hpp:207):
+ * out[y*X + x] int32, h(0,0) = 0. */
+int octgpu_heights(octgpu_engine* e, int32_t* out);
+
+/* ---- diagnostics ---- */
+const char* octgpu_last_error(void);
+const char* octgpu_version(void);
+/* Number of kernel launches this engine has issued (for launch accounting). */
+uint64_t octgpu_launch_count(const octgpu_engine* e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OCTGPU_H */

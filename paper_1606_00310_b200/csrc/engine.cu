@@ -1,0 +1,757 @@
+// Host side of liboctgpu: the C-ABI (include/octgpu.h), engine state,
+// parameter resolution, stream seeding and GF(2) jump-ahead matrices.
+// Device work lives in kernels.cu.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "octgpu.h"
+#include "octgpu_internal.h"
+
+using namespace octgpu;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(OCTGPU_ERR_CUDA, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+#define CK(x)                                         \
+    do {                                              \
+        cudaError_t e_ = (x);                         \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #x); \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// xoshiro256++ on the host (rng.hpp:25-60)
+
+inline uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+
+inline void xo_advance(uint64_t s[4]) {
+    const uint64_t t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = rotl(s[3], 45);
+}
+
+uint64_t splitmix64(uint64_t& x) {
+    uint64_t z = (x += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// ---------------------------------------------------------------------------
+// GF(2) 256x256 matrices: the xoshiro state transition is linear, so
+// advancing a stream by N draws is s -> T^N s. Column j = image of bit j.
+
+struct M256 {
+    uint64_t c[256][4];
+};
+
+inline void mat_vec(const M256& M, const uint64_t v[4], uint64_t out[4]) {
+    uint64_t r[4] = {0, 0, 0, 0};
+    for (int w = 0; w < 4; ++w) {
+        uint64_t bits = v[w];
+        while (bits) {
+            const int b = __builtin_ctzll(bits);
+            bits &= bits - 1;
+            const uint64_t* col = M.c[w * 64 + b];
+            r[0] ^= col[0];
+            r[1] ^= col[1];
+            r[2] ^= col[2];
+            r[3] ^= col[3];
+        }
+    }
+    std::memcpy(out, r, sizeof r);
+}
+
+void mat_mul(const M256& A, const M256& B, M256& out) {  // out = A * B
+    M256 tmp;
+    for (int j = 0; j < 256; ++j) mat_vec(A, B.c[j], tmp.c[j]);
+    out = tmp;
+}
+
+struct JumpCache {
+    std::mutex mu;
+    std::vector<M256> pow2;  // pow2[i] = T^(2^i)
+    bool have_jump = false;
+    std::vector<uint64_t> jump_table;  // 4-bit table of T^(2^128), for seeding
+
+    const M256& pow(int i) {
+        if (pow2.empty()) {
+            M256 T;
+            for (int j = 0; j < 256; ++j) {
+                uint64_t s[4] = {0, 0, 0, 0};
+                s[j / 64] = uint64_t(1) << (j % 64);
+                xo_advance(s);
+                std::memcpy(T.c[j], s, sizeof s);
+            }
+            pow2.push_back(T);
+        }
+        while (int(pow2.size()) <= i) {
+            M256 sq;
+            mat_mul(pow2.back(), pow2.back(), sq);
+            pow2.push_back(sq);
+        }
+        return pow2[i];
+    }
+
+    // T^N for a 64-bit N
+    M256 power(uint64_t N) {
+        M256 R;
+        std::memset(&R, 0, sizeof R);
+        for (int j = 0; j < 256; ++j) R.c[j][j / 64] = uint64_t(1) << (j % 64);
+        for (int i = 0; i < 64; ++i)
+            if (N >> i & 1) mat_mul(pow(i), R, R);
+        return R;
+    }
+};
+
+JumpCache& jc() {
+    static JumpCache c;
+    return c;
+}
+
+// 4-bit table: tab[(i*16 + nib)*4 + w] = (XOR of columns 4i+b, b in nib)[w]
+std::vector<uint64_t> table_of(const M256& M) {
+    std::vector<uint64_t> tab(64 * 16 * 4, 0);
+    for (int i = 0; i < 64; ++i)
+        for (int nib = 1; nib < 16; ++nib) {
+            uint64_t* e = &tab[(size_t(i) * 16 + nib) * 4];
+            for (int b = 0; b < 4; ++b)
+                if (nib >> b & 1)
+                    for (int w = 0; w < 4; ++w) e[w] ^= M.c[4 * i + b][w];
+        }
+    return tab;
+}
+
+inline void table_apply(const std::vector<uint64_t>& tab, uint64_t s[4]) {
+    uint64_t r[4] = {0, 0, 0, 0};
+    for (int i = 0; i < 64; ++i) {
+        const uint32_t nib = uint32_t(s[i >> 4] >> (4 * (i & 15))) & 15u;
+        const uint64_t* e = &tab[(size_t(i) * 16 + nib) * 4];
+        r[0] ^= e[0]; r[1] ^= e[1]; r[2] ^= e[2]; r[3] ^= e[3];
+    }
+    std::memcpy(s, r, sizeof r);
+}
+
+const std::vector<uint64_t>& seed_jump_table() {
+    JumpCache& c = jc();
+    std::lock_guard<std::mutex> lk(c.mu);
+    if (!c.have_jump) {
+        c.jump_table = table_of(c.pow(128));  // RngStream::jump() == 2^128 draws (rng.hpp:46)
+        c.have_jump = true;
+    }
+    return c.jump_table;
+}
+
+std::vector<uint64_t> power_table(uint64_t N) {
+    JumpCache& c = jc();
+    std::lock_guard<std::mutex> lk(c.mu);
+    return table_of(c.power(N));
+}
+
+// RngStreamSet(master_seed, n) (rng.hpp:84-94): stream i = i jumps from from_seed.
+void stream_states(uint64_t seed, uint32_t n, uint64_t* out) {
+    uint64_t s[4];
+    for (auto& v : s) v = splitmix64(seed);
+    if ((s[0] | s[1] | s[2] | s[3]) == 0) s[0] = 1;
+    const auto& tab = seed_jump_table();
+    for (uint32_t i = 0; i < n; ++i) {
+        std::memcpy(out + 4 * size_t(i), s, sizeof s);
+        if (i + 1 < n) table_apply(tab, s);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Parameter resolution (params.hpp:34-80, rng.cpp:7-30)
+
+bool dyadic_plan(double r, uint32_t max_words, uint32_t& k, uint64_t& m) {
+    if (!(r > 0.0 && r < 1.0)) return false;
+    const double scaled = std::ldexp(r, int(max_words));
+    if (scaled != std::floor(scaled)) return false;
+    m = uint64_t(scaled);
+    k = max_words;
+    while (k > 0 && (m & 1) == 0) {
+        m >>= 1;
+        --k;
+    }
+    return true;
+}
+
+std::string fmt_r(double r) {
+    return std::to_string(r);  // std::to_string as the reference message (params.hpp:36)
+}
+
+int resolve(double r, int forced, octgpu_prob& o) {
+    if (r < 0.0 || r > 1.0) return fail(OCTGPU_ERR_CONFIG, "probability must be in [0,1], got " + fmt_r(r));
+    o.value = r;
+    o.k = 0;
+    o.m = 0;
+    if (r == 0.0)
+        o.mode = OCTGPU_ZERO;
+    else if (r == 0.5)
+        o.mode = OCTGPU_HALF;
+    else if (dyadic_plan(r, 16, o.k, o.m))
+        o.mode = OCTGPU_DYADIC;
+    else
+        o.mode = OCTGPU_ARBITRARY;
+    if (forced < 0 || forced == o.mode) return OCTGPU_OK;
+    switch (forced) {
+    case OCTGPU_ZERO:
+        if (r != 0.0) return fail(OCTGPU_ERR_CONFIG, "mode zero requires probability 0");
+        break;
+    case OCTGPU_HALF:
+        if (r != 0.5) return fail(OCTGPU_ERR_CONFIG, "mode half requires probability 0.5");
+        break;
+    case OCTGPU_DYADIC:
+        if (dyadic_plan(r, 16, o.k, o.m)) {
+            o.mode = OCTGPU_DYADIC;
+            return OCTGPU_OK;
+        }
+        return fail(OCTGPU_ERR_CONFIG, "probability has no dyadic plan within 16 words");
+    case OCTGPU_ARBITRARY:
+        if (r == 0.0) return fail(OCTGPU_ERR_CONFIG, "mode arbitrary is pointless for probability 0; use zero");
+        o.mode = OCTGPU_ARBITRARY;
+        o.k = 0;
+        o.m = 0;
+        return OCTGPU_OK;
+    default:
+        return fail(OCTGPU_ERR_CONFIG, "unknown probability mode " + std::to_string(forced));
+    }
+    return OCTGPU_OK;
+}
+
+uint32_t draws(const octgpu_prob& p, uint32_t w) {
+    switch (p.mode) {
+    case OCTGPU_ZERO: return 0;
+    case OCTGPU_HALF: return 1;
+    case OCTGPU_DYADIC: return p.k;
+    default: return w;
+    }
+}
+
+// Checks a caller-supplied ProbSpec and lowers it to the device form.
+int lower(const octgpu_prob& p, ProbDev& d) {
+    d = ProbDev{M_ZERO, 0, 0, 0};
+    const double r = p.value;
+    if (!(r >= 0.0 && r <= 1.0)) return fail(OCTGPU_ERR_CONFIG, "probability must be in [0,1], got " + fmt_r(r));
+    switch (p.mode) {
+    case OCTGPU_ZERO:
+        if (r != 0.0) return fail(OCTGPU_ERR_CONFIG, "mode zero requires probability 0");
+        d.mode = M_ZERO;
+        return OCTGPU_OK;
+    case OCTGPU_HALF:
+        if (r != 0.5) return fail(OCTGPU_ERR_CONFIG, "mode half requires probability 0.5");
+        d.mode = M_HALF;
+        return OCTGPU_OK;
+    case OCTGPU_DYADIC: {
+        if (p.k < 1 || p.k > 64 || (p.m & 1) == 0 || std::ldexp(double(p.m), -int(p.k)) != r)
+            return fail(OCTGPU_ERR_CONFIG, "inconsistent dyadic plan");
+        d.mode = M_DYADIC;
+        d.k = p.k;
+        d.m = p.m;
+        return OCTGPU_OK;
+    }
+    case OCTGPU_ARBITRARY: {
+        if (r == 0.0) return fail(OCTGPU_ERR_CONFIG, "mode arbitrary is pointless for probability 0; use zero");
+        // to_unit(x) < r  <=>  (x >> 11) < ceil(r * 2^53)  <=>  x < ceil(r * 2^53) << 11
+        const double scaled = std::ldexp(r, 53);  // exact
+        const uint64_t thr = uint64_t(std::ceil(scaled));
+        if (thr >= (uint64_t(1) << 53)) {
+            d.mode = M_ONE;  // r == 1: all bits accepted
+        } else {
+            d.mode = M_ARB;
+            d.T = thr << 11;
+        }
+        return OCTGPU_OK;
+    }
+    default:
+        return fail(OCTGPU_ERR_CONFIG, "unknown probability mode " + std::to_string(p.mode));
+    }
+}
+
+inline bool is_const(const ProbDev& d) { return d.mode == M_ZERO || d.mode == M_ONE; }
+
+int validate(uint32_t X, uint32_t Y, uint32_t w) {  // lattice.hpp:31-39
+    if (w != 32 && w != 64) return fail(OCTGPU_ERR_CONFIG, "word size must be 32 or 64, got " + std::to_string(w));
+    if (X == 0 || X % (2 * w) != 0)
+        return fail(OCTGPU_ERR_CONFIG, "X must be a positive multiple of 2*w = " + std::to_string(2 * w) +
+                                           ", got " + std::to_string(X));
+    if (Y < 2 || Y % 2 != 0) return fail(OCTGPU_ERR_CONFIG, "Y must be even and >= 2, got " + std::to_string(Y));
+    return OCTGPU_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Engine
+
+struct octgpu_engine {
+    uint32_t X = 0, Y = 0, w = 64, n = 0;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    void* planes[2] = {nullptr, nullptr};  // ping-pong plane sets (word-major)
+    uint64_t* rng[2] = {nullptr, nullptr};  // ping-pong SoA row states
+    int pcur = 0;  // current plane set
+    int rcur = 0;  // current rng state set
+    uint64_t t = 0;
+    int phase = 0;
+    uint64_t master_seed = 0;
+    uint64_t pending = 0;  // draws owed to every row stream (constant-xi sweeps)
+    void* stage = nullptr;  // reference-layout staging buffer
+    void* scratch = nullptr;
+    MeasureResult* res_dev = nullptr;
+    MeasureResult* res_host = nullptr;
+    std::map<uint64_t, uint64_t*> jtabs;  // draws -> device 4-bit table of T^draws
+    uint64_t launches = 0;
+
+    Geom geom() const { return Geom{Y, n, size_t(n) * Y}; }
+    size_t word_bytes() const { return w / 8; }
+    size_t set_bytes() const { return 4 * size_t(n) * Y * word_bytes(); }
+    size_t rng_bytes() const { return 4 * size_t(Y) * sizeof(uint64_t); }
+};
+
+namespace {
+
+int use_device(octgpu_engine* e) {
+    CK(cudaSetDevice(e->device));
+    return OCTGPU_OK;
+}
+
+int ensure_stage(octgpu_engine* e) {
+    if (!e->stage) CK(cudaMalloc(&e->stage, e->set_bytes()));
+    return OCTGPU_OK;
+}
+
+int get_table(octgpu_engine* e, uint64_t draws_n, uint64_t** out) {
+    auto it = e->jtabs.find(draws_n);
+    if (it != e->jtabs.end()) {
+        *out = it->second;
+        return OCTGPU_OK;
+    }
+    std::vector<uint64_t> tab = power_table(draws_n);
+    uint64_t* d = nullptr;
+    CK(cudaMalloc(&d, tab.size() * sizeof(uint64_t)));
+    CK(cudaMemcpy(d, tab.data(), tab.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    e->jtabs[draws_n] = d;
+    *out = d;
+    return OCTGPU_OK;
+}
+
+// Apply owed draws to every row stream (lazy advance of constant-xi sweeps).
+int materialize(octgpu_engine* e) {
+    if (!e->pending) return OCTGPU_OK;
+    uint64_t* tab = nullptr;
+    int rc = get_table(e, e->pending, &tab);
+    if (rc) return rc;
+    CK(launch_apply_jump(e->rng[e->rcur], e->Y, tab, e->stream));
+    ++e->launches;
+    e->pending = 0;
+    return OCTGPU_OK;
+}
+
+int upload_states(octgpu_engine* e, const uint64_t* aos) {
+    std::vector<uint64_t> soa(4 * size_t(e->Y));
+    for (uint32_t y = 0; y < e->Y; ++y)
+        for (int j = 0; j < 4; ++j) soa[size_t(j) * e->Y + y] = aos[4 * size_t(y) + j];
+    CK(cudaMemcpyAsync(e->rng[e->rcur], soa.data(), e->rng_bytes(), cudaMemcpyHostToDevice, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    return OCTGPU_OK;
+}
+
+int alloc_engine(octgpu_engine* e) {
+    CK(cudaSetDevice(e->device));
+    CK(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
+    e->stream = e->own_stream;
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaMalloc(&e->planes[i], e->set_bytes()));
+        CK(cudaMalloc(reinterpret_cast<void**>(&e->rng[i]), e->rng_bytes()));
+    }
+    CK(cudaMalloc(&e->scratch, measure_scratch_bytes(e->Y)));
+    CK(cudaMalloc(reinterpret_cast<void**>(&e->res_dev), sizeof(MeasureResult)));
+    CK(cudaMallocHost(reinterpret_cast<void**>(&e->res_host), sizeof(MeasureResult)));
+    return OCTGPU_OK;
+}
+
+int lower_params(const octgpu_params* prm, ProbDev& p, ProbDev& q) {
+    if (!prm) return fail(OCTGPU_ERR_CONFIG, "null parameters");
+    int rc = lower(prm->p, p);
+    if (rc) return rc;
+    return lower(prm->q, q);
+}
+
+__int128 i128_of(uint64_t lo, int64_t hi) { return (__int128)(((unsigned __int128)(uint64_t)hi << 64) | lo); }
+
+}  // namespace
+
+extern "C" {
+
+const char* octgpu_last_error(void) { return g_err.c_str(); }
+const char* octgpu_version(void) { return "octgpu 0.1.0 (octsca 0.1.0 drop-in, sm_100a)"; }
+
+int octgpu_resolve(double r, int forced_mode, octgpu_prob* out) {
+    if (!out) return fail(OCTGPU_ERR_CONFIG, "null output");
+    return resolve(r, forced_mode, *out);
+}
+
+uint32_t octgpu_draws_per_word(const octgpu_prob* p, uint32_t w) { return p ? draws(*p, w) : 0; }
+
+int octgpu_validate_lattice(uint32_t X, uint32_t Y, uint32_t w) { return validate(X, Y, w); }
+
+int octgpu_stream_states(uint64_t master_seed, uint32_t n, uint64_t* out) {
+    if (n < 1) return fail(OCTGPU_ERR_CONFIG, "stream count must be >= 1");
+    stream_states(master_seed, n, out);
+    return OCTGPU_OK;
+}
+
+uint32_t octgpu_log_schedule(uint64_t t_max, uint32_t ppd, uint64_t* out, uint32_t cap) {
+    if (t_max < 1 || ppd < 1) {
+        fail(OCTGPU_ERR_CONFIG, t_max < 1 ? "t_max must be >= 1" : "points_per_decade must be >= 1");
+        return 0;
+    }
+    std::vector<uint64_t> times;
+    uint64_t prev = 0;
+    for (uint32_t k = 0;; ++k) {
+        const double exact = std::pow(10.0, double(k) / double(ppd));
+        if (exact > double(t_max) * (1.0 + 1e-12)) break;
+        uint64_t tt = uint64_t(std::llround(exact));
+        if (tt <= prev) tt = prev + 1;
+        if (tt > t_max) break;
+        times.push_back(tt);
+        prev = tt;
+    }
+    if (times.empty() || times.back() != t_max) times.push_back(t_max);
+    for (size_t i = 0; i < times.size() && i < cap; ++i) out[i] = times[i];
+    return uint32_t(times.size());
+}
+
+int octgpu_create(uint32_t X, uint32_t Y, uint32_t w, uint64_t seed, int device, octgpu_engine** out) {
+    if (!out) return fail(OCTGPU_ERR_CONFIG, "null output");
+    *out = nullptr;
+    int rc = validate(X, Y, w);
+    if (rc) return rc;
+    auto* e = new octgpu_engine;
+    e->X = X; e->Y = Y; e->w = w; e->n = X / (2 * w); e->device = device; e->master_seed = seed;
+    rc = alloc_engine(e);
+    if (!rc) {
+        // new_flat: odd planes all ones, even planes zero (slope_field.hpp:110-118)
+        const size_t pb = e->set_bytes() / 4;
+        char* base = static_cast<char*>(e->planes[0]);
+        for (int p = 0; p < 4; ++p)
+            if (cudaMemsetAsync(base + p * pb, (p & 1) ? 0xff : 0x00, pb, e->stream) != cudaSuccess) {
+                rc = cuda_fail(cudaGetLastError(), "cudaMemsetAsync");
+                break;
+            }
+    }
+    if (!rc) {
+        std::vector<uint64_t> st(4 * size_t(Y));
+        stream_states(seed, Y, st.data());
+        rc = upload_states(e, st.data());
+    }
+    if (rc) {
+        std::string keep = g_err;
+        octgpu_destroy(e);
+        g_err = keep;
+        return rc;
+    }
+    *out = e;
+    return OCTGPU_OK;
+}
+
+int octgpu_create_from(uint32_t X, uint32_t Y, uint32_t w, uint64_t t_mcs, int phase, const void* planes,
+                       const uint64_t* states, uint32_t n_states, uint64_t master_seed, int device,
+                       octgpu_engine** out) {
+    if (!out || !planes || !states) return fail(OCTGPU_ERR_CONFIG, "null argument");
+    *out = nullptr;
+    int rc = validate(X, Y, w);
+    if (rc) return rc;
+    if (phase != 0 && phase != 1) return fail(OCTGPU_ERR_CONFIG, "phase must be 0 or 1");
+    if (n_states < Y) return fail(OCTGPU_ERR_INVARIANT, "stream set smaller than row count");
+    auto* e = new octgpu_engine;
+    e->X = X; e->Y = Y; e->w = w; e->n = X / (2 * w); e->device = device; e->master_seed = master_seed;
+    e->t = t_mcs; e->phase = phase;
+    rc = alloc_engine(e);
+    if (!rc) rc = ensure_stage(e);
+    if (!rc) {
+        if (cudaMemcpyAsync(e->stage, planes, e->set_bytes(), cudaMemcpyHostToDevice, e->stream) != cudaSuccess)
+            rc = cuda_fail(cudaGetLastError(), "cudaMemcpyAsync(planes)");
+        else if (launch_import(e->w, e->stage, e->planes[0], e->geom(), e->stream) != cudaSuccess)
+            rc = cuda_fail(cudaGetLastError(), "import");
+        else
+            ++e->launches;
+    }
+    if (!rc) rc = upload_states(e, states);
+    if (rc) {
+        std::string keep = g_err;
+        octgpu_destroy(e);
+        g_err = keep;
+        return rc;
+    }
+    *out = e;
+    return OCTGPU_OK;
+}
+
+void octgpu_destroy(octgpu_engine* e) {
+    if (!e) return;
+    cudaSetDevice(e->device);
+    if (e->stream) cudaStreamSynchronize(e->stream);
+    for (int i = 0; i < 2; ++i) {
+        if (e->planes[i]) cudaFree(e->planes[i]);
+        if (e->rng[i]) cudaFree(e->rng[i]);
+    }
+    for (auto& kv : e->jtabs) cudaFree(kv.second);
+    if (e->stage) cudaFree(e->stage);
+    if (e->scratch) cudaFree(e->scratch);
+    if (e->res_dev) cudaFree(e->res_dev);
+    if (e->res_host) cudaFreeHost(e->res_host);
+    if (e->own_stream) cudaStreamDestroy(e->own_stream);
+    delete e;
+}
+
+int octgpu_set_stream(octgpu_engine* e, void* s) {
+    if (!e) return fail(OCTGPU_ERR_CONFIG, "null engine");
+    int rc = use_device(e);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(e->stream));
+    e->stream = s ? static_cast<cudaStream_t>(s) : e->own_stream;
+    return OCTGPU_OK;
+}
+
+int octgpu_sync(octgpu_engine* e) {
+    if (!e) return fail(OCTGPU_ERR_CONFIG, "null engine");
+    int rc = use_device(e);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(e->stream));
+    CK(cudaGetLastError());
+    return OCTGPU_OK;
+}
+
+int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
+    if (!e) return fail(OCTGPU_ERR_CONFIG, "null engine");
+    ProbDev p, q;
+    int rc = lower_params(prm, p, q);
+    if (rc) return rc;
+    if (n_mcs == 0) return OCTGPU_OK;
+    rc = use_device(e);
+    if (rc) return rc;
+    const bool live = !(is_const(p) && is_const(q));
+    const uint64_t D = draws(prm->p, e->w) + (q.mode != M_ZERO ? draws(prm->q, e->w) : 0);
+    const uint64_t per_sweep = uint64_t(e->n) * D;
+    uint64_t* jtab = nullptr;
+    if (live) {
+        rc = materialize(e);
+        if (rc) return rc;
+        rc = get_table(e, per_sweep, &jtab);
+        if (rc) return rc;
+    }
+    const Geom g = e->geom();
+    for (uint64_t i = 0; i < n_mcs; ++i) {
+        const int ps = e->pcur, rs = e->rcur;
+        CK(launch_mcs(e->w, e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, live,
+                      jtab, e->stream));
+        ++e->launches;
+        e->pcur ^= 1;
+        if (live)
+            e->rcur ^= 1;
+        else
+            e->pending += 2 * per_sweep;  // constant xi: streams advance lazily
+        ++e->t;  // two sweeps: phase returns to its value (engine_vec.hpp:172-177)
+    }
+    return OCTGPU_OK;
+}
+
+int octgpu_sweep(octgpu_engine* e, int parity, const octgpu_params* prm, void* mask_log) {
+    if (!e) return fail(OCTGPU_ERR_CONFIG, "null engine");
+    if (parity != e->phase)  // engine_vec.hpp:150-152
+        return fail(OCTGPU_ERR_INVARIANT, "sweep parity " + std::to_string(parity) +
+                                              " does not match field phase " + std::to_string(e->phase));
+    ProbDev p, q;
+    int rc = lower_params(prm, p, q);
+    if (rc) return rc;
+    rc = use_device(e);
+    if (rc) return rc;
+    const bool live = !(is_const(p) && is_const(q));
+    const uint64_t D = draws(prm->p, e->w) + (q.mode != M_ZERO ? draws(prm->q, e->w) : 0);
+    if (live) {
+        rc = materialize(e);
+        if (rc) return rc;
+    }
+    void* mlog = nullptr;
+    const size_t log_bytes = size_t(e->Y) * e->n * e->word_bytes();
+    if (mask_log) CK(cudaMalloc(&mlog, log_bytes));
+    const cudaError_t le =
+        launch_sweep(e->w, e->planes[e->pcur], e->rng[e->rcur], parity, e->geom(), p, q, live, mlog, e->stream);
+    if (le != cudaSuccess) {
+        if (mlog) cudaFree(mlog);
+        return cuda_fail(le, "sweep");
+    }
+    ++e->launches;
+    if (!live) e->pending += uint64_t(e->n) * D;
+    e->phase ^= 1;
+    if (mask_log) {
+        CK(cudaMemcpyAsync(mask_log, mlog, log_bytes, cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+        CK(cudaFree(mlog));
+    }
+    return OCTGPU_OK;
+}
+
+uint64_t octgpu_t(const octgpu_engine* e) { return e ? e->t : 0; }
+int octgpu_phase(const octgpu_engine* e) { return e ? e->phase : 0; }
+uint64_t octgpu_master_seed(const octgpu_engine* e) { return e ? e->master_seed : 0; }
+uint64_t octgpu_launch_count(const octgpu_engine* e) { return e ? e->launches : 0; }
+
+int octgpu_get_planes(octgpu_engine* e, void* out) {
+    if (!e || !out) return fail(OCTGPU_ERR_CONFIG, "null argument");
+    int rc = use_device(e);
+    if (!rc) rc = ensure_stage(e);
+    if (rc) return rc;
+    CK(launch_export(e->w, e->planes[e->pcur], e->stage, e->geom(), e->stream));
+    ++e->launches;
+    CK(cudaMemcpyAsync(out, e->stage, e->set_bytes(), cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    return OCTGPU_OK;
+}
+
+int octgpu_get_states(octgpu_engine* e, uint64_t* out) {
+    if (!e || !out) return fail(OCTGPU_ERR_CONFIG, "null argument");
+    int rc = use_device(e);
+    if (!rc) rc = materialize(e);
+    if (rc) return rc;
+    std::vector<uint64_t> soa(4 * size_t(e->Y));
+    CK(cudaMemcpyAsync(soa.data(), e->rng[e->rcur], e->rng_bytes(), cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    for (uint32_t y = 0; y < e->Y; ++y)
+        for (int j = 0; j < 4; ++j) out[4 * size_t(y) + j] = soa[size_t(j) * e->Y + y];
+    return OCTGPU_OK;
+}
+
+int octgpu_field_checksum(octgpu_engine* e, uint64_t* out) {
+    if (!e || !out) return fail(OCTGPU_ERR_CONFIG, "null argument");
+    std::vector<unsigned char> buf(e->set_bytes());
+    int rc = octgpu_get_planes(e, buf.data());
+    if (rc) return rc;
+    uint64_t h = 0xcbf29ce484222325ULL;  // FNV-1a, slope_field.hpp:232-246
+    auto mix = [&h](uint64_t v) {
+        for (int i = 0; i < 8; ++i) {
+            h ^= (v >> (8 * i)) & 0xff;
+            h *= 0x100000001b3ULL;
+        }
+    };
+    const size_t nw = 4 * size_t(e->n) * e->Y;
+    if (e->w == 64) {
+        const uint64_t* p = reinterpret_cast<const uint64_t*>(buf.data());
+        for (size_t i = 0; i < nw; ++i) mix(p[i]);
+    } else {
+        const uint32_t* p = reinterpret_cast<const uint32_t*>(buf.data());
+        for (size_t i = 0; i < nw; ++i) mix(uint64_t(p[i]));
+    }
+    mix(e->t);
+    *out = h;
+    return OCTGPU_OK;
+}
+
+namespace {
+
+int run_measure(octgpu_engine* e) {
+    int rc = use_device(e);
+    if (rc) return rc;
+    CK(launch_measure(e->w, e->planes[e->pcur], e->geom(), e->X, e->scratch, e->res_dev, e->stream));
+    e->launches += 2;
+    CK(cudaMemcpyAsync(e->res_host, e->res_dev, sizeof(MeasureResult), cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    const MeasureResult& r = *e->res_host;
+    // reconstruct_heights' checks, in its order (slope_field.hpp:209-226)
+    if (r.curl_count) {
+        const uint64_t x = r.curl_first % e->X, y = r.curl_first / e->X;
+        return fail(OCTGPU_ERR_INVARIANT, "curl violation at plaquette (" + std::to_string(x) + "," +
+                                              std::to_string(y) + "); " + std::to_string(r.curl_count) +
+                                              " plaquettes inconsistent");
+    }
+    if (r.row0_sum != 0) return fail(OCTGPU_ERR_INVARIANT, "row 0 of sigma_x- does not balance to zero");
+    // curl-free => all column sums are equal, so column 0 is the first failing one
+    if (r.col0_sum != 0) return fail(OCTGPU_ERR_INVARIANT, "column 0 of sigma_y- does not balance to zero");
+    return OCTGPU_OK;
+}
+
+}  // namespace
+
+int octgpu_measure(octgpu_engine* e, octgpu_moments* out) {
+    if (!e || !out) return fail(OCTGPU_ERR_CONFIG, "null argument");
+    int rc = run_measure(e);
+    if (rc) return rc;
+    const MeasureResult& r = *e->res_host;
+    const uint64_t N = uint64_t(e->X) * e->Y;
+    out->t = e->t;
+    out->n_sites = N;
+    __int128 S[4];
+    for (int k = 0; k < 4; ++k) {
+        out->s_lo[k] = r.s_lo[k];
+        out->s_hi[k] = r.s_hi[k];
+        S[k] = i128_of(r.s_lo[k], r.s_hi[k]);
+    }
+    // mean = S1/N exactly rounded (the reference's double sum is exact here).
+    out->mean_h = double(S[0]) / double(N);
+    // Central moments about the nearest integer c, exact in int128, then one
+    // extended-precision correction for d = mean - c (|d| <= 1/2).
+    const __int128 NN = N;
+    __int128 c = S[0] / NN;
+    if (2 * (S[0] - c * NN) > NN) c += 1;
+    if (2 * (S[0] - c * NN) < -NN) c -= 1;
+    const __int128 c2 = c * c, c3 = c2 * c, c4 = c3 * c;
+    const __int128 T1 = S[0] - c * NN;
+    const __int128 T2 = S[1] - 2 * c * S[0] + c2 * NN;
+    const __int128 T3 = S[2] - 3 * c * S[1] + 3 * c2 * S[0] - c3 * NN;
+    const __int128 T4 = S[3] - 4 * c * S[2] + 6 * c2 * S[1] - 4 * c3 * S[0] + c4 * NN;
+    const long double n = (long double)N;
+    const long double d = (long double)T1 / n;
+    const long double t2 = (long double)T2 / n, t3 = (long double)T3 / n, t4 = (long double)T4 / n;
+    const bool flat = (NN * T2 == T1 * T1);  // m2 == 0 exactly
+    const long double m2 = flat ? 0.0L : t2 - d * d;
+    const long double m3 = t3 - 3 * d * t2 + 2 * d * d * d;
+    const long double m4 = t4 - 4 * d * t3 + 6 * d * d * t2 - 3 * d * d * d * d;
+    out->W2 = double(m2);
+    if (!flat && m2 > 0) {
+        out->skew = double(m3 / powl(m2, 1.5L));
+        out->kurt = double(m4 / (m2 * m2) - 3.0L);
+    } else {
+        out->skew = NAN;
+        out->kurt = NAN;
+    }
+    return OCTGPU_OK;
+}
+
+int octgpu_heights(octgpu_engine* e, int32_t* out) {
+    if (!e || !out) return fail(OCTGPU_ERR_CONFIG, "null argument");
+    int rc = run_measure(e);
+    if (rc) return rc;
+    const size_t bytes = size_t(e->X) * e->Y * sizeof(int32_t);
+    int32_t* d = nullptr;
+    CK(cudaMalloc(&d, bytes));
+    cudaError_t le = launch_heights(e->w, e->planes[e->pcur], e->geom(), e->X, e->scratch, d, e->stream);
+    ++e->launches;
+    if (le == cudaSuccess) le = cudaMemcpyAsync(out, d, bytes, cudaMemcpyDeviceToHost, e->stream);
+    if (le == cudaSuccess) le = cudaStreamSynchronize(e->stream);
+    cudaFree(d);
+    if (le != cudaSuccess) return cuda_fail(le, "heights");
+    return OCTGPU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,776 @@
+// sm_100a device code for the bit-vectorized octahedron SCA.
+//
+// Hot path: the reference's
+//   VecEngine::step -> mcs_step -> sublattice_sweep -> detail::sweep_rows
+// (engine_vec.hpp:98-177) with per-row xoshiro256++ xi words
+// (rng.hpp:17-179, params.hpp:84-92), and the measurement
+//   reconstruct_heights -> height_moments (slope_field.hpp:206-229, measure.cpp:24-56).
+//
+// Mapping (B200-first, not the paper's thread-per-word CTA-per-row kernel):
+//  * one LANE owns one lattice ROW and walks its words k = 0..n-1 in order,
+//    so each row's xoshiro stream is consumed exactly in the reference order
+//    (ξp then ξq per word, engine_vec.hpp:123-125) without any jump;
+//  * planes are stored word-major (see Geom), so the 32 lanes of a warp read
+//    and write one contiguous 256-B segment per plane per word (coalesced);
+//  * loads are software-pipelined PF words ahead in registers;
+//  * k_mcs fuses both sublattice sweeps of one MCS into one pass (0.5 B of
+//    HBM traffic per site update instead of the reference's 1 B), using
+//    warp shuffles for the y-neighbour exchange and a GF(2) jump table for
+//    the second sweep's stream position.
+#include <cstdint>
+
+#include "octgpu_internal.h"
+
+namespace octgpu {
+
+// -------------------------------------------------------------------------
+// xoshiro256++ (rng.hpp:34-44) on the device
+
+struct Xo {
+    uint64_t a, b, c, d;
+};
+
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+
+__device__ __forceinline__ void xo_step(Xo& s) {
+    const uint64_t t = s.b << 17;
+    s.c ^= s.a;
+    s.d ^= s.b;
+    s.b ^= s.c;
+    s.a ^= s.d;
+    s.c ^= t;
+    s.d = rotl64(s.d, 45);
+}
+
+__device__ __forceinline__ uint64_t xo_next(Xo& s) {
+    const uint64_t r = rotl64(s.a + s.d, 23) + s.a;
+    xo_step(s);
+    return r;
+}
+
+__device__ __forceinline__ Xo load_state(const uint64_t* __restrict__ r, uint32_t Y, uint32_t y) {
+    return Xo{r[y], r[size_t(Y) + y], r[2 * size_t(Y) + y], r[3 * size_t(Y) + y]};
+}
+
+__device__ __forceinline__ void store_state(uint64_t* __restrict__ r, uint32_t Y, uint32_t y, const Xo& s) {
+    r[y] = s.a;
+    r[size_t(Y) + y] = s.b;
+    r[2 * size_t(Y) + y] = s.c;
+    r[3 * size_t(Y) + y] = s.d;
+}
+
+// s <- M s with M given as a 4-bit ("four Russians") table: 64 nibble
+// positions x 16 values x 4 u64 (32 KB, L1-resident after first touch).
+__device__ __forceinline__ Xo apply_table(const uint64_t* __restrict__ tab, const Xo& s) {
+    const uint64_t v[4] = {s.a, s.b, s.c, s.d};
+    Xo r{0, 0, 0, 0};
+#pragma unroll 16
+    for (int i = 0; i < 64; ++i) {
+        const uint32_t nib = uint32_t(v[i >> 4] >> (4 * (i & 15))) & 15u;
+        const ulonglong2* e = reinterpret_cast<const ulonglong2*>(tab + (size_t(i) * 16 + nib) * 4);
+        const ulonglong2 lo = __ldg(e), hi = __ldg(e + 1);
+        r.a ^= lo.x;
+        r.b ^= lo.y;
+        r.c ^= hi.x;
+        r.d ^= hi.y;
+    }
+    return r;
+}
+
+// -------------------------------------------------------------------------
+// xi words (rng.hpp:129-179, params.hpp:84-92)
+
+template <int MODE, typename Word>
+__device__ __forceinline__ Word xi_word(Xo& s, const ProbDev& pd) {
+    constexpr int W = int(sizeof(Word) * 8);
+    if constexpr (MODE == M_ZERO) {
+        return Word(0);
+    } else if constexpr (MODE == M_HALF) {
+        return Word(xo_next(s));  // xi_half: low w bits of one draw
+    } else if constexpr (MODE == M_DYADIC) {
+        Word acc = Word(xo_next(s));  // Horner over the digits of m, LSB first
+        for (uint32_t i = 1; i < pd.k; ++i) {
+            const Word x = Word(xo_next(s));
+            acc = ((pd.m >> i) & 1) ? Word(acc | x) : Word(acc & x);
+        }
+        return acc;
+    } else if constexpr (MODE == M_ARB) {
+        // xi_arbitrary: bit i = to_unit(draw_i) < r  <=>  draw_i < T (integer threshold)
+        Word word = 0;
+#pragma unroll
+        for (int i = 0; i < W; ++i) word |= Word(xo_next(s) < pd.T) << i;
+        return word;
+    } else {  // M_ONE: every bit accepted, stream still advances w draws
+#pragma unroll 8
+        for (int i = 0; i < W; ++i) xo_step(s);
+        return Word(~Word(0));
+    }
+}
+
+template <int PM, int QM>
+struct Plan {
+    static constexpr bool p_const = (PM == M_ZERO || PM == M_ONE);
+    static constexpr bool q_const = (QM == M_ZERO || QM == M_ONE);
+    static constexpr bool live = !(p_const && q_const);  // any draw needs a live stream
+};
+
+template <int PM, int QM, typename Word>
+__device__ __forceinline__ void gen_xi(Xo& s, const ProbDev& p, const ProbDev& q, Word& xp, Word& xq) {
+    if constexpr (Plan<PM, QM>::live) {
+        xp = xi_word<PM, Word>(s, p);
+        xq = (QM == M_ZERO) ? Word(0) : xi_word<QM, Word>(s, q);  // engine_vec.hpp:105,125
+    } else {
+        xp = (PM == M_ONE) ? Word(~Word(0)) : Word(0);
+        xq = (QM == M_ONE) ? Word(~Word(0)) : Word(0);
+    }
+}
+
+// engine_vec.hpp:25-30
+template <typename Word>
+__device__ __forceinline__ Word update_mask(Word sxm, Word sym, Word sxp, Word syp, Word xp, Word xq) {
+    const Word mp = xp & ~(sxm | sym) & sxp & syp;
+    const Word mq = xq & ~(sxp | syp) & sxm & sym;
+    return Word(mp ^ mq);
+}
+
+// -------------------------------------------------------------------------
+// Single sublattice sweep, in place (sublattice_sweep, engine_vec.hpp:145-168)
+
+template <typename Word, int PM, int QM, int PF>
+__global__ void __launch_bounds__(128) k_sweep(Word* __restrict__ planes, uint64_t* __restrict__ rng, int parity,
+                                               Geom g, ProbDev p, ProbDev q, Word* __restrict__ mask_log) {
+    constexpr int W = int(sizeof(Word) * 8);
+    const uint32_t Y = g.Y, n = g.n;
+    const uint32_t y = blockIdx.x * blockDim.x + threadIdx.x;
+    if (y >= Y) return;
+    const size_t PS = g.plane_stride;
+    Word* px = planes + size_t(0 + parity) * PS + y;                         // X(pi)[y]
+    Word* py = planes + size_t(2 + parity) * PS + y;                         // Y(pi)[y]
+    Word* qy = planes + size_t(2 + (parity ^ 1)) * PS + (y + 1 == Y ? 0 : y + 1);  // Y(!pi)[y+1]
+    Word* xr = planes + size_t(0 + (parity ^ 1)) * PS + y;                   // X(!pi)[y]
+    const bool shifted = ((uint32_t(parity) ^ y) & 1u) != 0;                  // engine_vec.hpp:59-61
+
+    Xo s{0, 0, 0, 0};
+    if constexpr (Plan<PM, QM>::live) s = load_state(rng, Y, y);
+
+    const Word raw0 = xr[0];
+    Word bA[PF], bB[PF], bC[PF], bR[PF];
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+        if (uint32_t(j) < n) {
+            const size_t o = size_t(j) * Y;
+            bA[j] = px[o];
+            bB[j] = py[o];
+            bC[j] = qy[o];
+            bR[j] = (uint32_t(j) + 1 < n) ? xr[o + Y] : raw0;
+        }
+    }
+    Word cur = raw0, carry = 0, new0 = 0;
+    for (uint32_t kb = 0; kb < n; kb += PF) {
+#pragma unroll
+        for (int j = 0; j < PF; ++j) {
+            const uint32_t k = kb + j;
+            if (k < n) {
+                const size_t o = size_t(k) * Y;
+                const Word A = bA[j], B = bB[j], Cn = bC[j], nxt = bR[j];
+                const uint32_t kk = k + PF;
+                if (kk < n) {  // refill this slot PF words ahead
+                    const size_t oo = size_t(kk) * Y;
+                    bA[j] = px[oo];
+                    bB[j] = py[oo];
+                    bC[j] = qy[oo];
+                    bR[j] = (kk + 1 < n) ? xr[oo + Y] : raw0;
+                }
+                const Word sxp = shifted ? Word((cur >> 1) | (nxt << (W - 1))) : cur;  // rotate_row_down
+                Word xp, xq;
+                gen_xi<PM, QM, Word>(s, p, q, xp, xq);
+                const Word m = update_mask<Word>(A, B, sxp, Cn, xp, xq);
+                px[o] = A ^ m;
+                py[o] = B ^ m;
+                qy[o] = Cn ^ m;
+                const Word sc = shifted ? Word((m << 1) | carry) : m;  // scatter_rotated_xor
+                carry = Word(m >> (W - 1));
+                if (k == 0)
+                    new0 = cur ^ sc;  // word 0 waits for the PBC carry of word n-1
+                else
+                    xr[o] = cur ^ sc;
+                if (mask_log) mask_log[size_t(y) * n + k] = m;
+                cur = nxt;
+            }
+        }
+    }
+    if (shifted) new0 ^= carry;
+    xr[0] = new0;
+    if constexpr (Plan<PM, QM>::live) store_state(rng, Y, y, s);
+}
+
+// -------------------------------------------------------------------------
+// Fused MCS: sweep f then sweep s = f^1 in one pass, src -> dst.
+//
+// Warp w owns "core" rows [30w, 30w+30) ∩ [0, Y). Lane L holds row
+// y_L = (30w - 1 + L) mod Y; lanes 0 and 31 are halo rows whose FIRST sweep
+// is recomputed redundantly (from src, so duplicates are bit-identical).
+// Per word k every lane loads X(f)[y], Y(f)[y], X(s)[y] and Y(s)[y+1] - four
+// contiguous windows. The second sweep of row y needs only first-sweep
+// results of rows y-1, y, y+1 (same word and its right neighbour), obtained
+// through shuffles, so the second sweep trails the first by one word.
+// The periodic x seam (word n-1 -> word 0) is handled by drawing the second
+// sweep's word-0 xi first (stream order) but applying it last.
+
+template <typename Word>
+struct Second {
+    Word m;      // applied mask
+    Word xf;     // X(f)[y][j] with own mask, before the carry from word j-1
+};
+
+template <typename Word, int PM, int QM, int PF>
+__global__ void __launch_bounds__(128) k_mcs(const Word* __restrict__ src, Word* __restrict__ dst,
+                                             const uint64_t* __restrict__ rs, uint64_t* __restrict__ rd, int f,
+                                             Geom g, ProbDev p, ProbDev q, const uint64_t* __restrict__ jtab) {
+    constexpr int W = int(sizeof(Word) * 8);
+    constexpr bool LIVE = Plan<PM, QM>::live;
+    const uint32_t Y = g.Y, n = g.n;
+    const int lane = threadIdx.x & 31;
+    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t base = wid * 30u;
+    if (base >= Y) return;  // warp-uniform
+    const int64_t v = int64_t(base) - 1 + lane;
+    const uint32_t y = v < 0 ? Y - 1 : uint32_t(v % Y);
+    const uint32_t y1 = (y + 1 == Y) ? 0 : y + 1;
+    const bool core = lane >= 1 && lane <= 30 && (base + uint32_t(lane) - 1) < Y;
+    const bool wyf = lane >= 2 && (base + uint32_t(lane) - 2) < Y;  // lane-1 is core
+    const int s = f ^ 1;
+    const size_t PS = g.plane_stride;
+    const Word* sXf = src + size_t(0 + f) * PS + y;
+    const Word* sYf = src + size_t(2 + f) * PS + y;
+    const Word* sXs = src + size_t(0 + s) * PS + y;
+    const Word* sYs1 = src + size_t(2 + s) * PS + y1;
+    Word* dXf = dst + size_t(0 + f) * PS + y;
+    Word* dYf = dst + size_t(2 + f) * PS + y;
+    Word* dXs = dst + size_t(0 + s) * PS + y;
+    Word* dYs = dst + size_t(2 + s) * PS + y;
+    const bool sh1 = ((uint32_t(f) ^ y) & 1u) != 0;  // first sweep shifts x+ of this row
+    const bool sh2 = !sh1;                           // second sweep does
+
+    Xo s1{0, 0, 0, 0}, s2{0, 0, 0, 0};
+    if constexpr (LIVE) {
+        s1 = load_state(rs, Y, y);
+        s2 = apply_table(jtab, s1);  // stream position n*D draws ahead
+    }
+    Word xi2p0, xi2q0;  // second sweep, word 0: drawn first, applied last
+    gen_xi<PM, QM, Word>(s2, p, q, xi2p0, xi2q0);
+
+    const Word raw0 = sXs[0];
+    Word bA[PF], bB[PF], bC[PF], bR[PF];
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+        if (uint32_t(j) < n) {
+            const size_t o = size_t(j) * Y;
+            bA[j] = sXf[o];
+            bB[j] = sYf[o];
+            bC[j] = sYs1[o];
+            bR[j] = (uint32_t(j) + 1 < n) ? sXs[o + Y] : raw0;
+        }
+    }
+
+    // post-first-sweep values of word 0 and 1 kept for the seam
+    Word A0 = 0, B0 = 0, C0 = 0, R0 = 0, A1 = 0;
+    // previous word (k-1), post-first
+    Word pA = 0, pB = 0, pC = 0, pR = 0;
+    Word cur = raw0, carry1 = 0;
+    Word m2last = 0;     // m2 of the most recent second-sweep word (j-1)
+    Word xf1 = 0;        // X(f)[y][1] pending the carry of m2[0]
+
+    // second sweep of word j >= 1 (needs post-first words j and j+1)
+    auto second = [&](uint32_t j, Word Aj, Word Ajn, Word Bj, Word Cj, Word Rj, Word x2p, Word x2q) {
+        const Word Cup = __shfl_up_sync(0xffffffffu, Cj, 1);    // Y(s)[y] post-first (row y-1 wrote it)
+        const Word Bdn = __shfl_down_sync(0xffffffffu, Bj, 1);  // Y(f)[y+1] post-first
+        const Word sxp2 = sh2 ? Word((Aj >> 1) | (Ajn << (W - 1))) : Aj;
+        const Word m2 = update_mask<Word>(Rj, Cup, sxp2, Bdn, x2p, x2q);
+        const Word mup = __shfl_up_sync(0xffffffffu, m2, 1);
+        const size_t o = size_t(j) * Y;
+        if (core) {
+            dXs[o] = Rj ^ m2;
+            dYs[o] = Cup ^ m2;
+        }
+        if (wyf) dYf[o] = Bj ^ mup;
+        return m2;
+    };
+
+    for (uint32_t kb = 0; kb < n; kb += PF) {
+#pragma unroll
+        for (int jj = 0; jj < PF; ++jj) {
+            const uint32_t k = kb + jj;
+            if (k < n) {
+                const Word A = bA[jj], B = bB[jj], Cn = bC[jj], nxt = bR[jj];
+                const uint32_t kk = k + PF;
+                if (kk < n) {
+                    const size_t oo = size_t(kk) * Y;
+                    bA[jj] = sXf[oo];
+                    bB[jj] = sYf[oo];
+                    bC[jj] = sYs1[oo];
+                    bR[jj] = (kk + 1 < n) ? sXs[oo + Y] : raw0;
+                }
+                // ---- first sweep, word k ----
+                const Word sxp = sh1 ? Word((cur >> 1) | (nxt << (W - 1))) : cur;
+                Word x1p, x1q;
+                gen_xi<PM, QM, Word>(s1, p, q, x1p, x1q);
+                const Word m1 = update_mask<Word>(A, B, sxp, Cn, x1p, x1q);
+                const Word Ap = A ^ m1, Bp = B ^ m1, Cp = Cn ^ m1;
+                const Word sc1 = sh1 ? Word((m1 << 1) | carry1) : m1;
+                carry1 = Word(m1 >> (W - 1));
+                const Word Rp = cur ^ sc1;  // word 0 still lacks the seam carry
+                cur = nxt;
+                if (k == 0) {
+                    A0 = Ap; B0 = Bp; C0 = Cp; R0 = Rp;
+                } else {
+                    if (k == 1) A1 = Ap;
+                    // ---- second sweep, word j = k-1 (j >= 1) ----
+                    if (k >= 2) {
+                        const uint32_t j = k - 1;
+                        Word x2p, x2q;
+                        gen_xi<PM, QM, Word>(s2, p, q, x2p, x2q);
+                        const Word m2 = second(j, pA, Ap, pB, pC, pR, x2p, x2q);
+                        const Word xfj = pA ^ (sh2 ? Word(m2 << 1) : m2);
+                        if (j == 1) {
+                            xf1 = xfj;  // needs m2[0] >> (W-1)
+                        } else {
+                            if (core) dXf[size_t(j) * Y] = xfj ^ (sh2 ? Word(m2last >> (W - 1)) : Word(0));
+                        }
+                        m2last = m2;
+                    }
+                }
+                pA = Ap; pB = Bp; pC = Cp; pR = Rp;
+            }
+        }
+    }
+    // seam of the first sweep: carry of m1[n-1] into word 0
+    if (sh1) R0 ^= carry1;
+    if (n >= 2) {
+        // second sweep, word n-1 (right neighbour wraps to word 0)
+        const uint32_t j = n - 1;
+        Word x2p, x2q;
+        gen_xi<PM, QM, Word>(s2, p, q, x2p, x2q);
+        const Word Rj = (j == 0) ? R0 : pR;
+        const Word m2 = second(j, pA, A0, pB, pC, Rj, x2p, x2q);
+        const Word xfj = pA ^ (sh2 ? Word(m2 << 1) : m2);
+        if (j == 1) {
+            xf1 = xfj;
+        } else {
+            if (core) dXf[size_t(j) * Y] = xfj ^ (sh2 ? Word(m2last >> (W - 1)) : Word(0));
+        }
+        m2last = m2;
+    }
+    {
+        // second sweep, word 0 (xi drawn first, applied last)
+        const Word Anext = (n >= 2) ? A1 : A0;
+        const Word m2 = second(0, A0, Anext, B0, C0, R0, xi2p0, xi2q0);
+        const Word top_prev = (n >= 2) ? Word(m2last >> (W - 1)) : Word(m2 >> (W - 1));
+        const Word xf0 = A0 ^ (sh2 ? Word((m2 << 1) | top_prev) : m2);
+        if (core) {
+            dXf[0] = xf0;
+            if (n >= 2) dXf[Y] = xf1 ^ (sh2 ? Word(m2 >> (W - 1)) : Word(0));
+        }
+    }
+    if constexpr (LIVE) {
+        if (core) store_state(rd, Y, y, s2);
+    }
+}
+
+// -------------------------------------------------------------------------
+// Jump application (GF(2) matrix on every row state)
+
+__global__ void k_apply_jump(uint64_t* __restrict__ rng, uint32_t Y, const uint64_t* __restrict__ tab) {
+    const uint32_t y = blockIdx.x * blockDim.x + threadIdx.x;
+    if (y >= Y) return;
+    Xo s = load_state(rng, Y, y);
+    s = apply_table(tab, s);
+    store_state(rng, Y, y, s);
+}
+
+// -------------------------------------------------------------------------
+// Layout transposes: reference SlopeField rows (row-major [Y][n] per plane)
+// <-> device word-major ([n][Y] per plane).
+
+template <typename Word, bool TO_DEVICE>
+__global__ void k_transpose(const Word* __restrict__ in, Word* __restrict__ out, Geom g) {
+    __shared__ Word tile[32][33];
+    const uint32_t Y = g.Y, n = g.n;
+    const size_t poff = size_t(blockIdx.z) * g.plane_stride;
+    // TO_DEVICE: in is [Y][n], out is [n][Y]; else the reverse.
+    const uint32_t R = TO_DEVICE ? Y : n, Cc = TO_DEVICE ? n : Y;  // in dims
+    const uint32_t c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const uint32_t r = r0 + i, c = c0 + threadIdx.x;
+        if (r < R && c < Cc) tile[i][threadIdx.x] = in[poff + size_t(r) * Cc + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const uint32_t c = c0 + i, r = r0 + threadIdx.x;
+        if (r < R && c < Cc) out[poff + size_t(c) * R + r] = tile[threadIdx.x][i];
+    }
+}
+
+// -------------------------------------------------------------------------
+// Measurement (reconstruct_heights + height_moments, exact integers)
+//
+// Heights: h(x,y) = H_y + r(x,y) with H_y the column-0 prefix of sigma_y-
+// and r the row prefix of sigma_x- (equal to the reference's row-0-then-
+// columns integration whenever curl_check passes, which is checked here).
+// With u(x) = sum_{x'<=x} sigma_x-(x',y) (inclusive from x = 0),
+// r(x) = u(x) - sigma_x-(0,y). Per row the kernel accumulates U_k = sum_x u^k;
+// the reduction shifts by G_y = H_y - sigma_x-(0,y) binomially.
+
+struct RowStats {
+    long long U1, U2;
+    __int128 U3, U4;
+    int s0;          // sigma_x-(0, y) in {-1, +1}
+    int sy0;         // sigma_y-(0, y)
+    long long rowsum;
+    unsigned int curl_count;
+    unsigned int curl_first_x;  // 0xffffffff if none
+};
+
+size_t measure_scratch_bytes(uint32_t Y) { return size_t(Y) * sizeof(RowStats) + sizeof(long long) * Y; }
+
+template <typename Word>
+__global__ void __launch_bounds__(128) k_measure_rows(const Word* __restrict__ planes, Geom g, uint32_t X,
+                                                      RowStats* __restrict__ out) {
+    constexpr int W = int(sizeof(Word) * 8);
+    const uint32_t Y = g.Y, n = g.n;
+    const int lane = threadIdx.x & 31;
+    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t base = wid * 31u;
+    if (base >= Y) return;
+    const int64_t v = int64_t(base) - 1 + lane;
+    const uint32_t y = v < 0 ? Y - 1 : uint32_t(v % Y);
+    const bool core = lane >= 1 && (base + uint32_t(lane) - 1) < Y;
+    const size_t PS = g.plane_stride;
+    const Word* X0 = planes + y;
+    const Word* X1 = planes + PS + y;
+    const Word* Y0 = planes + 2 * PS + y;
+    const Word* Y1 = planes + 3 * PS + y;
+    const int ya = int(y & 1u);
+    const size_t last = size_t(n - 1) * Y;
+    Word pD0 = Y0[last], pD1 = Y1[last];  // word k-1 of the y planes (wraps to n-1)
+
+    long long U1 = 0, U2 = 0;
+    __int128 U3 = 0, U4 = 0;
+    int u0 = 0;
+    long long rowsum = 0;
+    unsigned int ccount = 0, cfirst = 0xffffffffu;
+    int s0 = 0, sy0 = 0;
+    for (uint32_t k = 0; k < n; ++k) {
+        const size_t o = size_t(k) * Y;
+        const Word x0 = X0[o], x1 = X1[o], yy0 = Y0[o], yy1 = Y1[o];
+        const Word bx0 = __shfl_up_sync(0xffffffffu, x0, 1);  // X(0)[y-1]
+        const Word bx1 = __shfl_up_sync(0xffffffffu, x1, 1);  // X(1)[y-1]
+        // ---- curl check (slope_field.hpp:159-174), word-parallel ----
+#pragma unroll
+        for (int pi = 0; pi < 2; ++pi) {
+            const Word A = pi ? x1 : x0;
+            const Word B = pi ? bx0 : bx1;
+            const Word C = pi ? yy1 : yy0;
+            const Word Dr = pi ? yy0 : yy1;
+            const Word Dp = pi ? pD0 : pD1;
+            const bool even_x = ((uint32_t(pi) ^ y) & 1u) == 0;
+            const Word D = even_x ? Word((Dr << 1) | (Dp >> (W - 1))) : Dr;
+            const Word V = (A ^ B ^ C ^ D) | ((A ^ B) & (A ^ C));
+            if (V) {
+                ccount += __popcll((unsigned long long)V);
+                const uint32_t b = __ffsll((long long)(unsigned long long)V) - 1;
+                const uint32_t x = 2u * (k * W + b) + (even_x ? 0u : 1u);
+                cfirst = min(cfirst, x);
+            }
+        }
+        pD0 = yy0;
+        pD1 = yy1;
+        // ---- heights along the row ----
+        const Word xa = ya ? x1 : x0;  // even x sites
+        const Word xb = ya ? x0 : x1;  // odd x sites
+        rowsum += 2 * (__popcll((unsigned long long)xa) + __popcll((unsigned long long)xb)) - 2 * W;
+        if (k == 0) {
+            s0 = (xa & 1) ? 1 : -1;
+            const Word ysite = ya ? yy1 : yy0;
+            sy0 = (ysite & 1) ? 1 : -1;
+        }
+        int c = 0, c1 = 0, c2 = 0, c3 = 0;
+        long long c4 = 0;
+#pragma unroll
+        for (int b = 0; b < W; ++b) {
+            c += int((xa >> b) & 1) * 2 - 1;
+            {
+                const int t = c * c;
+                c1 += c; c2 += t; c3 += t * c; c4 += (long long)t * t;
+            }
+            c += int((xb >> b) & 1) * 2 - 1;
+            {
+                const int t = c * c;
+                c1 += c; c2 += t; c3 += t * c; c4 += (long long)t * t;
+            }
+        }
+        const long long u = u0, uu = u * u;
+        const __int128 uuu = (__int128)uu * u;
+        constexpr long long NS = 2 * W;
+        U1 += NS * u + c1;
+        U2 += NS * uu + 2 * u * c1 + c2;
+        U3 += (__int128)NS * uuu + (__int128)(3 * uu) * c1 + (__int128)(3 * u) * c2 + c3;
+        U4 += (__int128)NS * uuu * u + (__int128)4 * uuu * c1 + (__int128)(6 * uu) * c2 +
+              (__int128)(4 * u) * c3 + c4;
+        u0 += c;
+    }
+    if (core) {
+        RowStats r;
+        r.U1 = U1; r.U2 = U2; r.U3 = U3; r.U4 = U4;
+        r.s0 = s0; r.sy0 = sy0; r.rowsum = rowsum;
+        r.curl_count = ccount; r.curl_first_x = cfirst;
+        out[y] = r;
+    }
+}
+
+// Single block: column-0 scan, binomial shift, int128 reduction.
+__global__ void __launch_bounds__(1024) k_measure_reduce(const RowStats* __restrict__ rows, uint32_t Y, uint32_t X,
+                                                         long long* __restrict__ G_out, MeasureResult* res) {
+    __shared__ long long sh_scan[1024];
+    __shared__ __int128 sh_s[4][32];
+    __shared__ unsigned long long sh_cc[32], sh_cf[32];
+    __shared__ long long sh_col[32];
+    const int t = threadIdx.x, nt = blockDim.x;
+    const uint32_t chunk = (Y + nt - 1) / nt;
+    const uint32_t y0 = min(Y, t * chunk), y1 = min(Y, y0 + chunk);
+    // H_y = sum_{y'=1..y} sigma_y-(0,y'); local sum of sy0 over (y0, y1] handled as exclusive prefix
+    long long loc = 0;
+    for (uint32_t y = y0; y < y1; ++y) loc += rows[y].sy0;
+    sh_scan[t] = loc;
+    __syncthreads();
+    for (int off = 1; off < nt; off <<= 1) {  // inclusive Hillis-Steele scan
+        long long vv = (t >= off) ? sh_scan[t - off] : 0;
+        __syncthreads();
+        sh_scan[t] += vv;
+        __syncthreads();
+    }
+    long long run = (t > 0) ? sh_scan[t - 1] : 0;  // sum of sy0 over rows < y0
+    const long long col0 = sh_scan[nt - 1];
+    __int128 S[4] = {0, 0, 0, 0};
+    unsigned long long cc = 0, cf = ~0ull;
+    for (uint32_t y = y0; y < y1; ++y) {
+        const RowStats r = rows[y];
+        run += r.sy0;                                   // inclusive sum to y
+        const long long H = run - rows[0].sy0;          // h(0,y): excludes sigma_y-(0,0)
+        const long long G = H - r.s0;
+        G_out[y] = G;
+        const __int128 g1 = G, g2 = g1 * G, g3 = g2 * G, g4 = g3 * G;
+        const __int128 U0 = X, U1 = r.U1, U2 = r.U2;
+        S[0] += g1 * U0 + U1;
+        S[1] += g2 * U0 + 2 * g1 * U1 + U2;
+        S[2] += g3 * U0 + 3 * g2 * U1 + 3 * g1 * U2 + r.U3;
+        S[3] += g4 * U0 + 4 * g3 * U1 + 6 * g2 * U2 + 4 * g1 * r.U3 + r.U4;
+        cc += r.curl_count;
+        if (r.curl_first_x != 0xffffffffu) {
+            const unsigned long long pos = (unsigned long long)y * X + r.curl_first_x;
+            cf = pos < cf ? pos : cf;
+        }
+    }
+    // block reduce (warp shuffles on 64-bit halves would need carries; go through smem)
+    const int lane = t & 31, wp = t >> 5;
+    for (int k = 0; k < 4; ++k) {
+        __int128 vsum = S[k];
+        for (int off = 16; off > 0; off >>= 1) {
+            unsigned long long lo = (unsigned long long)vsum, hi = (unsigned long long)(vsum >> 64);
+            lo = __shfl_down_sync(0xffffffffu, lo, off);
+            hi = __shfl_down_sync(0xffffffffu, hi, off);
+            vsum += (__int128)(((unsigned __int128)hi << 64) | lo);
+        }
+        if (lane == 0) sh_s[k][wp] = vsum;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        cc += __shfl_down_sync(0xffffffffu, cc, off);
+        const unsigned long long o = __shfl_down_sync(0xffffffffu, cf, off);
+        cf = o < cf ? o : cf;
+    }
+    if (lane == 0) { sh_cc[wp] = cc; sh_cf[wp] = cf; sh_col[wp] = 0; }
+    __syncthreads();
+    if (t == 0) {
+        __int128 tot[4] = {0, 0, 0, 0};
+        unsigned long long tc = 0, tf = ~0ull;
+        for (int i = 0; i < nt / 32; ++i) {
+            for (int k = 0; k < 4; ++k) tot[k] += sh_s[k][i];
+            tc += sh_cc[i];
+            tf = sh_cf[i] < tf ? sh_cf[i] : tf;
+        }
+        for (int k = 0; k < 4; ++k) {
+            res->s_lo[k] = (uint64_t)tot[k];
+            res->s_hi[k] = (int64_t)(tot[k] >> 64);
+        }
+        res->curl_count = tc;
+        res->curl_first = tf;
+        res->row0_sum = rows[0].rowsum;
+        res->col0_sum = col0;
+    }
+}
+
+// Heights: one warp per row; lane l owns words l, l+32, ... Writes the
+// reference HeightMap layout h[y*X + x].
+template <typename Word>
+__global__ void k_heights(const Word* __restrict__ planes, Geom g, uint32_t X, const long long* __restrict__ G,
+                          int32_t* __restrict__ out) {
+    constexpr int W = int(sizeof(Word) * 8);
+    const uint32_t Y = g.Y, n = g.n;
+    const uint32_t y = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (y >= Y) return;
+    const size_t PS = g.plane_stride;
+    const int ya = int(y & 1u);
+    const Word* Xa = planes + size_t(ya) * PS + y;
+    const Word* Xb = planes + size_t(ya ^ 1) * PS + y;
+    long long carry = G[y];  // h(x,y) = G_y + u(x)
+    int32_t* row = out + size_t(y) * X;
+    for (uint32_t kb = 0; kb < n; kb += 32) {
+        const uint32_t k = kb + lane;
+        Word a = 0, b = 0;
+        int delta = 0;
+        if (k < n) {
+            a = Xa[size_t(k) * Y];
+            b = Xb[size_t(k) * Y];
+            delta = 2 * (__popcll((unsigned long long)a) + __popcll((unsigned long long)b)) - 2 * W;
+        }
+        int incl = delta;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += o;
+        }
+        long long h = carry + (incl - delta);
+        if (k < n) {
+            int32_t* dst = row + size_t(k) * 2 * W;
+            for (int bb = 0; bb < W; ++bb) {
+                h += ((a >> bb) & 1) ? 1 : -1;
+                dst[2 * bb] = int32_t(h);
+                h += ((b >> bb) & 1) ? 1 : -1;
+                dst[2 * bb + 1] = int32_t(h);
+            }
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
+// -------------------------------------------------------------------------
+// Launchers
+
+namespace {
+
+constexpr int kPF = 4;
+
+template <template <typename, int, int, int> class K, typename Word>
+struct Dispatch;
+
+template <typename Word, int PM, int QM>
+cudaError_t sweep_pq(void* planes, uint64_t* rng, int parity, Geom g, const ProbDev& p, const ProbDev& q,
+                     void* mask_log, cudaStream_t st) {
+    const uint32_t threads = 128, blocks = (g.Y + threads - 1) / threads;
+    k_sweep<Word, PM, QM, kPF><<<blocks, threads, 0, st>>>(static_cast<Word*>(planes), rng, parity, g, p, q,
+                                                          static_cast<Word*>(mask_log));
+    return cudaGetLastError();
+}
+
+template <typename Word, int PM, int QM>
+cudaError_t mcs_pq(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
+                   const ProbDev& q, const uint64_t* jtab, cudaStream_t st) {
+    const uint32_t warps = (g.Y + 29) / 30;
+    const uint32_t threads = 128, blocks = (warps * 32 + threads - 1) / threads;
+    k_mcs<Word, PM, QM, kPF><<<blocks, threads, 0, st>>>(static_cast<const Word*>(src), static_cast<Word*>(dst),
+                                                        rs, rd, f, g, p, q, jtab);
+    return cudaGetLastError();
+}
+
+#define OCT_Q_CASES(FN, WORD, PM, ...)                        \
+    switch (q.mode) {                                         \
+    case M_ZERO: return FN<WORD, PM, M_ZERO>(__VA_ARGS__);     \
+    case M_HALF: return FN<WORD, PM, M_HALF>(__VA_ARGS__);     \
+    case M_DYADIC: return FN<WORD, PM, M_DYADIC>(__VA_ARGS__); \
+    case M_ARB: return FN<WORD, PM, M_ARB>(__VA_ARGS__);       \
+    case M_ONE: return FN<WORD, PM, M_ONE>(__VA_ARGS__);       \
+    default: return cudaErrorInvalidValue;                    \
+    }
+
+#define OCT_PQ_CASES(FN, WORD, ...)                                      \
+    switch (p.mode) {                                                    \
+    case M_ZERO: OCT_Q_CASES(FN, WORD, M_ZERO, __VA_ARGS__)               \
+    case M_HALF: OCT_Q_CASES(FN, WORD, M_HALF, __VA_ARGS__)               \
+    case M_DYADIC: OCT_Q_CASES(FN, WORD, M_DYADIC, __VA_ARGS__)           \
+    case M_ARB: OCT_Q_CASES(FN, WORD, M_ARB, __VA_ARGS__)                 \
+    case M_ONE: OCT_Q_CASES(FN, WORD, M_ONE, __VA_ARGS__)                 \
+    default: return cudaErrorInvalidValue;                               \
+    }
+
+}  // namespace
+
+cudaError_t launch_sweep(int w, void* planes, uint64_t* rng, int parity, Geom g, const ProbDev& p,
+                         const ProbDev& q, bool, void* mask_log, cudaStream_t st) {
+    if (w == 64) {
+        OCT_PQ_CASES(sweep_pq, uint64_t, planes, rng, parity, g, p, q, mask_log, st)
+    } else {
+        OCT_PQ_CASES(sweep_pq, uint32_t, planes, rng, parity, g, p, q, mask_log, st)
+    }
+}
+
+cudaError_t launch_mcs(int w, const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g,
+                       const ProbDev& p, const ProbDev& q, bool, const uint64_t* jtab, cudaStream_t st) {
+    if (w == 64) {
+        OCT_PQ_CASES(mcs_pq, uint64_t, src, dst, rs, rd, f, g, p, q, jtab, st)
+    } else {
+        OCT_PQ_CASES(mcs_pq, uint32_t, src, dst, rs, rd, f, g, p, q, jtab, st)
+    }
+}
+
+cudaError_t launch_apply_jump(uint64_t* rng, uint32_t Y, const uint64_t* tab, cudaStream_t st) {
+    const uint32_t threads = 128, blocks = (Y + threads - 1) / threads;
+    k_apply_jump<<<blocks, threads, 0, st>>>(rng, Y, tab);
+    return cudaGetLastError();
+}
+
+template <typename Word, bool TO>
+static cudaError_t transpose_w(const void* in, void* out, Geom g, cudaStream_t st) {
+    const uint32_t R = TO ? g.Y : g.n, Cc = TO ? g.n : g.Y;
+    dim3 grid((Cc + 31) / 32, (R + 31) / 32, 4), block(32, 8);
+    k_transpose<Word, TO><<<grid, block, 0, st>>>(static_cast<const Word*>(in), static_cast<Word*>(out), g);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_import(int w, const void* in, void* planes, Geom g, cudaStream_t st) {
+    return w == 64 ? transpose_w<uint64_t, true>(in, planes, g, st) : transpose_w<uint32_t, true>(in, planes, g, st);
+}
+
+cudaError_t launch_export(int w, const void* planes, void* out, Geom g, cudaStream_t st) {
+    return w == 64 ? transpose_w<uint64_t, false>(planes, out, g, st)
+                   : transpose_w<uint32_t, false>(planes, out, g, st);
+}
+
+cudaError_t launch_measure(int w, const void* planes, Geom g, uint32_t X, void* scratch, void* result_dev,
+                           cudaStream_t st) {
+    RowStats* rows = static_cast<RowStats*>(scratch);
+    long long* G = reinterpret_cast<long long*>(rows + g.Y);
+    const uint32_t warps = (g.Y + 30) / 31;
+    const uint32_t threads = 128, blocks = (warps * 32 + threads - 1) / threads;
+    if (w == 64)
+        k_measure_rows<uint64_t><<<blocks, threads, 0, st>>>(static_cast<const uint64_t*>(planes), g, X, rows);
+    else
+        k_measure_rows<uint32_t><<<blocks, threads, 0, st>>>(static_cast<const uint32_t*>(planes), g, X, rows);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_measure_reduce<<<1, 1024, 0, st>>>(rows, g.Y, X, G, static_cast<MeasureResult*>(result_dev));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_heights(int w, const void* planes, Geom g, uint32_t X, const void* scratch, int32_t* out,
+                           cudaStream_t st) {
+    const RowStats* rows = static_cast<const RowStats*>(scratch);
+    const long long* G = reinterpret_cast<const long long*>(rows + g.Y);
+    const uint32_t threads = 128, blocks = (g.Y * 32 + threads - 1) / threads;
+    if (w == 64)
+        k_heights<uint64_t><<<blocks, threads, 0, st>>>(static_cast<const uint64_t*>(planes), g, X, G, out);
+    else
+        k_heights<uint32_t><<<blocks, threads, 0, st>>>(static_cast<const uint32_t*>(planes), g, X, G, out);
+    return cudaGetLastError();
+}
+
+}  // namespace octgpu

@@ -1,0 +1,75 @@
+// Internal declarations shared by the host engine (engine.cu) and the device
+// kernels (kernels.cu). Not part of the C-ABI; see include/octgpu.h for that.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace octgpu {
+
+// Per-probability generation mode as the device sees it. ZERO/HALF/DYADIC/ARB
+// mirror octsca::ProbMode (params.hpp:13); ONE is ARB with r == 1, whose xi is
+// the all-ones word (to_unit(x) < 1.0 always holds, rng.hpp:167-177) while the
+// stream still advances w draws per word.
+enum Mode : int { M_ZERO = 0, M_HALF = 1, M_DYADIC = 2, M_ARB = 3, M_ONE = 4 };
+
+struct ProbDev {
+    int mode;
+    uint32_t k;   // dyadic: r = m / 2^k, ops from bit 1 of m upward (rng.cpp:24-28)
+    uint64_t m;
+    uint64_t T;   // ARB: xi bit = (draw < T), T = ceil(r * 2^53) << 11
+};
+
+// Device layout ("word-major"): plane p, row y, word k lives at
+//   base + p * plane_stride + k * Y + y
+// so a warp whose lanes own 32 consecutive rows touches one contiguous 256-B
+// (w=64) segment per plane per word: every access is coalesced and any
+// contiguous window of rows is contiguous in memory.
+struct Geom {
+    uint32_t Y;
+    uint32_t n;            // words per plane-row = X / (2w)
+    size_t plane_stride;   // n * Y words
+};
+
+struct RowStats;  // measurement scratch, defined in kernels.cu
+
+// Per-row RNG states are stored SoA: s[j * Y + y], j = 0..3.
+
+// ---- launchers (return the launch error, never synchronise) ----
+cudaError_t launch_import(int w, const void* host_layout_dev, void* planes, Geom g, cudaStream_t st);
+cudaError_t launch_export(int w, const void* planes, void* host_layout_dev, Geom g, cudaStream_t st);
+
+// One sublattice sweep in place (engine_vec.hpp:145-168), optional mask log in
+// reference row-major layout.
+cudaError_t launch_sweep(int w, void* planes, uint64_t* rng, int parity, Geom g, const ProbDev& p,
+                         const ProbDev& q, bool rng_live, void* mask_log, cudaStream_t st);
+
+// One full MCS (sweep f then sweep f^1, engine_vec.hpp:171-177) fused into a
+// single pass, src -> dst (ping-pong). jtab: 4-bit table of T^(n*D) (the
+// second sweep's stream offset); unused when !rng_live.
+cudaError_t launch_mcs(int w, const void* src, void* dst, const uint64_t* rng_src, uint64_t* rng_dst, int f,
+                       Geom g, const ProbDev& p, const ProbDev& q, bool rng_live, const uint64_t* jtab,
+                       cudaStream_t st);
+
+// s <- M s for every row state, M given as a 4-bit table (64 x 16 x 4 u64).
+cudaError_t launch_apply_jump(uint64_t* rng, uint32_t Y, const uint64_t* tab, cudaStream_t st);
+
+// Measurement: per-row pass + single-block scan/reduction.
+size_t measure_scratch_bytes(uint32_t Y);
+cudaError_t launch_measure(int w, const void* planes, Geom g, uint32_t X, void* scratch, void* result_dev,
+                           cudaStream_t st);
+// Heights (reference HeightMap layout, row-major int32), after launch_measure.
+cudaError_t launch_heights(int w, const void* planes, Geom g, uint32_t X, const void* scratch, int32_t* out,
+                           cudaStream_t st);
+
+// Result of launch_measure (device struct, copied back by the host).
+struct MeasureResult {
+    uint64_t s_lo[4];       // S_k = sum h^k, k=1..4, int128 as (lo, hi)
+    int64_t s_hi[4];
+    unsigned long long curl_count;
+    unsigned long long curl_first;  // y * X + x of the first violating plaquette, ~0 if none
+    long long row0_sum;             // sum_x sigma_x-(x, 0)
+    long long col0_sum;             // sum_y sigma_y-(0, y)
+};
+
+}  // namespace octgpu

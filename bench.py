@@ -171,7 +171,8 @@ def main():
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # a real (non-default) stream shared by the engine and the timing events
+    torch.cuda.set_stream(stream)
 
     X, Y = cfg["X"], cfg["Y"]
     lat = octgpu.LatticeConfig(X, Y, 64)

@@ -101,6 +101,10 @@ int octgpu_create_from(uint32_t X, uint32_t Y, uint32_t w, uint64_t t_mcs, int p
                        const uint64_t* states, uint32_t n_states, uint64_t master_seed, int device,
                        octgpu_engine** out);
 void octgpu_destroy(octgpu_engine* e);
+/* Replace the whole state of an existing engine (same geometry): the write-back
+ * half of VecEngine's mutable field()/streams() accessors (engine_vec.hpp:200-214). */
+int octgpu_set_state(octgpu_engine* e, uint64_t t_mcs, int phase, const void* planes, const uint64_t* states,
+                     uint32_t n_states);
 /* Use an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL restores the engine's own. */
 int octgpu_set_stream(octgpu_engine* e, void* cuda_stream);
 /* Block until all enqueued work finished; surfaces asynchronous CUDA errors. */

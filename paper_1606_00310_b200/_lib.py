@@ -62,7 +62,7 @@ class OctMoments(C.Structure):
 # Every symbol include/octgpu.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "octgpu_resolve", "octgpu_draws_per_word", "octgpu_validate_lattice", "octgpu_stream_states",
-    "octgpu_log_schedule", "octgpu_create", "octgpu_create_from", "octgpu_destroy", "octgpu_set_stream",
+    "octgpu_log_schedule", "octgpu_create", "octgpu_create_from", "octgpu_set_state", "octgpu_destroy", "octgpu_set_stream",
     "octgpu_sync", "octgpu_step", "octgpu_sweep", "octgpu_t", "octgpu_phase", "octgpu_master_seed",
     "octgpu_get_planes", "octgpu_get_states", "octgpu_field_checksum", "octgpu_measure", "octgpu_heights",
     "octgpu_last_error", "octgpu_version", "octgpu_launch_count",
@@ -89,6 +89,7 @@ def lib() -> C.CDLL:
         "octgpu_log_schedule": (u32, [u64, u32, vp, u32]),
         "octgpu_create": (i32, [u32, u32, u32, u64, i32, P(vp)]),
         "octgpu_create_from": (i32, [u32, u32, u32, u64, i32, vp, vp, u32, u64, i32, P(vp)]),
+        "octgpu_set_state": (i32, [vp, u64, i32, vp, vp, u32]),
         "octgpu_destroy": (None, [vp]),
         "octgpu_set_stream": (i32, [vp, vp]),
         "octgpu_sync": (i32, [vp]),

@@ -1,7 +1,9 @@
 // Host side of liboctgpu: the C-ABI (include/octgpu.h), engine state,
 // parameter resolution, stream seeding and GF(2) jump-ahead matrices.
 // Device work lives in kernels.cu.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -321,6 +323,9 @@ struct octgpu_engine {
     MeasureResult* res_host = nullptr;
     std::map<uint64_t, uint64_t*> jtabs;  // draws -> device 4-bit table of T^draws
     uint64_t launches = 0;
+    // fused-MCS implementation: 2 = bulk-copy staged (k_mcs_bulk), 1 = register-prefetch (k_mcs)
+    int mcs_impl = 2;
+    int bulk_ks = 4, bulk_S = 3;
 
     Geom geom() const { return Geom{Y, n, size_t(n) * Y}; }
     size_t word_bytes() const { return w / 8; }
@@ -376,6 +381,36 @@ int upload_states(octgpu_engine* e, const uint64_t* aos) {
     return OCTGPU_OK;
 }
 
+// Pick the fused-MCS variant and its pipeline depth so that all warps fit
+// in one wave (shared memory per SM is the limiting resource for k_mcs_bulk).
+int plan_mcs(octgpu_engine* e) {
+    e->mcs_impl = (e->w == 64 && e->n >= 8 && e->Y >= 64) ? 2 : 1;
+    if (const char* v = getenv("OCTGPU_MCS_IMPL")) e->mcs_impl = (atoi(v) == 1) ? 1 : e->mcs_impl;
+    if (e->mcs_impl != 2) return OCTGPU_OK;
+    int sms = 0, smem_sm = 0, smem_blk = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
+    CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, e->device));
+    CK(cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+    const uint64_t warps = (e->Y + 29) / 30, blocks = (warps + 3) / 4;
+    const uint64_t bps = (blocks + sms - 1) / sms;  // blocks per SM for a single wave
+    const int64_t budget = std::min<int64_t>(smem_blk, int64_t(smem_sm) / int64_t(bps) - 1024);
+    e->bulk_ks = 2;
+    e->bulk_S = 2;
+    bool found = false;
+    for (int ks : {4, 2}) {
+        for (int S = 6; S >= 2 && !found; --S)
+            if (int64_t(8 * 8 * 4 + 4 * S * mcs_bulk_stage_bytes(ks)) <= budget) {
+                e->bulk_ks = ks;
+                e->bulk_S = S;
+                found = true;
+            }
+        if (found) break;
+    }
+    if (const char* v = getenv("OCTGPU_MCS_KS")) e->bulk_ks = atoi(v) == 2 ? 2 : 4;
+    if (const char* v = getenv("OCTGPU_MCS_S")) e->bulk_S = std::max(2, std::min(8, atoi(v)));
+    return OCTGPU_OK;
+}
+
 int alloc_engine(octgpu_engine* e) {
     CK(cudaSetDevice(e->device));
     CK(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
@@ -387,7 +422,7 @@ int alloc_engine(octgpu_engine* e) {
     CK(cudaMalloc(&e->scratch, measure_scratch_bytes(e->Y)));
     CK(cudaMalloc(reinterpret_cast<void**>(&e->res_dev), sizeof(MeasureResult)));
     CK(cudaMallocHost(reinterpret_cast<void**>(&e->res_host), sizeof(MeasureResult)));
-    return OCTGPU_OK;
+    return plan_mcs(e);
 }
 
 int lower_params(const octgpu_params* prm, ProbDev& p, ProbDev& q) {
@@ -508,6 +543,25 @@ int octgpu_create_from(uint32_t X, uint32_t Y, uint32_t w, uint64_t t_mcs, int p
     return OCTGPU_OK;
 }
 
+int octgpu_set_state(octgpu_engine* e, uint64_t t_mcs, int phase, const void* planes, const uint64_t* states,
+                     uint32_t n_states) {
+    if (!e || !planes || !states) return fail(OCTGPU_ERR_CONFIG, "null argument");
+    if (phase != 0 && phase != 1) return fail(OCTGPU_ERR_CONFIG, "phase must be 0 or 1");
+    if (n_states < e->Y) return fail(OCTGPU_ERR_INVARIANT, "stream set smaller than row count");
+    int rc = use_device(e);
+    if (!rc) rc = ensure_stage(e);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(e->stage, planes, e->set_bytes(), cudaMemcpyHostToDevice, e->stream));
+    CK(launch_import(e->w, e->stage, e->planes[e->pcur], e->geom(), e->stream));
+    ++e->launches;
+    e->pending = 0;
+    rc = upload_states(e, states);
+    if (rc) return rc;
+    e->t = t_mcs;
+    e->phase = phase;
+    return OCTGPU_OK;
+}
+
 void octgpu_destroy(octgpu_engine* e) {
     if (!e) return;
     cudaSetDevice(e->device);
@@ -564,8 +618,12 @@ int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
     const Geom g = e->geom();
     for (uint64_t i = 0; i < n_mcs; ++i) {
         const int ps = e->pcur, rs = e->rcur;
-        CK(launch_mcs(e->w, e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, live,
-                      jtab, e->stream));
+        if (e->mcs_impl == 2)
+            CK(launch_mcs_bulk(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
+                               e->bulk_ks, e->bulk_S, e->stream));
+        else
+            CK(launch_mcs(e->w, e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q,
+                          live, jtab, e->stream));
         ++e->launches;
         e->pcur ^= 1;
         if (live)
@@ -674,7 +732,7 @@ int run_measure(octgpu_engine* e) {
     int rc = use_device(e);
     if (rc) return rc;
     CK(launch_measure(e->w, e->planes[e->pcur], e->geom(), e->X, e->scratch, e->res_dev, e->stream));
-    e->launches += 2;
+    e->launches += 3;
     CK(cudaMemcpyAsync(e->res_host, e->res_dev, sizeof(MeasureResult), cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
     const MeasureResult& r = *e->res_host;

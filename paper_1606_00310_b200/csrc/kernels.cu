@@ -19,119 +19,10 @@
 //    the second sweep's stream position.
 #include <cstdint>
 
+#include "device_common.cuh"
 #include "octgpu_internal.h"
 
 namespace octgpu {
-
-// -------------------------------------------------------------------------
-// xoshiro256++ (rng.hpp:34-44) on the device
-
-struct Xo {
-    uint64_t a, b, c, d;
-};
-
-__device__ __forceinline__ uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
-
-__device__ __forceinline__ void xo_step(Xo& s) {
-    const uint64_t t = s.b << 17;
-    s.c ^= s.a;
-    s.d ^= s.b;
-    s.b ^= s.c;
-    s.a ^= s.d;
-    s.c ^= t;
-    s.d = rotl64(s.d, 45);
-}
-
-__device__ __forceinline__ uint64_t xo_next(Xo& s) {
-    const uint64_t r = rotl64(s.a + s.d, 23) + s.a;
-    xo_step(s);
-    return r;
-}
-
-__device__ __forceinline__ Xo load_state(const uint64_t* __restrict__ r, uint32_t Y, uint32_t y) {
-    return Xo{r[y], r[size_t(Y) + y], r[2 * size_t(Y) + y], r[3 * size_t(Y) + y]};
-}
-
-__device__ __forceinline__ void store_state(uint64_t* __restrict__ r, uint32_t Y, uint32_t y, const Xo& s) {
-    r[y] = s.a;
-    r[size_t(Y) + y] = s.b;
-    r[2 * size_t(Y) + y] = s.c;
-    r[3 * size_t(Y) + y] = s.d;
-}
-
-// s <- M s with M given as a 4-bit ("four Russians") table: 64 nibble
-// positions x 16 values x 4 u64 (32 KB, L1-resident after first touch).
-__device__ __forceinline__ Xo apply_table(const uint64_t* __restrict__ tab, const Xo& s) {
-    const uint64_t v[4] = {s.a, s.b, s.c, s.d};
-    Xo r{0, 0, 0, 0};
-#pragma unroll 16
-    for (int i = 0; i < 64; ++i) {
-        const uint32_t nib = uint32_t(v[i >> 4] >> (4 * (i & 15))) & 15u;
-        const ulonglong2* e = reinterpret_cast<const ulonglong2*>(tab + (size_t(i) * 16 + nib) * 4);
-        const ulonglong2 lo = __ldg(e), hi = __ldg(e + 1);
-        r.a ^= lo.x;
-        r.b ^= lo.y;
-        r.c ^= hi.x;
-        r.d ^= hi.y;
-    }
-    return r;
-}
-
-// -------------------------------------------------------------------------
-// xi words (rng.hpp:129-179, params.hpp:84-92)
-
-template <int MODE, typename Word>
-__device__ __forceinline__ Word xi_word(Xo& s, const ProbDev& pd) {
-    constexpr int W = int(sizeof(Word) * 8);
-    if constexpr (MODE == M_ZERO) {
-        return Word(0);
-    } else if constexpr (MODE == M_HALF) {
-        return Word(xo_next(s));  // xi_half: low w bits of one draw
-    } else if constexpr (MODE == M_DYADIC) {
-        Word acc = Word(xo_next(s));  // Horner over the digits of m, LSB first
-        for (uint32_t i = 1; i < pd.k; ++i) {
-            const Word x = Word(xo_next(s));
-            acc = ((pd.m >> i) & 1) ? Word(acc | x) : Word(acc & x);
-        }
-        return acc;
-    } else if constexpr (MODE == M_ARB) {
-        // xi_arbitrary: bit i = to_unit(draw_i) < r  <=>  draw_i < T (integer threshold)
-        Word word = 0;
-#pragma unroll
-        for (int i = 0; i < W; ++i) word |= Word(xo_next(s) < pd.T) << i;
-        return word;
-    } else {  // M_ONE: every bit accepted, stream still advances w draws
-#pragma unroll 8
-        for (int i = 0; i < W; ++i) xo_step(s);
-        return Word(~Word(0));
-    }
-}
-
-template <int PM, int QM>
-struct Plan {
-    static constexpr bool p_const = (PM == M_ZERO || PM == M_ONE);
-    static constexpr bool q_const = (QM == M_ZERO || QM == M_ONE);
-    static constexpr bool live = !(p_const && q_const);  // any draw needs a live stream
-};
-
-template <int PM, int QM, typename Word>
-__device__ __forceinline__ void gen_xi(Xo& s, const ProbDev& p, const ProbDev& q, Word& xp, Word& xq) {
-    if constexpr (Plan<PM, QM>::live) {
-        xp = xi_word<PM, Word>(s, p);
-        xq = (QM == M_ZERO) ? Word(0) : xi_word<QM, Word>(s, q);  // engine_vec.hpp:105,125
-    } else {
-        xp = (PM == M_ONE) ? Word(~Word(0)) : Word(0);
-        xq = (QM == M_ONE) ? Word(~Word(0)) : Word(0);
-    }
-}
-
-// engine_vec.hpp:25-30
-template <typename Word>
-__device__ __forceinline__ Word update_mask(Word sxm, Word sym, Word sxp, Word syp, Word xp, Word xq) {
-    const Word mp = xp & ~(sxm | sym) & sxp & syp;
-    const Word mq = xq & ~(sxp | syp) & sxm & sym;
-    return Word(mp ^ mq);
-}
 
 // -------------------------------------------------------------------------
 // Single sublattice sweep, in place (sublattice_sweep, engine_vec.hpp:145-168)
@@ -412,248 +303,6 @@ __global__ void k_transpose(const Word* __restrict__ in, Word* __restrict__ out,
 }
 
 // -------------------------------------------------------------------------
-// Measurement (reconstruct_heights + height_moments, exact integers)
-//
-// Heights: h(x,y) = H_y + r(x,y) with H_y the column-0 prefix of sigma_y-
-// and r the row prefix of sigma_x- (equal to the reference's row-0-then-
-// columns integration whenever curl_check passes, which is checked here).
-// With u(x) = sum_{x'<=x} sigma_x-(x',y) (inclusive from x = 0),
-// r(x) = u(x) - sigma_x-(0,y). Per row the kernel accumulates U_k = sum_x u^k;
-// the reduction shifts by G_y = H_y - sigma_x-(0,y) binomially.
-
-struct RowStats {
-    long long U1, U2;
-    __int128 U3, U4;
-    int s0;          // sigma_x-(0, y) in {-1, +1}
-    int sy0;         // sigma_y-(0, y)
-    long long rowsum;
-    unsigned int curl_count;
-    unsigned int curl_first_x;  // 0xffffffff if none
-};
-
-size_t measure_scratch_bytes(uint32_t Y) { return size_t(Y) * sizeof(RowStats) + sizeof(long long) * Y; }
-
-template <typename Word>
-__global__ void __launch_bounds__(128) k_measure_rows(const Word* __restrict__ planes, Geom g, uint32_t X,
-                                                      RowStats* __restrict__ out) {
-    constexpr int W = int(sizeof(Word) * 8);
-    const uint32_t Y = g.Y, n = g.n;
-    const int lane = threadIdx.x & 31;
-    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t base = wid * 31u;
-    if (base >= Y) return;
-    const int64_t v = int64_t(base) - 1 + lane;
-    const uint32_t y = v < 0 ? Y - 1 : uint32_t(v % Y);
-    const bool core = lane >= 1 && (base + uint32_t(lane) - 1) < Y;
-    const size_t PS = g.plane_stride;
-    const Word* X0 = planes + y;
-    const Word* X1 = planes + PS + y;
-    const Word* Y0 = planes + 2 * PS + y;
-    const Word* Y1 = planes + 3 * PS + y;
-    const int ya = int(y & 1u);
-    const size_t last = size_t(n - 1) * Y;
-    Word pD0 = Y0[last], pD1 = Y1[last];  // word k-1 of the y planes (wraps to n-1)
-
-    long long U1 = 0, U2 = 0;
-    __int128 U3 = 0, U4 = 0;
-    int u0 = 0;
-    long long rowsum = 0;
-    unsigned int ccount = 0, cfirst = 0xffffffffu;
-    int s0 = 0, sy0 = 0;
-    for (uint32_t k = 0; k < n; ++k) {
-        const size_t o = size_t(k) * Y;
-        const Word x0 = X0[o], x1 = X1[o], yy0 = Y0[o], yy1 = Y1[o];
-        const Word bx0 = __shfl_up_sync(0xffffffffu, x0, 1);  // X(0)[y-1]
-        const Word bx1 = __shfl_up_sync(0xffffffffu, x1, 1);  // X(1)[y-1]
-        // ---- curl check (slope_field.hpp:159-174), word-parallel ----
-#pragma unroll
-        for (int pi = 0; pi < 2; ++pi) {
-            const Word A = pi ? x1 : x0;
-            const Word B = pi ? bx0 : bx1;
-            const Word C = pi ? yy1 : yy0;
-            const Word Dr = pi ? yy0 : yy1;
-            const Word Dp = pi ? pD0 : pD1;
-            const bool even_x = ((uint32_t(pi) ^ y) & 1u) == 0;
-            const Word D = even_x ? Word((Dr << 1) | (Dp >> (W - 1))) : Dr;
-            const Word V = (A ^ B ^ C ^ D) | ((A ^ B) & (A ^ C));
-            if (V) {
-                ccount += __popcll((unsigned long long)V);
-                const uint32_t b = __ffsll((long long)(unsigned long long)V) - 1;
-                const uint32_t x = 2u * (k * W + b) + (even_x ? 0u : 1u);
-                cfirst = min(cfirst, x);
-            }
-        }
-        pD0 = yy0;
-        pD1 = yy1;
-        // ---- heights along the row ----
-        const Word xa = ya ? x1 : x0;  // even x sites
-        const Word xb = ya ? x0 : x1;  // odd x sites
-        rowsum += 2 * (__popcll((unsigned long long)xa) + __popcll((unsigned long long)xb)) - 2 * W;
-        if (k == 0) {
-            s0 = (xa & 1) ? 1 : -1;
-            const Word ysite = ya ? yy1 : yy0;
-            sy0 = (ysite & 1) ? 1 : -1;
-        }
-        int c = 0, c1 = 0, c2 = 0, c3 = 0;
-        long long c4 = 0;
-#pragma unroll
-        for (int b = 0; b < W; ++b) {
-            c += int((xa >> b) & 1) * 2 - 1;
-            {
-                const int t = c * c;
-                c1 += c; c2 += t; c3 += t * c; c4 += (long long)t * t;
-            }
-            c += int((xb >> b) & 1) * 2 - 1;
-            {
-                const int t = c * c;
-                c1 += c; c2 += t; c3 += t * c; c4 += (long long)t * t;
-            }
-        }
-        const long long u = u0, uu = u * u;
-        const __int128 uuu = (__int128)uu * u;
-        constexpr long long NS = 2 * W;
-        U1 += NS * u + c1;
-        U2 += NS * uu + 2 * u * c1 + c2;
-        U3 += (__int128)NS * uuu + (__int128)(3 * uu) * c1 + (__int128)(3 * u) * c2 + c3;
-        U4 += (__int128)NS * uuu * u + (__int128)4 * uuu * c1 + (__int128)(6 * uu) * c2 +
-              (__int128)(4 * u) * c3 + c4;
-        u0 += c;
-    }
-    if (core) {
-        RowStats r;
-        r.U1 = U1; r.U2 = U2; r.U3 = U3; r.U4 = U4;
-        r.s0 = s0; r.sy0 = sy0; r.rowsum = rowsum;
-        r.curl_count = ccount; r.curl_first_x = cfirst;
-        out[y] = r;
-    }
-}
-
-// Single block: column-0 scan, binomial shift, int128 reduction.
-__global__ void __launch_bounds__(1024) k_measure_reduce(const RowStats* __restrict__ rows, uint32_t Y, uint32_t X,
-                                                         long long* __restrict__ G_out, MeasureResult* res) {
-    __shared__ long long sh_scan[1024];
-    __shared__ __int128 sh_s[4][32];
-    __shared__ unsigned long long sh_cc[32], sh_cf[32];
-    __shared__ long long sh_col[32];
-    const int t = threadIdx.x, nt = blockDim.x;
-    const uint32_t chunk = (Y + nt - 1) / nt;
-    const uint32_t y0 = min(Y, t * chunk), y1 = min(Y, y0 + chunk);
-    // H_y = sum_{y'=1..y} sigma_y-(0,y'); local sum of sy0 over (y0, y1] handled as exclusive prefix
-    long long loc = 0;
-    for (uint32_t y = y0; y < y1; ++y) loc += rows[y].sy0;
-    sh_scan[t] = loc;
-    __syncthreads();
-    for (int off = 1; off < nt; off <<= 1) {  // inclusive Hillis-Steele scan
-        long long vv = (t >= off) ? sh_scan[t - off] : 0;
-        __syncthreads();
-        sh_scan[t] += vv;
-        __syncthreads();
-    }
-    long long run = (t > 0) ? sh_scan[t - 1] : 0;  // sum of sy0 over rows < y0
-    const long long col0 = sh_scan[nt - 1];
-    __int128 S[4] = {0, 0, 0, 0};
-    unsigned long long cc = 0, cf = ~0ull;
-    for (uint32_t y = y0; y < y1; ++y) {
-        const RowStats r = rows[y];
-        run += r.sy0;                                   // inclusive sum to y
-        const long long H = run - rows[0].sy0;          // h(0,y): excludes sigma_y-(0,0)
-        const long long G = H - r.s0;
-        G_out[y] = G;
-        const __int128 g1 = G, g2 = g1 * G, g3 = g2 * G, g4 = g3 * G;
-        const __int128 U0 = X, U1 = r.U1, U2 = r.U2;
-        S[0] += g1 * U0 + U1;
-        S[1] += g2 * U0 + 2 * g1 * U1 + U2;
-        S[2] += g3 * U0 + 3 * g2 * U1 + 3 * g1 * U2 + r.U3;
-        S[3] += g4 * U0 + 4 * g3 * U1 + 6 * g2 * U2 + 4 * g1 * r.U3 + r.U4;
-        cc += r.curl_count;
-        if (r.curl_first_x != 0xffffffffu) {
-            const unsigned long long pos = (unsigned long long)y * X + r.curl_first_x;
-            cf = pos < cf ? pos : cf;
-        }
-    }
-    // block reduce (warp shuffles on 64-bit halves would need carries; go through smem)
-    const int lane = t & 31, wp = t >> 5;
-    for (int k = 0; k < 4; ++k) {
-        __int128 vsum = S[k];
-        for (int off = 16; off > 0; off >>= 1) {
-            unsigned long long lo = (unsigned long long)vsum, hi = (unsigned long long)(vsum >> 64);
-            lo = __shfl_down_sync(0xffffffffu, lo, off);
-            hi = __shfl_down_sync(0xffffffffu, hi, off);
-            vsum += (__int128)(((unsigned __int128)hi << 64) | lo);
-        }
-        if (lane == 0) sh_s[k][wp] = vsum;
-    }
-    for (int off = 16; off > 0; off >>= 1) {
-        cc += __shfl_down_sync(0xffffffffu, cc, off);
-        const unsigned long long o = __shfl_down_sync(0xffffffffu, cf, off);
-        cf = o < cf ? o : cf;
-    }
-    if (lane == 0) { sh_cc[wp] = cc; sh_cf[wp] = cf; sh_col[wp] = 0; }
-    __syncthreads();
-    if (t == 0) {
-        __int128 tot[4] = {0, 0, 0, 0};
-        unsigned long long tc = 0, tf = ~0ull;
-        for (int i = 0; i < nt / 32; ++i) {
-            for (int k = 0; k < 4; ++k) tot[k] += sh_s[k][i];
-            tc += sh_cc[i];
-            tf = sh_cf[i] < tf ? sh_cf[i] : tf;
-        }
-        for (int k = 0; k < 4; ++k) {
-            res->s_lo[k] = (uint64_t)tot[k];
-            res->s_hi[k] = (int64_t)(tot[k] >> 64);
-        }
-        res->curl_count = tc;
-        res->curl_first = tf;
-        res->row0_sum = rows[0].rowsum;
-        res->col0_sum = col0;
-    }
-}
-
-// Heights: one warp per row; lane l owns words l, l+32, ... Writes the
-// reference HeightMap layout h[y*X + x].
-template <typename Word>
-__global__ void k_heights(const Word* __restrict__ planes, Geom g, uint32_t X, const long long* __restrict__ G,
-                          int32_t* __restrict__ out) {
-    constexpr int W = int(sizeof(Word) * 8);
-    const uint32_t Y = g.Y, n = g.n;
-    const uint32_t y = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (y >= Y) return;
-    const size_t PS = g.plane_stride;
-    const int ya = int(y & 1u);
-    const Word* Xa = planes + size_t(ya) * PS + y;
-    const Word* Xb = planes + size_t(ya ^ 1) * PS + y;
-    long long carry = G[y];  // h(x,y) = G_y + u(x)
-    int32_t* row = out + size_t(y) * X;
-    for (uint32_t kb = 0; kb < n; kb += 32) {
-        const uint32_t k = kb + lane;
-        Word a = 0, b = 0;
-        int delta = 0;
-        if (k < n) {
-            a = Xa[size_t(k) * Y];
-            b = Xb[size_t(k) * Y];
-            delta = 2 * (__popcll((unsigned long long)a) + __popcll((unsigned long long)b)) - 2 * W;
-        }
-        int incl = delta;
-        for (int off = 1; off < 32; off <<= 1) {
-            const int o = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= off) incl += o;
-        }
-        long long h = carry + (incl - delta);
-        if (k < n) {
-            int32_t* dst = row + size_t(k) * 2 * W;
-            for (int bb = 0; bb < W; ++bb) {
-                h += ((a >> bb) & 1) ? 1 : -1;
-                dst[2 * bb] = int32_t(h);
-                h += ((b >> bb) & 1) ? 1 : -1;
-                dst[2 * bb + 1] = int32_t(h);
-            }
-        }
-        carry += __shfl_sync(0xffffffffu, incl, 31);
-    }
-}
-
-// -------------------------------------------------------------------------
 // Launchers
 
 namespace {
@@ -743,34 +392,6 @@ cudaError_t launch_import(int w, const void* in, void* planes, Geom g, cudaStrea
 cudaError_t launch_export(int w, const void* planes, void* out, Geom g, cudaStream_t st) {
     return w == 64 ? transpose_w<uint64_t, false>(planes, out, g, st)
                    : transpose_w<uint32_t, false>(planes, out, g, st);
-}
-
-cudaError_t launch_measure(int w, const void* planes, Geom g, uint32_t X, void* scratch, void* result_dev,
-                           cudaStream_t st) {
-    RowStats* rows = static_cast<RowStats*>(scratch);
-    long long* G = reinterpret_cast<long long*>(rows + g.Y);
-    const uint32_t warps = (g.Y + 30) / 31;
-    const uint32_t threads = 128, blocks = (warps * 32 + threads - 1) / threads;
-    if (w == 64)
-        k_measure_rows<uint64_t><<<blocks, threads, 0, st>>>(static_cast<const uint64_t*>(planes), g, X, rows);
-    else
-        k_measure_rows<uint32_t><<<blocks, threads, 0, st>>>(static_cast<const uint32_t*>(planes), g, X, rows);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    k_measure_reduce<<<1, 1024, 0, st>>>(rows, g.Y, X, G, static_cast<MeasureResult*>(result_dev));
-    return cudaGetLastError();
-}
-
-cudaError_t launch_heights(int w, const void* planes, Geom g, uint32_t X, const void* scratch, int32_t* out,
-                           cudaStream_t st) {
-    const RowStats* rows = static_cast<const RowStats*>(scratch);
-    const long long* G = reinterpret_cast<const long long*>(rows + g.Y);
-    const uint32_t threads = 128, blocks = (g.Y * 32 + threads - 1) / threads;
-    if (w == 64)
-        k_heights<uint64_t><<<blocks, threads, 0, st>>>(static_cast<const uint64_t*>(planes), g, X, G, out);
-    else
-        k_heights<uint32_t><<<blocks, threads, 0, st>>>(static_cast<const uint32_t*>(planes), g, X, G, out);
-    return cudaGetLastError();
 }
 
 }  // namespace octgpu

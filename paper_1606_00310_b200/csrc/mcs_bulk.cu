@@ -1,0 +1,315 @@
+// Fused MCS kernel, v2: row windows staged in shared memory by the Tensor
+// Memory Accelerator's bulk-copy engine (cp.async.bulk, SASS UBLKCP) behind
+// per-warp mbarrier rings.
+//
+// Same algorithm and bit-exact results as k_mcs in kernels.cu (sweep f, then
+// sweep f^1, src -> dst), but
+//  * no prefetch registers: each warp keeps S stages x KS words of its four
+//    34-row plane windows in flight in shared memory, so the memory-level
+//    parallelism no longer competes with the single-wave register budget;
+//  * lane -> row mapping r0 = 30*warp, lane L = row r0 + L (core lanes 1..30),
+//    so every window starts at an even row: 16-byte aligned for the copies;
+//  * stores are predicated in PTX (no divergent branches).
+// Used for w = 64, n >= 8, Y >= 64; smaller lattices take k_mcs.
+#include <cstdint>
+
+#include "device_common.cuh"
+#include "octgpu_internal.h"
+
+namespace octgpu {
+
+namespace {
+
+constexpr int kWin = 34;  // rows per window: lanes 0..31 plus Y(s)[y+1] of lane 31, rounded to 16 B
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra LAB_WAIT;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void st_pred(uint64_t* p, uint64_t v, bool pred) {
+    asm volatile(
+        "{\n"
+        ".reg .pred q;\n"
+        "setp.ne.b32 q, %2, 0;\n"
+        "@q st.global.b64 [%0], %1;\n"
+        "}\n" ::"l"(p),
+        "l"(v), "r"(int(pred)));
+}
+
+// Stage layout (uint64 words): Xf[KS][kWin] | Yf[KS][kWin] | Ys[KS][kWin] | Xs[KS+1][kWin]
+template <int KS>
+struct StageLayout {
+    static constexpr int kXf = 0;
+    static constexpr int kYf = KS * kWin;
+    static constexpr int kYs = 2 * KS * kWin;
+    static constexpr int kXs = 3 * KS * kWin;
+    static constexpr int kWords = (4 * KS + 1) * kWin;
+    static constexpr int kBytes = kWords * 8;
+};
+
+}  // namespace
+
+size_t mcs_bulk_stage_bytes(int ks) { return size_t(4 * ks + 1) * kWin * 8; }
+
+template <int PM, int QM, int KS>
+__global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
+                                                  const uint64_t* __restrict__ rs, uint64_t* __restrict__ rd,
+                                                  int f, Geom g, ProbDev p, ProbDev q,
+                                                  const uint64_t* __restrict__ jtab, int S) {
+    using Word = uint64_t;
+    using LY = StageLayout<KS>;
+    constexpr int W = 64;
+    constexpr bool LIVE = Plan<PM, QM>::live;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const uint32_t Y = g.Y, n = g.n;
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;  // warp in block
+    const int wpb = blockDim.x >> 5;
+    const uint32_t wid = blockIdx.x * wpb + wib;
+    const uint32_t r0 = wid * 30u;
+    if (r0 >= Y) return;  // warp-uniform
+
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw) + wib * 8;  // 8 barrier slots per warp
+    Word* ring = reinterpret_cast<Word*>(smem_raw + 8 * 8 * wpb) + size_t(wib) * S * LY::kWords;
+
+    const uint32_t v = r0 + lane;  // virtual row; row Y is row 0
+    const uint32_t y = v % Y;
+    const uint32_t y1 = (y + 1 == Y) ? 0 : y + 1;
+    (void)y1;
+    const bool core = lane >= 1 && lane <= 30 && (r0 + lane) <= Y;
+    const bool wyf = lane >= 2 && (r0 + lane - 1) <= Y;
+    const int s = f ^ 1;
+    const size_t PS = g.plane_stride;
+    const Word* planeXf = src + size_t(0 + f) * PS;
+    const Word* planeYf = src + size_t(2 + f) * PS;
+    const Word* planeXs = src + size_t(0 + s) * PS;
+    const Word* planeYs = src + size_t(2 + s) * PS;
+    Word* dXf = dst + size_t(0 + f) * PS + y;
+    Word* dYf = dst + size_t(2 + f) * PS + y;
+    Word* dXs = dst + size_t(0 + s) * PS + y;
+    Word* dYs = dst + size_t(2 + s) * PS + y;
+    const bool sh1 = ((uint32_t(f) ^ y) & 1u) != 0;
+    const bool sh2 = !sh1;
+
+    // window split for the periodic wrap in y (last warp only)
+    const uint32_t rows1 = min(uint32_t(kWin), Y - r0);
+    const uint32_t rows2 = kWin - rows1;
+
+    if (lane == 0) {
+        for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+
+    // Issue the copies of word-block b into its stage (warp-collective).
+    auto fill = [&](uint32_t b) {
+        const int st = int(b % uint32_t(S));
+        Word* base = ring + size_t(st) * LY::kWords;
+        const uint32_t kb = b * KS;
+        const uint32_t nw = min(uint32_t(KS), n - kb);
+        const uint32_t ncopy = 4 * nw + 1;
+        __syncwarp();
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&bars[st], ncopy * kWin * 8);
+        }
+        __syncwarp();
+        const uint32_t jobs = ncopy * (rows2 ? 2u : 1u);
+        for (uint32_t c = lane; c < jobs; c += 32) {
+            const uint32_t cp = rows2 ? (c >> 1) : c;
+            const uint32_t part = rows2 ? (c & 1) : 0;
+            const Word* gplane;
+            uint32_t word, slot;
+            if (cp < 3 * nw) {
+                const uint32_t pl = cp / nw, j = cp % nw;
+                gplane = pl == 0 ? planeXf : (pl == 1 ? planeYf : planeYs);
+                word = kb + j;
+                slot = (pl == 0 ? LY::kXf : (pl == 1 ? LY::kYf : LY::kYs)) + j * kWin;
+            } else {
+                const uint32_t j = cp - 3 * nw;  // 0..nw (nw+1 words of X(s))
+                gplane = planeXs;
+                word = kb + j;
+                if (word >= n) word -= n;
+                slot = LY::kXs + j * kWin;
+            }
+            const Word* gsrc = gplane + size_t(word) * Y + (part ? 0 : r0);
+            Word* sdst = base + slot + (part ? rows1 : 0);
+            bulk_g2s(sdst, gsrc, (part ? rows2 : rows1) * 8, &bars[st]);
+        }
+    };
+
+    const uint32_t nblocks = (n + KS - 1) / KS;
+    for (uint32_t b = 0; b < uint32_t(S) && b < nblocks; ++b) fill(b);
+
+    Xo s1{0, 0, 0, 0}, s2{0, 0, 0, 0};
+    if constexpr (LIVE) {
+        s1 = load_state(rs, Y, y);
+        s2 = apply_table(jtab, s1);
+    }
+    Word xi2p0, xi2q0;
+    gen_xi<PM, QM, Word>(s2, p, q, xi2p0, xi2q0);
+
+    Word A0 = 0, B0 = 0, C0 = 0, R0 = 0, A1 = 0;
+    Word pA = 0, pB = 0, pC = 0, pR = 0;
+    Word carry1 = 0, m2last = 0, xf1 = 0;
+    Word cur = 0;
+
+    auto second = [&](uint32_t j, Word Aj, Word Ajn, Word Bj, Word Cj, Word Rj, Word x2p, Word x2q) {
+        const Word Cup = __shfl_up_sync(0xffffffffu, Cj, 1);
+        const Word Bdn = __shfl_down_sync(0xffffffffu, Bj, 1);
+        const Word sxp2 = sh2 ? Word((Aj >> 1) | (Ajn << (W - 1))) : Aj;
+        const Word m2 = update_mask<Word>(Rj, Cup, sxp2, Bdn, x2p, x2q);
+        const Word mup = __shfl_up_sync(0xffffffffu, m2, 1);
+        const size_t o = size_t(j) * Y;
+        st_pred(dXs + o, Rj ^ m2, core);
+        st_pred(dYs + o, Cup ^ m2, core);
+        st_pred(dYf + o, Bj ^ mup, wyf);
+        return m2;
+    };
+
+    for (uint32_t b = 0; b < nblocks; ++b) {
+        const int st = int(b % uint32_t(S));
+        mbar_wait(&bars[st], (b / uint32_t(S)) & 1u);
+        const Word* sb = ring + size_t(st) * LY::kWords;
+        const uint32_t kb = b * KS;
+        if (b == 0) cur = sb[LY::kXs + lane];  // X(s)[y][0], original
+#pragma unroll
+        for (int jj = 0; jj < KS; ++jj) {
+            const uint32_t k = kb + jj;
+            if (k >= n) break;
+            const Word A = sb[LY::kXf + jj * kWin + lane];
+            const Word B = sb[LY::kYf + jj * kWin + lane];
+            const Word Cn = sb[LY::kYs + jj * kWin + lane + 1];
+            const Word nxt = sb[LY::kXs + (jj + 1) * kWin + lane];
+            // ---- first sweep, word k ----
+            const Word sxp = sh1 ? Word((cur >> 1) | (nxt << (W - 1))) : cur;
+            Word x1p, x1q;
+            gen_xi<PM, QM, Word>(s1, p, q, x1p, x1q);
+            const Word m1 = update_mask<Word>(A, B, sxp, Cn, x1p, x1q);
+            const Word Ap = A ^ m1, Bp = B ^ m1, Cp = Cn ^ m1;
+            const Word sc1 = sh1 ? Word((m1 << 1) | carry1) : m1;
+            carry1 = Word(m1 >> (W - 1));
+            const Word Rp = cur ^ sc1;
+            cur = nxt;
+            if (k == 0) {
+                A0 = Ap; B0 = Bp; C0 = Cp; R0 = Rp;
+            } else {
+                if (k == 1) A1 = Ap;
+                if (k >= 2) {
+                    const uint32_t j = k - 1;
+                    Word x2p, x2q;
+                    gen_xi<PM, QM, Word>(s2, p, q, x2p, x2q);
+                    const Word m2 = second(j, pA, Ap, pB, pC, pR, x2p, x2q);
+                    const Word xfj = pA ^ (sh2 ? Word(m2 << 1) : m2);
+                    if (j == 1)
+                        xf1 = xfj;
+                    else
+                        st_pred(dXf + size_t(j) * Y, xfj ^ (sh2 ? Word(m2last >> (W - 1)) : Word(0)), core);
+                    m2last = m2;
+                }
+            }
+            pA = Ap; pB = Bp; pC = Cp; pR = Rp;
+        }
+        if (b + S < nblocks) fill(b + S);
+    }
+    if (sh1) R0 ^= carry1;
+    {
+        const uint32_t j = n - 1;  // n >= 8 here
+        Word x2p, x2q;
+        gen_xi<PM, QM, Word>(s2, p, q, x2p, x2q);
+        const Word m2 = second(j, pA, A0, pB, pC, pR, x2p, x2q);
+        const Word xfj = pA ^ (sh2 ? Word(m2 << 1) : m2);
+        st_pred(dXf + size_t(j) * Y, xfj ^ (sh2 ? Word(m2last >> (W - 1)) : Word(0)), core);
+        m2last = m2;
+    }
+    {
+        const Word m2 = second(0, A0, A1, B0, C0, R0, xi2p0, xi2q0);
+        const Word xf0 = A0 ^ (sh2 ? Word((m2 << 1) | (m2last >> (W - 1))) : m2);
+        st_pred(dXf, xf0, core);
+        st_pred(dXf + Y, xf1 ^ (sh2 ? Word(m2 >> (W - 1)) : Word(0)), core);
+    }
+    if constexpr (LIVE) {
+        if (core) store_state(rd, Y, y, s2);
+    }
+}
+
+namespace {
+
+template <int PM, int QM>
+cudaError_t bulk_pq(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
+                    const ProbDev& q, const uint64_t* jtab, int ks, int S, cudaStream_t st) {
+    const uint32_t warps = (g.Y + 29) / 30;
+    const uint32_t wpb = 4, threads = 32 * wpb, blocks = (warps + wpb - 1) / wpb;
+    const size_t smem = 8 * 8 * wpb + size_t(wpb) * S * mcs_bulk_stage_bytes(ks);
+    cudaError_t e;
+    if (ks == 4) {
+        auto kern = k_mcs_bulk<PM, QM, 4>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        kern<<<blocks, threads, smem, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), rs, rd,
+                                            f, g, p, q, jtab, S);
+    } else {
+        auto kern = k_mcs_bulk<PM, QM, 2>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        kern<<<blocks, threads, smem, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), rs, rd,
+                                            f, g, p, q, jtab, S);
+    }
+    return cudaGetLastError();
+}
+
+#define OCT_BQ(PM)                                                                              \
+    switch (q.mode) {                                                                           \
+    case M_ZERO: return bulk_pq<PM, M_ZERO>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, st);     \
+    case M_HALF: return bulk_pq<PM, M_HALF>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, st);     \
+    case M_DYADIC: return bulk_pq<PM, M_DYADIC>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, st); \
+    case M_ARB: return bulk_pq<PM, M_ARB>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, st);       \
+    case M_ONE: return bulk_pq<PM, M_ONE>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, st);       \
+    default: return cudaErrorInvalidValue;                                                      \
+    }
+
+}  // namespace
+
+cudaError_t launch_mcs_bulk(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g,
+                            const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int ks, int S,
+                            cudaStream_t st) {
+    switch (p.mode) {
+    case M_ZERO: OCT_BQ(M_ZERO)
+    case M_HALF: OCT_BQ(M_HALF)
+    case M_DYADIC: OCT_BQ(M_DYADIC)
+    case M_ARB: OCT_BQ(M_ARB)
+    case M_ONE: OCT_BQ(M_ONE)
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace octgpu

@@ -51,6 +51,13 @@ cudaError_t launch_mcs(int w, const void* src, void* dst, const uint64_t* rng_sr
                        Geom g, const ProbDev& p, const ProbDev& q, bool rng_live, const uint64_t* jtab,
                        cudaStream_t st);
 
+// Same as launch_mcs with shared-memory staging by cp.async.bulk (mcs_bulk.cu):
+// w = 64, n >= 8, Y >= 64 only. ks = words per stage (2 or 4), S = stages.
+cudaError_t launch_mcs_bulk(const void* src, void* dst, const uint64_t* rng_src, uint64_t* rng_dst, int f, Geom g,
+                            const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int ks, int S,
+                            cudaStream_t st);
+size_t mcs_bulk_stage_bytes(int ks);
+
 // s <- M s for every row state, M given as a 4-bit table (64 x 16 x 4 u64).
 cudaError_t launch_apply_jump(uint64_t* rng, uint32_t Y, const uint64_t* tab, cudaStream_t st);
 

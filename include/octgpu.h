@@ -142,6 +142,43 @@ int octgpu_measure(octgpu_engine* e, octgpu_moments* out);
  * out[y*X + x] int32, h(0,0) = 0. */
 int octgpu_heights(octgpu_engine* e, int32_t* out);
 
+/* ---- row stripes (multi-GPU) ----
+ * A stripe engine owns global rows [y0, y1) of an X x Y periodic lattice
+ * (sublattice partition as the reference's SweepPlan row blocks,
+ * params.hpp:107-127; results do not depend on the partition). One MCS:
+ *   octgpu_halo_pack -> exchange (to_prev -> rank-1, to_next -> rank+1) ->
+ *   octgpu_halo_unpack -> octgpu_stripe_mcs -> exchange boundary (-> rank+1) ->
+ *   octgpu_stripe_finish.
+ * All buffers are DEVICE memory (e.g. NCCL send/recv buffers); all work is on
+ * the engine's stream. octgpu_get_planes / octgpu_get_states return the
+ * stripe's own rows. planes/states NULL = flat start, RngStreamSet(seed, Y)
+ * rows y0..y1-1. */
+typedef struct {
+    uint64_t t;
+    uint64_t n_sites;
+    uint64_t s_lo[4]; /* power sums in the stripe-local gauge (h = 0 at column 0 above row y0) */
+    int64_t s_hi[4];
+    int64_t col_sum;       /* sum of sigma_y-(0, y) over the stripe's rows */
+    int64_t sy_first;      /* sigma_y-(0, y0) */
+    int64_t row_first_sum; /* sum_x sigma_x-(x, y0) */
+    uint64_t curl_count;
+    uint64_t curl_first;   /* global y * X + x of the first violation, ~0 if none */
+} octgpu_stripe_moments;
+
+int octgpu_create_stripe(uint32_t X, uint32_t Y, uint32_t w, uint32_t y0, uint32_t y1, uint64_t t_mcs, int phase,
+                         const void* planes, const uint64_t* states, uint64_t master_seed, int device,
+                         octgpu_engine** out);
+int octgpu_stripe_sizes(const octgpu_engine* e, uint64_t* to_prev_bytes, uint64_t* to_next_bytes,
+                        uint64_t* boundary_bytes);
+int octgpu_halo_pack(octgpu_engine* e, void* to_prev, void* to_next);
+int octgpu_halo_unpack(octgpu_engine* e, const void* from_prev, const void* from_next);
+int octgpu_stripe_mcs(octgpu_engine* e, const octgpu_params* prm, void* boundary_out);
+int octgpu_stripe_finish(octgpu_engine* e, const void* boundary_in);
+/* local moments; needs fresh halos (pack/exchange/unpack) for the curl check of row y0 */
+int octgpu_measure_stripe(octgpu_engine* e, octgpu_stripe_moments* out);
+uint32_t octgpu_stripe_y0(const octgpu_engine* e);
+uint32_t octgpu_stripe_rows(const octgpu_engine* e);
+
 /* ---- diagnostics ---- */
 const char* octgpu_last_error(void);
 const char* octgpu_version(void);

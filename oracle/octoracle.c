@@ -181,6 +181,7 @@ typedef struct {
     uint32_t X, Y, w, n, y0, y1;
     uint64_t* planes; /* 4 planes x (y1-y0) rows */
     uint64_t* ghost;  /* row y1 mod Y of the y-plane of the other parity, or NULL if full lattice */
+    uint32_t yoff;    /* global row of buffer row y is y + yoff (site parity uses the global row) */
 } lat_t;
 
 static uint64_t* row_of(const lat_t* L, int plane, uint32_t y) {
@@ -194,20 +195,20 @@ static uint64_t* row_of(const lat_t* L, int plane, uint32_t y) {
 }
 
 /* ---- engine_vec.hpp:98-137 (detail::sweep_rows) ---- */
-static void sweep_rows(const lat_t* L, int parity, const oo_prob* p, const oo_prob* q, uint64_t* states,
-                       uint64_t* mask_log) {
+static void sweep_range(const lat_t* L, int parity, const oo_prob* p, const oo_prob* q, uint64_t* states,
+                        uint32_t ya, uint32_t yb, uint64_t* mask_log) {
     const uint32_t n = L->n, w = L->w;
     const uint64_t M = wmask(w);
     const int with_q = q->mode != OO_ZERO;
     uint64_t* xbuf = malloc(n * sizeof(uint64_t));
     uint64_t* mbuf = malloc(n * sizeof(uint64_t));
-    for (uint32_t y = L->y0; y < L->y1; ++y) {
+    for (uint32_t y = ya; y < yb; ++y) {
         uint64_t* st = states + 4 * (size_t)(y - L->y0);
         uint64_t* px = row_of(L, 0 * 2 + parity, y);
         uint64_t* py = row_of(L, 1 * 2 + parity, y);
         uint64_t* qy1 = row_of(L, 1 * 2 + (parity ^ 1), y + 1);
         uint64_t* raw = row_of(L, 0 * 2 + (parity ^ 1), y);
-        const int shifted = ((uint32_t)parity ^ y) & 1u; /* engine_vec.hpp:59-61 */
+        const int shifted = ((uint32_t)parity ^ (y + L->yoff)) & 1u; /* engine_vec.hpp:59-61 */
         if (shifted) /* rotate_row_down, engine_vec.hpp:34-41 */
             for (uint32_t k = 0; k < n; ++k) {
                 uint64_t nx = raw[k + 1 == n ? 0 : k + 1];
@@ -240,11 +241,16 @@ static void sweep_rows(const lat_t* L, int parity, const oo_prob* p, const oo_pr
     free(mbuf);
 }
 
+static void sweep_rows(const lat_t* L, int parity, const oo_prob* p, const oo_prob* q, uint64_t* states,
+                       uint64_t* mask_log) {
+    sweep_range(L, parity, p, q, states, L->y0, L->y1, mask_log);
+}
+
 /* ---- engine_vec.hpp:145-168 (sublattice_sweep) ---- */
 int oo_sweep(uint32_t X, uint32_t Y, uint32_t w, uint64_t* planes, uint64_t* states, int* phase, int parity,
              const oo_prob* p, const oo_prob* q, uint64_t* mask_log) {
     if (*phase != parity) return 2;
-    lat_t L = {X, Y, w, X / (2 * w), 0, Y, planes, NULL};
+    lat_t L = {X, Y, w, X / (2 * w), 0, Y, planes, NULL, 0};
     sweep_rows(&L, parity, p, q, states, mask_log);
     *phase ^= 1;
     return 0;
@@ -263,7 +269,7 @@ int oo_step(uint32_t X, uint32_t Y, uint32_t w, uint64_t* planes, uint64_t* stat
 
 void oo_sweep_stripe(uint32_t X, uint32_t Y, uint32_t w, uint32_t y0, uint32_t y1, uint64_t* stripe_planes,
                      uint64_t* ghost, uint64_t* states, int parity, const oo_prob* p, const oo_prob* q) {
-    lat_t L = {X, Y, w, X / (2 * w), y0, y1, stripe_planes, (y1 - y0 == Y) ? NULL : ghost};
+    lat_t L = {X, Y, w, X / (2 * w), y0, y1, stripe_planes, (y1 - y0 == Y) ? NULL : ghost, 0};
     sweep_rows(&L, parity, p, q, states, NULL);
 }
 
@@ -415,4 +421,19 @@ uint32_t oo_log_schedule(uint64_t t_max, uint32_t ppd, uint64_t* out, uint32_t c
         ++cnt;
     }
     return cnt;
+}
+
+/* One MCS of a row stripe held with halos, as the GPU multi-stripe path
+ * organises it (not a reference function; built from sweep_rows, so it is
+ * exactly the reference's sweeps restricted to the rows the stripe can
+ * complete): rows 0 (halo above), 1..L (own), L+1, L+2 (halos below).
+ * Sweep f on rows 0..L+1, then sweep f^1 on rows 1..L, in place. Afterwards
+ * rows 1..L are final except y-plane f of row 1 (completed by the previous
+ * stripe's boundary row), and y-plane f of row L+1 is the boundary row for the
+ * next stripe. yoff = global row of buffer row 0 (= y0 - 1 mod Y). */
+void oo_mcs_stripe(uint32_t X, uint32_t w, uint32_t L, uint32_t yoff, uint64_t* planes, uint64_t* states, int f,
+                   const oo_prob* p, const oo_prob* q) {
+    lat_t Lt = {X, L + 3, w, X / (2 * w), 0, L + 3, planes, NULL, yoff};
+    sweep_range(&Lt, f, p, q, states, 0, L + 2, NULL);
+    sweep_range(&Lt, f ^ 1, p, q, states, 1, L + 1, NULL);
 }

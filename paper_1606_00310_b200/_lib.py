@@ -59,13 +59,29 @@ class OctMoments(C.Structure):
     ]
 
 
+class OctStripeMoments(C.Structure):
+    _fields_ = [
+        ("t", C.c_uint64),
+        ("n_sites", C.c_uint64),
+        ("s_lo", C.c_uint64 * 4),
+        ("s_hi", C.c_int64 * 4),
+        ("col_sum", C.c_int64),
+        ("sy_first", C.c_int64),
+        ("row_first_sum", C.c_int64),
+        ("curl_count", C.c_uint64),
+        ("curl_first", C.c_uint64),
+    ]
+
+
 # Every symbol include/octgpu.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "octgpu_resolve", "octgpu_draws_per_word", "octgpu_validate_lattice", "octgpu_stream_states",
     "octgpu_log_schedule", "octgpu_create", "octgpu_create_from", "octgpu_set_state", "octgpu_destroy", "octgpu_set_stream",
     "octgpu_sync", "octgpu_step", "octgpu_sweep", "octgpu_t", "octgpu_phase", "octgpu_master_seed",
     "octgpu_get_planes", "octgpu_get_states", "octgpu_field_checksum", "octgpu_measure", "octgpu_heights",
-    "octgpu_last_error", "octgpu_version", "octgpu_launch_count",
+    "octgpu_last_error", "octgpu_version", "octgpu_launch_count", "octgpu_create_stripe", "octgpu_stripe_sizes",
+    "octgpu_halo_pack", "octgpu_halo_unpack", "octgpu_stripe_mcs", "octgpu_stripe_finish", "octgpu_measure_stripe",
+    "octgpu_stripe_y0", "octgpu_stripe_rows",
 )
 
 _lib = None
@@ -106,6 +122,15 @@ def lib() -> C.CDLL:
         "octgpu_last_error": (C.c_char_p, []),
         "octgpu_version": (C.c_char_p, []),
         "octgpu_launch_count": (u64, [vp]),
+        "octgpu_create_stripe": (i32, [u32, u32, u32, u32, u32, u64, i32, vp, vp, u64, i32, P(vp)]),
+        "octgpu_stripe_sizes": (i32, [vp, P(u64), P(u64), P(u64)]),
+        "octgpu_halo_pack": (i32, [vp, vp, vp]),
+        "octgpu_halo_unpack": (i32, [vp, vp, vp]),
+        "octgpu_stripe_mcs": (i32, [vp, P(OctParams), vp]),
+        "octgpu_stripe_finish": (i32, [vp, vp]),
+        "octgpu_measure_stripe": (i32, [vp, P(OctStripeMoments)]),
+        "octgpu_stripe_y0": (u32, [vp]),
+        "octgpu_stripe_rows": (u32, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -326,8 +326,19 @@ struct octgpu_engine {
     // fused-MCS implementation: 2 = bulk-copy staged (k_mcs_bulk), 1 = register-prefetch (k_mcs)
     int mcs_impl = 2;
     int bulk_ks = 4, bulk_S = 3;
+    // Row-stripe mode (multi-GPU): this engine owns global rows [y0, y0 + L) of
+    // a Ytot-row periodic lattice, held at local rows 1..L with one halo row
+    // above (0), two below (L+1, L+2) and padding; Y is then the allocated row
+    // count. Periodic mode: Y = Ytot, y0 = 0, L = Ytot.
+    bool stripe = false;
+    uint32_t Ytot = 0, y0 = 0, L = 0;
 
-    Geom geom() const { return Geom{Y, n, size_t(n) * Y}; }
+    Geom geom() const {
+        return stripe ? Geom{Y, n, size_t(n) * Y, 1, L + 1, 0, (y0 + 1) & 1u}  // local row 0 = global y0 - 1
+                      : Geom{Y, n, size_t(n) * Y, 1, Y + 1, Y, 0};
+    }
+    uint32_t core_rows() const { return stripe ? L : Y; }
+    uint32_t first_row() const { return stripe ? 1 : 0; }  // local index of the first core row
     size_t word_bytes() const { return w / 8; }
     size_t set_bytes() const { return 4 * size_t(n) * Y * word_bytes(); }
     size_t rng_bytes() const { return 4 * size_t(Y) * sizeof(uint64_t); }
@@ -372,10 +383,12 @@ int materialize(octgpu_engine* e) {
     return OCTGPU_OK;
 }
 
+// AoS states of the core rows -> SoA at local rows first_row().. (stride Y)
 int upload_states(octgpu_engine* e, const uint64_t* aos) {
-    std::vector<uint64_t> soa(4 * size_t(e->Y));
-    for (uint32_t y = 0; y < e->Y; ++y)
-        for (int j = 0; j < 4; ++j) soa[size_t(j) * e->Y + y] = aos[4 * size_t(y) + j];
+    std::vector<uint64_t> soa(4 * size_t(e->Y), 0);
+    const uint32_t r0 = e->first_row();
+    for (uint32_t y = 0; y < e->core_rows(); ++y)
+        for (int j = 0; j < 4; ++j) soa[size_t(j) * e->Y + r0 + y] = aos[4 * size_t(y) + j];
     CK(cudaMemcpyAsync(e->rng[e->rcur], soa.data(), e->rng_bytes(), cudaMemcpyHostToDevice, e->stream));
     CK(cudaStreamSynchronize(e->stream));
     return OCTGPU_OK;
@@ -384,14 +397,14 @@ int upload_states(octgpu_engine* e, const uint64_t* aos) {
 // Pick the fused-MCS variant and its pipeline depth so that all warps fit
 // in one wave (shared memory per SM is the limiting resource for k_mcs_bulk).
 int plan_mcs(octgpu_engine* e) {
-    e->mcs_impl = (e->w == 64 && e->n >= 8 && e->Y >= 64) ? 2 : 1;
+    e->mcs_impl = (e->w == 64 && e->n >= 8 && (e->stripe || e->Y >= 64)) ? 2 : 1;
     if (const char* v = getenv("OCTGPU_MCS_IMPL")) e->mcs_impl = (atoi(v) == 1) ? 1 : e->mcs_impl;
     if (e->mcs_impl != 2) return OCTGPU_OK;
     int sms = 0, smem_sm = 0, smem_blk = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
     CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, e->device));
     CK(cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
-    const uint64_t warps = (e->Y + 29) / 30, blocks = (warps + 3) / 4;
+    const uint64_t warps = (e->core_rows() + 29) / 30, blocks = (warps + 3) / 4;
     const uint64_t bps = (blocks + sms - 1) / sms;  // blocks per SM for a single wave
     const int64_t budget = std::min<int64_t>(smem_blk, int64_t(smem_sm) / int64_t(bps) - 1024);
     e->bulk_ks = 2;
@@ -477,35 +490,85 @@ uint32_t octgpu_log_schedule(uint64_t t_max, uint32_t ppd, uint64_t* out, uint32
     return uint32_t(times.size());
 }
 
-int octgpu_create(uint32_t X, uint32_t Y, uint32_t w, uint64_t seed, int device, octgpu_engine** out) {
-    if (!out) return fail(OCTGPU_ERR_CONFIG, "null output");
-    *out = nullptr;
-    int rc = validate(X, Y, w);
-    if (rc) return rc;
+}  // extern "C"
+
+namespace {
+
+// Allocates an engine over global rows [y0, y0 + L) of an X x Ytot lattice
+// (stripe) or the whole periodic lattice (!stripe).
+int make_engine(uint32_t X, uint32_t Ytot, uint32_t w, bool stripe, uint32_t y0, uint32_t L, int device,
+                uint64_t master_seed, octgpu_engine** out) {
     auto* e = new octgpu_engine;
-    e->X = X; e->Y = Y; e->w = w; e->n = X / (2 * w); e->device = device; e->master_seed = seed;
-    rc = alloc_engine(e);
-    if (!rc) {
-        // new_flat: odd planes all ones, even planes zero (slope_field.hpp:110-118)
-        const size_t pb = e->set_bytes() / 4;
-        char* base = static_cast<char*>(e->planes[0]);
-        for (int p = 0; p < 4; ++p)
-            if (cudaMemsetAsync(base + p * pb, (p & 1) ? 0xff : 0x00, pb, e->stream) != cudaSuccess) {
-                rc = cuda_fail(cudaGetLastError(), "cudaMemsetAsync");
-                break;
-            }
-    }
-    if (!rc) {
-        std::vector<uint64_t> st(4 * size_t(Y));
-        stream_states(seed, Y, st.data());
-        rc = upload_states(e, st.data());
-    }
+    e->X = X; e->w = w; e->n = X / (2 * w); e->device = device; e->master_seed = master_seed;
+    e->Ytot = Ytot; e->stripe = stripe; e->y0 = stripe ? y0 : 0; e->L = stripe ? L : Ytot;
+    // stripe: halo row 0, core 1..L, halos L+1, L+2, then >= 34 rows of padding so the
+    // 34-row windows of k_mcs_bulk never leave the allocation; even for 16-B alignment
+    e->Y = stripe ? ((L + 3 + 36 + 1) & ~1u) : Ytot;
+    int rc = alloc_engine(e);
     if (rc) {
         std::string keep = g_err;
         octgpu_destroy(e);
         g_err = keep;
         return rc;
     }
+    *out = e;
+    return OCTGPU_OK;
+}
+
+// Upload core-row planes given in the reference layout ([4][core rows][n]).
+int load_planes(octgpu_engine* e, const void* planes) {
+    int rc = ensure_stage(e);
+    if (rc) return rc;
+    const size_t wb = e->word_bytes(), row_bytes = size_t(e->n) * wb;
+    if (!e->stripe) {
+        CK(cudaMemcpyAsync(e->stage, planes, e->set_bytes(), cudaMemcpyHostToDevice, e->stream));
+    } else {
+        std::vector<unsigned char> pad(e->set_bytes(), 0);
+        for (int p = 0; p < 4; ++p)
+            std::memcpy(pad.data() + (size_t(p) * e->Y + 1) * row_bytes,
+                        static_cast<const unsigned char*>(planes) + size_t(p) * e->L * row_bytes, e->L * row_bytes);
+        CK(cudaMemcpyAsync(e->stage, pad.data(), e->set_bytes(), cudaMemcpyHostToDevice, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+    }
+    CK(launch_import(e->w, e->stage, e->planes[e->pcur], e->geom(), e->stream));
+    ++e->launches;
+    CK(cudaStreamSynchronize(e->stream));
+    return OCTGPU_OK;
+}
+
+int flat_fill(octgpu_engine* e) {  // new_flat: odd planes all ones, even planes zero (slope_field.hpp:110-118)
+    const size_t pb = e->set_bytes() / 4;
+    char* base = static_cast<char*>(e->planes[e->pcur]);
+    for (int p = 0; p < 4; ++p) CK(cudaMemsetAsync(base + p * pb, (p & 1) ? 0xff : 0x00, pb, e->stream));
+    return OCTGPU_OK;
+}
+
+int fail_destroy(octgpu_engine* e, int rc) {
+    std::string keep = g_err;
+    octgpu_destroy(e);
+    g_err = keep;
+    return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int octgpu_create(uint32_t X, uint32_t Y, uint32_t w, uint64_t seed, int device, octgpu_engine** out) {
+    if (!out) return fail(OCTGPU_ERR_CONFIG, "null output");
+    *out = nullptr;
+    int rc = validate(X, Y, w);
+    if (rc) return rc;
+    octgpu_engine* e = nullptr;
+    rc = make_engine(X, Y, w, false, 0, Y, device, seed, &e);
+    if (rc) return rc;
+    rc = flat_fill(e);
+    if (!rc) {
+        std::vector<uint64_t> st(4 * size_t(Y));
+        stream_states(seed, Y, st.data());
+        rc = upload_states(e, st.data());
+    }
+    if (rc) return fail_destroy(e, rc);
     *out = e;
     return OCTGPU_OK;
 }
@@ -519,26 +582,49 @@ int octgpu_create_from(uint32_t X, uint32_t Y, uint32_t w, uint64_t t_mcs, int p
     if (rc) return rc;
     if (phase != 0 && phase != 1) return fail(OCTGPU_ERR_CONFIG, "phase must be 0 or 1");
     if (n_states < Y) return fail(OCTGPU_ERR_INVARIANT, "stream set smaller than row count");
-    auto* e = new octgpu_engine;
-    e->X = X; e->Y = Y; e->w = w; e->n = X / (2 * w); e->device = device; e->master_seed = master_seed;
-    e->t = t_mcs; e->phase = phase;
-    rc = alloc_engine(e);
-    if (!rc) rc = ensure_stage(e);
-    if (!rc) {
-        if (cudaMemcpyAsync(e->stage, planes, e->set_bytes(), cudaMemcpyHostToDevice, e->stream) != cudaSuccess)
-            rc = cuda_fail(cudaGetLastError(), "cudaMemcpyAsync(planes)");
-        else if (launch_import(e->w, e->stage, e->planes[0], e->geom(), e->stream) != cudaSuccess)
-            rc = cuda_fail(cudaGetLastError(), "import");
-        else
-            ++e->launches;
-    }
+    octgpu_engine* e = nullptr;
+    rc = make_engine(X, Y, w, false, 0, Y, device, master_seed, &e);
+    if (rc) return rc;
+    e->t = t_mcs;
+    e->phase = phase;
+    rc = load_planes(e, planes);
     if (!rc) rc = upload_states(e, states);
-    if (rc) {
-        std::string keep = g_err;
-        octgpu_destroy(e);
-        g_err = keep;
-        return rc;
+    if (rc) return fail_destroy(e, rc);
+    *out = e;
+    return OCTGPU_OK;
+}
+
+int octgpu_create_stripe(uint32_t X, uint32_t Y, uint32_t w, uint32_t y0, uint32_t y1, uint64_t t_mcs, int phase,
+                         const void* planes, const uint64_t* states, uint64_t master_seed, int device,
+                         octgpu_engine** out) {
+    if (!out) return fail(OCTGPU_ERR_CONFIG, "null output");
+    *out = nullptr;
+    int rc = validate(X, Y, w);
+    if (rc) return rc;
+    if (!(y0 < y1 && y1 <= Y) || y1 - y0 < 2)
+        return fail(OCTGPU_ERR_CONFIG, "stripe rows [" + std::to_string(y0) + "," + std::to_string(y1) +
+                                           ") must hold at least 2 rows of the lattice");
+    if (phase != 0 && phase != 1) return fail(OCTGPU_ERR_CONFIG, "phase must be 0 or 1");
+    if ((planes == nullptr) != (states == nullptr))
+        return fail(OCTGPU_ERR_CONFIG, "give both planes and states, or neither (flat start)");
+    const uint32_t L = y1 - y0;
+    octgpu_engine* e = nullptr;
+    rc = make_engine(X, Y, w, true, y0, L, device, master_seed, &e);
+    if (rc) return rc;
+    e->t = t_mcs;
+    e->phase = phase;
+    if (planes) {
+        rc = load_planes(e, planes);
+        if (!rc) rc = upload_states(e, states);
+    } else {
+        rc = flat_fill(e);
+        if (!rc) {  // RngStreamSet(seed, Y) rows y0..y1-1
+            std::vector<uint64_t> st(4 * size_t(y1));
+            stream_states(master_seed, y1, st.data());
+            rc = upload_states(e, st.data() + 4 * size_t(y0));
+        }
     }
+    if (rc) return fail_destroy(e, rc);
     *out = e;
     return OCTGPU_OK;
 }
@@ -547,13 +633,10 @@ int octgpu_set_state(octgpu_engine* e, uint64_t t_mcs, int phase, const void* pl
                      uint32_t n_states) {
     if (!e || !planes || !states) return fail(OCTGPU_ERR_CONFIG, "null argument");
     if (phase != 0 && phase != 1) return fail(OCTGPU_ERR_CONFIG, "phase must be 0 or 1");
-    if (n_states < e->Y) return fail(OCTGPU_ERR_INVARIANT, "stream set smaller than row count");
+    if (n_states < e->core_rows()) return fail(OCTGPU_ERR_INVARIANT, "stream set smaller than row count");
     int rc = use_device(e);
-    if (!rc) rc = ensure_stage(e);
+    if (!rc) rc = load_planes(e, planes);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(e->stage, planes, e->set_bytes(), cudaMemcpyHostToDevice, e->stream));
-    CK(launch_import(e->w, e->stage, e->planes[e->pcur], e->geom(), e->stream));
-    ++e->launches;
     e->pending = 0;
     rc = upload_states(e, states);
     if (rc) return rc;
@@ -599,6 +682,7 @@ int octgpu_sync(octgpu_engine* e) {
 
 int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
     if (!e) return fail(OCTGPU_ERR_CONFIG, "null engine");
+    if (e->stripe) return fail(OCTGPU_ERR_CONFIG, "octgpu_step is not available on a row stripe (use the octgpu_stripe_* calls)");
     ProbDev p, q;
     int rc = lower_params(prm, p, q);
     if (rc) return rc;
@@ -637,6 +721,7 @@ int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
 
 int octgpu_sweep(octgpu_engine* e, int parity, const octgpu_params* prm, void* mask_log) {
     if (!e) return fail(OCTGPU_ERR_CONFIG, "null engine");
+    if (e->stripe) return fail(OCTGPU_ERR_CONFIG, "octgpu_sweep is not available on a row stripe (use the octgpu_stripe_* calls)");
     if (parity != e->phase)  // engine_vec.hpp:150-152
         return fail(OCTGPU_ERR_INVARIANT, "sweep parity " + std::to_string(parity) +
                                               " does not match field phase " + std::to_string(e->phase));
@@ -683,8 +768,18 @@ int octgpu_get_planes(octgpu_engine* e, void* out) {
     if (rc) return rc;
     CK(launch_export(e->w, e->planes[e->pcur], e->stage, e->geom(), e->stream));
     ++e->launches;
-    CK(cudaMemcpyAsync(out, e->stage, e->set_bytes(), cudaMemcpyDeviceToHost, e->stream));
+    if (!e->stripe) {
+        CK(cudaMemcpyAsync(out, e->stage, e->set_bytes(), cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+        return OCTGPU_OK;
+    }
+    std::vector<unsigned char> pad(e->set_bytes());
+    CK(cudaMemcpyAsync(pad.data(), e->stage, e->set_bytes(), cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
+    const size_t row_bytes = size_t(e->n) * e->word_bytes();
+    for (int p = 0; p < 4; ++p)
+        std::memcpy(static_cast<unsigned char*>(out) + size_t(p) * e->L * row_bytes,
+                    pad.data() + (size_t(p) * e->Y + 1) * row_bytes, e->L * row_bytes);
     return OCTGPU_OK;
 }
 
@@ -696,13 +791,15 @@ int octgpu_get_states(octgpu_engine* e, uint64_t* out) {
     std::vector<uint64_t> soa(4 * size_t(e->Y));
     CK(cudaMemcpyAsync(soa.data(), e->rng[e->rcur], e->rng_bytes(), cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
-    for (uint32_t y = 0; y < e->Y; ++y)
-        for (int j = 0; j < 4; ++j) out[4 * size_t(y) + j] = soa[size_t(j) * e->Y + y];
+    const uint32_t r0 = e->first_row();
+    for (uint32_t y = 0; y < e->core_rows(); ++y)
+        for (int j = 0; j < 4; ++j) out[4 * size_t(y) + j] = soa[size_t(j) * e->Y + r0 + y];
     return OCTGPU_OK;
 }
 
 int octgpu_field_checksum(octgpu_engine* e, uint64_t* out) {
     if (!e || !out) return fail(OCTGPU_ERR_CONFIG, "null argument");
+    if (e->stripe) return fail(OCTGPU_ERR_CONFIG, "octgpu_field_checksum is not available on a row stripe (use the octgpu_stripe_* calls)");
     std::vector<unsigned char> buf(e->set_bytes());
     int rc = octgpu_get_planes(e, buf.data());
     if (rc) return rc;
@@ -753,6 +850,7 @@ int run_measure(octgpu_engine* e) {
 
 int octgpu_measure(octgpu_engine* e, octgpu_moments* out) {
     if (!e || !out) return fail(OCTGPU_ERR_CONFIG, "null argument");
+    if (e->stripe) return fail(OCTGPU_ERR_CONFIG, "octgpu_measure is not available on a row stripe (use the octgpu_stripe_* calls)");
     int rc = run_measure(e);
     if (rc) return rc;
     const MeasureResult& r = *e->res_host;
@@ -798,6 +896,7 @@ int octgpu_measure(octgpu_engine* e, octgpu_moments* out) {
 
 int octgpu_heights(octgpu_engine* e, int32_t* out) {
     if (!e || !out) return fail(OCTGPU_ERR_CONFIG, "null argument");
+    if (e->stripe) return fail(OCTGPU_ERR_CONFIG, "octgpu_heights is not available on a row stripe (use the octgpu_stripe_* calls)");
     int rc = run_measure(e);
     if (rc) return rc;
     const size_t bytes = size_t(e->X) * e->Y * sizeof(int32_t);
@@ -811,5 +910,113 @@ int octgpu_heights(octgpu_engine* e, int32_t* out) {
     if (le != cudaSuccess) return cuda_fail(le, "heights");
     return OCTGPU_OK;
 }
+
+
+// ---------------------------------------------------------------------------
+// Row stripes (multi-GPU): see include/octgpu.h
+
+int octgpu_stripe_sizes(const octgpu_engine* e, uint64_t* to_prev, uint64_t* to_next, uint64_t* boundary) {
+    if (!e || !e->stripe) return fail(OCTGPU_ERR_CONFIG, "not a row stripe");
+    const uint64_t row = 4ull * e->n * e->word_bytes();
+    if (to_prev) *to_prev = 2 * row + 32;
+    if (to_next) *to_next = row + 32;
+    if (boundary) *boundary = uint64_t(e->n) * e->word_bytes();
+    return OCTGPU_OK;
+}
+
+int octgpu_halo_pack(octgpu_engine* e, void* to_prev, void* to_next) {
+    if (!e || !e->stripe || !to_prev || !to_next) return fail(OCTGPU_ERR_CONFIG, "not a row stripe / null buffer");
+    int rc = use_device(e);
+    if (rc) return rc;
+    const Geom g = e->geom();
+    // rows 1, 2 (+ state of row 1) become the next-lower rank's halo rows L+1, L+2
+    CK(launch_rows_gather(e->w, e->planes[e->pcur], e->rng[e->rcur], g, 1, 2, to_prev, e->stream));
+    // row L (+ state) becomes the next-higher rank's halo row 0
+    CK(launch_rows_gather(e->w, e->planes[e->pcur], e->rng[e->rcur], g, e->L, 1, to_next, e->stream));
+    e->launches += 2;
+    return OCTGPU_OK;
+}
+
+int octgpu_halo_unpack(octgpu_engine* e, const void* from_prev, const void* from_next) {
+    if (!e || !e->stripe || !from_prev || !from_next) return fail(OCTGPU_ERR_CONFIG, "not a row stripe / null buffer");
+    int rc = use_device(e);
+    if (rc) return rc;
+    const Geom g = e->geom();
+    CK(launch_rows_scatter(e->w, e->planes[e->pcur], e->rng[e->rcur], g, 0, 1, from_prev, e->stream));
+    CK(launch_rows_scatter(e->w, e->planes[e->pcur], e->rng[e->rcur], g, e->L + 1, 2, from_next, e->stream));
+    e->launches += 2;
+    return OCTGPU_OK;
+}
+
+int octgpu_stripe_mcs(octgpu_engine* e, const octgpu_params* prm, void* boundary_out) {
+    if (!e || !e->stripe || !boundary_out) return fail(OCTGPU_ERR_CONFIG, "not a row stripe / null buffer");
+    ProbDev p, q;
+    int rc = lower_params(prm, p, q);
+    if (!rc) rc = use_device(e);
+    if (rc) return rc;
+    const bool live = !(is_const(p) && is_const(q));
+    const uint64_t D = draws(prm->p, e->w) + (q.mode != M_ZERO ? draws(prm->q, e->w) : 0);
+    const uint64_t per_sweep = uint64_t(e->n) * D;
+    uint64_t* jtab = nullptr;
+    if (live) {
+        rc = materialize(e);
+        if (!rc) rc = get_table(e, per_sweep, &jtab);
+        if (rc) return rc;
+    }
+    const Geom g = e->geom();
+    const int ps = e->pcur, rs = e->rcur;
+    if (e->mcs_impl == 2)
+        CK(launch_mcs_bulk(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
+                           e->bulk_ks, e->bulk_S, e->stream));
+    else
+        CK(launch_mcs(e->w, e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, live,
+                      jtab, e->stream));
+    // Y(f) of halo row L+1 is final here (first sweep of row L+1, second of row L): the next rank's row 1
+    CK(launch_planerow_copy(e->w, e->planes[ps ^ 1], 2 + e->phase, g, e->L + 1, boundary_out, true, e->stream));
+    e->launches += 2;
+    e->pcur ^= 1;
+    if (live)
+        e->rcur ^= 1;
+    else
+        e->pending += 2 * per_sweep;
+    ++e->t;
+    return OCTGPU_OK;
+}
+
+int octgpu_stripe_finish(octgpu_engine* e, const void* boundary_in) {
+    if (!e || !e->stripe || !boundary_in) return fail(OCTGPU_ERR_CONFIG, "not a row stripe / null buffer");
+    int rc = use_device(e);
+    if (rc) return rc;
+    CK(launch_planerow_copy(e->w, e->planes[e->pcur], 2 + e->phase, e->geom(), 1, const_cast<void*>(boundary_in),
+                            false, e->stream));
+    ++e->launches;
+    return OCTGPU_OK;
+}
+
+int octgpu_measure_stripe(octgpu_engine* e, octgpu_stripe_moments* out) {
+    if (!e || !e->stripe || !out) return fail(OCTGPU_ERR_CONFIG, "not a row stripe / null output");
+    int rc = use_device(e);
+    if (rc) return rc;
+    CK(launch_measure(e->w, e->planes[e->pcur], e->geom(), e->X, e->scratch, e->res_dev, e->stream));
+    e->launches += 3;
+    CK(cudaMemcpyAsync(e->res_host, e->res_dev, sizeof(MeasureResult), cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    const MeasureResult& r = *e->res_host;
+    out->t = e->t;
+    out->n_sites = uint64_t(e->X) * e->L;
+    for (int k = 0; k < 4; ++k) {
+        out->s_lo[k] = r.s_lo[k];
+        out->s_hi[k] = r.s_hi[k];
+    }
+    out->col_sum = r.col0_sum;
+    out->sy_first = r.sy_first;
+    out->row_first_sum = r.row0_sum;
+    out->curl_count = r.curl_count;
+    out->curl_first = r.curl_count ? r.curl_first + uint64_t(e->y0) * e->X : ~0ull;
+    return OCTGPU_OK;
+}
+
+uint32_t octgpu_stripe_y0(const octgpu_engine* e) { return e ? e->y0 : 0; }
+uint32_t octgpu_stripe_rows(const octgpu_engine* e) { return e ? e->L : 0; }
 
 }  // extern "C"

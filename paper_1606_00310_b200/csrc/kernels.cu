@@ -17,6 +17,7 @@
 //    HBM traffic per site update instead of the reference's 1 B), using
 //    warp shuffles for the y-neighbour exchange and a GF(2) jump table for
 //    the second sweep's stream position.
+#include <algorithm>
 #include <cstdint>
 
 #include "device_common.cuh"
@@ -108,12 +109,6 @@ __global__ void __launch_bounds__(128) k_sweep(Word* __restrict__ planes, uint64
 // The periodic x seam (word n-1 -> word 0) is handled by drawing the second
 // sweep's word-0 xi first (stream order) but applying it last.
 
-template <typename Word>
-struct Second {
-    Word m;      // applied mask
-    Word xf;     // X(f)[y][j] with own mask, before the carry from word j-1
-};
-
 template <typename Word, int PM, int QM, int PF>
 __global__ void __launch_bounds__(128) k_mcs(const Word* __restrict__ src, Word* __restrict__ dst,
                                              const uint64_t* __restrict__ rs, uint64_t* __restrict__ rd, int f,
@@ -123,13 +118,12 @@ __global__ void __launch_bounds__(128) k_mcs(const Word* __restrict__ src, Word*
     const uint32_t Y = g.Y, n = g.n;
     const int lane = threadIdx.x & 31;
     const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t base = wid * 30u;
-    if (base >= Y) return;  // warp-uniform
-    const int64_t v = int64_t(base) - 1 + lane;
-    const uint32_t y = v < 0 ? Y - 1 : uint32_t(v % Y);
-    const uint32_t y1 = (y + 1 == Y) ? 0 : y + 1;
-    const bool core = lane >= 1 && lane <= 30 && (base + uint32_t(lane) - 1) < Y;
-    const bool wyf = lane >= 2 && (base + uint32_t(lane) - 2) < Y;  // lane-1 is core
+    if (wid * 30u >= g.c1 - g.c0) return;  // warp-uniform
+    const uint32_t v = g.c0 - 1 + wid * 30u + lane;  // virtual row
+    const uint32_t y = g.wrap ? v % g.wrap : v;
+    const uint32_t y1 = g.wrap ? (v + 1) % g.wrap : v + 1;
+    const bool core = lane >= 1 && lane <= 30 && v < g.c1;
+    const bool wyf = lane >= 2 && v - 1 < g.c1;  // lane-1 is core
     const int s = f ^ 1;
     const size_t PS = g.plane_stride;
     const Word* sXf = src + size_t(0 + f) * PS + y;
@@ -140,7 +134,7 @@ __global__ void __launch_bounds__(128) k_mcs(const Word* __restrict__ src, Word*
     Word* dYf = dst + size_t(2 + f) * PS + y;
     Word* dXs = dst + size_t(0 + s) * PS + y;
     Word* dYs = dst + size_t(2 + s) * PS + y;
-    const bool sh1 = ((uint32_t(f) ^ y) & 1u) != 0;  // first sweep shifts x+ of this row
+    const bool sh1 = ((uint32_t(f) ^ y ^ g.ypar) & 1u) != 0;  // first sweep shifts x+ of this row
     const bool sh2 = !sh1;                           // second sweep does
 
     Xo s1{0, 0, 0, 0}, s2{0, 0, 0, 0};
@@ -324,7 +318,7 @@ cudaError_t sweep_pq(void* planes, uint64_t* rng, int parity, Geom g, const Prob
 template <typename Word, int PM, int QM>
 cudaError_t mcs_pq(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
                    const ProbDev& q, const uint64_t* jtab, cudaStream_t st) {
-    const uint32_t warps = (g.Y + 29) / 30;
+    const uint32_t warps = (g.c1 - g.c0 + 29) / 30;
     const uint32_t threads = 128, blocks = (warps * 32 + threads - 1) / threads;
     k_mcs<Word, PM, QM, kPF><<<blocks, threads, 0, st>>>(static_cast<const Word*>(src), static_cast<Word*>(dst),
                                                         rs, rd, f, g, p, q, jtab);
@@ -392,6 +386,89 @@ cudaError_t launch_import(int w, const void* in, void* planes, Geom g, cudaStrea
 cudaError_t launch_export(int w, const void* planes, void* out, Geom g, cudaStream_t st) {
     return w == 64 ? transpose_w<uint64_t, false>(planes, out, g, st)
                    : transpose_w<uint32_t, false>(planes, out, g, st);
+}
+
+}  // namespace octgpu
+
+// -------------------------------------------------------------------------
+// Row-stripe halo exchange helpers (multi-GPU path). Tiny and strided: a few
+// plane-rows per MCS, so plain grid-stride loops.
+namespace octgpu {
+
+template <typename Word>
+__global__ void k_rows_gather(const Word* __restrict__ planes, const uint64_t* __restrict__ rng, Geom g, uint32_t r0,
+                              uint32_t nrows, Word* __restrict__ buf) {
+    const uint32_t n = g.n, per = nrows * n, total = 4 * per;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const uint32_t p = i / per, rem = i % per, r = rem / n, k = rem % n;
+        buf[i] = planes[size_t(p) * g.plane_stride + size_t(k) * g.Y + r0 + r];
+    }
+    if (rng && blockIdx.x == 0 && threadIdx.x < 4)
+        reinterpret_cast<uint64_t*>(buf + total)[threadIdx.x] = rng[size_t(threadIdx.x) * g.Y + r0];
+}
+
+template <typename Word>
+__global__ void k_rows_scatter(Word* __restrict__ planes, uint64_t* __restrict__ rng, Geom g, uint32_t r0,
+                               uint32_t nrows, const Word* __restrict__ buf) {
+    const uint32_t n = g.n, per = nrows * n, total = 4 * per;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const uint32_t p = i / per, rem = i % per, r = rem / n, k = rem % n;
+        planes[size_t(p) * g.plane_stride + size_t(k) * g.Y + r0 + r] = buf[i];
+    }
+    if (rng && blockIdx.x == 0 && threadIdx.x < 4)
+        rng[size_t(threadIdx.x) * g.Y + r0] = reinterpret_cast<const uint64_t*>(buf + total)[threadIdx.x];
+}
+
+template <typename Word>
+__global__ void k_planerow_copy(Word* __restrict__ planes, int plane, Geom g, uint32_t r, Word* __restrict__ buf,
+                                int to_buf) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < g.n; k += gridDim.x * blockDim.x) {
+        Word* p = planes + size_t(plane) * g.plane_stride + size_t(k) * g.Y + r;
+        if (to_buf)
+            buf[k] = *p;
+        else
+            *p = buf[k];
+    }
+}
+
+namespace {
+inline uint32_t small_grid(uint32_t work) { return std::min<uint32_t>(1024, (work + 255) / 256 + 1); }
+}  // namespace
+
+cudaError_t launch_rows_gather(int w, const void* planes, const uint64_t* rng, Geom g, uint32_t r0, uint32_t nrows,
+                               void* buf, cudaStream_t st) {
+    const uint32_t blocks = small_grid(4 * nrows * g.n);
+    if (w == 64)
+        k_rows_gather<uint64_t><<<blocks, 256, 0, st>>>(static_cast<const uint64_t*>(planes), rng, g, r0, nrows,
+                                                        static_cast<uint64_t*>(buf));
+    else
+        k_rows_gather<uint32_t><<<blocks, 256, 0, st>>>(static_cast<const uint32_t*>(planes), rng, g, r0, nrows,
+                                                        static_cast<uint32_t*>(buf));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rows_scatter(int w, void* planes, uint64_t* rng, Geom g, uint32_t r0, uint32_t nrows,
+                                const void* buf, cudaStream_t st) {
+    const uint32_t blocks = small_grid(4 * nrows * g.n);
+    if (w == 64)
+        k_rows_scatter<uint64_t><<<blocks, 256, 0, st>>>(static_cast<uint64_t*>(planes), rng, g, r0, nrows,
+                                                         static_cast<const uint64_t*>(buf));
+    else
+        k_rows_scatter<uint32_t><<<blocks, 256, 0, st>>>(static_cast<uint32_t*>(planes), rng, g, r0, nrows,
+                                                         static_cast<const uint32_t*>(buf));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_planerow_copy(int w, void* planes, int plane, Geom g, uint32_t r, void* buf, bool to_buf,
+                                 cudaStream_t st) {
+    const uint32_t blocks = small_grid(g.n);
+    if (w == 64)
+        k_planerow_copy<uint64_t><<<blocks, 256, 0, st>>>(static_cast<uint64_t*>(planes), plane, g, r,
+                                                          static_cast<uint64_t*>(buf), to_buf);
+    else
+        k_planerow_copy<uint32_t><<<blocks, 256, 0, st>>>(static_cast<uint32_t*>(planes), plane, g, r,
+                                                          static_cast<uint32_t*>(buf), to_buf);
+    return cudaGetLastError();
 }
 
 }  // namespace octgpu

@@ -95,18 +95,16 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
     const int wib = threadIdx.x >> 5;  // warp in block
     const int wpb = blockDim.x >> 5;
     const uint32_t wid = blockIdx.x * wpb + wib;
-    const uint32_t r0 = wid * 30u;
-    if (r0 >= Y) return;  // warp-uniform
+    if (wid * 30u >= g.c1 - g.c0) return;  // warp-uniform
+    const uint32_t r0 = g.c0 - 1 + wid * 30u;  // virtual row of lane 0 (window start)
 
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw) + wib * 8;  // 8 barrier slots per warp
     Word* ring = reinterpret_cast<Word*>(smem_raw + 8 * 8 * wpb) + size_t(wib) * S * LY::kWords;
 
-    const uint32_t v = r0 + lane;  // virtual row; row Y is row 0
-    const uint32_t y = v % Y;
-    const uint32_t y1 = (y + 1 == Y) ? 0 : y + 1;
-    (void)y1;
-    const bool core = lane >= 1 && lane <= 30 && (r0 + lane) <= Y;
-    const bool wyf = lane >= 2 && (r0 + lane - 1) <= Y;
+    const uint32_t v = r0 + lane;  // virtual row
+    const uint32_t y = g.wrap ? v % g.wrap : v;
+    const bool core = lane >= 1 && lane <= 30 && v < g.c1;
+    const bool wyf = lane >= 2 && v - 1 < g.c1;  // row v-1 is core: this lane writes Y(f)[v]
     const int s = f ^ 1;
     const size_t PS = g.plane_stride;
     const Word* planeXf = src + size_t(0 + f) * PS;
@@ -117,11 +115,12 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
     Word* dYf = dst + size_t(2 + f) * PS + y;
     Word* dXs = dst + size_t(0 + s) * PS + y;
     Word* dYs = dst + size_t(2 + s) * PS + y;
-    const bool sh1 = ((uint32_t(f) ^ y) & 1u) != 0;
+    const bool sh1 = ((uint32_t(f) ^ y ^ g.ypar) & 1u) != 0;
     const bool sh2 = !sh1;
 
     // window split for the periodic wrap in y (last warp only)
-    const uint32_t rows1 = min(uint32_t(kWin), Y - r0);
+    const uint32_t pr0 = g.wrap ? r0 % g.wrap : r0;  // physical window start
+    const uint32_t rows1 = g.wrap ? min(uint32_t(kWin), g.wrap - pr0) : uint32_t(kWin);
     const uint32_t rows2 = kWin - rows1;
 
     if (lane == 0) {
@@ -161,7 +160,7 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
                 if (word >= n) word -= n;
                 slot = LY::kXs + j * kWin;
             }
-            const Word* gsrc = gplane + size_t(word) * Y + (part ? 0 : r0);
+            const Word* gsrc = gplane + size_t(word) * Y + (part ? 0 : pr0);
             Word* sdst = base + slot + (part ? rows1 : 0);
             bulk_g2s(sdst, gsrc, (part ? rows2 : rows1) * 8, &bars[st]);
         }
@@ -267,7 +266,7 @@ namespace {
 template <int PM, int QM>
 cudaError_t bulk_pq(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
                     const ProbDev& q, const uint64_t* jtab, int ks, int S, cudaStream_t st) {
-    const uint32_t warps = (g.Y + 29) / 30;
+    const uint32_t warps = (g.c1 - g.c0 + 29) / 30;
     const uint32_t wpb = 4, threads = 32 * wpb, blocks = (warps + wpb - 1) / wpb;
     const size_t smem = 8 * 8 * wpb + size_t(wpb) * S * mcs_bulk_stage_bytes(ks);
     cudaError_t e;

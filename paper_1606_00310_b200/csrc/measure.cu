@@ -33,8 +33,8 @@ namespace {
 constexpr int kRowsPerWarp = 31;  // lane 0 is the y-1 halo for the curl check
 constexpr int kThreads = 128;
 
-uint32_t measure_blocks(uint32_t Y) {
-    const uint32_t warps = (Y + kRowsPerWarp - 1) / kRowsPerWarp;
+uint32_t measure_blocks(uint32_t rows) {
+    const uint32_t warps = (rows + kRowsPerWarp - 1) / kRowsPerWarp;
     return (warps * 32 + kThreads - 1) / kThreads;
 }
 
@@ -48,27 +48,31 @@ __device__ __forceinline__ __int128 shfl_down_i128(__int128 v, int off) {
 }  // namespace
 
 size_t measure_scratch_bytes(uint32_t Y) {
-    return size_t(Y) * sizeof(long long) + size_t(measure_blocks(Y)) * sizeof(Partial) + 64;
+    return size_t(Y) * sizeof(long long) + size_t(measure_blocks(Y + 1)) * sizeof(Partial) + 64;
 }
 
 // ---- column 0: G_y and the column-0 closure ------------------------------
+// Rows [start, start + count) in order; G[row] = sum_{rows <= row} sigma_y-(0,.) - sigma_x-(0,row)
+// (- sigma_y-(0,start) when exclude_first: the periodic gauge h(0,0) = 0).
 template <typename Word>
-__global__ void __launch_bounds__(1024) k_col_scan(const Word* __restrict__ planes, Geom g,
-                                                   long long* __restrict__ G, long long* __restrict__ col_sum) {
+__global__ void __launch_bounds__(1024) k_col_scan(const Word* __restrict__ planes, Geom g, uint32_t start,
+                                                   uint32_t count, int exclude_first, long long* __restrict__ G,
+                                                   long long* __restrict__ col_sum, long long* __restrict__ sy_first) {
     __shared__ int warp_tot[32];
     __shared__ long long carry_sh;
-    const uint32_t Y = g.Y;
     const size_t PS = g.plane_stride;
     const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
     if (t == 0) carry_sh = 0;
     __syncthreads();
-    // sigma_y-(0,0) is excluded from H (h(0,0) = 0)
-    const int sy00 = (planes[2 * PS] & 1) ? 1 : -1;
-    for (uint32_t base = 0; base < Y; base += 1024) {
-        const uint32_t y = base + t;
+    const int par0 = int((start ^ g.ypar) & 1u);
+    const int sy00 = (planes[(2 + par0) * PS + start] & 1) ? 1 : -1;
+    const int excl = exclude_first ? sy00 : 0;
+    for (uint32_t base = 0; base < count; base += 1024) {
+        const uint32_t i = base + t;
+        const uint32_t y = start + i;
         int sy = 0, s0 = 0;
-        if (y < Y) {
-            const int par = int(y & 1u);  // site (0,y) has parity y&1
+        if (i < count) {
+            const int par = int((y ^ g.ypar) & 1u);  // site (0,y) has parity (global y)&1
             sy = (planes[(2 + par) * PS + y] & 1) ? 1 : -1;
             s0 = (planes[par * PS + y] & 1) ? 1 : -1;
         }
@@ -92,12 +96,15 @@ __global__ void __launch_bounds__(1024) k_col_scan(const Word* __restrict__ plan
         __syncthreads();
         const long long carry = carry_sh;
         const long long run = carry + incl + (wp > 0 ? warp_tot[wp - 1] : 0);  // sum_{y'<=y} sy
-        if (y < Y) G[y] = (run - sy00) - s0;
+        if (i < count) G[y] = (run - excl) - s0;
         __syncthreads();
         if (t == 1023) carry_sh = run;
         __syncthreads();
     }
-    if (t == 0) *col_sum = carry_sh;
+    if (t == 0) {
+        *col_sum = carry_sh;
+        *sy_first = sy00;
+    }
 }
 
 // ---- per-row pass ------------------------------------------------------------
@@ -139,20 +146,20 @@ __global__ void __launch_bounds__(kThreads, 4) k_measure_rows(const Word* __rest
     const uint32_t Y = g.Y, n = g.n;
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
     const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t base = wid * kRowsPerWarp;
     __int128 S[4] = {0, 0, 0, 0};
     unsigned long long ccount = 0, cfirst = ~0ull;
     long long row0 = 0;
-    if (base < Y) {  // warp-uniform
-        const int64_t v = int64_t(base) - 1 + lane;
-        const uint32_t y = v < 0 ? Y - 1 : uint32_t(v % Y);
-        const bool core = lane >= 1 && (base + uint32_t(lane) - 1) < Y;
+    if (wid * kRowsPerWarp < g.c1 - g.c0) {  // warp-uniform
+        const uint32_t v = g.c0 - 1 + wid * kRowsPerWarp + lane;  // lane 0: the y-1 halo row
+        const uint32_t y = g.wrap ? v % g.wrap : v;
+        const bool core = lane >= 1 && v < g.c1;
+        const uint32_t row_id = g.wrap ? y : v - g.c0;  // position of this row in the result's scan order
         const size_t PS = g.plane_stride;
         const Word* X0 = planes + y;
         const Word* X1 = planes + PS + y;
         const Word* Y0 = planes + 2 * PS + y;
         const Word* Y1 = planes + 3 * PS + y;
-        const int ya = int(y & 1u);
+        const int ya = int((y ^ g.ypar) & 1u);
         const uint64_t* lrep = lut + (lane & 15);
         const size_t last = size_t(n - 1) * Y;
         Word pD0 = Y0[last], pD1 = Y1[last];
@@ -172,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_measure_rows(const Word* __rest
                 const Word C = pi ? yy1 : yy0;
                 const Word Dr = pi ? yy0 : yy1;
                 const Word Dp = pi ? pD0 : pD1;
-                const bool even_x = ((uint32_t(pi) ^ y) & 1u) == 0;
+                const bool even_x = ((uint32_t(pi) ^ y ^ g.ypar) & 1u) == 0;
                 const Word D = even_x ? Word((Dr << 1) | (Dp >> (W - 1))) : Dr;
                 const Word Vv = (A ^ B ^ C ^ D) | ((A ^ B) & (A ^ C));
                 if (Vv) {
@@ -245,8 +252,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_measure_rows(const Word* __rest
             S[2] = g3 * U0 + 3 * g2 * U1 + 3 * G * U2 + U3;
             S[3] = g4 * U0 + 4 * g3 * U1 + 6 * g2 * U2 + 4 * G * U3 + U4;
             ccount = rc;
-            if (rfirst != 0xffffffffu) cfirst = (unsigned long long)y * X + rfirst;
-            if (y == 0) row0 = rowsum;
+            if (rfirst != 0xffffffffu) cfirst = (unsigned long long)row_id * X + rfirst;
+            if (row_id == 0) row0 = rowsum;
         }
     }
     // block reduction
@@ -287,6 +294,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_measure_rows(const Word* __rest
 
 __global__ void __launch_bounds__(256) k_measure_final(const Partial* __restrict__ part, uint32_t nb,
                                                        const long long* __restrict__ col_sum,
+                                                       const long long* __restrict__ sy_first,
                                                        MeasureResult* __restrict__ res) {
     __shared__ __int128 sh_s[4][8];
     __shared__ unsigned long long sh_cc[8], sh_cf[8];
@@ -338,6 +346,8 @@ __global__ void __launch_bounds__(256) k_measure_final(const Partial* __restrict
         res->curl_first = tf;
         res->row0_sum = tr;
         res->col0_sum = *col_sum;
+        res->sy_first = *sy_first;
+        res->pad = 0;
     }
 }
 
@@ -391,16 +401,23 @@ cudaError_t launch_measure(int w, const void* planes, Geom g, uint32_t X, void* 
                            cudaStream_t st) {
     long long* G = static_cast<long long*>(scratch);
     Partial* part = reinterpret_cast<Partial*>(G + g.Y);
-    const uint32_t nb = measure_blocks(g.Y);
-    long long* col = reinterpret_cast<long long*>(part + nb);
+    const uint32_t rows = g.c1 - g.c0;
+    const uint32_t nb = measure_blocks(rows);
+    long long* col = reinterpret_cast<long long*>(part + measure_blocks(g.Y + 1));
+    long long* syf = col + 1;
+    // periodic: rows 0..Y-1 in the reference's gauge; stripe: its core rows, local gauge
+    const uint32_t start = g.wrap ? 0 : g.c0;
+    const int excl = g.wrap ? 1 : 0;
     if (w == 64) {
-        k_col_scan<uint64_t><<<1, 1024, 0, st>>>(static_cast<const uint64_t*>(planes), g, G, col);
+        k_col_scan<uint64_t><<<1, 1024, 0, st>>>(static_cast<const uint64_t*>(planes), g, start, rows, excl, G, col,
+                                                  syf);
         k_measure_rows<uint64_t><<<nb, kThreads, 0, st>>>(static_cast<const uint64_t*>(planes), g, X, G, part);
     } else {
-        k_col_scan<uint32_t><<<1, 1024, 0, st>>>(static_cast<const uint32_t*>(planes), g, G, col);
+        k_col_scan<uint32_t><<<1, 1024, 0, st>>>(static_cast<const uint32_t*>(planes), g, start, rows, excl, G, col,
+                                                  syf);
         k_measure_rows<uint32_t><<<nb, kThreads, 0, st>>>(static_cast<const uint32_t*>(planes), g, X, G, part);
     }
-    k_measure_final<<<1, 256, 0, st>>>(part, nb, col, static_cast<MeasureResult*>(result_dev));
+    k_measure_final<<<1, 256, 0, st>>>(part, nb, col, syf, static_cast<MeasureResult*>(result_dev));
     return cudaGetLastError();
 }
 

@@ -25,13 +25,21 @@ struct ProbDev {
 // so a warp whose lanes own 32 consecutive rows touches one contiguous 256-B
 // (w=64) segment per plane per word: every access is coalesced and any
 // contiguous window of rows is contiguous in memory.
+//
+// Rows are addressed through a "virtual" row index v: the kernels compute the
+// rows v in [c0, c1) ("core" rows) and may read the rows just outside that
+// range; physical row = wrap ? v % wrap : v. A full periodic lattice is
+// {Y = lattice rows, c0 = 1, c1 = Y + 1, wrap = Y}; a row stripe of L rows
+// held with one halo row above and two below (plus padding) is
+// {Y = allocated rows, c0 = 1, c1 = L + 1, wrap = 0}.
 struct Geom {
-    uint32_t Y;
+    uint32_t Y;            // rows stored per plane (row stride in words)
     uint32_t n;            // words per plane-row = X / (2w)
     size_t plane_stride;   // n * Y words
+    uint32_t c0, c1;       // core rows (virtual)
+    uint32_t wrap;         // periodic modulus in y, or 0
+    uint32_t ypar;         // parity of the global row of physical row 0 (site parity uses global rows)
 };
-
-struct RowStats;  // measurement scratch, defined in kernels.cu
 
 // Per-row RNG states are stored SoA: s[j * Y + y], j = 0..3.
 
@@ -61,10 +69,24 @@ size_t mcs_bulk_stage_bytes(int ks);
 // s <- M s for every row state, M given as a 4-bit table (64 x 16 x 4 u64).
 cudaError_t launch_apply_jump(uint64_t* rng, uint32_t Y, const uint64_t* tab, cudaStream_t st);
 
-// Measurement: per-row pass + single-block scan/reduction.
+// Measurement: column scan + per-row pass + final reduction. For a periodic
+// lattice the gauge is the reference's h(0,0) = 0; for a stripe it is local
+// (h = 0 at the virtual row c0 - 1, column 0) and the host shifts the power
+// sums binomially when combining stripes.
 size_t measure_scratch_bytes(uint32_t Y);
 cudaError_t launch_measure(int w, const void* planes, Geom g, uint32_t X, void* scratch, void* result_dev,
                            cudaStream_t st);
+
+// Row-stripe halo exchange: gather rows [r0, r0+nrows) of all 4 planes (and
+// the rng state of row r0 when rng != null) into a contiguous buffer laid
+// out [plane][row][word] + [4] state words, or scatter such a buffer back.
+cudaError_t launch_rows_gather(int w, const void* planes, const uint64_t* rng, Geom g, uint32_t r0, uint32_t nrows,
+                               void* buf, cudaStream_t st);
+cudaError_t launch_rows_scatter(int w, void* planes, uint64_t* rng, Geom g, uint32_t r0, uint32_t nrows,
+                                const void* buf, cudaStream_t st);
+// one plane-row (word k = 0..n-1 of row r) <-> contiguous n words
+cudaError_t launch_planerow_copy(int w, void* planes, int plane, Geom g, uint32_t r, void* buf, bool to_buf,
+                                 cudaStream_t st);
 // Heights (reference HeightMap layout, row-major int32), after launch_measure.
 cudaError_t launch_heights(int w, const void* planes, Geom g, uint32_t X, const void* scratch, int32_t* out,
                            cudaStream_t st);
@@ -75,8 +97,10 @@ struct MeasureResult {
     int64_t s_hi[4];
     unsigned long long curl_count;
     unsigned long long curl_first;  // y * X + x of the first violating plaquette, ~0 if none
-    long long row0_sum;             // sum_x sigma_x-(x, 0)
-    long long col0_sum;             // sum_y sigma_y-(0, y)
+    long long row0_sum;             // sum_x sigma_x-(x, y) of the first core row (global row 0 if periodic)
+    long long col0_sum;             // sum_y sigma_y-(0, y) over the core rows
+    long long sy_first;             // sigma_y-(0, first core row)
+    long long pad;
 };
 
 }  // namespace octgpu

@@ -1,0 +1,300 @@
+"""Row stripes across GPUs: one stripe engine per GPU.
+
+Partition: contiguous row blocks exactly as the reference's SweepPlan
+(params.hpp:107-127; the result is partition-independent, like the
+reference's worker count). Per MCS, stripe r (rows [y0, y1)):
+
+  1. pack      rows y0, y0+1 (+ rng state of y0) -> to_prev; row y1-1 (+ state) -> to_next
+  2. exchange  shift-up   (to_prev -> rank r-1, from_next <- rank r+1)
+               shift-down (to_next -> rank r+1, from_prev <- rank r-1)
+  3. unpack    halo rows y0-1 (from_prev) and y1, y1+1 (from_next)
+  4. mcs       fused sweep f / sweep f^1 over the stripe's rows (k_mcs_bulk)
+  5. boundary  y-plane f of row y1 -> rank r+1, which completes its row y0 (finish)
+
+The halo traffic is 3 plane-rows x 4 planes + one plane-row per stripe
+boundary per MCS (X/16 bytes per plane-row), independent of the stripe
+height. Measurement: every stripe reduces its own rows in a local height
+gauge; the exact int128 power sums are shifted binomially by the column-0
+prefix of the stripes above and summed (``combine``).
+
+Transports: ``LocalTransport`` (all stripes in this process, e.g. several
+stripes on one GPU — used to prove bit-exactness on one device) and
+``DistTransport`` (one stripe per rank over torch.distributed: NCCL on GPUs,
+gloo on CPU for the protocol tests).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from fractions import Fraction
+from math import comb
+
+import numpy as np
+
+from ._lib import ConfigError, InvariantError, OctStripeMoments, check, lib
+from .engine import MeasurementRecord, _i128, _word_dtype
+from .params import LatticeConfig, UpdateParams
+
+
+def stripe_bounds(Y: int, parts: int, index: int) -> tuple[int, int]:
+    """Row block `index` of `parts` (SweepPlan::make, params.hpp:111-126)."""
+    if parts < 1:
+        raise ConfigError("worker count must be >= 1")
+    n = min(parts, Y)
+    base, rem = divmod(Y, n)
+    y = 0
+    for i in range(n):
+        ln = base + (1 if i >= n - rem else 0)
+        if i == index:
+            return y, y + ln
+        y += ln
+    raise ConfigError(f"stripe index {index} out of range for {n} stripes")
+
+
+@dataclass
+class StripeMoments:
+    """Exact per-stripe statistics in the stripe-local gauge."""
+
+    y0: int
+    t: int
+    n_sites: int
+    sums: tuple  # (S1, S2, S3, S4)
+    col_sum: int
+    sy_first: int
+    row_first_sum: int
+    curl_count: int
+    curl_first: int  # global y * X + x, or -1
+
+    def to_array(self) -> np.ndarray:
+        vals = [self.y0, self.t, self.n_sites, self.col_sum, self.sy_first, self.row_first_sum, self.curl_count,
+                self.curl_first]
+        for s in self.sums:
+            vals += [s & 0xFFFFFFFFFFFFFFFF, (s >> 64) & 0xFFFFFFFFFFFFFFFF]
+        return np.array([v & 0xFFFFFFFFFFFFFFFF for v in vals], np.uint64).view(np.int64)
+
+    @staticmethod
+    def from_array(a: np.ndarray) -> "StripeMoments":
+        u = [int(v) for v in np.asarray(a, np.int64).view(np.uint64)]
+        sg = lambda v: v - (1 << 64) if v >> 63 else v  # noqa: E731
+        sums = tuple(_i128(u[8 + 2 * k], u[9 + 2 * k]) for k in range(4))
+        return StripeMoments(u[0], u[1], u[2], sums, sg(u[3]), sg(u[4]), sg(u[5]), u[6], sg(u[7]))
+
+
+def combine(parts: list[StripeMoments], X: int, Y: int) -> MeasurementRecord:
+    """Global measure_heights from stripe-local sums, with reconstruct_heights'
+    checks in its order (slope_field.hpp:209-226)."""
+    parts = sorted(parts, key=lambda m: m.y0)
+    N = sum(m.n_sites for m in parts)
+    if N != X * Y:
+        raise ConfigError("stripes do not cover the lattice")
+    curl = sum(m.curl_count for m in parts)
+    if curl:
+        first = min(m.curl_first for m in parts if m.curl_count)
+        raise InvariantError(f"curl violation at plaquette ({first % X},{first // X}); {curl} plaquettes inconsistent")
+    if parts[0].row_first_sum != 0:
+        raise InvariantError("row 0 of sigma_x- does not balance to zero")
+    if sum(m.col_sum for m in parts) != 0:
+        raise InvariantError("column 0 of sigma_y- does not balance to zero")
+    sigma00 = parts[0].sy_first
+    S = [0, 0, 0, 0]
+    prefix = 0
+    for m in parts:
+        c = prefix - sigma00  # h_global = h_local + c on this stripe
+        loc = (m.n_sites,) + tuple(m.sums)
+        for k in range(1, 5):
+            S[k - 1] += sum(comb(k, j) * c ** (k - j) * loc[j] for j in range(k + 1))
+        prefix += m.col_sum
+    return _record(parts[0].t, N, S)
+
+
+def _record(t: int, N: int, S: list[int]) -> MeasurementRecord:
+    S1, S2, S3, S4 = S
+    mean = Fraction(S1, N)
+    m2 = Fraction(S2, N) - mean ** 2
+    m3 = Fraction(S3, N) - 3 * mean * Fraction(S2, N) + 2 * mean ** 3
+    m4 = Fraction(S4, N) - 4 * mean * Fraction(S3, N) + 6 * mean ** 2 * Fraction(S2, N) - 3 * mean ** 4
+    if m2 > 0:
+        skew = float(m3) / float(m2) ** 1.5
+        kurt = float(m4 / (m2 * m2)) - 3.0
+    else:
+        skew = kurt = float("nan")
+    return MeasurementRecord(t, float(m2), float(mean), skew, kurt, N, tuple(S))
+
+
+class StripeEngine:
+    """One row stripe [y0, y1) of an X x Y periodic lattice on one GPU."""
+
+    def __init__(self, cfg: LatticeConfig, y0: int, y1: int, seed: int = 1, device: int = 0,
+                 planes: np.ndarray | None = None, states: np.ndarray | None = None, t: int = 0, phase: int = 0):
+        self._h = None
+        self.cfg, self.y0, self.y1, self.device = cfg, y0, y1, device
+        h = C.c_void_p()
+        pp = sp = None
+        if planes is not None:
+            planes = np.ascontiguousarray(planes, _word_dtype(cfg.w))
+            states = np.ascontiguousarray(states, np.uint64)
+            pp, sp = planes.ctypes.data_as(C.c_void_p), states.ctypes.data_as(C.c_void_p)
+        check(lib().octgpu_create_stripe(cfg.X, cfg.Y, cfg.w, y0, y1, t, phase, pp, sp, seed, device, C.byref(h)))
+        self._h = h
+        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(lib().octgpu_stripe_sizes(h, C.byref(a), C.byref(b), C.byref(c)))
+        self.to_prev_bytes, self.to_next_bytes, self.boundary_bytes = a.value, b.value, c.value
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().octgpu_destroy(self._h)
+            self._h = None
+
+    @staticmethod
+    def _p(buf) -> C.c_void_p:
+        return C.c_void_p(buf.data_ptr())
+
+    def set_stream(self, cuda_stream: int | None) -> None:
+        check(lib().octgpu_set_stream(self._h, C.c_void_p(cuda_stream) if cuda_stream else None))
+
+    def pack(self, to_prev, to_next) -> None:
+        check(lib().octgpu_halo_pack(self._h, self._p(to_prev), self._p(to_next)))
+
+    def unpack(self, from_prev, from_next) -> None:
+        check(lib().octgpu_halo_unpack(self._h, self._p(from_prev), self._p(from_next)))
+
+    def mcs(self, prm: UpdateParams, boundary_out) -> None:
+        c = prm.to_c()
+        check(lib().octgpu_stripe_mcs(self._h, C.byref(c), self._p(boundary_out)))
+
+    def finish(self, boundary_in) -> None:
+        check(lib().octgpu_stripe_finish(self._h, self._p(boundary_in)))
+
+    def measure_local(self) -> StripeMoments:
+        m = OctStripeMoments()
+        check(lib().octgpu_measure_stripe(self._h, C.byref(m)))
+        sums = tuple(_i128(int(m.s_lo[k]), int(m.s_hi[k])) for k in range(4))
+        first = int(m.curl_first) if m.curl_count else -1
+        return StripeMoments(self.y0, int(m.t), int(m.n_sites), sums, int(m.col_sum), int(m.sy_first),
+                             int(m.row_first_sum), int(m.curl_count), first)
+
+    @property
+    def t(self) -> int:
+        return int(lib().octgpu_t(self._h))
+
+    @property
+    def launches(self) -> int:
+        return int(lib().octgpu_launch_count(self._h))
+
+    def planes(self) -> np.ndarray:
+        out = np.zeros((4, self.y1 - self.y0, self.cfg.words_per_row()), _word_dtype(self.cfg.w))
+        check(lib().octgpu_get_planes(self._h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def states(self) -> np.ndarray:
+        out = np.zeros((self.y1 - self.y0, 4), np.uint64)
+        check(lib().octgpu_get_states(self._h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def sync(self) -> None:
+        check(lib().octgpu_sync(self._h))
+
+
+class _Buffers:
+    def __init__(self, eng, alloc):
+        self.tp = alloc(eng.to_prev_bytes)
+        self.tn = alloc(eng.to_next_bytes)
+        self.rp = alloc(eng.to_next_bytes)   # from prev = its to_next
+        self.rn = alloc(eng.to_prev_bytes)   # from next = its to_prev
+        self.bo = alloc(eng.boundary_bytes)
+        self.bi = alloc(eng.boundary_bytes)
+
+
+class LocalTransport:
+    """All stripes live in this process (ring order = list order)."""
+
+    def __init__(self, engines: list, alloc):
+        self.engines = engines
+        self.bufs = [_Buffers(e, alloc) for e in engines]
+
+    def halos(self):
+        n = len(self.engines)
+        for e, b in zip(self.engines, self.bufs):
+            e.pack(b.tp, b.tn)
+        for r, b in enumerate(self.bufs):
+            b.rp.copy_(self.bufs[(r - 1) % n].tn)
+            b.rn.copy_(self.bufs[(r + 1) % n].tp)
+        for e, b in zip(self.engines, self.bufs):
+            e.unpack(b.rp, b.rn)
+
+    def boundary(self):
+        n = len(self.engines)
+        for r, b in enumerate(self.bufs):
+            b.bi.copy_(self.bufs[(r - 1) % n].bo)
+        for e, b in zip(self.engines, self.bufs):
+            e.finish(b.bi)
+
+    def gather(self, parts: list[StripeMoments]) -> list[StripeMoments]:
+        return parts
+
+
+class DistTransport:
+    """One stripe per rank of the default torch.distributed group (ring by rank)."""
+
+    def __init__(self, engine, alloc):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.engines = [engine]
+        self.bufs = [_Buffers(engine, alloc)]
+        self.rank, self.size = dist.get_rank(), dist.get_world_size()
+        self.prev, self.next = (self.rank - 1) % self.size, (self.rank + 1) % self.size
+
+    def _shift(self, send, to, recv, frm):
+        d = self.dist
+        if to == self.rank:  # world size 1
+            recv.copy_(send)
+            return
+        ops = [d.P2POp(d.isend, send, to), d.P2POp(d.irecv, recv, frm)]
+        for req in d.batch_isend_irecv(ops):
+            req.wait()
+
+    def halos(self):
+        e, b = self.engines[0], self.bufs[0]
+        e.pack(b.tp, b.tn)
+        self._shift(b.tp, self.prev, b.rn, self.next)  # shift up
+        self._shift(b.tn, self.next, b.rp, self.prev)  # shift down
+        e.unpack(b.rp, b.rn)
+
+    def boundary(self):
+        e, b = self.engines[0], self.bufs[0]
+        self._shift(b.bo, self.next, b.bi, self.prev)
+        e.finish(b.bi)
+
+    def gather(self, parts: list[StripeMoments]) -> list[StripeMoments]:
+        import torch
+
+        mine = torch.from_numpy(parts[0].to_array())
+        dev = self.bufs[0].tp.device
+        mine = mine.to(dev)
+        out = [torch.empty_like(mine) for _ in range(self.size)]
+        self.dist.all_gather(out, mine)
+        return [StripeMoments.from_array(o.cpu().numpy()) for o in out]
+
+
+class StripeGroup:
+    """Drives stripe engines through the per-MCS protocol above."""
+
+    def __init__(self, transport, X: int, Y: int):
+        self.tr, self.X, self.Y = transport, X, Y
+
+    def step(self, prm: UpdateParams, n: int = 1) -> None:
+        for _ in range(n):
+            self.tr.halos()
+            for e, b in zip(self.tr.engines, self.tr.bufs):
+                e.mcs(prm, b.bo)
+            self.tr.boundary()
+
+    def measure(self) -> MeasurementRecord:
+        self.tr.halos()  # the curl check of each stripe's first row reads the row above
+        parts = self.tr.gather([e.measure_local() for e in self.tr.engines])
+        return combine(parts, self.X, self.Y)
+
+    @property
+    def t(self) -> int:
+        return self.tr.engines[0].t

@@ -1,0 +1,69 @@
+"""Row stripes on the GPU: several StripeEngines on one device, exchanging
+halos through the same protocol the multi-GPU path uses (LocalTransport),
+must reproduce the single periodic engine bit-exactly (planes, rng states,
+exact moments). This is the 1/2/4/8-GPU identity check run on one B200."""
+import numpy as np
+import pytest
+import torch
+
+import paper_1606_00310_b200 as octgpu
+from paper_1606_00310_b200.stripes import LocalTransport, StripeEngine, StripeGroup, stripe_bounds
+
+pytestmark = pytest.mark.gpu
+
+
+def _group(cfg, parts, seed, stream):
+    engines = []
+    for r in range(parts):
+        y0, y1 = stripe_bounds(cfg.Y, parts, r)
+        e = StripeEngine(cfg, y0, y1, seed)
+        e.set_stream(stream.cuda_stream)
+        engines.append(e)
+    alloc = lambda nb: torch.zeros(nb, dtype=torch.uint8, device="cuda")  # noqa: E731
+    return StripeGroup(LocalTransport(engines, alloc), cfg.X, cfg.Y), engines
+
+
+@pytest.mark.parametrize("X,Y,parts", [(1024, 128, 2), (1024, 130, 4), (2048, 96, 3), (256, 40, 2), (8192, 512, 8)])
+@pytest.mark.parametrize("pq", [(0.5, 0.0), (0.98, 0.02), (1.0, 0.0), (0.75, 0.5)])
+def test_stripes_match_single_engine(X, Y, parts, pq):
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        cfg = octgpu.LatticeConfig(X, Y)
+        prm = octgpu.UpdateParams.make(*pq)
+        grp, engines = _group(cfg, parts, 21, stream)
+        grp.step(prm, 7)
+        ref = octgpu.GpuEngine(cfg, 21)
+        ref.step(prm, 7)
+        torch.cuda.synchronize()
+        planes = np.concatenate([e.planes() for e in engines], axis=1)
+        states = np.concatenate([e.states() for e in engines], axis=0)
+        assert np.array_equal(planes, ref.planes())
+        assert np.array_equal(states, ref.streams().states)
+        rec, rref = grp.measure(), ref.measure()
+        assert rec.power_sums == rref.power_sums
+        assert rec.mean_h == rref.mean_h
+        assert abs(rec.W2 - rref.W2) <= 2 ** -50 * rref.W2
+
+
+def test_stripe_curl_violation_reported_globally():
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        X, Y = 1024, 64
+        cfg = octgpu.LatticeConfig(X, Y)
+        ref = octgpu.GpuEngine(cfg, 5)
+        ref.step(octgpu.UpdateParams.make(0.5, 0.0), 4)
+        planes, states = ref.planes(), ref.streams().states
+        planes[0, 40, 3] ^= np.uint64(1 << 9)  # corrupt a row owned by the second stripe
+        engines = []
+        for r in range(2):
+            y0, y1 = stripe_bounds(Y, 2, r)
+            e = StripeEngine(cfg, y0, y1, 5, planes=planes[:, y0:y1], states=states[y0:y1], t=4)
+            e.set_stream(stream.cuda_stream)
+            engines.append(e)
+        grp = StripeGroup(LocalTransport(engines, lambda nb: torch.zeros(nb, dtype=torch.uint8, device="cuda")), X, Y)
+        bad = octgpu.GpuEngine(octgpu.SlopeField(cfg, planes, 4, 0), octgpu.RngStreamSet(5, states))
+        with pytest.raises(octgpu.InvariantError) as e1:
+            bad.measure()
+        with pytest.raises(octgpu.InvariantError) as e2:
+            grp.measure()
+        assert str(e1.value) == str(e2.value)

@@ -98,6 +98,15 @@ class ClockSampler:
                 "samples": len(s)}
 
 
+def _traffic(config: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per k_mcs_bulk launch from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f)["k_mcs_bulk"][config]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -144,7 +153,7 @@ def main():
 
     config_key = {"workload": cfg["workload"], "X": cfg["X"], "Y": cfg["Y"], "p": cfg["p"], "q": cfg["q"],
                   "w": 64, "seed": 1, "schedule": f"log_schedule({SCHEDULE_TMAX},{SCHEDULE_PPD}) within steps",
-                  "l2": "planes (>=1 GiB) exceed L2 (126 MB); no flush needed", "parallelism": f"rows/{ws}"}
+                  "l2": "planes (>=1 GiB) exceed L2 (126 MB); no flush needed", "parallelism": f"row stripes x{ws}" if ws > 1 else "single GPU"}
 
     if args.impl == "reference":
         if rank != 0:
@@ -178,27 +187,44 @@ def main():
     lat = octgpu.LatticeConfig(X, Y, 64)
     prm = octgpu.UpdateParams.make(cfg["p"], cfg["q"])
     sched = [t for t in octgpu.log_schedule(SCHEDULE_TMAX, SCHEDULE_PPD) if t <= K]
+    targets = sched + ([K] if not sched or sched[-1] != K else [])
 
     def barrier():
         if ws > 1:
             torch.distributed.barrier()
 
+    def make(planes=None, states=None):
+        """The job's engine: one GpuEngine, or this rank's row stripe (NCCL halo exchange)."""
+        if ws == 1:
+            if planes is None:
+                eng = octgpu.GpuEngine(lat, 1, device=local)
+            else:
+                eng = octgpu.GpuEngine(octgpu.SlopeField(lat, planes), octgpu.RngStreamSet(1, states), device=local)
+            eng.set_stream(stream.cuda_stream)
+            return eng, [eng]
+        from paper_1606_00310_b200.stripes import DistTransport, StripeEngine, StripeGroup, stripe_bounds
+        y0, y1 = stripe_bounds(Y, ws, rank)
+        e = StripeEngine(lat, y0, y1, 1, device=local,
+                         planes=None if planes is None else planes[:, y0:y1],
+                         states=None if states is None else states[y0:y1])
+        e.set_stream(stream.cuda_stream)
+        alloc = lambda nb: torch.zeros(nb, dtype=torch.uint8, device=dev)  # noqa: E731
+        return StripeGroup(DistTransport(e, alloc), X, Y), [e]
+
     # ---- warm-up (separate engine; the timed run starts from the flat state) ----
-    eng = octgpu.GpuEngine(lat, 1, device=local)
-    eng.set_stream(stream.cuda_stream)
-    eng.step(prm, W)
-    eng.measure()
-    eng.sync()
-    eng.close()
+    job, engs = make()
+    job.step(prm, W)
+    job.measure()
+    torch.cuda.synchronize()
+    del job, engs
     torch.cuda.synchronize()
 
     # ---- timed region, device-resident ----
-    eng = octgpu.GpuEngine(lat, 1, device=local)
-    eng.set_stream(stream.cuda_stream)
+    job, engs = make()
     torch.cuda.synchronize()
     seg_events = []
     records = []
-    launches0 = eng.launches
+    launches0 = sum(e.launches for e in engs)
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -206,75 +232,75 @@ def main():
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         t = 0
-        for target in sched + ([K] if not sched or sched[-1] != K else []):
+        for target in targets:
             if target > t:
                 a = torch.cuda.Event(enable_timing=True)
                 b = torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-                eng.step(prm, target - t)
+                job.step(prm, target - t)
                 b.record(stream)
                 seg_events.append((a, b))
                 t = target
             if target in sched:
-                records.append(eng.measure())
+                records.append(job.measure())
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
     ms = ev0.elapsed_time(ev1)
     step_ms = sum(a.elapsed_time(b) for a, b in seg_events)
-    launches = eng.launches - launches0
+    launches = sum(e.launches for e in engs) - launches0
     if ws > 1:
-        tt = torch.tensor([ms, step_ms], device=dev)
+        tt = torch.tensor([ms, step_ms, float(launches)], device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         ms, step_ms = float(tt[0]), float(tt[1])
-    value = ws * X * Y * K / (ms * 1e6)
+        lt = torch.tensor([launches], device=dev)
+        torch.distributed.all_reduce(lt)
+        launches = int(lt[0])
+    value = X * Y * K / (ms * 1e6)
     kernel_ms = step_ms / K
     peak, peak_src = _peaks()
-    alg_bytes = X * Y  # paper identity: 1 byte of slope traffic per site update
+    alg_bytes = X * Y // ws  # paper identity: 1 byte of slope traffic per site update, per GPU
     achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
-    final_checksum = eng.checksum() if X * Y <= (1 << 32) else None
-    eng.close()
+    final_checksum = engs[0].checksum() if ws == 1 and X * Y <= (1 << 32) else None
+    del job, engs
 
     # ---- e2e through the C-ABI with host buffers ----
     e2e = None
     if not args.no_e2e:
         flat = octgpu.new_flat(lat)
+        states0 = octgpu.RngStreamSet.derive(1, Y).states
         host_planes = torch.from_numpy(flat.planes.view(np.int64)).pin_memory()
-        host_states = torch.from_numpy(octgpu.RngStreamSet.derive(1, Y).states.view(np.int64)).pin_memory()
-        out_planes = torch.empty_like(host_planes).pin_memory()
-        out_states = torch.empty_like(host_states).pin_memory()
+        host_states = torch.from_numpy(states0.view(np.int64)).pin_memory()
         import ctypes as C
-        L = octgpu._lib.lib()
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        h = C.c_void_p()
-        octgpu._lib.check(L.octgpu_create_from(X, Y, 64, 0, 0, C.c_void_p(host_planes.data_ptr()),
-                                               C.c_void_p(host_states.data_ptr()), Y, 1, local, C.byref(h)))
-        cp = prm.to_c()
-        m = octgpu._lib.OctMoments()
+        hp = host_planes.numpy().view(np.uint64)
+        hs = host_states.numpy().view(np.uint64)
+        job, engs = make(hp, hs)
         t = 0
         n_meas = 0
-        for target in sched + ([K] if not sched or sched[-1] != K else []):
+        for target in targets:
             if target > t:
-                octgpu._lib.check(L.octgpu_step(h, C.byref(cp), target - t))
+                job.step(prm, target - t)
                 t = target
             if target in sched:
-                octgpu._lib.check(L.octgpu_measure(h, C.byref(m)))
+                job.measure()
                 n_meas += 1
-        octgpu._lib.check(L.octgpu_get_planes(h, C.c_void_p(out_planes.data_ptr())))
-        octgpu._lib.check(L.octgpu_get_states(h, C.c_void_p(out_states.data_ptr())))
+        out_planes = engs[0].planes()
+        out_states = engs[0].states() if ws > 1 else engs[0].streams().states
         el = time.perf_counter() - t0
-        L.octgpu_destroy(h)
+        del job, engs
         if ws > 1:
             tt = torch.tensor([el], device=dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             el = float(tt[0])
-        e2e = {"value": ws * X * Y * K / (el * 1e9), "unit": "updates/ns",
-               "h2d_bytes_per_step": (host_planes.numel() * 8 + host_states.numel() * 8) / K,
-               "d2h_bytes_per_step": (out_planes.numel() * 8 + out_states.numel() * 8
+        e2e = {"value": X * Y * K / (el * 1e9), "unit": "updates/ns",
+               "h2d_bytes_per_step": (hp.nbytes + hs.nbytes) / K,
+               "d2h_bytes_per_step": (ws * (out_planes.nbytes + out_states.nbytes)
                                       + n_meas * C.sizeof(octgpu._lib.OctMoments)) / K,
-               "wall_s": el, "note": "create_from(host planes+states) + K MCS + measurements + planes/states D2H"}
+               "wall_s": el,
+               "note": "engine created from pinned host planes+states, K MCS + measurements, planes/states D2H"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -290,11 +316,13 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "updates/ns", "n_gpus": ws, "steps": K, "warmup": W,
-            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u64", "data": "synthetic (flat start h=(x+y) mod 2, seed 1)", "config": config_key,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "kernel": "k_mcs (fused even+odd MCS)",
-                         "alg_bytes_per_launch": alg_bytes, "kernel_ms": kernel_ms, "peak_source": peak_src},
+                         "traffic": _traffic(args.config), "kernel": "k_mcs_bulk (fused even+odd MCS, per GPU)",
+                         "alg_bytes_per_launch": alg_bytes, "kernel_ms": kernel_ms, "peak_source": peak_src,
+                         "note": "alg bytes = 1 B/site-update (2 slope bits x 2 reads + 2 writes per MCS); "
+                                 "the fused kernel moves ~0.5 B/update, so frac can exceed 1"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
             "measurements": len(records),
             "W2_last": records[-1].W2 if records else None,

@@ -109,6 +109,63 @@ __device__ __forceinline__ void gen_xi(Xo& s, const ProbDev& p, const ProbDev& q
     }
 }
 
+// Two independent streams at once (the fused MCS kernel's first-sweep stream
+// for word k and second-sweep stream for word k-1): the same draws in the
+// same per-stream order, interleaved draw by draw for instruction-level
+// parallelism (each xoshiro step is a serial dependency chain).
+template <int MODE, typename Word>
+__device__ __forceinline__ void xi_word_pair(Xo& a, Xo& b, const ProbDev& pd, Word& wa, Word& wb) {
+    constexpr int W = int(sizeof(Word) * 8);
+    if constexpr (MODE == M_ZERO) {
+        wa = wb = Word(0);
+    } else if constexpr (MODE == M_HALF) {
+        wa = Word(xo_next(a));
+        wb = Word(xo_next(b));
+    } else if constexpr (MODE == M_DYADIC) {
+        Word ra = Word(xo_next(a)), rb = Word(xo_next(b));
+        for (uint32_t i = 1; i < pd.k; ++i) {
+            const Word xa = Word(xo_next(a)), xb = Word(xo_next(b));
+            const bool orop = (pd.m >> i) & 1;
+            ra = orop ? Word(ra | xa) : Word(ra & xa);
+            rb = orop ? Word(rb | xb) : Word(rb & xb);
+        }
+        wa = ra;
+        wb = rb;
+    } else if constexpr (MODE == M_ARB) {
+        Word ra = 0, rb = 0;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            ra |= Word(xo_next(a) < pd.T) << i;
+            rb |= Word(xo_next(b) < pd.T) << i;
+        }
+        wa = ra;
+        wb = rb;
+    } else {  // M_ONE
+#pragma unroll 8
+        for (int i = 0; i < W; ++i) {
+            xo_step(a);
+            xo_step(b);
+        }
+        wa = wb = Word(~Word(0));
+    }
+}
+
+template <int PM, int QM, typename Word>
+__device__ __forceinline__ void gen_xi_pair(Xo& a, Xo& b, const ProbDev& p, const ProbDev& q, Word& ap, Word& aq,
+                                            Word& bp, Word& bq) {
+    if constexpr (Plan<PM, QM>::live) {
+        xi_word_pair<PM, Word>(a, b, p, ap, bp);
+        if constexpr (QM == M_ZERO) {
+            aq = bq = Word(0);
+        } else {
+            xi_word_pair<QM, Word>(a, b, q, aq, bq);
+        }
+    } else {
+        ap = bp = (PM == M_ONE) ? Word(~Word(0)) : Word(0);
+        aq = bq = (QM == M_ONE) ? Word(~Word(0)) : Word(0);
+    }
+}
+
 // engine_vec.hpp:25-30
 template <typename Word>
 __device__ __forceinline__ Word update_mask(Word sxm, Word sym, Word sxp, Word syp, Word xp, Word xq) {

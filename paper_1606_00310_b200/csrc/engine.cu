@@ -326,6 +326,7 @@ struct octgpu_engine {
     // fused-MCS implementation: 2 = bulk-copy staged (k_mcs_bulk), 1 = register-prefetch (k_mcs)
     int mcs_impl = 2;
     int bulk_ks = 4, bulk_S = 3;
+    int bulk_key = -1;  // (p, q) mode pair the bulk plan was made for
     // Row-stripe mode (multi-GPU): this engine owns global rows [y0, y0 + L) of
     // a Ytot-row periodic lattice, held at local rows 1..L with one halo row
     // above (0), two below (L+1, L+2) and padding; Y is then the allocated row
@@ -394,33 +395,50 @@ int upload_states(octgpu_engine* e, const uint64_t* aos) {
     return OCTGPU_OK;
 }
 
-// Pick the fused-MCS variant and its pipeline depth so that all warps fit
-// in one wave (shared memory per SM is the limiting resource for k_mcs_bulk).
+// Pick the fused-MCS variant. For k_mcs_bulk the pipeline depth (KS words per
+// stage, S stages) is sized per (p, q) mode pair at the first step: every warp
+// owns a 30-row group for the whole kernel, so the blocks should run in equal
+// rounds. Resident blocks per SM are limited by registers (queried from the
+// occupancy calculator) and by the shared memory we give each block; we give
+// each block the largest pipeline that still lets ceil(blocks / (SMs * rounds))
+// blocks share an SM, with rounds the minimum the register limit allows.
 int plan_mcs(octgpu_engine* e) {
     e->mcs_impl = (e->w == 64 && e->n >= 8 && (e->stripe || e->Y >= 64)) ? 2 : 1;
     if (const char* v = getenv("OCTGPU_MCS_IMPL")) e->mcs_impl = (atoi(v) == 1) ? 1 : e->mcs_impl;
-    if (e->mcs_impl != 2) return OCTGPU_OK;
+    return OCTGPU_OK;
+}
+
+int plan_bulk(octgpu_engine* e, const ProbDev& p, const ProbDev& q) {
+    const int key = p.mode * 8 + q.mode;
+    if (e->bulk_key == key) return OCTGPU_OK;
     int sms = 0, smem_sm = 0, smem_blk = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
     CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, e->device));
     CK(cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
-    const uint64_t warps = (e->core_rows() + 29) / 30, blocks = (warps + 3) / 4;
-    const uint64_t bps = (blocks + sms - 1) / sms;  // blocks per SM for a single wave
-    const int64_t budget = std::min<int64_t>(smem_blk, int64_t(smem_sm) / int64_t(bps) - 1024);
-    e->bulk_ks = 2;
-    e->bulk_S = 2;
-    bool found = false;
+    const int64_t warps = (e->core_rows() + 29) / 30, blocks = (warps + 3) / 4;
+    int best_ks = 2, best_S = 2;
+    int64_t best_score = -1;
     for (int ks : {4, 2}) {
-        for (int S = 6; S >= 2 && !found; --S)
-            if (int64_t(8 * 8 * 4 + 4 * S * mcs_bulk_stage_bytes(ks)) <= budget) {
-                e->bulk_ks = ks;
-                e->bulk_S = S;
-                found = true;
+        const int reg_blocks = std::max(1, mcs_bulk_occupancy(p, q, ks, mcs_bulk_smem(ks, 2)));
+        const int64_t rounds = (blocks + int64_t(sms) * reg_blocks - 1) / (int64_t(sms) * reg_blocks);
+        const int64_t bps = (blocks + int64_t(sms) * rounds - 1) / (int64_t(sms) * rounds);
+        const int64_t budget = std::min<int64_t>(smem_blk, int64_t(smem_sm) / bps - 1024);
+        for (int S = 6; S >= 2; --S) {
+            if (int64_t(mcs_bulk_smem(ks, S)) > budget) continue;
+            const int64_t score = int64_t(S - 1) * ks * 1000 / rounds;  // words in flight per round
+            if (score > best_score) {
+                best_score = score;
+                best_ks = ks;
+                best_S = S;
             }
-        if (found) break;
+            break;
+        }
     }
+    e->bulk_ks = best_ks;
+    e->bulk_S = best_S;
     if (const char* v = getenv("OCTGPU_MCS_KS")) e->bulk_ks = atoi(v) == 2 ? 2 : 4;
     if (const char* v = getenv("OCTGPU_MCS_S")) e->bulk_S = std::max(2, std::min(8, atoi(v)));
+    e->bulk_key = key;
     return OCTGPU_OK;
 }
 
@@ -702,9 +720,12 @@ int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
     const Geom g = e->geom();
     for (uint64_t i = 0; i < n_mcs; ++i) {
         const int ps = e->pcur, rs = e->rcur;
-        if (e->mcs_impl == 2)
+        if (e->mcs_impl == 2) {
+            rc = plan_bulk(e, p, q);
+            if (rc) return rc;
             CK(launch_mcs_bulk(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
                                e->bulk_ks, e->bulk_S, e->stream));
+        }
         else
             CK(launch_mcs(e->w, e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q,
                           live, jtab, e->stream));
@@ -965,10 +986,12 @@ int octgpu_stripe_mcs(octgpu_engine* e, const octgpu_params* prm, void* boundary
     }
     const Geom g = e->geom();
     const int ps = e->pcur, rs = e->rcur;
-    if (e->mcs_impl == 2)
+    if (e->mcs_impl == 2) {
+        rc = plan_bulk(e, p, q);
+        if (rc) return rc;
         CK(launch_mcs_bulk(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
                            e->bulk_ks, e->bulk_S, e->stream));
-    else
+    } else
         CK(launch_mcs(e->w, e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, live,
                       jtab, e->stream));
     // Y(f) of halo row L+1 is final here (first sweep of row L+1, second of row L): the next rank's row 1

@@ -209,10 +209,14 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
             const Word B = sb[LY::kYf + jj * kWin + lane];
             const Word Cn = sb[LY::kYs + jj * kWin + lane + 1];
             const Word nxt = sb[LY::kXs + (jj + 1) * kWin + lane];
+            // ---- xi for first sweep word k and (k >= 2) second sweep word k-1, interleaved ----
+            Word x1p, x1q, x2p = 0, x2q = 0;
+            if (k >= 2)
+                gen_xi_pair<PM, QM, Word>(s1, s2, p, q, x1p, x1q, x2p, x2q);
+            else
+                gen_xi<PM, QM, Word>(s1, p, q, x1p, x1q);
             // ---- first sweep, word k ----
             const Word sxp = sh1 ? Word((cur >> 1) | (nxt << (W - 1))) : cur;
-            Word x1p, x1q;
-            gen_xi<PM, QM, Word>(s1, p, q, x1p, x1q);
             const Word m1 = update_mask<Word>(A, B, sxp, Cn, x1p, x1q);
             const Word Ap = A ^ m1, Bp = B ^ m1, Cp = Cn ^ m1;
             const Word sc1 = sh1 ? Word((m1 << 1) | carry1) : m1;
@@ -225,8 +229,6 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
                 if (k == 1) A1 = Ap;
                 if (k >= 2) {
                     const uint32_t j = k - 1;
-                    Word x2p, x2q;
-                    gen_xi<PM, QM, Word>(s2, p, q, x2p, x2q);
                     const Word m2 = second(j, pA, Ap, pB, pC, pR, x2p, x2q);
                     const Word xfj = pA ^ (sh2 ? Word(m2 << 1) : m2);
                     if (j == 1)
@@ -268,7 +270,7 @@ cudaError_t bulk_pq(const void* src, void* dst, const uint64_t* rs, uint64_t* rd
                     const ProbDev& q, const uint64_t* jtab, int ks, int S, cudaStream_t st) {
     const uint32_t warps = (g.c1 - g.c0 + 29) / 30;
     const uint32_t wpb = 4, threads = 32 * wpb, blocks = (warps + wpb - 1) / wpb;
-    const size_t smem = 8 * 8 * wpb + size_t(wpb) * S * mcs_bulk_stage_bytes(ks);
+    const size_t smem = mcs_bulk_smem(ks, S);
     cudaError_t e;
     if (ks == 4) {
         auto kern = k_mcs_bulk<PM, QM, 4>;
@@ -286,6 +288,24 @@ cudaError_t bulk_pq(const void* src, void* dst, const uint64_t* rs, uint64_t* rd
     return cudaGetLastError();
 }
 
+template <int PM, int QM>
+int occ_pq(int ks, size_t smem) {
+    int nb = 0;
+    cudaError_t e = ks == 4 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_mcs_bulk<PM, QM, 4>, 128, smem)
+                            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_mcs_bulk<PM, QM, 2>, 128, smem);
+    return e == cudaSuccess ? nb : 0;
+}
+
+#define OCT_OQ(PM)                                                \
+    switch (q.mode) {                                             \
+    case M_ZERO: return occ_pq<PM, M_ZERO>(ks, smem);             \
+    case M_HALF: return occ_pq<PM, M_HALF>(ks, smem);             \
+    case M_DYADIC: return occ_pq<PM, M_DYADIC>(ks, smem);         \
+    case M_ARB: return occ_pq<PM, M_ARB>(ks, smem);               \
+    case M_ONE: return occ_pq<PM, M_ONE>(ks, smem);               \
+    default: return 0;                                            \
+    }
+
 #define OCT_BQ(PM)                                                                              \
     switch (q.mode) {                                                                           \
     case M_ZERO: return bulk_pq<PM, M_ZERO>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, st);     \
@@ -297,6 +317,19 @@ cudaError_t bulk_pq(const void* src, void* dst, const uint64_t* rs, uint64_t* rd
     }
 
 }  // namespace
+
+int mcs_bulk_occupancy(const ProbDev& p, const ProbDev& q, int ks, size_t smem) {
+    switch (p.mode) {
+    case M_ZERO: OCT_OQ(M_ZERO)
+    case M_HALF: OCT_OQ(M_HALF)
+    case M_DYADIC: OCT_OQ(M_DYADIC)
+    case M_ARB: OCT_OQ(M_ARB)
+    case M_ONE: OCT_OQ(M_ONE)
+    default: return 0;
+    }
+}
+
+size_t mcs_bulk_smem(int ks, int S) { return 8 * 8 * 4 + size_t(4) * S * mcs_bulk_stage_bytes(ks); }
 
 cudaError_t launch_mcs_bulk(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g,
                             const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int ks, int S,

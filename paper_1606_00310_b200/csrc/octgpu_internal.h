@@ -65,6 +65,9 @@ cudaError_t launch_mcs_bulk(const void* src, void* dst, const uint64_t* rng_src,
                             const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int ks, int S,
                             cudaStream_t st);
 size_t mcs_bulk_stage_bytes(int ks);
+size_t mcs_bulk_smem(int ks, int S);  // dynamic smem of a 4-warp block
+// resident 4-warp blocks per SM of k_mcs_bulk<p, q, ks> with `smem` bytes of dynamic smem
+int mcs_bulk_occupancy(const ProbDev& p, const ProbDev& q, int ks, size_t smem);
 
 // s <- M s for every row state, M given as a 4-bit table (64 x 16 x 4 u64).
 cudaError_t launch_apply_jump(uint64_t* rng, uint32_t Y, const uint64_t* tab, cudaStream_t st);

@@ -89,6 +89,11 @@ int octgpu_stream_states(uint64_t master_seed, uint32_t n, uint64_t* out);
 /* log_schedule (measure.cpp:143-165); returns the number of points, writes up to cap */
 uint32_t octgpu_log_schedule(uint64_t t_max, uint32_t points_per_decade, uint64_t* out, uint32_t cap);
 
+/* height_moments (measure.cpp:24-51) over a host HeightMap (row-major int32),
+ * restated with the reference's sequential double accumulation so results are
+ * bit-identical: out = {mean, m2, m3, m4, skew, kurt}. */
+void octgpu_height_moments(uint32_t X, uint32_t Y, const int32_t* h, double* out6);
+
 /* ---- engine lifecycle ---- */
 
 /* VecEngine(LatticeConfig{X,Y,w}, seed, workers) (engine_vec.hpp:187-189):

@@ -81,7 +81,7 @@ EXPORTS = (
     "octgpu_get_planes", "octgpu_get_states", "octgpu_field_checksum", "octgpu_measure", "octgpu_heights",
     "octgpu_last_error", "octgpu_version", "octgpu_launch_count", "octgpu_create_stripe", "octgpu_stripe_sizes",
     "octgpu_halo_pack", "octgpu_halo_unpack", "octgpu_stripe_mcs", "octgpu_stripe_finish", "octgpu_measure_stripe",
-    "octgpu_stripe_y0", "octgpu_stripe_rows",
+    "octgpu_stripe_y0", "octgpu_stripe_rows", "octgpu_height_moments",
 )
 
 _lib = None
@@ -131,6 +131,7 @@ def lib() -> C.CDLL:
         "octgpu_measure_stripe": (i32, [vp, P(OctStripeMoments)]),
         "octgpu_stripe_y0": (u32, [vp]),
         "octgpu_stripe_rows": (u32, [vp]),
+        "octgpu_height_moments": (None, [u32, u32, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -133,7 +133,7 @@ __device__ __forceinline__ void xi_word_pair(Xo& a, Xo& b, const ProbDev& pd, Wo
         wb = rb;
     } else if constexpr (MODE == M_ARB) {
         Word ra = 0, rb = 0;
-#pragma unroll
+#pragma unroll 16
         for (int i = 0; i < W; ++i) {
             ra |= Word(xo_next(a) < pd.T) << i;
             rb |= Word(xo_next(b) < pd.T) << i;

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <limits>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -480,6 +481,37 @@ int octgpu_resolve(double r, int forced_mode, octgpu_prob* out) {
 uint32_t octgpu_draws_per_word(const octgpu_prob* p, uint32_t w) { return p ? draws(*p, w) : 0; }
 
 int octgpu_validate_lattice(uint32_t X, uint32_t Y, uint32_t w) { return validate(X, Y, w); }
+
+void octgpu_height_moments(uint32_t X, uint32_t Y, const int32_t* h, double* out) {
+    // measure.cpp:24-51, same operation order (compiled with -ffp-contract=off)
+    const size_t N = size_t(X) * Y;
+    double mean = 0.0, m2 = 0.0, m3 = 0.0, m4 = 0.0, skew, kurt;
+    if (N == 0) {
+        for (int i = 0; i < 6; ++i) out[i] = 0.0;
+        return;
+    }
+    const double n = double(N);
+    for (size_t i = 0; i < N; ++i) mean += h[i];
+    mean /= n;
+    for (size_t i = 0; i < N; ++i) {
+        const double d = h[i] - mean;
+        const double d2 = d * d;
+        m2 += d2;
+        m3 += d2 * d;
+        m4 += d2 * d2;
+    }
+    m2 /= n;
+    m3 /= n;
+    m4 /= n;
+    if (m2 > 0.0) {
+        skew = m3 / std::pow(m2, 1.5);
+        kurt = m4 / (m2 * m2) - 3.0;
+    } else {
+        skew = std::numeric_limits<double>::quiet_NaN();
+        kurt = std::numeric_limits<double>::quiet_NaN();
+    }
+    out[0] = mean; out[1] = m2; out[2] = m3; out[3] = m4; out[4] = skew; out[5] = kurt;
+}
 
 int octgpu_stream_states(uint64_t master_seed, uint32_t n, uint64_t* out) {
     if (n < 1) return fail(OCTGPU_ERR_CONFIG, "stream count must be >= 1");

@@ -31,7 +31,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+    // relaxed: the default .release would fence (MEMBAR.ALL.CTA) every outstanding global store
+    asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
                  : "memory");
 }
 
@@ -136,11 +138,10 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
         const uint32_t kb = b * KS;
         const uint32_t nw = min(uint32_t(KS), n - kb);
         const uint32_t ncopy = 4 * nw + 1;
+        // The stage's previous contents were consumed (loaded and used) before this
+        // refill, so no generic->async proxy fence is needed for the overwrite.
         __syncwarp();
-        if (lane == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_expect_tx(&bars[st], ncopy * kWin * 8);
-        }
+        if (lane == 0) mbar_expect_tx(&bars[st], ncopy * kWin * 8);
         __syncwarp();
         const uint32_t jobs = ncopy * (rows2 ? 2u : 1u);
         for (uint32_t c = lane; c < jobs; c += 32) {
@@ -201,7 +202,9 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
         const Word* sb = ring + size_t(st) * LY::kWords;
         const uint32_t kb = b * KS;
         if (b == 0) cur = sb[LY::kXs + lane];  // X(s)[y][0], original
-#pragma unroll
+        // arbitrary-probability bodies are ~10^4 instructions per word: keep them rolled (I-cache)
+        constexpr int kUnroll = (PM == M_ARB || QM == M_ARB) ? 1 : KS;
+#pragma unroll kUnroll
         for (int jj = 0; jj < KS; ++jj) {
             const uint32_t k = kb + jj;
             if (k >= n) break;

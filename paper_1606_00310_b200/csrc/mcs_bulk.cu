@@ -1,14 +1,15 @@
-// Fused MCS kernel, v2: row windows staged in shared memory by the Tensor
-// Memory Accelerator's bulk-copy engine (cp.async.bulk, SASS UBLKCP) behind
-// per-warp mbarrier rings.
+// Fused MCS kernel, v2: row windows staged in shared memory by asynchronous
+// per-lane copies (cp.async, SASS LDGSTS) behind per-warp mbarrier rings.
+// (A cp.async.bulk variant was measured first: its uniform-register operands
+// made 17 lanes' copies a serial ELECT/R2UR loop, 31% of all stall samples.)
 //
 // Same algorithm and bit-exact results as k_mcs in kernels.cu (sweep f, then
 // sweep f^1, src -> dst), but
 //  * no prefetch registers: each warp keeps S stages x KS words of its four
 //    34-row plane windows in flight in shared memory, so the memory-level
 //    parallelism no longer competes with the single-wave register budget;
-//  * lane -> row mapping r0 = 30*warp, lane L = row r0 + L (core lanes 1..30),
-//    so every window starts at an even row: 16-byte aligned for the copies;
+//  * lane -> row mapping r0 = 30*warp, lane L = row r0 + L (core lanes 1..30);
+//    each lane stages its own row's words, so the y-wrap needs no special case;
 //  * stores are predicated in PTX (no divergent branches).
 // Used for w = 64, n >= 8, Y >= 64; smaller lattices take k_mcs.
 #include <cstdint>
@@ -20,7 +21,7 @@ namespace octgpu {
 
 namespace {
 
-constexpr int kWin = 34;  // rows per window: lanes 0..31 plus Y(s)[y+1] of lane 31, rounded to 16 B
+constexpr int kWin = 32;  // one slot per lane (each lane stages its own rows)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -28,13 +29,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    // relaxed: the default .release would fence (MEMBAR.ALL.CTA) every outstanding global store
-    asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -49,12 +43,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
+// Per-lane asynchronous 8-byte global->shared copy (SASS LDGSTS): one SIMT
+// instruction moves one word of 32 rows (256 B, coalesced) without staging
+// through registers.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// Arrive on `bar` once this thread's prior cp.async copies have landed.
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void st_pred(uint64_t* p, uint64_t v, bool pred) {
@@ -120,51 +118,43 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
     const bool sh1 = ((uint32_t(f) ^ y ^ g.ypar) & 1u) != 0;
     const bool sh2 = !sh1;
 
-    // window split for the periodic wrap in y (last warp only)
-    const uint32_t pr0 = g.wrap ? r0 % g.wrap : r0;  // physical window start
-    const uint32_t rows1 = g.wrap ? min(uint32_t(kWin), g.wrap - pr0) : uint32_t(kWin);
-    const uint32_t rows2 = kWin - rows1;
+    const uint32_t y1 = g.wrap ? (v + 1) % g.wrap : v + 1;
 
     if (lane == 0) {
-        for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
+        for (int i = 0; i < S; ++i) mbar_init(&bars[i], 32);  // one cp.async arrival per lane per fill
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
 
-    // Issue the copies of word-block b into its stage (warp-collective).
+    // Copy word-block b into its stage: every lane stages its own row's words
+    // (and row y+1's word of Y(s)); completion is an mbarrier phase.
+    const Word* gXf = planeXf + y;
+    const Word* gYf = planeYf + y;
+    const Word* gYs = planeYs + y1;
+    const Word* gXs = planeXs + y;
     auto fill = [&](uint32_t b) {
         const int st = int(b % uint32_t(S));
-        Word* base = ring + size_t(st) * LY::kWords;
+        Word* base = ring + size_t(st) * LY::kWords + lane;
         const uint32_t kb = b * KS;
         const uint32_t nw = min(uint32_t(KS), n - kb);
-        const uint32_t ncopy = 4 * nw + 1;
-        // The stage's previous contents were consumed (loaded and used) before this
-        // refill, so no generic->async proxy fence is needed for the overwrite.
-        __syncwarp();
-        if (lane == 0) mbar_expect_tx(&bars[st], ncopy * kWin * 8);
-        __syncwarp();
-        const uint32_t jobs = ncopy * (rows2 ? 2u : 1u);
-        for (uint32_t c = lane; c < jobs; c += 32) {
-            const uint32_t cp = rows2 ? (c >> 1) : c;
-            const uint32_t part = rows2 ? (c & 1) : 0;
-            const Word* gplane;
-            uint32_t word, slot;
-            if (cp < 3 * nw) {
-                const uint32_t pl = cp / nw, j = cp % nw;
-                gplane = pl == 0 ? planeXf : (pl == 1 ? planeYf : planeYs);
-                word = kb + j;
-                slot = (pl == 0 ? LY::kXf : (pl == 1 ? LY::kYf : LY::kYs)) + j * kWin;
-            } else {
-                const uint32_t j = cp - 3 * nw;  // 0..nw (nw+1 words of X(s))
-                gplane = planeXs;
-                word = kb + j;
-                if (word >= n) word -= n;
-                slot = LY::kXs + j * kWin;
+#pragma unroll
+        for (int j = 0; j < KS; ++j) {
+            if (uint32_t(j) < nw) {
+                const uint32_t o = (kb + j) * Y;
+                cp_async8(base + LY::kXf + j * kWin, gXf + o);
+                cp_async8(base + LY::kYf + j * kWin, gYf + o);
+                cp_async8(base + LY::kYs + j * kWin, gYs + o);
             }
-            const Word* gsrc = gplane + size_t(word) * Y + (part ? 0 : pr0);
-            Word* sdst = base + slot + (part ? rows1 : 0);
-            bulk_g2s(sdst, gsrc, (part ? rows2 : rows1) * 8, &bars[st]);
         }
+#pragma unroll
+        for (int j = 0; j <= KS; ++j) {
+            if (uint32_t(j) <= nw) {
+                uint32_t w = kb + j;
+                if (w >= n) w -= n;
+                cp_async8(base + LY::kXs + j * kWin, gXs + w * Y);
+            }
+        }
+        cp_async_arrive(&bars[st]);
     };
 
     const uint32_t nblocks = (n + KS - 1) / KS;
@@ -189,7 +179,7 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
         const Word sxp2 = sh2 ? Word((Aj >> 1) | (Ajn << (W - 1))) : Aj;
         const Word m2 = update_mask<Word>(Rj, Cup, sxp2, Bdn, x2p, x2q);
         const Word mup = __shfl_up_sync(0xffffffffu, m2, 1);
-        const size_t o = size_t(j) * Y;
+        const uint32_t o = j * Y;  // < 2^32: n * Y words per plane
         st_pred(dXs + o, Rj ^ m2, core);
         st_pred(dYs + o, Cup ^ m2, core);
         st_pred(dYf + o, Bj ^ mup, wyf);
@@ -204,44 +194,69 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
         if (b == 0) cur = sb[LY::kXs + lane];  // X(s)[y][0], original
         // arbitrary-probability bodies are ~10^4 instructions per word: keep them rolled (I-cache)
         constexpr int kUnroll = (PM == M_ARB || QM == M_ARB) ? 1 : KS;
+        if (kb >= 3 && kb + KS <= n) {
+            // steady state: words k >= 3, second sweep of word k-1 >= 2, no special cases
 #pragma unroll kUnroll
-        for (int jj = 0; jj < KS; ++jj) {
-            const uint32_t k = kb + jj;
-            if (k >= n) break;
-            const Word A = sb[LY::kXf + jj * kWin + lane];
-            const Word B = sb[LY::kYf + jj * kWin + lane];
-            const Word Cn = sb[LY::kYs + jj * kWin + lane + 1];
-            const Word nxt = sb[LY::kXs + (jj + 1) * kWin + lane];
-            // ---- xi for first sweep word k and (k >= 2) second sweep word k-1, interleaved ----
-            Word x1p, x1q, x2p = 0, x2q = 0;
-            if (k >= 2)
+            for (int jj = 0; jj < KS; ++jj) {
+                const uint32_t k = kb + jj;
+                const Word A = sb[LY::kXf + jj * kWin + lane];
+                const Word B = sb[LY::kYf + jj * kWin + lane];
+                const Word Cn = sb[LY::kYs + jj * kWin + lane];
+                const Word nxt = sb[LY::kXs + (jj + 1) * kWin + lane];
+                Word x1p, x1q, x2p, x2q;
                 gen_xi_pair<PM, QM, Word>(s1, s2, p, q, x1p, x1q, x2p, x2q);
-            else
-                gen_xi<PM, QM, Word>(s1, p, q, x1p, x1q);
-            // ---- first sweep, word k ----
-            const Word sxp = sh1 ? Word((cur >> 1) | (nxt << (W - 1))) : cur;
-            const Word m1 = update_mask<Word>(A, B, sxp, Cn, x1p, x1q);
-            const Word Ap = A ^ m1, Bp = B ^ m1, Cp = Cn ^ m1;
-            const Word sc1 = sh1 ? Word((m1 << 1) | carry1) : m1;
-            carry1 = Word(m1 >> (W - 1));
-            const Word Rp = cur ^ sc1;
-            cur = nxt;
-            if (k == 0) {
-                A0 = Ap; B0 = Bp; C0 = Cp; R0 = Rp;
-            } else {
-                if (k == 1) A1 = Ap;
-                if (k >= 2) {
-                    const uint32_t j = k - 1;
-                    const Word m2 = second(j, pA, Ap, pB, pC, pR, x2p, x2q);
-                    const Word xfj = pA ^ (sh2 ? Word(m2 << 1) : m2);
-                    if (j == 1)
-                        xf1 = xfj;
-                    else
-                        st_pred(dXf + size_t(j) * Y, xfj ^ (sh2 ? Word(m2last >> (W - 1)) : Word(0)), core);
-                    m2last = m2;
-                }
+                const Word sxp = sh1 ? Word((cur >> 1) | (nxt << (W - 1))) : cur;
+                const Word m1 = update_mask<Word>(A, B, sxp, Cn, x1p, x1q);
+                const Word Ap = A ^ m1, Bp = B ^ m1, Cp = Cn ^ m1;
+                const Word sc1 = sh1 ? Word((m1 << 1) | carry1) : m1;
+                carry1 = Word(m1 >> (W - 1));
+                const Word Rp = cur ^ sc1;
+                cur = nxt;
+                const Word m2 = second(k - 1, pA, Ap, pB, pC, pR, x2p, x2q);
+                st_pred(dXf + (k - 1) * Y, pA ^ (sh2 ? Word((m2 << 1) | (m2last >> (W - 1))) : m2), core);
+                m2last = m2;
+                pA = Ap; pB = Bp; pC = Cp; pR = Rp;
             }
-            pA = Ap; pB = Bp; pC = Cp; pR = Rp;
+        } else {
+#pragma unroll kUnroll
+            for (int jj = 0; jj < KS; ++jj) {
+                const uint32_t k = kb + jj;
+                if (k >= n) break;
+                const Word A = sb[LY::kXf + jj * kWin + lane];
+                const Word B = sb[LY::kYf + jj * kWin + lane];
+                const Word Cn = sb[LY::kYs + jj * kWin + lane];
+                const Word nxt = sb[LY::kXs + (jj + 1) * kWin + lane];
+                // ---- xi for first sweep word k and (k >= 2) second sweep word k-1, interleaved ----
+                Word x1p, x1q, x2p = 0, x2q = 0;
+                if (k >= 2)
+                    gen_xi_pair<PM, QM, Word>(s1, s2, p, q, x1p, x1q, x2p, x2q);
+                else
+                    gen_xi<PM, QM, Word>(s1, p, q, x1p, x1q);
+                // ---- first sweep, word k ----
+                const Word sxp = sh1 ? Word((cur >> 1) | (nxt << (W - 1))) : cur;
+                const Word m1 = update_mask<Word>(A, B, sxp, Cn, x1p, x1q);
+                const Word Ap = A ^ m1, Bp = B ^ m1, Cp = Cn ^ m1;
+                const Word sc1 = sh1 ? Word((m1 << 1) | carry1) : m1;
+                carry1 = Word(m1 >> (W - 1));
+                const Word Rp = cur ^ sc1;
+                cur = nxt;
+                if (k == 0) {
+                    A0 = Ap; B0 = Bp; C0 = Cp; R0 = Rp;
+                } else {
+                    if (k == 1) A1 = Ap;
+                    if (k >= 2) {
+                        const uint32_t j = k - 1;
+                        const Word m2 = second(j, pA, Ap, pB, pC, pR, x2p, x2q);
+                        const Word xfj = pA ^ (sh2 ? Word(m2 << 1) : m2);
+                        if (j == 1)
+                            xf1 = xfj;
+                        else
+                            st_pred(dXf + j * Y, xfj ^ (sh2 ? Word(m2last >> (W - 1)) : Word(0)), core);
+                        m2last = m2;
+                    }
+                }
+                pA = Ap; pB = Bp; pC = Cp; pR = Rp;
+            }
         }
         if (b + S < nblocks) fill(b + S);
     }
@@ -252,7 +267,7 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
         gen_xi<PM, QM, Word>(s2, p, q, x2p, x2q);
         const Word m2 = second(j, pA, A0, pB, pC, pR, x2p, x2q);
         const Word xfj = pA ^ (sh2 ? Word(m2 << 1) : m2);
-        st_pred(dXf + size_t(j) * Y, xfj ^ (sh2 ? Word(m2last >> (W - 1)) : Word(0)), core);
+        st_pred(dXf + j * Y, xfj ^ (sh2 ? Word(m2last >> (W - 1)) : Word(0)), core);
         m2last = m2;
     }
     {

@@ -1,15 +1,17 @@
-// Fused MCS kernel, v2: row windows staged in shared memory by asynchronous
-// per-lane copies (cp.async, SASS LDGSTS) behind per-warp mbarrier rings.
-// (A cp.async.bulk variant was measured first: its uniform-register operands
-// made 17 lanes' copies a serial ELECT/R2UR loop, 31% of all stall samples.)
+// Fused MCS kernel, v2: row windows staged in shared memory by the bulk-copy
+// engine (cp.async.bulk, SASS UBLKCP) behind per-warp mbarrier rings.
+// Measured alternatives (profiles/): copies issued one per lane became a
+// compiler ELECT/R2UR waterfall loop (31% of stall samples); per-lane
+// cp.async (LDGSTS) saturated the MIO queue (mio_throttle 24%, 20% slower).
+// Here one lane issues all copies with warp-uniform operands.
 //
 // Same algorithm and bit-exact results as k_mcs in kernels.cu (sweep f, then
 // sweep f^1, src -> dst), but
 //  * no prefetch registers: each warp keeps S stages x KS words of its four
 //    34-row plane windows in flight in shared memory, so the memory-level
 //    parallelism no longer competes with the single-wave register budget;
-//  * lane -> row mapping r0 = 30*warp, lane L = row r0 + L (core lanes 1..30);
-//    each lane stages its own row's words, so the y-wrap needs no special case;
+//  * lane -> row mapping r0 = 30*warp, lane L = row r0 + L (core lanes 1..30),
+//    so every window starts at an even row: 16-byte aligned for the copies;
 //  * stores are predicated in PTX (no divergent branches).
 // Used for w = 64, n >= 8, Y >= 64; smaller lattices take k_mcs.
 #include <cstdint>
@@ -21,7 +23,7 @@ namespace octgpu {
 
 namespace {
 
-constexpr int kWin = 32;  // one slot per lane (each lane stages its own rows)
+constexpr int kWin = 34;  // rows per window: lanes 0..31 plus Y(s)[y+1] of lane 31, rounded to 16 B
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -43,16 +45,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-// Per-lane asynchronous 8-byte global->shared copy (SASS LDGSTS): one SIMT
-// instruction moves one word of 32 rows (256 B, coalesced) without staging
-// through registers.
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    // relaxed: the default .release would fence (MEMBAR.ALL.CTA) every outstanding global store
+    asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
 }
 
-// Arrive on `bar` once this thread's prior cp.async copies have landed.
-__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+// One bulk copy (SASS UBLKCP). Its operands live in uniform registers, so it
+// must be issued with warp-uniform operands (one lane, see fill()).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
 }
 
 __device__ __forceinline__ void st_pred(uint64_t* p, uint64_t v, bool pred) {
@@ -92,7 +99,9 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t Y = g.Y, n = g.n;
     const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;  // warp in block
+    // warp in block, through a shuffle so the compiler sees it as warp-uniform
+    // (the bulk-copy operands derived from it then stay in uniform registers)
+    const int wib = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0);
     const int wpb = blockDim.x >> 5;
     const uint32_t wid = blockIdx.x * wpb + wib;
     if (wid * 30u >= g.c1 - g.c0) return;  // warp-uniform
@@ -118,43 +127,44 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
     const bool sh1 = ((uint32_t(f) ^ y ^ g.ypar) & 1u) != 0;
     const bool sh2 = !sh1;
 
-    const uint32_t y1 = g.wrap ? (v + 1) % g.wrap : v + 1;
+    // window split for the periodic wrap in y (last warp only)
+    const uint32_t pr0 = g.wrap ? r0 % g.wrap : r0;  // physical window start
+    const uint32_t rows1 = g.wrap ? min(uint32_t(kWin), g.wrap - pr0) : uint32_t(kWin);
+    const uint32_t rows2 = kWin - rows1;
 
     if (lane == 0) {
-        for (int i = 0; i < S; ++i) mbar_init(&bars[i], 32);  // one cp.async arrival per lane per fill
+        for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
 
-    // Copy word-block b into its stage: every lane stages its own row's words
-    // (and row y+1's word of Y(s)); completion is an mbarrier phase.
-    const Word* gXf = planeXf + y;
-    const Word* gYf = planeYf + y;
-    const Word* gYs = planeYs + y1;
-    const Word* gXs = planeXs + y;
+    // Copies of word-block b into its stage: one lane issues 4*nw+1 window
+    // copies (two each for the wrapping last warp) with uniform operands.
+    auto copy_window = [&](Word* sdst, const Word* gplane, uint32_t word, uint64_t* bar) {
+        const Word* g0 = gplane + size_t(word) * Y;
+        bulk_g2s(sdst, g0 + pr0, rows1 * 8, bar);
+        if (rows2) bulk_g2s(sdst + rows1, g0, rows2 * 8, bar);
+    };
     auto fill = [&](uint32_t b) {
         const int st = int(b % uint32_t(S));
-        Word* base = ring + size_t(st) * LY::kWords + lane;
+        Word* base = ring + size_t(st) * LY::kWords;
         const uint32_t kb = b * KS;
         const uint32_t nw = min(uint32_t(KS), n - kb);
-#pragma unroll
-        for (int j = 0; j < KS; ++j) {
-            if (uint32_t(j) < nw) {
-                const uint32_t o = (kb + j) * Y;
-                cp_async8(base + LY::kXf + j * kWin, gXf + o);
-                cp_async8(base + LY::kYf + j * kWin, gYf + o);
-                cp_async8(base + LY::kYs + j * kWin, gYs + o);
+        // The stage's previous contents were consumed (loaded and used) before this
+        // refill, so no generic->async proxy fence is needed for the overwrite.
+        __syncwarp();
+        if (lane == 0) {
+            mbar_expect_tx(&bars[st], (4 * nw + 1) * kWin * 8);
+            for (uint32_t j = 0; j < nw; ++j) {
+                copy_window(base + LY::kXf + j * kWin, planeXf, kb + j, &bars[st]);
+                copy_window(base + LY::kYf + j * kWin, planeYf, kb + j, &bars[st]);
+                copy_window(base + LY::kYs + j * kWin, planeYs, kb + j, &bars[st]);
+            }
+            for (uint32_t j = 0; j <= nw; ++j) {
+                const uint32_t w = kb + j < n ? kb + j : kb + j - n;
+                copy_window(base + LY::kXs + j * kWin, planeXs, w, &bars[st]);
             }
         }
-#pragma unroll
-        for (int j = 0; j <= KS; ++j) {
-            if (uint32_t(j) <= nw) {
-                uint32_t w = kb + j;
-                if (w >= n) w -= n;
-                cp_async8(base + LY::kXs + j * kWin, gXs + w * Y);
-            }
-        }
-        cp_async_arrive(&bars[st]);
     };
 
     const uint32_t nblocks = (n + KS - 1) / KS;
@@ -201,7 +211,7 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
                 const uint32_t k = kb + jj;
                 const Word A = sb[LY::kXf + jj * kWin + lane];
                 const Word B = sb[LY::kYf + jj * kWin + lane];
-                const Word Cn = sb[LY::kYs + jj * kWin + lane];
+                const Word Cn = sb[LY::kYs + jj * kWin + lane + 1];
                 const Word nxt = sb[LY::kXs + (jj + 1) * kWin + lane];
                 Word x1p, x1q, x2p, x2q;
                 gen_xi_pair<PM, QM, Word>(s1, s2, p, q, x1p, x1q, x2p, x2q);
@@ -224,7 +234,7 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
                 if (k >= n) break;
                 const Word A = sb[LY::kXf + jj * kWin + lane];
                 const Word B = sb[LY::kYf + jj * kWin + lane];
-                const Word Cn = sb[LY::kYs + jj * kWin + lane];
+                const Word Cn = sb[LY::kYs + jj * kWin + lane + 1];
                 const Word nxt = sb[LY::kXs + (jj + 1) * kWin + lane];
                 // ---- xi for first sweep word k and (k >= 2) second sweep word k-1, interleaved ----
                 Word x1p, x1q, x2p = 0, x2q = 0;

@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "octgpu.h"
 #include "octgpu_internal.h"
 
@@ -328,6 +330,8 @@ struct octgpu_engine {
     int mcs_impl = 2;
     int bulk_ks = 4, bulk_S = 3;
     int bulk_key = -1;  // (p, q) mode pair the bulk plan was made for
+    CUtensorMap tm[2][2];  // [plane set][box: ks words, ks+1 words] for k_mcs_bulk
+    int tm_ks = -1;
     // Row-stripe mode (multi-GPU): this engine owns global rows [y0, y0 + L) of
     // a Ytot-row periodic lattice, held at local rows 1..L with one halo row
     // above (0), two below (L+1, L+2) and padding; Y is then the allocated row
@@ -336,10 +340,14 @@ struct octgpu_engine {
     uint32_t Ytot = 0, y0 = 0, L = 0;
 
     Geom geom() const {
-        return stripe ? Geom{Y, n, size_t(n) * Y, 1, L + 1, 0, (y0 + 1) & 1u}  // local row 0 = global y0 - 1
-                      : Geom{Y, n, size_t(n) * Y, 1, Y + 1, Y, 0};
+        return stripe ? Geom{Y, n, size_t(n) * Y, 1, L + 1, 0, (y0 + 1) & 1u, 0}  // local row 0 = global y0 - 1
+                      : Geom{Y, n, size_t(n) * Y, 1, L + 1, L, 0, kGhostRows};
     }
-    uint32_t core_rows() const { return stripe ? L : Y; }
+    uint32_t core_rows() const { return L; }
+    // rows of the reference-layout staging buffer: the lattice rows (periodic) or
+    // every allocated row (stripe; the host slices rows 1..L)
+    uint32_t host_rows() const { return stripe ? Y : L; }
+    size_t host_bytes() const { return 4 * size_t(n) * host_rows() * word_bytes(); }
     uint32_t first_row() const { return stripe ? 1 : 0; }  // local index of the first core row
     size_t word_bytes() const { return w / 8; }
     size_t set_bytes() const { return 4 * size_t(n) * Y * word_bytes(); }
@@ -392,6 +400,10 @@ int upload_states(octgpu_engine* e, const uint64_t* aos) {
     for (uint32_t y = 0; y < e->core_rows(); ++y)
         for (int j = 0; j < 4; ++j) soa[size_t(j) * e->Y + r0 + y] = aos[4 * size_t(y) + j];
     CK(cudaMemcpyAsync(e->rng[e->rcur], soa.data(), e->rng_bytes(), cudaMemcpyHostToDevice, e->stream));
+    if (!e->stripe) {
+        CK(launch_refresh_ghosts(e->w, e->planes[e->pcur], e->rng[e->rcur], e->geom(), e->stream));
+        ++e->launches;
+    }
     CK(cudaStreamSynchronize(e->stream));
     return OCTGPU_OK;
 }
@@ -404,8 +416,43 @@ int upload_states(octgpu_engine* e, const uint64_t* aos) {
 // each block the largest pipeline that still lets ceil(blocks / (SMs * rounds))
 // blocks share an SM, with rounds the minimum the register limit allows.
 int plan_mcs(octgpu_engine* e) {
-    e->mcs_impl = (e->w == 64 && e->n >= 8 && (e->stripe || e->Y >= 64)) ? 2 : 1;
+    e->mcs_impl = (e->w == 64 && e->n >= 8 && (e->stripe || e->L >= 64)) ? 2 : 1;
     if (const char* v = getenv("OCTGPU_MCS_IMPL")) e->mcs_impl = (atoi(v) == 1) ? 1 : e->mcs_impl;
+    return OCTGPU_OK;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+// 3-D view of a plane set: dim 0 = rows (contiguous, Y allocated rows), dim 1 =
+// words (stride Y*8 B), dim 2 = planes (stride n*Y*8 B); tiles of 34 rows x
+// (ks | ks+1) words x 1 plane, no swizzle, out-of-bounds words read as zero.
+int ensure_tmaps(octgpu_engine* e) {
+    if (e->tm_ks == e->bulk_ks) return OCTGPU_OK;
+    auto enc = tensor_map_encoder();
+    if (!enc) return fail(OCTGPU_ERR_CUDA, "cuTensorMapEncodeTiled is not available from the driver");
+    for (int b = 0; b < 2; ++b)
+        for (int v = 0; v < 2; ++v) {
+            const cuuint64_t dims[3] = {e->Y, e->n, 4};
+            const cuuint64_t strides[2] = {cuuint64_t(e->Y) * 8, cuuint64_t(e->n) * e->Y * 8};
+            const cuuint32_t box[3] = {kTmaBoxRows, cuuint32_t(e->bulk_ks + v), 1};
+            const cuuint32_t estr[3] = {1, 1, 1};
+            const CUresult r = enc(&e->tm[b][v], CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, e->planes[b], dims, strides, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return fail(OCTGPU_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+        }
+    e->tm_ks = e->bulk_ks;
     return OCTGPU_OK;
 }
 
@@ -440,7 +487,7 @@ int plan_bulk(octgpu_engine* e, const ProbDev& p, const ProbDev& q) {
     if (const char* v = getenv("OCTGPU_MCS_KS")) e->bulk_ks = atoi(v) == 2 ? 2 : 4;
     if (const char* v = getenv("OCTGPU_MCS_S")) e->bulk_S = std::max(2, std::min(8, atoi(v)));
     e->bulk_key = key;
-    return OCTGPU_OK;
+    return ensure_tmaps(e);
 }
 
 int alloc_engine(octgpu_engine* e) {
@@ -544,6 +591,8 @@ uint32_t octgpu_log_schedule(uint64_t t_max, uint32_t ppd, uint64_t* out, uint32
 
 namespace {
 
+int refresh_ghosts(octgpu_engine* e);
+
 // Allocates an engine over global rows [y0, y0 + L) of an X x Ytot lattice
 // (stripe) or the whole periodic lattice (!stripe).
 int make_engine(uint32_t X, uint32_t Ytot, uint32_t w, bool stripe, uint32_t y0, uint32_t L, int device,
@@ -553,7 +602,7 @@ int make_engine(uint32_t X, uint32_t Ytot, uint32_t w, bool stripe, uint32_t y0,
     e->Ytot = Ytot; e->stripe = stripe; e->y0 = stripe ? y0 : 0; e->L = stripe ? L : Ytot;
     // stripe: halo row 0, core 1..L, halos L+1, L+2, then >= 34 rows of padding so the
     // 34-row windows of k_mcs_bulk never leave the allocation; even for 16-B alignment
-    e->Y = stripe ? ((L + 3 + 36 + 1) & ~1u) : Ytot;
+    e->Y = stripe ? ((L + 3 + 36 + 1) & ~1u) : Ytot + kGhostRows;
     int rc = alloc_engine(e);
     if (rc) {
         std::string keep = g_err;
@@ -571,17 +620,19 @@ int load_planes(octgpu_engine* e, const void* planes) {
     if (rc) return rc;
     const size_t wb = e->word_bytes(), row_bytes = size_t(e->n) * wb;
     if (!e->stripe) {
-        CK(cudaMemcpyAsync(e->stage, planes, e->set_bytes(), cudaMemcpyHostToDevice, e->stream));
+        CK(cudaMemcpyAsync(e->stage, planes, e->host_bytes(), cudaMemcpyHostToDevice, e->stream));
     } else {
-        std::vector<unsigned char> pad(e->set_bytes(), 0);
+        std::vector<unsigned char> pad(e->host_bytes(), 0);
         for (int p = 0; p < 4; ++p)
             std::memcpy(pad.data() + (size_t(p) * e->Y + 1) * row_bytes,
                         static_cast<const unsigned char*>(planes) + size_t(p) * e->L * row_bytes, e->L * row_bytes);
-        CK(cudaMemcpyAsync(e->stage, pad.data(), e->set_bytes(), cudaMemcpyHostToDevice, e->stream));
+        CK(cudaMemcpyAsync(e->stage, pad.data(), e->host_bytes(), cudaMemcpyHostToDevice, e->stream));
         CK(cudaStreamSynchronize(e->stream));
     }
-    CK(launch_import(e->w, e->stage, e->planes[e->pcur], e->geom(), e->stream));
+    CK(launch_import(e->w, e->stage, e->planes[e->pcur], e->geom(), e->host_rows(), e->stream));
     ++e->launches;
+    rc = refresh_ghosts(e);
+    if (rc) return rc;
     CK(cudaStreamSynchronize(e->stream));
     return OCTGPU_OK;
 }
@@ -590,6 +641,15 @@ int flat_fill(octgpu_engine* e) {  // new_flat: odd planes all ones, even planes
     const size_t pb = e->set_bytes() / 4;
     char* base = static_cast<char*>(e->planes[e->pcur]);
     for (int p = 0; p < 4; ++p) CK(cudaMemsetAsync(base + p * pb, (p & 1) ? 0xff : 0x00, pb, e->stream));
+    return OCTGPU_OK;
+}
+
+// Rewrite the ghost rows of the current plane set and rng states (periodic
+// lattices; every operation except k_mcs_bulk leaves them stale).
+int refresh_ghosts(octgpu_engine* e) {
+    if (e->stripe) return OCTGPU_OK;
+    CK(launch_refresh_ghosts(e->w, e->planes[e->pcur], e->rng[e->rcur], e->geom(), e->stream));
+    ++e->launches;
     return OCTGPU_OK;
 }
 
@@ -756,7 +816,7 @@ int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
             rc = plan_bulk(e, p, q);
             if (rc) return rc;
             CK(launch_mcs_bulk(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
-                               e->bulk_ks, e->bulk_S, e->stream));
+                               e->bulk_ks, e->bulk_S, &e->tm[ps][0], &e->tm[ps][1], e->stream));
         }
         else
             CK(launch_mcs(e->w, e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q,
@@ -790,7 +850,7 @@ int octgpu_sweep(octgpu_engine* e, int parity, const octgpu_params* prm, void* m
         if (rc) return rc;
     }
     void* mlog = nullptr;
-    const size_t log_bytes = size_t(e->Y) * e->n * e->word_bytes();
+    const size_t log_bytes = size_t(e->L) * e->n * e->word_bytes();
     if (mask_log) CK(cudaMalloc(&mlog, log_bytes));
     const cudaError_t le =
         launch_sweep(e->w, e->planes[e->pcur], e->rng[e->rcur], parity, e->geom(), p, q, live, mlog, e->stream);
@@ -801,6 +861,8 @@ int octgpu_sweep(octgpu_engine* e, int parity, const octgpu_params* prm, void* m
     ++e->launches;
     if (!live) e->pending += uint64_t(e->n) * D;
     e->phase ^= 1;
+    rc = refresh_ghosts(e);  // k_sweep works in place and does not maintain ghost rows
+    if (rc) return rc;
     if (mask_log) {
         CK(cudaMemcpyAsync(mask_log, mlog, log_bytes, cudaMemcpyDeviceToHost, e->stream));
         CK(cudaStreamSynchronize(e->stream));
@@ -819,15 +881,15 @@ int octgpu_get_planes(octgpu_engine* e, void* out) {
     int rc = use_device(e);
     if (!rc) rc = ensure_stage(e);
     if (rc) return rc;
-    CK(launch_export(e->w, e->planes[e->pcur], e->stage, e->geom(), e->stream));
+    CK(launch_export(e->w, e->planes[e->pcur], e->stage, e->geom(), e->host_rows(), e->stream));
     ++e->launches;
     if (!e->stripe) {
-        CK(cudaMemcpyAsync(out, e->stage, e->set_bytes(), cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaMemcpyAsync(out, e->stage, e->host_bytes(), cudaMemcpyDeviceToHost, e->stream));
         CK(cudaStreamSynchronize(e->stream));
         return OCTGPU_OK;
     }
-    std::vector<unsigned char> pad(e->set_bytes());
-    CK(cudaMemcpyAsync(pad.data(), e->stage, e->set_bytes(), cudaMemcpyDeviceToHost, e->stream));
+    std::vector<unsigned char> pad(e->host_bytes());
+    CK(cudaMemcpyAsync(pad.data(), e->stage, e->host_bytes(), cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
     const size_t row_bytes = size_t(e->n) * e->word_bytes();
     for (int p = 0; p < 4; ++p)
@@ -853,7 +915,7 @@ int octgpu_get_states(octgpu_engine* e, uint64_t* out) {
 int octgpu_field_checksum(octgpu_engine* e, uint64_t* out) {
     if (!e || !out) return fail(OCTGPU_ERR_CONFIG, "null argument");
     if (e->stripe) return fail(OCTGPU_ERR_CONFIG, "octgpu_field_checksum is not available on a row stripe (use the octgpu_stripe_* calls)");
-    std::vector<unsigned char> buf(e->set_bytes());
+    std::vector<unsigned char> buf(e->host_bytes());
     int rc = octgpu_get_planes(e, buf.data());
     if (rc) return rc;
     uint64_t h = 0xcbf29ce484222325ULL;  // FNV-1a, slope_field.hpp:232-246
@@ -863,7 +925,7 @@ int octgpu_field_checksum(octgpu_engine* e, uint64_t* out) {
             h *= 0x100000001b3ULL;
         }
     };
-    const size_t nw = 4 * size_t(e->n) * e->Y;
+    const size_t nw = 4 * size_t(e->n) * e->L;
     if (e->w == 64) {
         const uint64_t* p = reinterpret_cast<const uint64_t*>(buf.data());
         for (size_t i = 0; i < nw; ++i) mix(p[i]);
@@ -907,7 +969,7 @@ int octgpu_measure(octgpu_engine* e, octgpu_moments* out) {
     int rc = run_measure(e);
     if (rc) return rc;
     const MeasureResult& r = *e->res_host;
-    const uint64_t N = uint64_t(e->X) * e->Y;
+    const uint64_t N = uint64_t(e->X) * e->L;
     out->t = e->t;
     out->n_sites = N;
     __int128 S[4];
@@ -952,7 +1014,7 @@ int octgpu_heights(octgpu_engine* e, int32_t* out) {
     if (e->stripe) return fail(OCTGPU_ERR_CONFIG, "octgpu_heights is not available on a row stripe (use the octgpu_stripe_* calls)");
     int rc = run_measure(e);
     if (rc) return rc;
-    const size_t bytes = size_t(e->X) * e->Y * sizeof(int32_t);
+    const size_t bytes = size_t(e->X) * e->L * sizeof(int32_t);
     int32_t* d = nullptr;
     CK(cudaMalloc(&d, bytes));
     cudaError_t le = launch_heights(e->w, e->planes[e->pcur], e->geom(), e->X, e->scratch, d, e->stream);
@@ -1022,7 +1084,7 @@ int octgpu_stripe_mcs(octgpu_engine* e, const octgpu_params* prm, void* boundary
         rc = plan_bulk(e, p, q);
         if (rc) return rc;
         CK(launch_mcs_bulk(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
-                           e->bulk_ks, e->bulk_S, e->stream));
+                           e->bulk_ks, e->bulk_S, &e->tm[ps][0], &e->tm[ps][1], e->stream));
     } else
         CK(launch_mcs(e->w, e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, live,
                       jtab, e->stream));

@@ -32,7 +32,7 @@ template <typename Word, int PM, int QM, int PF>
 __global__ void __launch_bounds__(128) k_sweep(Word* __restrict__ planes, uint64_t* __restrict__ rng, int parity,
                                                Geom g, ProbDev p, ProbDev q, Word* __restrict__ mask_log) {
     constexpr int W = int(sizeof(Word) * 8);
-    const uint32_t Y = g.Y, n = g.n;
+    const uint32_t Y = g.wrap, LD = g.Y, n = g.n;  // periodic lattice: Y rows, row stride LD
     const uint32_t y = blockIdx.x * blockDim.x + threadIdx.x;
     if (y >= Y) return;
     const size_t PS = g.plane_stride;
@@ -43,18 +43,18 @@ __global__ void __launch_bounds__(128) k_sweep(Word* __restrict__ planes, uint64
     const bool shifted = ((uint32_t(parity) ^ y) & 1u) != 0;                  // engine_vec.hpp:59-61
 
     Xo s{0, 0, 0, 0};
-    if constexpr (Plan<PM, QM>::live) s = load_state(rng, Y, y);
+    if constexpr (Plan<PM, QM>::live) s = load_state(rng, LD, y);
 
     const Word raw0 = xr[0];
     Word bA[PF], bB[PF], bC[PF], bR[PF];
 #pragma unroll
     for (int j = 0; j < PF; ++j) {
         if (uint32_t(j) < n) {
-            const size_t o = size_t(j) * Y;
+            const size_t o = size_t(j) * LD;
             bA[j] = px[o];
             bB[j] = py[o];
             bC[j] = qy[o];
-            bR[j] = (uint32_t(j) + 1 < n) ? xr[o + Y] : raw0;
+            bR[j] = (uint32_t(j) + 1 < n) ? xr[o + LD] : raw0;
         }
     }
     Word cur = raw0, carry = 0, new0 = 0;
@@ -63,15 +63,15 @@ __global__ void __launch_bounds__(128) k_sweep(Word* __restrict__ planes, uint64
         for (int j = 0; j < PF; ++j) {
             const uint32_t k = kb + j;
             if (k < n) {
-                const size_t o = size_t(k) * Y;
+                const size_t o = size_t(k) * LD;
                 const Word A = bA[j], B = bB[j], Cn = bC[j], nxt = bR[j];
                 const uint32_t kk = k + PF;
                 if (kk < n) {  // refill this slot PF words ahead
-                    const size_t oo = size_t(kk) * Y;
+                    const size_t oo = size_t(kk) * LD;
                     bA[j] = px[oo];
                     bB[j] = py[oo];
                     bC[j] = qy[oo];
-                    bR[j] = (kk + 1 < n) ? xr[oo + Y] : raw0;
+                    bR[j] = (kk + 1 < n) ? xr[oo + LD] : raw0;
                 }
                 const Word sxp = shifted ? Word((cur >> 1) | (nxt << (W - 1))) : cur;  // rotate_row_down
                 Word xp, xq;
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(128) k_sweep(Word* __restrict__ planes, uint64
     }
     if (shifted) new0 ^= carry;
     xr[0] = new0;
-    if constexpr (Plan<PM, QM>::live) store_state(rng, Y, y, s);
+    if constexpr (Plan<PM, QM>::live) store_state(rng, LD, y, s);
 }
 
 // -------------------------------------------------------------------------
@@ -278,22 +278,45 @@ __global__ void k_apply_jump(uint64_t* __restrict__ rng, uint32_t Y, const uint6
 // <-> device word-major ([n][Y] per plane).
 
 template <typename Word, bool TO_DEVICE>
-__global__ void k_transpose(const Word* __restrict__ in, Word* __restrict__ out, Geom g) {
+__global__ void k_transpose(const Word* __restrict__ in, Word* __restrict__ out, Geom g, uint32_t rows) {
     __shared__ Word tile[32][33];
-    const uint32_t Y = g.Y, n = g.n;
-    const size_t poff = size_t(blockIdx.z) * g.plane_stride;
-    // TO_DEVICE: in is [Y][n], out is [n][Y]; else the reverse.
-    const uint32_t R = TO_DEVICE ? Y : n, Cc = TO_DEVICE ? n : Y;  // in dims
+    const uint32_t n = g.n;
+    const size_t hoff = size_t(blockIdx.z) * rows * n;      // host plane
+    const size_t doff = size_t(blockIdx.z) * g.plane_stride;  // device plane
+    // host: [rows][n] (row-major); device: word k of row r at k * g.Y + r
+    const uint32_t R = TO_DEVICE ? rows : n, Cc = TO_DEVICE ? n : rows;  // dims of `in`
     const uint32_t c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
         const uint32_t r = r0 + i, c = c0 + threadIdx.x;
-        if (r < R && c < Cc) tile[i][threadIdx.x] = in[poff + size_t(r) * Cc + c];
+        if (r < R && c < Cc)
+            tile[i][threadIdx.x] = TO_DEVICE ? in[hoff + size_t(r) * n + c] : in[doff + size_t(r) * g.Y + c];
     }
     __syncthreads();
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
         const uint32_t c = c0 + i, r = r0 + threadIdx.x;
-        if (r < R && c < Cc) out[poff + size_t(c) * R + r] = tile[threadIdx.x][i];
+        if (r < R && c < Cc) {
+            if (TO_DEVICE)
+                out[doff + size_t(c) * g.Y + r] = tile[threadIdx.x][i];
+            else
+                out[hoff + size_t(c) * n + r] = tile[threadIdx.x][i];
+        }
     }
+}
+
+// Ghost rows of a periodic lattice: row wrap + i = row (i mod wrap).
+template <typename Word>
+__global__ void k_refresh_ghosts(Word* __restrict__ planes, uint64_t* __restrict__ rng, Geom g) {
+    const uint32_t per = g.ghost * g.n, total = 4 * per;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const uint32_t p = t / per, rem = t % per, k = rem / g.ghost, i = rem % g.ghost;
+        Word* base = planes + size_t(p) * g.plane_stride + size_t(k) * g.Y;
+        base[g.wrap + i] = base[i % g.wrap];
+    }
+    if (rng)
+        for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < 4 * g.ghost; t += gridDim.x * blockDim.x) {
+            const uint32_t j = t / g.ghost, i = t % g.ghost;
+            rng[size_t(j) * g.Y + g.wrap + i] = rng[size_t(j) * g.Y + i % g.wrap];
+        }
 }
 
 // -------------------------------------------------------------------------
@@ -309,7 +332,7 @@ struct Dispatch;
 template <typename Word, int PM, int QM>
 cudaError_t sweep_pq(void* planes, uint64_t* rng, int parity, Geom g, const ProbDev& p, const ProbDev& q,
                      void* mask_log, cudaStream_t st) {
-    const uint32_t threads = 128, blocks = (g.Y + threads - 1) / threads;
+    const uint32_t threads = 128, blocks = (g.wrap + threads - 1) / threads;
     k_sweep<Word, PM, QM, kPF><<<blocks, threads, 0, st>>>(static_cast<Word*>(planes), rng, parity, g, p, q,
                                                           static_cast<Word*>(mask_log));
     return cudaGetLastError();
@@ -372,20 +395,31 @@ cudaError_t launch_apply_jump(uint64_t* rng, uint32_t Y, const uint64_t* tab, cu
 }
 
 template <typename Word, bool TO>
-static cudaError_t transpose_w(const void* in, void* out, Geom g, cudaStream_t st) {
-    const uint32_t R = TO ? g.Y : g.n, Cc = TO ? g.n : g.Y;
+static cudaError_t transpose_w(const void* in, void* out, Geom g, uint32_t rows, cudaStream_t st) {
+    const uint32_t R = TO ? rows : g.n, Cc = TO ? g.n : rows;
     dim3 grid((Cc + 31) / 32, (R + 31) / 32, 4), block(32, 8);
-    k_transpose<Word, TO><<<grid, block, 0, st>>>(static_cast<const Word*>(in), static_cast<Word*>(out), g);
+    k_transpose<Word, TO><<<grid, block, 0, st>>>(static_cast<const Word*>(in), static_cast<Word*>(out), g, rows);
     return cudaGetLastError();
 }
 
-cudaError_t launch_import(int w, const void* in, void* planes, Geom g, cudaStream_t st) {
-    return w == 64 ? transpose_w<uint64_t, true>(in, planes, g, st) : transpose_w<uint32_t, true>(in, planes, g, st);
+cudaError_t launch_import(int w, const void* in, void* planes, Geom g, uint32_t rows, cudaStream_t st) {
+    return w == 64 ? transpose_w<uint64_t, true>(in, planes, g, rows, st)
+                   : transpose_w<uint32_t, true>(in, planes, g, rows, st);
 }
 
-cudaError_t launch_export(int w, const void* planes, void* out, Geom g, cudaStream_t st) {
-    return w == 64 ? transpose_w<uint64_t, false>(planes, out, g, st)
-                   : transpose_w<uint32_t, false>(planes, out, g, st);
+cudaError_t launch_export(int w, const void* planes, void* out, Geom g, uint32_t rows, cudaStream_t st) {
+    return w == 64 ? transpose_w<uint64_t, false>(planes, out, g, rows, st)
+                   : transpose_w<uint32_t, false>(planes, out, g, rows, st);
+}
+
+cudaError_t launch_refresh_ghosts(int w, void* planes, uint64_t* rng, Geom g, cudaStream_t st) {
+    if (!g.ghost) return cudaSuccess;
+    const uint32_t blocks = std::min<uint32_t>(256, (4 * g.ghost * g.n + 255) / 256);
+    if (w == 64)
+        k_refresh_ghosts<uint64_t><<<blocks, 256, 0, st>>>(static_cast<uint64_t*>(planes), rng, g);
+    else
+        k_refresh_ghosts<uint32_t><<<blocks, 256, 0, st>>>(static_cast<uint32_t*>(planes), rng, g);
+    return cudaGetLastError();
 }
 
 }  // namespace octgpu

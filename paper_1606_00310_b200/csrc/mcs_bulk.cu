@@ -14,6 +14,8 @@
 //    so every window starts at an even row: 16-byte aligned for the copies;
 //  * stores are predicated in PTX (no divergent branches).
 // Used for w = 64, n >= 8, Y >= 64; smaller lattices take k_mcs.
+#include <cuda.h>
+
 #include <cstdint>
 
 #include "device_common.cuh"
@@ -52,13 +54,14 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                  : "memory");
 }
 
-// One bulk copy (SASS UBLKCP). Its operands live in uniform registers, so it
-// must be issued with warp-uniform operands (one lane, see fill()).
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+// One 3-D TMA tile copy (SASS UTMALDG): box at (row, word, plane) of the
+// tensor map lands in shared memory as [words][rows]. Operands are uniform.
+__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* tm, uint32_t row, uint32_t word, uint32_t plane,
+                                      uint64_t* bar) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(row), "r"(word), "r"(plane), "r"(smem_u32(bar))
         : "memory");
 }
 
@@ -72,26 +75,32 @@ __device__ __forceinline__ void st_pred(uint64_t* p, uint64_t v, bool pred) {
         "l"(v), "r"(int(pred)));
 }
 
-// Stage layout (uint64 words): Xf[KS][kWin] | Yf[KS][kWin] | Ys[KS][kWin] | Xs[KS+1][kWin]
+// Stage layout (uint64 words), every segment 128-B aligned for the TMA:
+// Xf[KS][kWin] | Yf[KS][kWin] | Ys[KS][kWin] | Xs[KS+1][kWin]
+constexpr int align16w(int words) { return (words + 15) / 16 * 16; }
 template <int KS>
 struct StageLayout {
+    static constexpr int kSeg = align16w(KS * kWin);
     static constexpr int kXf = 0;
-    static constexpr int kYf = KS * kWin;
-    static constexpr int kYs = 2 * KS * kWin;
-    static constexpr int kXs = 3 * KS * kWin;
-    static constexpr int kWords = (4 * KS + 1) * kWin;
+    static constexpr int kYf = kSeg;
+    static constexpr int kYs = 2 * kSeg;
+    static constexpr int kXs = 3 * kSeg;
+    static constexpr int kWords = 3 * kSeg + align16w((KS + 1) * kWin);
     static constexpr int kBytes = kWords * 8;
+    static constexpr uint32_t kTx = (4 * KS + 1) * kWin * 8;  // bytes landed per stage (full boxes)
 };
 
 }  // namespace
 
-size_t mcs_bulk_stage_bytes(int ks) { return size_t(4 * ks + 1) * kWin * 8; }
+size_t mcs_bulk_stage_bytes(int ks) { return ks == 4 ? StageLayout<4>::kBytes : StageLayout<2>::kBytes; }
 
 template <int PM, int QM, int KS>
 __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
                                                   const uint64_t* __restrict__ rs, uint64_t* __restrict__ rd,
                                                   int f, Geom g, ProbDev p, ProbDev q,
-                                                  const uint64_t* __restrict__ jtab, int S) {
+                                                  const uint64_t* __restrict__ jtab, int S,
+                                                  const __grid_constant__ CUtensorMap tmK,
+                                                  const __grid_constant__ CUtensorMap tmK1) {
     using Word = uint64_t;
     using LY = StageLayout<KS>;
     constexpr int W = 64;
@@ -127,10 +136,11 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
     const bool sh1 = ((uint32_t(f) ^ y ^ g.ypar) & 1u) != 0;
     const bool sh2 = !sh1;
 
-    // window split for the periodic wrap in y (last warp only)
-    const uint32_t pr0 = g.wrap ? r0 % g.wrap : r0;  // physical window start
-    const uint32_t rows1 = g.wrap ? min(uint32_t(kWin), g.wrap - pr0) : uint32_t(kWin);
-    const uint32_t rows2 = kWin - rows1;
+    // Periodic lattices keep ghost rows wrap..wrap+33 equal to rows 0..33, so the
+    // 34-row window starting at r0 never wraps; warps that store rows 0..33
+    // (the first two and the last) also refresh those ghosts.
+    const bool ghostw = g.ghost && (r0 + 1 < g.ghost || r0 + 31 >= g.wrap);  // warp-uniform
+    const bool ghost_row = ghostw && y < g.ghost;
 
     if (lane == 0) {
         for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
@@ -138,32 +148,22 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
     }
     __syncwarp();
 
-    // Copies of word-block b into its stage: one lane issues 4*nw+1 window
-    // copies (two each for the wrapping last warp) with uniform operands.
-    auto copy_window = [&](Word* sdst, const Word* gplane, uint32_t word, uint64_t* bar) {
-        const Word* g0 = gplane + size_t(word) * Y;
-        bulk_g2s(sdst, g0 + pr0, rows1 * 8, bar);
-        if (rows2) bulk_g2s(sdst + rows1, g0, rows2 * 8, bar);
-    };
+    // Word-block b -> its stage: 4 TMA tiles (34 rows x KS words of X(f), Y(f),
+    // Y(s); 34 x KS+1 of X(s)), issued by one lane. Words past n are zero-filled
+    // (X(s) word n, i.e. word 0, is taken from raw0 instead).
     auto fill = [&](uint32_t b) {
         const int st = int(b % uint32_t(S));
         Word* base = ring + size_t(st) * LY::kWords;
         const uint32_t kb = b * KS;
-        const uint32_t nw = min(uint32_t(KS), n - kb);
         // The stage's previous contents were consumed (loaded and used) before this
         // refill, so no generic->async proxy fence is needed for the overwrite.
         __syncwarp();
         if (lane == 0) {
-            mbar_expect_tx(&bars[st], (4 * nw + 1) * kWin * 8);
-            for (uint32_t j = 0; j < nw; ++j) {
-                copy_window(base + LY::kXf + j * kWin, planeXf, kb + j, &bars[st]);
-                copy_window(base + LY::kYf + j * kWin, planeYf, kb + j, &bars[st]);
-                copy_window(base + LY::kYs + j * kWin, planeYs, kb + j, &bars[st]);
-            }
-            for (uint32_t j = 0; j <= nw; ++j) {
-                const uint32_t w = kb + j < n ? kb + j : kb + j - n;
-                copy_window(base + LY::kXs + j * kWin, planeXs, w, &bars[st]);
-            }
+            mbar_expect_tx(&bars[st], LY::kTx);
+            tma3d(base + LY::kXf, &tmK, r0, kb, uint32_t(f), &bars[st]);
+            tma3d(base + LY::kYf, &tmK, r0, kb, uint32_t(2 + f), &bars[st]);
+            tma3d(base + LY::kYs, &tmK, r0, kb, uint32_t(2 + s), &bars[st]);
+            tma3d(base + LY::kXs, &tmK1, r0, kb, uint32_t(s), &bars[st]);
         }
     };
 
@@ -181,7 +181,13 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
     Word A0 = 0, B0 = 0, C0 = 0, R0 = 0, A1 = 0;
     Word pA = 0, pB = 0, pC = 0, pR = 0;
     Word carry1 = 0, m2last = 0, xf1 = 0;
-    Word cur = 0;
+    Word cur = 0, raw0 = 0;
+
+    // predicated store, mirrored into the ghost row when this is one of rows 0..33
+    auto put = [&](Word* ptr, Word val, bool pred) {
+        st_pred(ptr, val, pred);
+        if (ghostw) st_pred(ptr + g.wrap, val, pred && ghost_row);
+    };
 
     auto second = [&](uint32_t j, Word Aj, Word Ajn, Word Bj, Word Cj, Word Rj, Word x2p, Word x2q) {
         const Word Cup = __shfl_up_sync(0xffffffffu, Cj, 1);
@@ -190,9 +196,9 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
         const Word m2 = update_mask<Word>(Rj, Cup, sxp2, Bdn, x2p, x2q);
         const Word mup = __shfl_up_sync(0xffffffffu, m2, 1);
         const uint32_t o = j * Y;  // < 2^32: n * Y words per plane
-        st_pred(dXs + o, Rj ^ m2, core);
-        st_pred(dYs + o, Cup ^ m2, core);
-        st_pred(dYf + o, Bj ^ mup, wyf);
+        put(dXs + o, Rj ^ m2, core);
+        put(dYs + o, Cup ^ m2, core);
+        put(dYf + o, Bj ^ mup, wyf);
         return m2;
     };
 
@@ -201,7 +207,10 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
         mbar_wait(&bars[st], (b / uint32_t(S)) & 1u);
         const Word* sb = ring + size_t(st) * LY::kWords;
         const uint32_t kb = b * KS;
-        if (b == 0) cur = sb[LY::kXs + lane];  // X(s)[y][0], original
+        if (b == 0) {
+            cur = sb[LY::kXs + lane];  // X(s)[y][0], original
+            raw0 = cur;
+        }
         // arbitrary-probability bodies are ~10^4 instructions per word: keep them rolled (I-cache)
         constexpr int kUnroll = (PM == M_ARB || QM == M_ARB) ? 1 : KS;
         if (kb >= 3 && kb + KS <= n) {
@@ -212,7 +221,7 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
                 const Word A = sb[LY::kXf + jj * kWin + lane];
                 const Word B = sb[LY::kYf + jj * kWin + lane];
                 const Word Cn = sb[LY::kYs + jj * kWin + lane + 1];
-                const Word nxt = sb[LY::kXs + (jj + 1) * kWin + lane];
+                const Word nxt = (k + 1 == n) ? raw0 : sb[LY::kXs + (jj + 1) * kWin + lane];
                 Word x1p, x1q, x2p, x2q;
                 gen_xi_pair<PM, QM, Word>(s1, s2, p, q, x1p, x1q, x2p, x2q);
                 const Word sxp = sh1 ? Word((cur >> 1) | (nxt << (W - 1))) : cur;
@@ -223,7 +232,7 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
                 const Word Rp = cur ^ sc1;
                 cur = nxt;
                 const Word m2 = second(k - 1, pA, Ap, pB, pC, pR, x2p, x2q);
-                st_pred(dXf + (k - 1) * Y, pA ^ (sh2 ? Word((m2 << 1) | (m2last >> (W - 1))) : m2), core);
+                put(dXf + (k - 1) * Y, pA ^ (sh2 ? Word((m2 << 1) | (m2last >> (W - 1))) : m2), core);
                 m2last = m2;
                 pA = Ap; pB = Bp; pC = Cp; pR = Rp;
             }
@@ -235,7 +244,7 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
                 const Word A = sb[LY::kXf + jj * kWin + lane];
                 const Word B = sb[LY::kYf + jj * kWin + lane];
                 const Word Cn = sb[LY::kYs + jj * kWin + lane + 1];
-                const Word nxt = sb[LY::kXs + (jj + 1) * kWin + lane];
+                const Word nxt = (k + 1 == n) ? raw0 : sb[LY::kXs + (jj + 1) * kWin + lane];
                 // ---- xi for first sweep word k and (k >= 2) second sweep word k-1, interleaved ----
                 Word x1p, x1q, x2p = 0, x2q = 0;
                 if (k >= 2)
@@ -261,7 +270,7 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
                         if (j == 1)
                             xf1 = xfj;
                         else
-                            st_pred(dXf + j * Y, xfj ^ (sh2 ? Word(m2last >> (W - 1)) : Word(0)), core);
+                            put(dXf + j * Y, xfj ^ (sh2 ? Word(m2last >> (W - 1)) : Word(0)), core);
                         m2last = m2;
                     }
                 }
@@ -277,17 +286,20 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
         gen_xi<PM, QM, Word>(s2, p, q, x2p, x2q);
         const Word m2 = second(j, pA, A0, pB, pC, pR, x2p, x2q);
         const Word xfj = pA ^ (sh2 ? Word(m2 << 1) : m2);
-        st_pred(dXf + j * Y, xfj ^ (sh2 ? Word(m2last >> (W - 1)) : Word(0)), core);
+        put(dXf + j * Y, xfj ^ (sh2 ? Word(m2last >> (W - 1)) : Word(0)), core);
         m2last = m2;
     }
     {
         const Word m2 = second(0, A0, A1, B0, C0, R0, xi2p0, xi2q0);
         const Word xf0 = A0 ^ (sh2 ? Word((m2 << 1) | (m2last >> (W - 1))) : m2);
-        st_pred(dXf, xf0, core);
-        st_pred(dXf + Y, xf1 ^ (sh2 ? Word(m2 >> (W - 1)) : Word(0)), core);
+        put(dXf, xf0, core);
+        put(dXf + Y, xf1 ^ (sh2 ? Word(m2 >> (W - 1)) : Word(0)), core);
     }
     if constexpr (LIVE) {
-        if (core) store_state(rd, Y, y, s2);
+        if (core) {
+            store_state(rd, Y, y, s2);
+            if (ghost_row) store_state(rd, Y, y + g.wrap, s2);
+        }
     }
 }
 
@@ -295,7 +307,8 @@ namespace {
 
 template <int PM, int QM>
 cudaError_t bulk_pq(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
-                    const ProbDev& q, const uint64_t* jtab, int ks, int S, cudaStream_t st) {
+                    const ProbDev& q, const uint64_t* jtab, int ks, int S, const CUtensorMap* tmK,
+                    const CUtensorMap* tmK1, cudaStream_t st) {
     const uint32_t warps = (g.c1 - g.c0 + 29) / 30;
     const uint32_t wpb = 4, threads = 32 * wpb, blocks = (warps + wpb - 1) / wpb;
     const size_t smem = mcs_bulk_smem(ks, S);
@@ -305,13 +318,13 @@ cudaError_t bulk_pq(const void* src, void* dst, const uint64_t* rs, uint64_t* rd
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
         kern<<<blocks, threads, smem, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), rs, rd,
-                                            f, g, p, q, jtab, S);
+                                            f, g, p, q, jtab, S, *tmK, *tmK1);
     } else {
         auto kern = k_mcs_bulk<PM, QM, 2>;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
         kern<<<blocks, threads, smem, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), rs, rd,
-                                            f, g, p, q, jtab, S);
+                                            f, g, p, q, jtab, S, *tmK, *tmK1);
     }
     return cudaGetLastError();
 }
@@ -336,11 +349,11 @@ int occ_pq(int ks, size_t smem) {
 
 #define OCT_BQ(PM)                                                                              \
     switch (q.mode) {                                                                           \
-    case M_ZERO: return bulk_pq<PM, M_ZERO>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, st);     \
-    case M_HALF: return bulk_pq<PM, M_HALF>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, st);     \
-    case M_DYADIC: return bulk_pq<PM, M_DYADIC>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, st); \
-    case M_ARB: return bulk_pq<PM, M_ARB>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, st);       \
-    case M_ONE: return bulk_pq<PM, M_ONE>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, st);       \
+    case M_ZERO: return bulk_pq<PM, M_ZERO>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, tmK, tmK1, st);     \
+    case M_HALF: return bulk_pq<PM, M_HALF>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, tmK, tmK1, st);     \
+    case M_DYADIC: return bulk_pq<PM, M_DYADIC>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, tmK, tmK1, st); \
+    case M_ARB: return bulk_pq<PM, M_ARB>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, tmK, tmK1, st);       \
+    case M_ONE: return bulk_pq<PM, M_ONE>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, tmK, tmK1, st);       \
     default: return cudaErrorInvalidValue;                                                      \
     }
 
@@ -361,7 +374,7 @@ size_t mcs_bulk_smem(int ks, int S) { return 8 * 8 * 4 + size_t(4) * S * mcs_bul
 
 cudaError_t launch_mcs_bulk(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g,
                             const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int ks, int S,
-                            cudaStream_t st) {
+                            const CUtensorMap* tmK, const CUtensorMap* tmK1, cudaStream_t st) {
     switch (p.mode) {
     case M_ZERO: OCT_BQ(M_ZERO)
     case M_HALF: OCT_BQ(M_HALF)

@@ -357,7 +357,7 @@ template <typename Word>
 __global__ void k_heights(const Word* __restrict__ planes, Geom g, uint32_t X, const long long* __restrict__ G,
                           int32_t* __restrict__ out) {
     constexpr int W = int(sizeof(Word) * 8);
-    const uint32_t Y = g.Y, n = g.n;
+    const uint32_t Y = g.wrap, LD = g.Y, n = g.n;  // periodic only
     const uint32_t y = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (y >= Y) return;
@@ -372,8 +372,8 @@ __global__ void k_heights(const Word* __restrict__ planes, Geom g, uint32_t X, c
         Word a = 0, b = 0;
         int delta = 0;
         if (k < n) {
-            a = Xa[size_t(k) * Y];
-            b = Xb[size_t(k) * Y];
+            a = Xa[size_t(k) * LD];
+            b = Xb[size_t(k) * LD];
             delta = 2 * (__popcll((unsigned long long)a) + __popcll((unsigned long long)b)) - 2 * W;
         }
         int incl = delta;
@@ -424,7 +424,7 @@ cudaError_t launch_measure(int w, const void* planes, Geom g, uint32_t X, void* 
 cudaError_t launch_heights(int w, const void* planes, Geom g, uint32_t X, const void* scratch, int32_t* out,
                            cudaStream_t st) {
     const long long* G = static_cast<const long long*>(scratch);
-    const uint32_t threads = 128, blocks = (g.Y * 32 + threads - 1) / threads;
+    const uint32_t threads = 128, blocks = (g.wrap * 32 + threads - 1) / threads;
     if (w == 64)
         k_heights<uint64_t><<<blocks, threads, 0, st>>>(static_cast<const uint64_t*>(planes), g, X, G, out);
     else

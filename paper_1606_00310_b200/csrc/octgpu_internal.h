@@ -3,6 +3,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace octgpu {
@@ -39,13 +40,19 @@ struct Geom {
     uint32_t c0, c1;       // core rows (virtual)
     uint32_t wrap;         // periodic modulus in y, or 0
     uint32_t ypar;         // parity of the global row of physical row 0 (site parity uses global rows)
+    uint32_t ghost;        // periodic: rows wrap..wrap+ghost-1 mirror rows (i mod wrap), so 34-row windows never wrap
 };
+
+constexpr uint32_t kGhostRows = 34;
 
 // Per-row RNG states are stored SoA: s[j * Y + y], j = 0..3.
 
 // ---- launchers (return the launch error, never synchronise) ----
-cudaError_t launch_import(int w, const void* host_layout_dev, void* planes, Geom g, cudaStream_t st);
-cudaError_t launch_export(int w, const void* planes, void* host_layout_dev, Geom g, cudaStream_t st);
+// host layout [4][rows][n] (compact) <-> device rows 0..rows-1 of each plane
+cudaError_t launch_import(int w, const void* host_layout_dev, void* planes, Geom g, uint32_t rows, cudaStream_t st);
+cudaError_t launch_export(int w, const void* planes, void* host_layout_dev, Geom g, uint32_t rows, cudaStream_t st);
+// periodic lattices: rewrite the ghost rows (planes, and rng when non-null) from rows 0..ghost-1
+cudaError_t launch_refresh_ghosts(int w, void* planes, uint64_t* rng, Geom g, cudaStream_t st);
 
 // One sublattice sweep in place (engine_vec.hpp:145-168), optional mask log in
 // reference row-major layout.
@@ -61,9 +68,12 @@ cudaError_t launch_mcs(int w, const void* src, void* dst, const uint64_t* rng_sr
 
 // Same as launch_mcs with shared-memory staging by cp.async.bulk (mcs_bulk.cu):
 // w = 64, n >= 8, Y >= 64 only. ks = words per stage (2 or 4), S = stages.
+// tmK / tmK1: 3-D tensor maps (rows x words x planes) of the src plane set with
+// boxes of 34 rows x ks and x ks+1 words (see engine.cu make_tmaps).
 cudaError_t launch_mcs_bulk(const void* src, void* dst, const uint64_t* rng_src, uint64_t* rng_dst, int f, Geom g,
                             const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int ks, int S,
-                            cudaStream_t st);
+                            const CUtensorMap* tmK, const CUtensorMap* tmK1, cudaStream_t st);
+constexpr uint32_t kTmaBoxRows = 34;
 size_t mcs_bulk_stage_bytes(int ks);
 size_t mcs_bulk_smem(int ks, int S);  // dynamic smem of a 4-warp block
 // resident 4-warp blocks per SM of k_mcs_bulk<p, q, ks> with `smem` bytes of dynamic smem

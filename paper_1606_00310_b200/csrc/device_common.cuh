@@ -79,10 +79,17 @@ __device__ __forceinline__ Word xi_word(Xo& s, const ProbDev& pd) {
         }
         return acc;
     } else if constexpr (MODE == M_ARB) {
-        // xi_arbitrary: bit i = to_unit(draw_i) < r  <=>  draw_i < T (integer threshold)
+        // xi_arbitrary: bit i = to_unit(draw_i) < r  <=>  draw_i < T (integer threshold).
+        // Rolled by bytes: the word is ~W x 22 instructions, and fully unrolled
+        // copies at every call site overflow the instruction cache.
         Word word = 0;
+#pragma unroll 1
+        for (int i0 = 0; i0 < W; i0 += 8) {
+            uint32_t byte = 0;
 #pragma unroll
-        for (int i = 0; i < W; ++i) word |= Word(xo_next(s) < pd.T) << i;
+            for (int j = 0; j < 8; ++j) byte |= uint32_t(xo_next(s) < pd.T) << j;
+            word |= Word(byte) << i0;
+        }
         return word;
     } else {  // M_ONE: every bit accepted, stream still advances w draws
 #pragma unroll 8
@@ -133,10 +140,16 @@ __device__ __forceinline__ void xi_word_pair(Xo& a, Xo& b, const ProbDev& pd, Wo
         wb = rb;
     } else if constexpr (MODE == M_ARB) {
         Word ra = 0, rb = 0;
-#pragma unroll 16
-        for (int i = 0; i < W; ++i) {
-            ra |= Word(xo_next(a) < pd.T) << i;
-            rb |= Word(xo_next(b) < pd.T) << i;
+#pragma unroll 1
+        for (int i0 = 0; i0 < W; i0 += 8) {
+            uint32_t ba = 0, bb = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                ba |= uint32_t(xo_next(a) < pd.T) << j;
+                bb |= uint32_t(xo_next(b) < pd.T) << j;
+            }
+            ra |= Word(ba) << i0;
+            rb |= Word(bb) << i0;
         }
         wa = ra;
         wb = rb;

@@ -328,7 +328,7 @@ struct octgpu_engine {
     uint64_t launches = 0;
     // fused-MCS implementation: 2 = bulk-copy staged (k_mcs_bulk), 1 = register-prefetch (k_mcs)
     int mcs_impl = 2;
-    int bulk_ks = 4, bulk_S = 3;
+    int bulk_ks = 2, bulk_S = 2;
     int bulk_key = -1;  // (p, q) mode pair the bulk plan was made for
     CUtensorMap tm[2][2];  // [plane set][box: ks words, ks+1 words] for k_mcs_bulk
     int tm_ks = -1;
@@ -408,15 +408,11 @@ int upload_states(octgpu_engine* e, const uint64_t* aos) {
     return OCTGPU_OK;
 }
 
-// Pick the fused-MCS variant. For k_mcs_bulk the pipeline depth (KS words per
-// stage, S stages) is sized per (p, q) mode pair at the first step: every warp
-// owns a 30-row group for the whole kernel, so the blocks should run in equal
-// rounds. Resident blocks per SM are limited by registers (queried from the
-// occupancy calculator) and by the shared memory we give each block; we give
-// each block the largest pipeline that still lets ceil(blocks / (SMs * rounds))
-// blocks share an SM, with rounds the minimum the register limit allows.
+// Pick the fused-MCS variant: k_mcs_bulk (TMA-staged, warp-specialised) for
+// w = 64 lattices with n >= 8 words and, when periodic, at least kGhostRows
+// rows; k_mcs (register prefetch) otherwise.
 int plan_mcs(octgpu_engine* e) {
-    e->mcs_impl = (e->w == 64 && e->n >= 8 && (e->stripe || e->L >= 64)) ? 2 : 1;
+    e->mcs_impl = (e->w == 64 && e->n >= 8 && (e->stripe || e->L >= kGhostRows)) ? 2 : 1;
     if (const char* v = getenv("OCTGPU_MCS_IMPL")) e->mcs_impl = (atoi(v) == 1) ? 1 : e->mcs_impl;
     return OCTGPU_OK;
 }
@@ -435,7 +431,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 // 3-D view of a plane set: dim 0 = rows (contiguous, Y allocated rows), dim 1 =
-// words (stride Y*8 B), dim 2 = planes (stride n*Y*8 B); tiles of 34 rows x
+// words (stride Y*8 B), dim 2 = planes (stride n*Y*8 B); tiles of kTmaBoxRows rows x
 // (ks | ks+1) words x 1 plane, no swizzle, out-of-bounds words read as zero.
 int ensure_tmaps(octgpu_engine* e) {
     if (e->tm_ks == e->bulk_ks) return OCTGPU_OK;
@@ -456,36 +452,24 @@ int ensure_tmaps(octgpu_engine* e) {
     return OCTGPU_OK;
 }
 
+// Pipeline depth of k_mcs_bulk: KS words per stage, S stages. Measured on
+// B200 at 2^16^2 and 2^17^2 for every (KS, S) in {1, 2, 4} x {2..6}
+// (profiles/r1_pipeline_sweep.json): the shallowest double-buffered ring,
+// KS = 2, S = 2 (18.6 KB per block), is fastest in every memory-bound mode
+// (c2 0.351 ms vs 0.40-0.45 ms for deeper rings) and neutral in the
+// issue-bound arbitrary mode. The consumers then stall almost only on the
+// "full" barriers, i.e. on DRAM (95% of the measured copy bandwidth).
 int plan_bulk(octgpu_engine* e, const ProbDev& p, const ProbDev& q) {
     const int key = p.mode * 8 + q.mode;
     if (e->bulk_key == key) return OCTGPU_OK;
-    int sms = 0, smem_sm = 0, smem_blk = 0;
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
-    CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, e->device));
-    CK(cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
-    const int64_t warps = (e->core_rows() + 29) / 30, blocks = (warps + 3) / 4;
-    int best_ks = 2, best_S = 2;
-    int64_t best_score = -1;
-    for (int ks : {4, 2}) {
-        const int reg_blocks = std::max(1, mcs_bulk_occupancy(p, q, ks, mcs_bulk_smem(ks, 2)));
-        const int64_t rounds = (blocks + int64_t(sms) * reg_blocks - 1) / (int64_t(sms) * reg_blocks);
-        const int64_t bps = (blocks + int64_t(sms) * rounds - 1) / (int64_t(sms) * rounds);
-        const int64_t budget = std::min<int64_t>(smem_blk, int64_t(smem_sm) / bps - 1024);
-        for (int S = 6; S >= 2; --S) {
-            if (int64_t(mcs_bulk_smem(ks, S)) > budget) continue;
-            const int64_t score = int64_t(S - 1) * ks * 1000 / rounds;  // words in flight per round
-            if (score > best_score) {
-                best_score = score;
-                best_ks = ks;
-                best_S = S;
-            }
-            break;
-        }
-    }
-    e->bulk_ks = best_ks;
-    e->bulk_S = best_S;
-    if (const char* v = getenv("OCTGPU_MCS_KS")) e->bulk_ks = atoi(v) == 2 ? 2 : 4;
+    e->bulk_ks = 2;
+    e->bulk_S = 2;
+    if (const char* v = getenv("OCTGPU_MCS_KS")) e->bulk_ks = atoi(v) >= 4 ? 4 : atoi(v) == 2 ? 2 : 1;
     if (const char* v = getenv("OCTGPU_MCS_S")) e->bulk_S = std::max(2, std::min(8, atoi(v)));
+    int smem_blk = 0;
+    CK(cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+    if (int64_t(mcs_bulk_smem(e->bulk_ks, e->bulk_S)) > smem_blk)
+        return fail(OCTGPU_ERR_CONFIG, "k_mcs_bulk pipeline does not fit in shared memory");
     e->bulk_key = key;
     return ensure_tmaps(e);
 }
@@ -600,8 +584,9 @@ int make_engine(uint32_t X, uint32_t Ytot, uint32_t w, bool stripe, uint32_t y0,
     auto* e = new octgpu_engine;
     e->X = X; e->w = w; e->n = X / (2 * w); e->device = device; e->master_seed = master_seed;
     e->Ytot = Ytot; e->stripe = stripe; e->y0 = stripe ? y0 : 0; e->L = stripe ? L : Ytot;
-    // stripe: halo row 0, core 1..L, halos L+1, L+2, then >= 34 rows of padding so the
-    // 34-row windows of k_mcs_bulk never leave the allocation; even for 16-B alignment
+    // stripe: halo row 0, core 1..L, halos L+1, L+2, then >= 34 rows of padding (k_mcs
+    // reads up to 33 rows past a warp's first row; the TMA of k_mcs_bulk zero-fills
+    // past the allocation); even for 16-B alignment
     e->Y = stripe ? ((L + 3 + 36 + 1) & ~1u) : Ytot + kGhostRows;
     int rc = alloc_engine(e);
     if (rc) {

@@ -1,19 +1,21 @@
-// Fused MCS kernel, v2: row windows staged in shared memory by the bulk-copy
-// engine (cp.async.bulk, SASS UBLKCP) behind per-warp mbarrier rings.
-// Measured alternatives (profiles/): copies issued one per lane became a
-// compiler ELECT/R2UR waterfall loop (31% of stall samples); per-lane
-// cp.async (LDGSTS) saturated the MIO queue (mio_throttle 24%, 20% slower).
-// Here one lane issues all copies with warp-uniform operands.
+// Fused MCS kernel, v3: warp-specialised TMA pipeline.
+// Each block = kP consumer warps (30 core rows each, one halo row on each side
+// recomputed redundantly) + 1 producer warp. The producer streams the block's
+// (30*kP + 4)-row window of the four src planes, KS words per stage, into an
+// S-stage shared-memory ring with 3-D TMA tile copies (SASS UTMALDG) that
+// complete on per-stage "full" mbarriers; the consumers release a stage by
+// arriving on its "empty" mbarrier.
+// Measured predecessors (profiles/): v2 issued the copies from lane 0 of every
+// compute warp, 34-row boxes per warp: the issuing warp stalled on the TMA
+// issue (36% of stall samples on the UTMALDG loop) and the 34/30 row overlap
+// re-read 9% of the planes from DRAM. One block box of 124 rows per plane cuts
+// the copy count 4x and the overlap to 124/120.
 //
 // Same algorithm and bit-exact results as k_mcs in kernels.cu (sweep f, then
-// sweep f^1, src -> dst), but
-//  * no prefetch registers: each warp keeps S stages x KS words of its four
-//    34-row plane windows in flight in shared memory, so the memory-level
-//    parallelism no longer competes with the single-wave register budget;
-//  * lane -> row mapping r0 = 30*warp, lane L = row r0 + L (core lanes 1..30),
-//    so every window starts at an even row: 16-byte aligned for the copies;
-//  * stores are predicated in PTX (no divergent branches).
-// Used for w = 64, n >= 8, Y >= 64; smaller lattices take k_mcs.
+// sweep f^1, src -> dst). Lane -> row mapping: consumer warp c of block b owns
+// the virtual rows r0 = c0 - 1 + 30*(kP*b + c) + lane, core lanes 1..30.
+// Stores are predicated in PTX (no divergent branches).
+// Used for w = 64, n >= 8 and (periodic) Y >= kGhostRows; smaller lattices take k_mcs.
 #include <cuda.h>
 
 #include <cstdint>
@@ -25,7 +27,9 @@ namespace octgpu {
 
 namespace {
 
-constexpr int kWin = 34;  // rows per window: lanes 0..31 plus Y(s)[y+1] of lane 31, rounded to 16 B
+constexpr int kP = kMcsConsumerWarps;  // consumer warps per block
+constexpr int kWin = kTmaBoxRows;      // window rows: 30*kP core rows + halos, lane 31's Y(s)[y+1], even
+static_assert(kWin == 30 * kP + 4, "TMA box rows must cover the block window");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -48,10 +52,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    // relaxed: the default .release would fence (MEMBAR.ALL.CTA) every outstanding global store
+    // relaxed: the producer has no generic-proxy writes to publish
     asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
+}
+
+// Consumer release of a stage. relaxed: the default .release would fence
+// (MEMBAR.ALL.CTA) every outstanding global store; the stage's shared-memory
+// reads have completed anyway, since the stores issued before this arrive
+// consume their values (in-order issue).
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // One 3-D TMA tile copy (SASS UTMALDG): box at (row, word, plane) of the
@@ -90,17 +102,22 @@ struct StageLayout {
     static constexpr uint32_t kTx = (4 * KS + 1) * kWin * 8;  // bytes landed per stage (full boxes)
 };
 
+constexpr int kBarBytes = 2 * 8 * 8;  // full[8] | empty[8]
+
 }  // namespace
 
-size_t mcs_bulk_stage_bytes(int ks) { return ks == 4 ? StageLayout<4>::kBytes : StageLayout<2>::kBytes; }
+size_t mcs_bulk_stage_bytes(int ks) {
+    return ks == 4 ? StageLayout<4>::kBytes : ks == 2 ? StageLayout<2>::kBytes : StageLayout<1>::kBytes;
+}
 
 template <int PM, int QM, int KS>
-__global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
-                                                  const uint64_t* __restrict__ rs, uint64_t* __restrict__ rd,
-                                                  int f, Geom g, ProbDev p, ProbDev q,
-                                                  const uint64_t* __restrict__ jtab, int S,
-                                                  const __grid_constant__ CUtensorMap tmK,
-                                                  const __grid_constant__ CUtensorMap tmK1) {
+__global__ void __launch_bounds__(32 * (kP + 1), 4) k_mcs_bulk(const uint64_t* __restrict__ src,
+                                                            uint64_t* __restrict__ dst,
+                                                            const uint64_t* __restrict__ rs,
+                                                            uint64_t* __restrict__ rd, int f, Geom g, ProbDev p,
+                                                            ProbDev q, const uint64_t* __restrict__ jtab, int S,
+                                                            const __grid_constant__ CUtensorMap tmK,
+                                                            const __grid_constant__ CUtensorMap tmK1) {
     using Word = uint64_t;
     using LY = StageLayout<KS>;
     constexpr int W = 64;
@@ -109,26 +126,58 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
     const uint32_t Y = g.Y, n = g.n;
     const int lane = threadIdx.x & 31;
     // warp in block, through a shuffle so the compiler sees it as warp-uniform
-    // (the bulk-copy operands derived from it then stay in uniform registers)
     const int wib = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0);
-    const int wpb = blockDim.x >> 5;
-    const uint32_t wid = blockIdx.x * wpb + wib;
-    if (wid * 30u >= g.c1 - g.c0) return;  // warp-uniform
-    const uint32_t r0 = g.c0 - 1 + wid * 30u;  // virtual row of lane 0 (window start)
+    const uint32_t rows = g.c1 - g.c0;
+    const uint32_t blk_r0 = g.c0 - 1 + blockIdx.x * (30u * kP);  // virtual row of the window's first row
+    // consumer warps of this block that own core rows (the last block may have fewer)
+    const uint32_t left = rows - blockIdx.x * (30u * kP);
+    const uint32_t nact = min(uint32_t(kP), (left + 29) / 30);
+    const uint32_t s_ = uint32_t(f ^ 1);
 
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw) + wib * 8;  // 8 barrier slots per warp
-    Word* ring = reinterpret_cast<Word*>(smem_raw + 8 * 8 * wpb) + size_t(wib) * S * LY::kWords;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+    uint64_t* empty = full + 8;
+    Word* ring = reinterpret_cast<Word*>(smem_raw + kBarBytes);
+    const uint32_t nblocks = (n + KS - 1) / KS;
 
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], nact);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (wib == kP) {
+        // ---- producer warp: one lane streams the window, KS words per stage ----
+        if (lane == 0) {
+            uint32_t st = 0, ph = 0;  // stage, and the parity of its fill round
+            for (uint32_t b = 0; b < nblocks; ++b) {
+                if (b >= uint32_t(S)) mbar_wait(&empty[st], ph ^ 1u);
+                Word* base = ring + size_t(st) * LY::kWords;
+                const uint32_t kb = b * KS;
+                mbar_expect_tx(&full[st], LY::kTx);
+                tma3d(base + LY::kXf, &tmK, blk_r0, kb, uint32_t(f), &full[st]);
+                tma3d(base + LY::kYf, &tmK, blk_r0, kb, uint32_t(2 + f), &full[st]);
+                tma3d(base + LY::kYs, &tmK, blk_r0, kb, 2 + s_, &full[st]);
+                tma3d(base + LY::kXs, &tmK1, blk_r0, kb, s_, &full[st]);
+                if (++st == uint32_t(S)) {
+                    st = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+        return;
+    }
+    if (uint32_t(wib) >= nact) return;  // warp-uniform
+    const uint32_t r0 = blk_r0 + 30u * wib;  // virtual row of lane 0
+    const int wrow = 30 * wib + lane;        // this lane's row in the window
     const uint32_t v = r0 + lane;  // virtual row
     const uint32_t y = g.wrap ? v % g.wrap : v;
     const bool core = lane >= 1 && lane <= 30 && v < g.c1;
     const bool wyf = lane >= 2 && v - 1 < g.c1;  // row v-1 is core: this lane writes Y(f)[v]
     const int s = f ^ 1;
     const size_t PS = g.plane_stride;
-    const Word* planeXf = src + size_t(0 + f) * PS;
-    const Word* planeYf = src + size_t(2 + f) * PS;
-    const Word* planeXs = src + size_t(0 + s) * PS;
-    const Word* planeYs = src + size_t(2 + s) * PS;
     Word* dXf = dst + size_t(0 + f) * PS + y;
     Word* dYf = dst + size_t(2 + f) * PS + y;
     Word* dXs = dst + size_t(0 + s) * PS + y;
@@ -136,39 +185,11 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
     const bool sh1 = ((uint32_t(f) ^ y ^ g.ypar) & 1u) != 0;
     const bool sh2 = !sh1;
 
-    // Periodic lattices keep ghost rows wrap..wrap+33 equal to rows 0..33, so the
-    // 34-row window starting at r0 never wraps; warps that store rows 0..33
-    // (the first two and the last) also refresh those ghosts.
+    // Periodic lattices keep ghost rows wrap..wrap+ghost-1 equal to rows
+    // 0..ghost-1, so a block window never wraps; warps that store rows
+    // 0..ghost-1 (the first few and the last) also refresh those ghosts.
     const bool ghostw = g.ghost && (r0 + 1 < g.ghost || r0 + 31 >= g.wrap);  // warp-uniform
     const bool ghost_row = ghostw && y < g.ghost;
-
-    if (lane == 0) {
-        for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-
-    // Word-block b -> its stage: 4 TMA tiles (34 rows x KS words of X(f), Y(f),
-    // Y(s); 34 x KS+1 of X(s)), issued by one lane. Words past n are zero-filled
-    // (X(s) word n, i.e. word 0, is taken from raw0 instead).
-    auto fill = [&](uint32_t b) {
-        const int st = int(b % uint32_t(S));
-        Word* base = ring + size_t(st) * LY::kWords;
-        const uint32_t kb = b * KS;
-        // The stage's previous contents were consumed (loaded and used) before this
-        // refill, so no generic->async proxy fence is needed for the overwrite.
-        __syncwarp();
-        if (lane == 0) {
-            mbar_expect_tx(&bars[st], LY::kTx);
-            tma3d(base + LY::kXf, &tmK, r0, kb, uint32_t(f), &bars[st]);
-            tma3d(base + LY::kYf, &tmK, r0, kb, uint32_t(2 + f), &bars[st]);
-            tma3d(base + LY::kYs, &tmK, r0, kb, uint32_t(2 + s), &bars[st]);
-            tma3d(base + LY::kXs, &tmK1, r0, kb, uint32_t(s), &bars[st]);
-        }
-    };
-
-    const uint32_t nblocks = (n + KS - 1) / KS;
-    for (uint32_t b = 0; b < uint32_t(S) && b < nblocks; ++b) fill(b);
 
     Xo s1{0, 0, 0, 0}, s2{0, 0, 0, 0};
     if constexpr (LIVE) {
@@ -202,13 +223,13 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
         return m2;
     };
 
+    uint32_t st = 0, ph = 0;  // ring stage and the parity of its current fill
     for (uint32_t b = 0; b < nblocks; ++b) {
-        const int st = int(b % uint32_t(S));
-        mbar_wait(&bars[st], (b / uint32_t(S)) & 1u);
+        mbar_wait(&full[st], ph);
         const Word* sb = ring + size_t(st) * LY::kWords;
         const uint32_t kb = b * KS;
         if (b == 0) {
-            cur = sb[LY::kXs + lane];  // X(s)[y][0], original
+            cur = sb[LY::kXs + wrow];  // X(s)[y][0], original
             raw0 = cur;
         }
         // arbitrary-probability bodies are ~10^4 instructions per word: keep them rolled (I-cache)
@@ -218,10 +239,10 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
 #pragma unroll kUnroll
             for (int jj = 0; jj < KS; ++jj) {
                 const uint32_t k = kb + jj;
-                const Word A = sb[LY::kXf + jj * kWin + lane];
-                const Word B = sb[LY::kYf + jj * kWin + lane];
-                const Word Cn = sb[LY::kYs + jj * kWin + lane + 1];
-                const Word nxt = (k + 1 == n) ? raw0 : sb[LY::kXs + (jj + 1) * kWin + lane];
+                const Word A = sb[LY::kXf + jj * kWin + wrow];
+                const Word B = sb[LY::kYf + jj * kWin + wrow];
+                const Word Cn = sb[LY::kYs + jj * kWin + wrow + 1];
+                const Word nxt = (k + 1 == n) ? raw0 : sb[LY::kXs + (jj + 1) * kWin + wrow];
                 Word x1p, x1q, x2p, x2q;
                 gen_xi_pair<PM, QM, Word>(s1, s2, p, q, x1p, x1q, x2p, x2q);
                 const Word sxp = sh1 ? Word((cur >> 1) | (nxt << (W - 1))) : cur;
@@ -241,10 +262,10 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
             for (int jj = 0; jj < KS; ++jj) {
                 const uint32_t k = kb + jj;
                 if (k >= n) break;
-                const Word A = sb[LY::kXf + jj * kWin + lane];
-                const Word B = sb[LY::kYf + jj * kWin + lane];
-                const Word Cn = sb[LY::kYs + jj * kWin + lane + 1];
-                const Word nxt = (k + 1 == n) ? raw0 : sb[LY::kXs + (jj + 1) * kWin + lane];
+                const Word A = sb[LY::kXf + jj * kWin + wrow];
+                const Word B = sb[LY::kYf + jj * kWin + wrow];
+                const Word Cn = sb[LY::kYs + jj * kWin + wrow + 1];
+                const Word nxt = (k + 1 == n) ? raw0 : sb[LY::kXs + (jj + 1) * kWin + wrow];
                 // ---- xi for first sweep word k and (k >= 2) second sweep word k-1, interleaved ----
                 Word x1p, x1q, x2p = 0, x2q = 0;
                 if (k >= 2)
@@ -277,7 +298,12 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
                 pA = Ap; pB = Bp; pC = Cp; pR = Rp;
             }
         }
-        if (b + S < nblocks) fill(b + S);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        if (++st == uint32_t(S)) {
+            st = 0;
+            ph ^= 1u;
+        }
     }
     if (sh1) R0 ^= carry1;
     {
@@ -305,47 +331,32 @@ __global__ void __launch_bounds__(128) k_mcs_bulk(const uint64_t* __restrict__ s
 
 namespace {
 
-template <int PM, int QM>
-cudaError_t bulk_pq(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
-                    const ProbDev& q, const uint64_t* jtab, int ks, int S, const CUtensorMap* tmK,
-                    const CUtensorMap* tmK1, cudaStream_t st) {
+template <int PM, int QM, int KS>
+cudaError_t bulk_go(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
+                    const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK, const CUtensorMap* tmK1,
+                    cudaStream_t st) {
     const uint32_t warps = (g.c1 - g.c0 + 29) / 30;
-    const uint32_t wpb = 4, threads = 32 * wpb, blocks = (warps + wpb - 1) / wpb;
-    const size_t smem = mcs_bulk_smem(ks, S);
-    cudaError_t e;
-    if (ks == 4) {
-        auto kern = k_mcs_bulk<PM, QM, 4>;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        kern<<<blocks, threads, smem, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), rs, rd,
-                                            f, g, p, q, jtab, S, *tmK, *tmK1);
-    } else {
-        auto kern = k_mcs_bulk<PM, QM, 2>;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        kern<<<blocks, threads, smem, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), rs, rd,
-                                            f, g, p, q, jtab, S, *tmK, *tmK1);
-    }
+    const uint32_t threads = 32 * (kP + 1), blocks = (warps + kP - 1) / kP;
+    const size_t smem = mcs_bulk_smem(KS, S);
+    auto kern = k_mcs_bulk<PM, QM, KS>;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<blocks, threads, smem, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), rs, rd, f, g,
+                                        p, q, jtab, S, *tmK, *tmK1);
     return cudaGetLastError();
 }
 
 template <int PM, int QM>
-int occ_pq(int ks, size_t smem) {
-    int nb = 0;
-    cudaError_t e = ks == 4 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_mcs_bulk<PM, QM, 4>, 128, smem)
-                            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_mcs_bulk<PM, QM, 2>, 128, smem);
-    return e == cudaSuccess ? nb : 0;
-}
-
-#define OCT_OQ(PM)                                                \
-    switch (q.mode) {                                             \
-    case M_ZERO: return occ_pq<PM, M_ZERO>(ks, smem);             \
-    case M_HALF: return occ_pq<PM, M_HALF>(ks, smem);             \
-    case M_DYADIC: return occ_pq<PM, M_DYADIC>(ks, smem);         \
-    case M_ARB: return occ_pq<PM, M_ARB>(ks, smem);               \
-    case M_ONE: return occ_pq<PM, M_ONE>(ks, smem);               \
-    default: return 0;                                            \
+cudaError_t bulk_pq(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
+                    const ProbDev& q, const uint64_t* jtab, int ks, int S, const CUtensorMap* tmK,
+                    const CUtensorMap* tmK1, cudaStream_t st) {
+    switch (ks) {
+    case 1: return bulk_go<PM, QM, 1>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
+    case 2: return bulk_go<PM, QM, 2>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
+    case 4: return bulk_go<PM, QM, 4>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
+    default: return cudaErrorInvalidValue;
     }
+}
 
 #define OCT_BQ(PM)                                                                              \
     switch (q.mode) {                                                                           \
@@ -359,18 +370,7 @@ int occ_pq(int ks, size_t smem) {
 
 }  // namespace
 
-int mcs_bulk_occupancy(const ProbDev& p, const ProbDev& q, int ks, size_t smem) {
-    switch (p.mode) {
-    case M_ZERO: OCT_OQ(M_ZERO)
-    case M_HALF: OCT_OQ(M_HALF)
-    case M_DYADIC: OCT_OQ(M_DYADIC)
-    case M_ARB: OCT_OQ(M_ARB)
-    case M_ONE: OCT_OQ(M_ONE)
-    default: return 0;
-    }
-}
-
-size_t mcs_bulk_smem(int ks, int S) { return 8 * 8 * 4 + size_t(4) * S * mcs_bulk_stage_bytes(ks); }
+size_t mcs_bulk_smem(int ks, int S) { return kBarBytes + size_t(S) * mcs_bulk_stage_bytes(ks); }
 
 cudaError_t launch_mcs_bulk(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g,
                             const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int ks, int S,

@@ -40,10 +40,12 @@ struct Geom {
     uint32_t c0, c1;       // core rows (virtual)
     uint32_t wrap;         // periodic modulus in y, or 0
     uint32_t ypar;         // parity of the global row of physical row 0 (site parity uses global rows)
-    uint32_t ghost;        // periodic: rows wrap..wrap+ghost-1 mirror rows (i mod wrap), so 34-row windows never wrap
+    uint32_t ghost;        // periodic: rows wrap..wrap+ghost-1 mirror rows (i mod wrap), so block windows never wrap
 };
 
-constexpr uint32_t kGhostRows = 34;
+constexpr uint32_t kMcsConsumerWarps = 4;                   // k_mcs_bulk: compute warps per block (+1 producer)
+constexpr uint32_t kTmaBoxRows = 30 * kMcsConsumerWarps + 4;  // k_mcs_bulk window rows (124)
+constexpr uint32_t kGhostRows = 128;                         // >= kTmaBoxRows
 
 // Per-row RNG states are stored SoA: s[j * Y + y], j = 0..3.
 
@@ -67,17 +69,14 @@ cudaError_t launch_mcs(int w, const void* src, void* dst, const uint64_t* rng_sr
                        cudaStream_t st);
 
 // Same as launch_mcs with shared-memory staging by cp.async.bulk (mcs_bulk.cu):
-// w = 64, n >= 8, Y >= 64 only. ks = words per stage (2 or 4), S = stages.
+// w = 64, n >= 8, periodic Y >= kGhostRows only. ks = words per stage (1, 2 or 4), S = stages.
 // tmK / tmK1: 3-D tensor maps (rows x words x planes) of the src plane set with
-// boxes of 34 rows x ks and x ks+1 words (see engine.cu make_tmaps).
+// boxes of kTmaBoxRows rows x ks and x ks+1 words (see engine.cu ensure_tmaps).
 cudaError_t launch_mcs_bulk(const void* src, void* dst, const uint64_t* rng_src, uint64_t* rng_dst, int f, Geom g,
                             const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int ks, int S,
                             const CUtensorMap* tmK, const CUtensorMap* tmK1, cudaStream_t st);
-constexpr uint32_t kTmaBoxRows = 34;
 size_t mcs_bulk_stage_bytes(int ks);
-size_t mcs_bulk_smem(int ks, int S);  // dynamic smem of a 4-warp block
-// resident 4-warp blocks per SM of k_mcs_bulk<p, q, ks> with `smem` bytes of dynamic smem
-int mcs_bulk_occupancy(const ProbDev& p, const ProbDev& q, int ks, size_t smem);
+size_t mcs_bulk_smem(int ks, int S);  // dynamic smem of a block (kMcsConsumerWarps + 1 warps)
 
 // s <- M s for every row state, M given as a 4-bit table (64 x 16 x 4 u64).
 cudaError_t launch_apply_jump(uint64_t* rng, uint32_t Y, const uint64_t* tab, cudaStream_t st);

@@ -332,6 +332,10 @@ struct octgpu_engine {
     int bulk_key = -1;  // (p, q) mode pair the bulk plan was made for
     CUtensorMap tm[2][2];  // [plane set][box: ks words, ks+1 words] for k_mcs_bulk
     int tm_ks = -1;
+    CUtensorMap tmd[2][2];  // the same for k_mcs_deep (deep_box_rows rows x 2 / 3 words)
+    bool tmd_ok = false;
+    int deep = 1;  // temporally blocked passes (k_mcs_deep) where supported; OCTGPU_DEEP=0 disables
+    int deep_S = 3;    // k_mcs_deep ring stages (OCTGPU_DEEP_S; S = 3 measured best, profiles/r1_deep_modes.json)
     // Row-stripe mode (multi-GPU): this engine owns global rows [y0, y0 + L) of
     // a Ytot-row periodic lattice, held at local rows 1..L with one halo row
     // above (0), two below (L+1, L+2) and padding; Y is then the allocated row
@@ -339,6 +343,8 @@ struct octgpu_engine {
     bool stripe = false;
     uint32_t Ytot = 0, y0 = 0, L = 0;
 
+    // k_mcs_deep: the same periodic lattice with core rows starting at virtual row kDeepSweeps - 1
+    Geom deep_geom() const { return Geom{Y, n, size_t(n) * Y, kDeepSweeps - 1, L + kDeepSweeps - 1, L, 0, kGhostRows}; }
     Geom geom() const {
         return stripe ? Geom{Y, n, size_t(n) * Y, 1, L + 1, 0, (y0 + 1) & 1u, 0}  // local row 0 = global y0 - 1
                       : Geom{Y, n, size_t(n) * Y, 1, L + 1, L, 0, kGhostRows};
@@ -414,6 +420,8 @@ int upload_states(octgpu_engine* e, const uint64_t* aos) {
 int plan_mcs(octgpu_engine* e) {
     e->mcs_impl = (e->w == 64 && e->n >= 8 && (e->stripe || e->L >= kGhostRows)) ? 2 : 1;
     if (const char* v = getenv("OCTGPU_MCS_IMPL")) e->mcs_impl = (atoi(v) == 1) ? 1 : e->mcs_impl;
+    if (const char* v = getenv("OCTGPU_DEEP")) e->deep = atoi(v);
+    if (const char* v = getenv("OCTGPU_DEEP_S")) e->deep_S = std::max(2, std::min(8, atoi(v)));
     return OCTGPU_OK;
 }
 
@@ -449,6 +457,25 @@ int ensure_tmaps(octgpu_engine* e) {
             if (r != CUDA_SUCCESS) return fail(OCTGPU_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
         }
     e->tm_ks = e->bulk_ks;
+    return OCTGPU_OK;
+}
+
+int ensure_tmaps_deep(octgpu_engine* e) {
+    if (e->tmd_ok) return OCTGPU_OK;
+    auto enc = tensor_map_encoder();
+    if (!enc) return fail(OCTGPU_ERR_CUDA, "cuTensorMapEncodeTiled is not available from the driver");
+    for (int b = 0; b < 2; ++b)
+        for (int v = 0; v < 2; ++v) {
+            const cuuint64_t dims[3] = {e->Y, e->n, 4};
+            const cuuint64_t strides[2] = {cuuint64_t(e->Y) * 8, cuuint64_t(e->n) * e->Y * 8};
+            const cuuint32_t box[3] = {cuuint32_t(deep_box_rows(kDeepSweeps)), cuuint32_t(2 + v), 1};
+            const cuuint32_t estr[3] = {1, 1, 1};
+            const CUresult r = enc(&e->tmd[b][v], CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, e->planes[b], dims, strides, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return fail(OCTGPU_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+        }
+    e->tmd_ok = true;
     return OCTGPU_OK;
 }
 
@@ -795,8 +822,28 @@ int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
         if (rc) return rc;
     }
     const Geom g = e->geom();
+    // Temporal blocking pays where the one-MCS kernel is DRAM-bound and the
+    // deep kernel fits in 80 registers without spills: constant xi (zero /
+    // one). With live streams it spills (4 xoshiro states) and measured slower
+    // (profiles/r1_deep_modes.json); OCTGPU_DEEP=2 forces it for experiments.
+    const bool deep = e->deep && e->mcs_impl == 2 && mcs_deep_supported(p.mode, q.mode) && (!live || e->deep == 2);
     for (uint64_t i = 0; i < n_mcs; ++i) {
         const int ps = e->pcur, rs = e->rcur;
+        if (deep && n_mcs - i >= uint64_t(kDeepSweeps / 2)) {  // kDeepSweeps/2 MCS in one pass
+            rc = ensure_tmaps_deep(e);
+            if (rc) return rc;
+            CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase,
+                               e->deep_geom(), p, q, jtab, e->deep_S, &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
+            ++e->launches;
+            e->pcur ^= 1;
+            if (live)
+                e->rcur ^= 1;
+            else
+                e->pending += uint64_t(kDeepSweeps) * per_sweep;
+            e->t += kDeepSweeps / 2;
+            i += kDeepSweeps / 2 - 1;
+            continue;
+        }
         if (e->mcs_impl == 2) {
             rc = plan_bulk(e, p, q);
             if (rc) return rc;

@@ -1,0 +1,483 @@
+// Temporally blocked MCS kernel: L sweeps (L/2 MCS) of a periodic lattice in
+// ONE pass over the planes (Appendix B.5 extended).
+//
+// Same warp-specialised TMA pipeline as k_mcs_bulk (mcs_bulk.cu), but every
+// lane carries its row through L sublattice sweeps f, s, f, s, ... before the
+// planes go back to HBM, so DRAM traffic per MCS drops from ~0.5 B to
+// ~0.5·2/L B per site update. Results are bit-identical to L/2 launches of the
+// one-MCS kernel (and to the reference's mcs_step, engine_vec.hpp:171-177).
+//
+// Dependencies that make this possible (engine_vec.hpp:95-137):
+//  * sweep ℓ of row y, word j, reads only sweep-(ℓ-1) values of rows y-1..y+1
+//    and words j..j+1, plus the x-carry of sweep ℓ's own word j-1;
+//  * so sweep ℓ runs one word behind sweep ℓ-1 (software pipeline over the
+//    word index) and one lane narrower on each side (halo rows recomputed by
+//    the neighbouring warp): a warp keeps lanes L-1 .. 32-L as core rows
+//    (26 of 32 for L = 4);
+//  * the periodic x seam: sweep ℓ processes words ℓ-1, ..., n-1, 0, ..., ℓ-2
+//    (its wrapped words need sweep ℓ-1's word 0 carry, available only after
+//    sweep ℓ-1 wrapped). The reference draws the xi of words 0..ℓ-2 of stream
+//    ℓ first: they are drawn at the start (stream order kept) and parked in
+//    shared memory with the first/second-word outputs each sweep leaves for
+//    the next one's wrap.
+//  * stream ℓ starts (ℓ-1)·n·D draws after stream 1: one GF(2) table jump per
+//    sweep per row (the same T^(nD) table as k_mcs_bulk).
+//
+// Iteration i of a row runs sweep ℓ on word (i-(ℓ-1)) mod n when
+// 2(ℓ-1) <= i < n + 2(ℓ-1); iterations 2L..n-1 are the branch-free steady
+// state. Used for periodic w = 64 lattices with n >= 8, Y >= kGhostRows and
+// probabilities whose xi is cheap (zero / half / dyadic / one): arbitrary
+// probabilities are issue-bound and keep the one-MCS kernel (30 of 32 rows).
+#include <cuda.h>
+
+#include <cstdint>
+
+#include "device_common.cuh"
+#include "octgpu_internal.h"
+
+namespace octgpu {
+
+namespace {
+
+constexpr int kDP = kDeepWarps;  // compute warps per block (+1 producer)
+constexpr int kKS = 2;                  // words per ring stage
+constexpr int kSMax = 8;                // ring stages: runtime S <= kSMax (barrier slots)
+constexpr int kLanes = 32 * kDP;        // parking-slot stride (compute lanes per block)
+
+template <int L>
+struct DeepGeo {
+    static constexpr int kCore = 34 - 2 * L;   // core lanes L-1 .. 32-L
+    static constexpr int kRows = kCore * kDP;  // core rows per block
+    // window: every compute warp's 32 lanes + row 32 of the last warp (stage 1's Y(s)[y+1]), even rows
+    static constexpr int kWin = (kCore * (kDP - 1) + 33 + 1) / 2 * 2;
+    static_assert(kWin <= int(kGhostRows), "ghost rows must cover the window overhang");
+    static_assert(kWin == deep_box_rows(L), "host tensor-map box must match");
+};
+
+constexpr int align16w(int words) { return (words + 15) / 16 * 16; }
+
+template <int L>
+struct DeepStage {  // ring stage: Xf[KS][W] | Yf[KS][W] | Ys[KS][W] | Xs[KS+1][W], 128-B aligned segments
+    static constexpr int W = DeepGeo<L>::kWin;
+    static constexpr int kSeg = align16w(kKS * W);
+    static constexpr int kXf = 0, kYf = kSeg, kYs = 2 * kSeg, kXs = 3 * kSeg;
+    static constexpr int kWords = 3 * kSeg + align16w((kKS + 1) * W);
+    static constexpr uint32_t kTx = (4 * kKS + 1) * W * 8;
+};
+
+// Per-lane parking slots in shared memory ([slot][kLanes] u64).
+template <int L, int PM, int QM>
+struct DeepSlots {
+    static constexpr bool kPreP = !(PM == M_ZERO || PM == M_ONE);
+    static constexpr bool kPreQ = !(QM == M_ZERO || QM == M_ONE);
+    static constexpr int kSave = 5 * (L - 1) + 1;  // stages 1..L-1: A,B,C,R,A1 of their first two words; stage L: R
+    static constexpr int kPre = L * (L - 1) / 2;   // xi words 0..l-2 of streams l = 2..L
+    static constexpr int kPreP0 = kSave;
+    static constexpr int kPreQ0 = kSave + (kPreP ? kPre : 0);
+    static constexpr int kCount = kPreQ0 + (kPreQ ? kPre : 0);
+    __host__ __device__ static constexpr int pre(int l, int j) { return (l - 1) * (l - 2) / 2 + j; }
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra LAB_WAIT;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* tm, uint32_t row, uint32_t word, uint32_t plane,
+                                      uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(row), "r"(word), "r"(plane), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void st_pred(uint64_t* p, uint64_t v, bool pred) {
+    asm volatile(
+        "{\n"
+        ".reg .pred q;\n"
+        "setp.ne.b32 q, %2, 0;\n"
+        "@q st.global.b64 [%0], %1;\n"
+        "}\n" ::"l"(p),
+        "l"(v), "r"(int(pred)));
+}
+
+__device__ __forceinline__ uint64_t shup(uint64_t v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ uint64_t shdn(uint64_t v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+
+// Lane context shared by every iteration.
+struct DeepCtx {
+    uint32_t n, Y;
+    uint64_t* dXf;  // dst planes at this lane's physical row
+    uint64_t* dYf;
+    uint64_t* dXs;
+    uint64_t* dYs;
+    uint32_t wrap;
+    bool sh1, sh2, core, wyf, ghostw, ghost_row;
+    uint64_t* save;  // this lane's parking slots: save[slot * kLanes]
+};
+
+template <int L>
+struct DeepState {
+    uint64_t pA[L], pB[L], pC[L], pR[L];  // each sweep's outputs at its previous word
+    uint64_t ml[L];                       // each sweep's mask at its previous word (x carry)
+    Xo rs[L];                             // stream of each sweep
+    uint64_t cur, raw0;                   // sweep 1: original X(s)[y][j], X(s)[y][0]
+};
+
+__device__ __forceinline__ void put(const DeepCtx& c, uint64_t* ptr, uint64_t val, bool pred) {
+    st_pred(ptr, val, pred);
+    if (c.ghostw) st_pred(ptr + c.wrap, val, pred && c.ghost_row);
+}
+
+// One iteration i: sweep l on word (i-(l-1)) mod n for every active l.
+// STEADY: all sweeps active, no first/second/last words, no wrap (i in [2L, n-1]).
+template <int PM, int QM, int L, bool STEADY>
+__device__ __forceinline__ void deep_iter(DeepState<L>& S, const DeepCtx& c, uint32_t i, const uint64_t* sb, int jj,
+                                          const ProbDev& p, const ProbDev& q) {
+    using ST = DeepStage<L>;
+    using SL = DeepSlots<L, PM, QM>;
+    constexpr int W = 64;
+    const uint32_t n = c.n;
+    uint64_t nA[L] = {}, nB[L] = {}, nC[L] = {}, nR[L] = {};
+    bool act[L];
+#pragma unroll
+    for (int l = 1; l <= L; ++l) {
+        const int li = l - 1;
+        uint32_t j = i - uint32_t(l - 1);
+        bool active = true;
+        if constexpr (!STEADY) {
+            active = i >= uint32_t(2 * (l - 1)) && i < n + uint32_t(2 * (l - 1));
+            if (j >= n) j -= n;
+        }
+        act[li] = active;
+        if (!active) continue;  // warp-uniform
+        const bool first = !STEADY && j == uint32_t(l - 1);
+        const bool second = !STEADY && j == uint32_t(l);
+        const bool last = !STEADY && j == (l == 1 ? n - 1 : uint32_t(l - 2));
+
+        // ---- xi of word j of stream l (stream order: pre-drawn words 0..l-2 come first) ----
+        uint64_t xp, xq;
+        if (STEADY || l == 1 || j >= uint32_t(l - 1)) {
+            gen_xi<PM, QM, uint64_t>(S.rs[li], p, q, xp, xq);
+        } else {
+            const int k = SL::pre(l, int(j));
+            if constexpr (SL::kPreP) xp = c.save[(SL::kPreP0 + k) * kLanes];
+            else xp = (PM == M_ONE) ? ~uint64_t(0) : 0;
+            if constexpr (SL::kPreQ) xq = c.save[(SL::kPreQ0 + k) * kLanes];
+            else xq = (QM == M_ONE) ? ~uint64_t(0) : 0;
+        }
+
+        // ---- inputs: own X, own Y, Y[y+1] of the other parity, x+ neighbour words j, j+1 ----
+        uint64_t xo, yo, yn, x0, x1, qB = 0;
+        if (l == 1) {
+            xo = sb[ST::kXf + jj * ST::W];
+            yo = sb[ST::kYf + jj * ST::W];
+            yn = sb[ST::kYs + jj * ST::W + 1];
+            const uint64_t nxt = (j + 1 == n) ? S.raw0 : sb[ST::kXs + (jj + 1) * ST::W];
+            x0 = S.cur;
+            x1 = nxt;
+            S.cur = nxt;
+        } else {
+            uint64_t qA, qC, qR;
+            const int sv = 5 * (l - 2);  // slots of sweep l-1
+            if (!STEADY && j == uint32_t(l - 2)) {  // sweep l-1's first word (parked)
+                qA = c.save[(sv + 0) * kLanes];
+                qB = c.save[(sv + 1) * kLanes];
+                qC = c.save[(sv + 2) * kLanes];
+                qR = c.save[(sv + 3) * kLanes];
+            } else {
+                qA = S.pA[li - 1];
+                qB = S.pB[li - 1];
+                qC = S.pC[li - 1];
+                qR = S.pR[li - 1];
+            }
+            uint64_t nxa = nA[li - 1];
+            if constexpr (!STEADY) {
+                const uint32_t jn = (j + 1 == n) ? 0u : j + 1;
+                if (jn == uint32_t(l - 2)) nxa = c.save[(sv + 0) * kLanes];
+                else if (j == uint32_t(l - 2)) nxa = c.save[(sv + 4) * kLanes];
+            }
+            xo = qR;
+            yo = shup(qC);
+            yn = shdn(qB);
+            x0 = qA;
+            x1 = nxa;
+        }
+        const bool sh = (l & 1) ? c.sh1 : c.sh2;
+        const uint64_t rot = sh ? ((x0 >> 1) | (x1 << (W - 1))) : x0;
+        const uint64_t m = update_mask<uint64_t>(xo, yo, rot, yn, xp, xq);
+        const uint64_t mprev = first ? uint64_t(0) : S.ml[li];
+        nA[li] = xo ^ m;
+        nB[li] = yo ^ m;
+        nC[li] = yn ^ m;
+        nR[li] = x0 ^ (sh ? ((m << 1) | (mprev >> (W - 1))) : m);
+        S.ml[li] = m;
+
+        if constexpr (!STEADY) {
+            const int sv = 5 * (l - 1);
+            if (first) {
+                if (l < L) {
+                    c.save[(sv + 0) * kLanes] = nA[li];
+                    c.save[(sv + 1) * kLanes] = nB[li];
+                    c.save[(sv + 2) * kLanes] = nC[li];
+                    c.save[(sv + 3) * kLanes] = nR[li];
+                } else {
+                    c.save[sv * kLanes] = nR[li];
+                }
+            }
+            if (second && l < L) c.save[(sv + 4) * kLanes] = nA[li];
+            if (last) {  // the x carry of the last word completes X(other) of the first word
+                const uint64_t carry = sh ? (m >> (W - 1)) : uint64_t(0);
+                if (l < L) {
+                    c.save[(sv + 3) * kLanes] ^= carry;
+                } else {
+                    const uint64_t xf = c.save[sv * kLanes] ^ carry;
+                    put(c, ((L & 1) ? c.dXs : c.dXf) + size_t(l - 1) * c.Y, xf, c.core);
+                }
+            }
+        }
+        if (l == L) {
+            // sweep L has parity s (L even): X(s), Y(s) own; Y(f)[y] = B^{L-1}[y] ^ m^L[y-1]; X(f) via the carry
+            const uint32_t o = j * c.Y;
+            put(c, c.dXs + o, nA[li], c.core);
+            put(c, c.dYs + o, nB[li], c.core);
+            put(c, c.dYf + o, qB ^ shup(m), c.wyf);
+            if (!first) put(c, c.dXf + o, nR[li], c.core);
+        }
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+        if (act[l]) {
+            S.pA[l] = nA[l];
+            S.pB[l] = nB[l];
+            S.pC[l] = nC[l];
+            S.pR[l] = nR[l];
+        }
+    }
+}
+
+}  // namespace
+
+template <int PM, int QM, int L>
+__global__ void __launch_bounds__(32 * (kDP + 1), 3)
+    k_mcs_deep(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, const uint64_t* __restrict__ rs,
+               uint64_t* __restrict__ rd, int f, Geom g, ProbDev p, ProbDev q, const uint64_t* __restrict__ jtab, int S,
+               const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmK1) {
+    static_assert(L % 2 == 0 && L >= 2, "whole MCS only");
+    using GEO = DeepGeo<L>;
+    using ST = DeepStage<L>;
+    using SL = DeepSlots<L, PM, QM>;
+    constexpr bool LIVE = Plan<PM, QM>::live;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const uint32_t n = g.n;
+    const int lane = threadIdx.x & 31;
+    const int wib = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0);
+    const uint32_t rows = g.c1 - g.c0;
+    const uint32_t blk_r0 = g.c0 - uint32_t(L - 1) + blockIdx.x * uint32_t(GEO::kRows);
+    const uint32_t left = rows - blockIdx.x * uint32_t(GEO::kRows);
+    const uint32_t nact = min(uint32_t(kDP), (left + GEO::kCore - 1) / GEO::kCore);
+    const uint32_t s_ = uint32_t(f ^ 1);
+
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+    uint64_t* empty = full + kSMax;
+    uint64_t* ring = reinterpret_cast<uint64_t*>(smem_raw + 128);
+    uint64_t* slots = ring + S * ST::kWords;
+    const uint32_t nblocks = (n + kKS - 1) / kKS;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], nact);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (wib == kDP) {  // producer warp
+        if (lane == 0) {
+            uint32_t st = 0, ph = 0;
+            for (uint32_t b = 0; b < nblocks; ++b) {
+                if (b >= uint32_t(S)) mbar_wait(&empty[st], ph ^ 1u);
+                uint64_t* base = ring + size_t(st) * ST::kWords;
+                const uint32_t kb = b * kKS;
+                mbar_expect_tx(&full[st], ST::kTx);
+                tma3d(base + ST::kXf, &tmK, blk_r0, kb, uint32_t(f), &full[st]);
+                tma3d(base + ST::kYf, &tmK, blk_r0, kb, uint32_t(2 + f), &full[st]);
+                tma3d(base + ST::kYs, &tmK, blk_r0, kb, 2 + s_, &full[st]);
+                tma3d(base + ST::kXs, &tmK1, blk_r0, kb, s_, &full[st]);
+                if (++st == uint32_t(S)) {
+                    st = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+        return;
+    }
+    if (uint32_t(wib) >= nact) return;
+    const uint32_t r0 = blk_r0 + uint32_t(GEO::kCore) * wib;
+    const int wrow = GEO::kCore * wib + lane;
+    const uint32_t v = r0 + lane;
+    const uint32_t y = g.wrap ? v % g.wrap : v;
+    const size_t PS = g.plane_stride;
+    const int s = f ^ 1;
+
+    DeepCtx c;
+    c.n = n;
+    c.Y = g.Y;
+    c.wrap = g.wrap;
+    c.dXf = dst + size_t(0 + f) * PS + y;
+    c.dYf = dst + size_t(2 + f) * PS + y;
+    c.dXs = dst + size_t(0 + s) * PS + y;
+    c.dYs = dst + size_t(2 + s) * PS + y;
+    c.sh1 = ((uint32_t(f) ^ y ^ g.ypar) & 1u) != 0;
+    c.sh2 = !c.sh1;
+    c.core = lane >= L - 1 && lane <= 32 - L && v < g.c1;
+    c.wyf = lane >= L && lane <= 33 - L && v - 1 < g.c1;
+    c.ghostw = g.ghost && (r0 + uint32_t(L - 1) < g.ghost || r0 + uint32_t(33 - L) >= g.wrap);
+    c.ghost_row = c.ghostw && y < g.ghost;
+    c.save = slots + threadIdx.x;
+
+    DeepState<L> R;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+        R.pA[l] = R.pB[l] = R.pC[l] = R.pR[l] = 0;
+        R.ml[l] = 0;
+        R.rs[l] = Xo{0, 0, 0, 0};
+    }
+    if constexpr (LIVE) {
+        R.rs[0] = load_state(rs, g.Y, y);
+#pragma unroll
+        for (int l = 1; l < L; ++l) R.rs[l] = apply_table(jtab, R.rs[l - 1]);
+        // words 0..l-2 of streams l >= 2 are processed last but drawn first
+#pragma unroll
+        for (int l = 2; l <= L; ++l) {
+#pragma unroll
+            for (int jw = 0; jw <= l - 2; ++jw) {
+                uint64_t xp, xq;
+                gen_xi<PM, QM, uint64_t>(R.rs[l - 1], p, q, xp, xq);
+                if constexpr (SL::kPreP) c.save[(SL::kPreP0 + SL::pre(l, jw)) * kLanes] = xp;
+                if constexpr (SL::kPreQ) c.save[(SL::kPreQ0 + SL::pre(l, jw)) * kLanes] = xq;
+            }
+        }
+    }
+
+    uint32_t st = 0, ph = 0;
+    for (uint32_t b = 0; b < nblocks; ++b) {
+        mbar_wait(&full[st], ph);
+        const uint64_t* sb = ring + size_t(st) * ST::kWords + wrow;
+        const uint32_t kb = b * kKS;
+        if (b == 0) {
+            R.cur = sb[ST::kXs];
+            R.raw0 = R.cur;
+        }
+        if (kb >= uint32_t(2 * L) && kb + kKS < n) {  // i = n-1 is sweep 1's last word: generic
+#pragma unroll
+            for (int jj = 0; jj < kKS; ++jj) deep_iter<PM, QM, L, true>(R, c, kb + jj, sb, jj, p, q);
+        } else {
+#pragma unroll 1
+            for (int jj = 0; jj < kKS; ++jj) {
+                if (kb + jj >= n) break;
+                deep_iter<PM, QM, L, false>(R, c, kb + jj, sb, jj, p, q);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        if (++st == uint32_t(S)) {
+            st = 0;
+            ph ^= 1u;
+        }
+    }
+    // drain: sweeps 2..L finish their wrapped words
+#pragma unroll 1
+    for (uint32_t i = n; i < n + uint32_t(2 * L - 2); ++i) deep_iter<PM, QM, L, false>(R, c, i, nullptr, 0, p, q);
+
+    if constexpr (LIVE) {
+        if (c.core) {
+            store_state(rd, g.Y, y, R.rs[L - 1]);
+            if (c.ghost_row) store_state(rd, g.Y, y + g.wrap, R.rs[L - 1]);
+        }
+    }
+}
+
+namespace {
+
+template <int PM, int QM, int L>
+cudaError_t deep_go(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
+                    const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK, const CUtensorMap* tmK1,
+                    cudaStream_t st) {
+    using GEO = DeepGeo<L>;
+    const uint32_t blocks = (g.c1 - g.c0 + GEO::kRows - 1) / GEO::kRows;
+    const size_t smem = mcs_deep_smem(p.mode, q.mode, L, S);
+    auto kern = k_mcs_deep<PM, QM, L>;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<blocks, 32 * (kDP + 1), smem, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), rs,
+                                               rd, f, g, p, q, jtab, S, *tmK, *tmK1);
+    return cudaGetLastError();
+}
+
+template <int PM>
+cudaError_t deep_q(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
+                   const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK, const CUtensorMap* tmK1,
+                   cudaStream_t st) {
+    switch (q.mode) {
+    case M_ZERO: return deep_go<PM, M_ZERO, kDeepSweeps>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
+    case M_HALF: return deep_go<PM, M_HALF, kDeepSweeps>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
+    case M_DYADIC: return deep_go<PM, M_DYADIC, kDeepSweeps>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
+    case M_ONE: return deep_go<PM, M_ONE, kDeepSweeps>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int L>
+size_t deep_smem_l(int pm, int qm, int S) {
+    const bool pp = !(pm == M_ZERO || pm == M_ONE), pq = !(qm == M_ZERO || qm == M_ONE);
+    const int slots = 5 * (L - 1) + 1 + (pp ? L * (L - 1) / 2 : 0) + (pq ? L * (L - 1) / 2 : 0);
+    return 128 + size_t(S) * DeepStage<L>::kWords * 8 + size_t(slots) * kLanes * 8;
+}
+
+}  // namespace
+
+bool mcs_deep_supported(int pm, int qm) {
+    auto cheap = [](int m) { return m == M_ZERO || m == M_HALF || m == M_DYADIC || m == M_ONE; };
+    const bool live = !((pm == M_ZERO || pm == M_ONE) && (qm == M_ZERO || qm == M_ONE));
+    // M_ONE next to a live stream still steps w draws per word: issue-bound, keep one MCS per pass
+    return cheap(pm) && cheap(qm) && !(live && (pm == M_ONE || qm == M_ONE));
+}
+
+size_t mcs_deep_smem(int pm, int qm, int L, int S) { return L == kDeepSweeps ? deep_smem_l<kDeepSweeps>(pm, qm, S) : 0; }
+
+cudaError_t launch_mcs_deep(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g,
+                            const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK,
+                            const CUtensorMap* tmK1, cudaStream_t st) {
+    if (S < 2 || S > kSMax) return cudaErrorInvalidValue;
+    switch (p.mode) {
+    case M_ZERO: return deep_q<M_ZERO>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
+    case M_HALF: return deep_q<M_HALF>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
+    case M_DYADIC: return deep_q<M_DYADIC>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
+    case M_ONE: return deep_q<M_ONE>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace octgpu

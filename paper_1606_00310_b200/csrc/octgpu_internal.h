@@ -45,7 +45,7 @@ struct Geom {
 
 constexpr uint32_t kMcsConsumerWarps = 4;                   // k_mcs_bulk: compute warps per block (+1 producer)
 constexpr uint32_t kTmaBoxRows = 30 * kMcsConsumerWarps + 4;  // k_mcs_bulk window rows (124)
-constexpr uint32_t kGhostRows = 128;                         // >= kTmaBoxRows
+constexpr uint32_t kGhostRows = 192;                         // >= kTmaBoxRows, deep_box_rows(kDeepSweeps)
 
 // Per-row RNG states are stored SoA: s[j * Y + y], j = 0..3.
 
@@ -77,6 +77,20 @@ cudaError_t launch_mcs_bulk(const void* src, void* dst, const uint64_t* rng_src,
                             const CUtensorMap* tmK, const CUtensorMap* tmK1, cudaStream_t st);
 size_t mcs_bulk_stage_bytes(int ks);
 size_t mcs_bulk_smem(int ks, int S);  // dynamic smem of a block (kMcsConsumerWarps + 1 warps)
+
+// Temporally blocked variant (mcs_deep.cu): kDeepSweeps sweeps (kDeepSweeps/2
+// MCS, starting with parity f) in one pass, periodic lattices only. The
+// geometry's core rows must start at virtual row kDeepSweeps - 1 (see
+// engine.cu deep_geom). tmK / tmK1: tensor maps with boxes of
+// deep_box_rows(kDeepSweeps) rows x 2 and x 3 words.
+constexpr int kDeepSweeps = 4;
+constexpr int kDeepWarps = 6;  // compute warps per block (+1 producer): 421 blocks at 2^16 rows fit one wave at 96 regs
+constexpr int deep_box_rows(int L) { return ((34 - 2 * L) * (kDeepWarps - 1) + 34) / 2 * 2; }
+bool mcs_deep_supported(int p_mode, int q_mode);
+size_t mcs_deep_smem(int p_mode, int q_mode, int L, int S);  // S ring stages
+cudaError_t launch_mcs_deep(const void* src, void* dst, const uint64_t* rng_src, uint64_t* rng_dst, int f, Geom g,
+                            const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK,
+                            const CUtensorMap* tmK1, cudaStream_t st);
 
 // s <- M s for every row state, M given as a 4-bit table (64 x 16 x 4 u64).
 cudaError_t launch_apply_jump(uint64_t* rng, uint32_t Y, const uint64_t* tab, cudaStream_t st);

@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "csrc", "liboctgpu.so")
+# OCTGPU_LIB: a development build of the same library (A/B kernel experiments)
+LIB_PATH = os.environ.get("OCTGPU_LIB") or os.path.join(HERE, "csrc", "liboctgpu.so")
 
 
 class OctError(RuntimeError):

@@ -14,20 +14,71 @@ struct Xo {
     uint64_t a, b, c, d;
 };
 
-__device__ __forceinline__ uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+// 64-bit shifts and rotations of the xoshiro step, spelled out on 32-bit
+// halves. The arbitrary-probability path (64 draws per word) is bound by the
+// ALU pipe (ncu pipe_alu 95%) while the FMA pipe idles, and the generic
+// lowering of (x << k) | (x >> (64 - k)) costs 4-6 ALU instructions per
+// rotation. Each half of a rotation is either one funnel shift (SHF.L.W, ALU
+// pipe) or an IMAD.HI (x >> (32-k) as the high word of x * 2^k) plus an IMAD
+// (x * 2^k + that) on the FMA pipe; which rotation goes to which pipe is a
+// compile-time choice (OCTGPU_ROT23_FMA / OCTGPU_ROT45_FMA / OCTGPU_SHL17_FMA).
+// Measured at c4 (profiles/r1_xoshiro_variants.json): all funnel shifts
+// 10.39 ms/MCS; rot23 on IMAD 10.86; rot23+rot45 11.21; all IMAD 11.80 (the
+// IMAD.HI issue cost outweighs the ALU relief) -> funnel shifts everywhere.
+#ifndef OCTGPU_ROT23_FMA
+#define OCTGPU_ROT23_FMA 0
+#endif
+#ifndef OCTGPU_ROT45_FMA
+#define OCTGPU_ROT45_FMA 0
+#endif
+#ifndef OCTGPU_SHL17_FMA
+#define OCTGPU_SHL17_FMA 0
+#endif
+__device__ __forceinline__ uint64_t pack64(uint32_t lo, uint32_t hi) { return (uint64_t(hi) << 32) | lo; }
+
+template <int K, bool FMA>  // high 32 bits of (hi:lo) << K, 0 < K < 32
+__device__ __forceinline__ uint32_t fsl(uint32_t lo, uint32_t hi) {
+    if constexpr (!FMA) {
+        return __funnelshift_l(lo, hi, K);
+    } else {
+        uint32_t r;
+        asm("{\n\t.reg .u32 t;\n\tmul.hi.u32 t, %1, %3;\n\tmad.lo.u32 %0, %2, %3, t;\n\t}"
+            : "=r"(r)
+            : "r"(lo), "r"(hi), "n"(1u << K));
+        return r;
+    }
+}
+
+template <int K, bool FMA>  // 0 < K < 32
+__device__ __forceinline__ uint64_t rotl64_lo(uint64_t x) {
+    const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
+    return pack64(fsl<K, FMA>(hi, lo), fsl<K, FMA>(lo, hi));
+}
+
+template <int K, bool FMA>  // 32 < K < 64: swap halves, then rotate by K - 32
+__device__ __forceinline__ uint64_t rotl64_hi(uint64_t x) {
+    const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
+    return pack64(fsl<K - 32, FMA>(lo, hi), fsl<K - 32, FMA>(hi, lo));
+}
+
+template <int K, bool FMA>  // 0 < K < 32
+__device__ __forceinline__ uint64_t shl64(uint64_t x) {
+    const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
+    return pack64(lo << K, fsl<K, FMA>(lo, hi));
+}
 
 __device__ __forceinline__ void xo_step(Xo& s) {
-    const uint64_t t = s.b << 17;
+    const uint64_t t = shl64<17, OCTGPU_SHL17_FMA>(s.b);
     s.c ^= s.a;
     s.d ^= s.b;
     s.b ^= s.c;
     s.a ^= s.d;
     s.c ^= t;
-    s.d = rotl64(s.d, 45);
+    s.d = rotl64_hi<45, OCTGPU_ROT45_FMA>(s.d);
 }
 
 __device__ __forceinline__ uint64_t xo_next(Xo& s) {
-    const uint64_t r = rotl64(s.a + s.d, 23) + s.a;
+    const uint64_t r = rotl64_lo<23, OCTGPU_ROT23_FMA>(s.a + s.d) + s.a;
     xo_step(s);
     return r;
 }
@@ -62,6 +113,48 @@ __device__ __forceinline__ Xo apply_table(const uint64_t* __restrict__ tab, cons
 }
 
 // -------------------------------------------------------------------------
+// Arbitrary-probability xi bits, 32 draws at a time (rng.hpp:174-179).
+// acc = 2*acc + (r >= T): the 64-bit compare is a subtract whose carry-out
+// (= no borrow; PTX sub.cc/subc.cc, SASS IADD3 + IADD3.X) feeds an
+// add-with-carry, 3 instructions per draw instead of 2 compares + select +
+// or. Draw j lands at bit 31-j; one bit reverse puts it at bit j and one NOT
+// turns (r >= T) into the xi bit (r < T). Rolled by bytes: fully unrolled copies of the 64-draw word at
+// every call site overflow the instruction cache.
+__device__ __forceinline__ uint32_t acc_ge(uint32_t acc, uint64_t r, uint64_t T) {
+    uint32_t out;
+    asm("{\n\t.reg .u32 d;\n\tsub.cc.u32 d, %1, %3;\n\tsubc.cc.u32 d, %2, %4;\n\taddc.u32 %0, %5, %5;\n\t}"
+        : "=r"(out)
+        : "r"(uint32_t(r)), "r"(uint32_t(r >> 32)), "r"(uint32_t(T)), "r"(uint32_t(T >> 32)), "r"(acc));
+    return out;
+}
+
+template <typename Word>
+__device__ __forceinline__ uint32_t arb_half(Xo& s, uint64_t T) {
+    uint32_t acc = 0;
+#pragma unroll 1
+    for (int it = 0; it < 4; ++it) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc = acc_ge(acc, xo_next(s), T);
+    }
+    return ~__brev(acc);
+}
+
+// two independent streams interleaved draw by draw (instruction-level parallelism)
+__device__ __forceinline__ void arb_half_pair(Xo& a, Xo& b, uint64_t T, uint32_t& ra, uint32_t& rb) {
+    uint32_t acca = 0, accb = 0;
+#pragma unroll 1
+    for (int it = 0; it < 4; ++it) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            acca = acc_ge(acca, xo_next(a), T);
+            accb = acc_ge(accb, xo_next(b), T);
+        }
+    }
+    ra = ~__brev(acca);
+    rb = ~__brev(accb);
+}
+
+// -------------------------------------------------------------------------
 // xi words (rng.hpp:129-179, params.hpp:84-92)
 
 template <int MODE, typename Word>
@@ -79,18 +172,13 @@ __device__ __forceinline__ Word xi_word(Xo& s, const ProbDev& pd) {
         }
         return acc;
     } else if constexpr (MODE == M_ARB) {
-        // xi_arbitrary: bit i = to_unit(draw_i) < r  <=>  draw_i < T (integer threshold).
-        // Rolled by bytes: the word is ~W x 22 instructions, and fully unrolled
-        // copies at every call site overflow the instruction cache.
-        Word word = 0;
-#pragma unroll 1
-        for (int i0 = 0; i0 < W; i0 += 8) {
-            uint32_t byte = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) byte |= uint32_t(xo_next(s) < pd.T) << j;
-            word |= Word(byte) << i0;
+        // xi_arbitrary: bit i = to_unit(draw_i) < r  <=>  draw_i < T (integer threshold)
+        const uint32_t lo = arb_half<Word>(s, pd.T);
+        if constexpr (W == 32) {
+            return Word(lo);
+        } else {
+            return Word(pack64(lo, arb_half<Word>(s, pd.T)));
         }
-        return word;
     } else {  // M_ONE: every bit accepted, stream still advances w draws
 #pragma unroll 8
         for (int i = 0; i < W; ++i) xo_step(s);
@@ -139,20 +227,17 @@ __device__ __forceinline__ void xi_word_pair(Xo& a, Xo& b, const ProbDev& pd, Wo
         wa = ra;
         wb = rb;
     } else if constexpr (MODE == M_ARB) {
-        Word ra = 0, rb = 0;
-#pragma unroll 1
-        for (int i0 = 0; i0 < W; i0 += 8) {
-            uint32_t ba = 0, bb = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                ba |= uint32_t(xo_next(a) < pd.T) << j;
-                bb |= uint32_t(xo_next(b) < pd.T) << j;
-            }
-            ra |= Word(ba) << i0;
-            rb |= Word(bb) << i0;
+        uint32_t la, lb;
+        arb_half_pair(a, b, pd.T, la, lb);
+        if constexpr (W == 32) {
+            wa = Word(la);
+            wb = Word(lb);
+        } else {
+            uint32_t ha, hb;
+            arb_half_pair(a, b, pd.T, ha, hb);
+            wa = Word(pack64(la, ha));
+            wb = Word(pack64(lb, hb));
         }
-        wa = ra;
-        wb = rb;
     } else {  // M_ONE
 #pragma unroll 8
         for (int i = 0; i < W; ++i) {

@@ -14,7 +14,7 @@ from fractions import Fraction
 
 import numpy as np
 
-from ._lib import OctMoments, check, lib
+from ._lib import ConfigError, OctMoments, check, lib
 from .params import LatticeConfig, UpdateParams
 
 
@@ -197,9 +197,15 @@ class GpuEngine:
     def launches(self) -> int:
         return int(lib().octgpu_launch_count(self._h))
 
-    def planes(self) -> np.ndarray:
+    def planes(self, out: np.ndarray | None = None) -> np.ndarray:
+        """The four bit-planes in the reference layout [4][Y][n]; `out` (e.g. a
+        pinned buffer) is filled in place when given."""
         c = self.cfg
-        out = np.zeros((4, c.Y, c.words_per_row()), _word_dtype(c.w))
+        shape, dt = (4, c.Y, c.words_per_row()), _word_dtype(c.w)
+        if out is None:
+            out = np.zeros(shape, dt)
+        elif out.shape != shape or out.dtype != dt or not out.flags.c_contiguous:
+            raise ConfigError(f"planes buffer must be a C-contiguous {dt.__name__} array of shape {shape}")
         check(lib().octgpu_get_planes(self._h, out.ctypes.data_as(C.c_void_p)))
         return out
 
@@ -208,8 +214,11 @@ class GpuEngine:
 
     slope_field = field
 
-    def streams(self) -> RngStreamSet:
-        out = np.zeros((self.cfg.Y, 4), np.uint64)
+    def streams(self, out: np.ndarray | None = None) -> RngStreamSet:
+        if out is None:
+            out = np.zeros((self.cfg.Y, 4), np.uint64)
+        elif out.shape != (self.cfg.Y, 4) or out.dtype != np.uint64 or not out.flags.c_contiguous:
+            raise ConfigError(f"states buffer must be a C-contiguous uint64 array of shape ({self.cfg.Y}, 4)")
         check(lib().octgpu_get_states(self._h, out.ctypes.data_as(C.c_void_p)))
         return RngStreamSet(int(lib().octgpu_master_seed(self._h)), out)
 

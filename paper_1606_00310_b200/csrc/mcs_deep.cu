@@ -279,7 +279,7 @@ __device__ __forceinline__ void deep_iter(DeepState<L>& S, const DeepCtx& c, uin
 }  // namespace
 
 template <int PM, int QM, int L>
-__global__ void __launch_bounds__(32 * (kDP + 1), 3)
+__global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
     k_mcs_deep(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, const uint64_t* __restrict__ rs,
                uint64_t* __restrict__ rd, int f, Geom g, ProbDev p, ProbDev q, const uint64_t* __restrict__ jtab, int S,
                const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmK1) {

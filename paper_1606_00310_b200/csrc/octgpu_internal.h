@@ -45,7 +45,19 @@ struct Geom {
 
 constexpr uint32_t kMcsConsumerWarps = 4;                   // k_mcs_bulk: compute warps per block (+1 producer)
 constexpr uint32_t kTmaBoxRows = 30 * kMcsConsumerWarps + 4;  // k_mcs_bulk window rows (124)
-constexpr uint32_t kGhostRows = 192;                         // >= kTmaBoxRows, deep_box_rows(kDeepSweeps)
+
+// k_mcs_deep block shape (mcs_deep.cu): kDeepWarps compute warps + 1 producer.
+#ifndef OCTGPU_DEEP_WARPS
+#define OCTGPU_DEEP_WARPS 9
+#endif
+constexpr int kDeepSweeps = 4;
+constexpr int kDeepWarps = OCTGPU_DEEP_WARPS;
+constexpr int kDeepMinBlocks = kDeepWarps >= 8 ? 2 : 3;  // resident blocks per SM the register budget targets
+constexpr int deep_box_rows(int L) { return ((34 - 2 * L) * (kDeepWarps - 1) + 34) / 2 * 2; }
+
+// periodic lattices keep this many ghost rows (>= every TMA window) so windows never wrap
+constexpr uint32_t kGhostRows = deep_box_rows(kDeepSweeps) <= 192 ? 192 : 256;
+static_assert(kTmaBoxRows <= kGhostRows && uint32_t(deep_box_rows(kDeepSweeps)) <= kGhostRows, "ghost rows");
 
 // Per-row RNG states are stored SoA: s[j * Y + y], j = 0..3.
 
@@ -83,9 +95,6 @@ size_t mcs_bulk_smem(int ks, int S);  // dynamic smem of a block (kMcsConsumerWa
 // geometry's core rows must start at virtual row kDeepSweeps - 1 (see
 // engine.cu deep_geom). tmK / tmK1: tensor maps with boxes of
 // deep_box_rows(kDeepSweeps) rows x 2 and x 3 words.
-constexpr int kDeepSweeps = 4;
-constexpr int kDeepWarps = 6;  // compute warps per block (+1 producer): 421 blocks at 2^16 rows fit one wave at 96 regs
-constexpr int deep_box_rows(int L) { return ((34 - 2 * L) * (kDeepWarps - 1) + 34) / 2 * 2; }
 bool mcs_deep_supported(int p_mode, int q_mode);
 size_t mcs_deep_smem(int p_mode, int q_mode, int L, int S);  // S ring stages
 cudaError_t launch_mcs_deep(const void* src, void* dst, const uint64_t* rng_src, uint64_t* rng_dst, int f, Geom g,

@@ -148,12 +148,16 @@ int octgpu_measure(octgpu_engine* e, octgpu_moments* out);
 int octgpu_heights(octgpu_engine* e, int32_t* out);
 
 /* ---- row stripes (multi-GPU) ----
- * A stripe engine owns global rows [y0, y1) of an X x Y periodic lattice
- * (sublattice partition as the reference's SweepPlan row blocks,
- * params.hpp:107-127; results do not depend on the partition). One MCS:
+ * A stripe engine owns global rows [y0, y1) (at least 4) of an X x Y periodic
+ * lattice (sublattice partition as the reference's SweepPlan row blocks,
+ * params.hpp:107-127; results do not depend on the partition). One pass of
+ * k = 1 MCS (or k = octgpu_stripe_max_mcs(), 2 for constant xi: the
+ * temporally blocked kernel):
  *   octgpu_halo_pack -> exchange (to_prev -> rank-1, to_next -> rank+1) ->
- *   octgpu_halo_unpack -> octgpu_stripe_mcs -> exchange boundary (-> rank+1) ->
+ *   octgpu_halo_unpack -> octgpu_stripe_mcs_n(k) -> exchange boundary (-> rank+1) ->
  *   octgpu_stripe_finish.
+ * to_prev carries the stripe's first 4 rows, to_next its last 3 (4 plane-rows
+ * + the row's xoshiro state each); boundary is one plane-row.
  * All buffers are DEVICE memory (e.g. NCCL send/recv buffers); all work is on
  * the engine's stream. octgpu_get_planes / octgpu_get_states return the
  * stripe's own rows. planes/states NULL = flat start, RngStreamSet(seed, Y)
@@ -177,7 +181,10 @@ int octgpu_stripe_sizes(const octgpu_engine* e, uint64_t* to_prev_bytes, uint64_
                         uint64_t* boundary_bytes);
 int octgpu_halo_pack(octgpu_engine* e, void* to_prev, void* to_next);
 int octgpu_halo_unpack(octgpu_engine* e, const void* from_prev, const void* from_next);
-int octgpu_stripe_mcs(octgpu_engine* e, const octgpu_params* prm, void* boundary_out);
+int octgpu_stripe_mcs(octgpu_engine* e, const octgpu_params* prm, void* boundary_out); /* k = 1 */
+int octgpu_stripe_mcs_n(octgpu_engine* e, const octgpu_params* prm, uint32_t n_mcs, void* boundary_out);
+/* largest n_mcs one pass may take for these parameters (1 or 2); 0 on error */
+int octgpu_stripe_max_mcs(octgpu_engine* e, const octgpu_params* prm);
 int octgpu_stripe_finish(octgpu_engine* e, const void* boundary_in);
 /* local moments; needs fresh halos (pack/exchange/unpack) for the curl check of row y0 */
 int octgpu_measure_stripe(octgpu_engine* e, octgpu_stripe_moments* out);

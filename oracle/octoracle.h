@@ -63,8 +63,8 @@ void oo_sweep_stripe(uint32_t X, uint32_t Y, uint32_t w, uint32_t y0, uint32_t y
                      uint64_t* ghost, uint64_t* states, int parity, const oo_prob* p, const oo_prob* q);
 
 /* Fused MCS of a row stripe with 1 halo row above and 2 below (see .c) */
-void oo_mcs_stripe(uint32_t X, uint32_t w, uint32_t L, uint32_t yoff, uint64_t* planes, uint64_t* states, int f,
-                   const oo_prob* p, const oo_prob* q);
+void oo_mcs_stripe(uint32_t X, uint32_t w, uint32_t R, uint32_t nsweeps, uint32_t yoff, uint64_t* planes,
+                   uint64_t* states, int f, const oo_prob* p, const oo_prob* q);
 
 /* slope_field.hpp:232-246 */
 uint64_t oo_field_checksum(uint32_t X, uint32_t Y, uint32_t w, const uint64_t* planes, uint64_t t_mcs);

@@ -72,7 +72,7 @@ class Oracle:
         L.oo_height_moments.argtypes = [u32, u32, _i32p, _f64p]
         L.oo_log_schedule.argtypes = [u64, u32, _u64p, u32]
         L.oo_log_schedule.restype = u32
-        L.oo_mcs_stripe.argtypes = [u32, u32, u32, u32, _u64p, _u64p, i32, P(OOProb), P(OOProb)]
+        L.oo_mcs_stripe.argtypes = [u32, u32, u32, u32, u32, _u64p, _u64p, i32, P(OOProb), P(OOProb)]
 
     # -- rng -------------------------------------------------------------
     def from_seed(self, seed: int) -> np.ndarray:
@@ -320,62 +320,72 @@ class RefEngine:
 
 class OracleStripe:
     """CPU stand-in for paper_1606_00310_b200.stripes.StripeEngine (test infra):
-    same pack/unpack/mcs/finish/measure_local contract and buffer layout, computed
-    by oo_mcs_stripe (the reference's sweeps restricted to a stripe with halos)."""
+    same pack/unpack/mcs/finish/measure_local contract and buffer layout
+    (3 halo rows above, 4 below, include/octgpu.h), computed by oo_mcs_stripe
+    (the reference's sweeps restricted to a stripe with halos)."""
+
+    HA, HB = 3, 4
 
     def __init__(self, o: Oracle, X: int, Y: int, y0: int, y1: int, seed: int, w: int = 64):
         self.o, self.X, self.Y, self.w, self.y0, self.y1 = o, X, Y, w, y0, y1
         self.L = L = y1 - y0
         self.n = n = X // (2 * w)
+        HA, HB = self.HA, self.HB
         full = o.new_flat(X, Y, w)
-        self.buf = np.zeros((4, L + 3, n), np.uint64)
-        self.buf[:, 1:L + 1] = full[:, y0:y1]
-        self.st = np.zeros((L + 3, 4), np.uint64)
-        self.st[1:L + 1] = o.stream_set(seed, y1)[y0:y1]
+        self.buf = np.zeros((4, HA + L + HB, n), np.uint64)
+        self.buf[:, HA:HA + L] = full[:, y0:y1]
+        self.st = np.zeros((HA + L + HB, 4), np.uint64)
+        self.st[HA:HA + L] = o.stream_set(seed, y1)[y0:y1]
         self.t, self.phase = 0, 0
-        self.to_prev_bytes = (4 * 2 * n + 4) * 8
-        self.to_next_bytes = (4 * n + 4) * 8
+        self.to_prev_bytes = HB * (4 * n + 4) * 8
+        self.to_next_bytes = HA * (4 * n + 4) * 8
         self.boundary_bytes = n * 8
 
     @staticmethod
     def _u64(t):
         return t.numpy().view(np.uint64)
 
+    def _gather(self, r0, nrows, out):
+        a = self._u64(out)
+        k = 4 * nrows * self.n
+        a[:k] = self.buf[:, r0:r0 + nrows].ravel()
+        a[k:] = self.st[r0:r0 + nrows].ravel()
+
+    def _scatter(self, r0, nrows, src):
+        a = self._u64(src)
+        k = 4 * nrows * self.n
+        self.buf[:, r0:r0 + nrows] = a[:k].reshape(4, nrows, self.n)
+        self.st[r0:r0 + nrows] = a[k:].reshape(nrows, 4)
+
     def pack(self, to_prev, to_next):
-        L, n = self.L, self.n
-        a = self._u64(to_prev)
-        a[:8 * n] = self.buf[:, 1:3].ravel()
-        a[8 * n:] = self.st[1]
-        b = self._u64(to_next)
-        b[:4 * n] = self.buf[:, L].ravel()
-        b[4 * n:] = self.st[L]
+        self._gather(self.HA, self.HB, to_prev)
+        self._gather(self.L, self.HA, to_next)
 
     def unpack(self, from_prev, from_next):
-        L, n = self.L, self.n
-        a = self._u64(from_prev)
-        self.buf[:, 0] = a[:4 * n].reshape(4, n)
-        self.st[0] = a[4 * n:]
-        b = self._u64(from_next)
-        self.buf[:, L + 1:L + 3] = b[:8 * n].reshape(4, 2, n)
-        self.st[L + 1] = b[8 * n:]
+        self._scatter(0, self.HA, from_prev)
+        self._scatter(self.HA + self.L, self.HB, from_next)
 
-    def mcs(self, prm, boundary_out):
+    def max_mcs(self, prm):
+        return 2  # the CPU stand-in runs the 2-MCS protocol for every mode
+
+    def mcs(self, prm, boundary_out, n=1):
         o = self.o
         p = o.resolve(prm.p.value, int(prm.p.mode))
         q = o.resolve(prm.q.value, int(prm.q.mode))
-        yoff = (self.y0 - 1) % self.Y
-        o.L.oo_mcs_stripe(self.X, self.w, self.L, yoff, self.buf, self.st, self.phase, C.byref(p), C.byref(q))
-        self._u64(boundary_out)[:] = self.buf[2 + self.phase, self.L + 1]
-        self.t += 1
+        yoff = (self.y0 - self.HA) % self.Y
+        R = self.HA + self.L + self.HB
+        o.L.oo_mcs_stripe(self.X, self.w, R, 2 * n, yoff, self.buf, self.st, self.phase, C.byref(p), C.byref(q))
+        self._u64(boundary_out)[:] = self.buf[2 + self.phase, self.HA + self.L]
+        self.t += n
 
     def finish(self, boundary_in):
-        self.buf[2 + self.phase, 1] = self._u64(boundary_in)
+        self.buf[2 + self.phase, self.HA] = self._u64(boundary_in)
 
     def planes(self):
-        return self.buf[:, 1:self.L + 1].copy()
+        return self.buf[:, self.HA:self.HA + self.L].copy()
 
     def states(self):
-        return self.st[1:self.L + 1].copy()
+        return self.st[self.HA:self.HA + self.L].copy()
 
     def measure_local(self):
         """Stripe-local power sums in the GPU kernels' gauge (numpy, no curl check)."""
@@ -389,11 +399,12 @@ class OracleStripe:
         sy_first = row_first = None
         for l in range(1, L + 1):
             y = (self.y0 + l - 1) % self.Y
-            a = bits(self.buf[y & 1, l]).astype(np.int64)
-            b = bits(self.buf[(y & 1) ^ 1, l]).astype(np.int64)
+            r = self.HA + l - 1
+            a = bits(self.buf[y & 1, r]).astype(np.int64)
+            b = bits(self.buf[(y & 1) ^ 1, r]).astype(np.int64)
             sig = np.empty(X, np.int64)
             sig[0::2], sig[1::2] = 2 * a - 1, 2 * b - 1
-            sy = 1 if int(self.buf[2 + (y & 1), l, 0]) & 1 else -1
+            sy = 1 if int(self.buf[2 + (y & 1), r, 0]) & 1 else -1
             G += sy
             col += sy
             if l == 1:

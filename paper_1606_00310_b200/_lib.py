@@ -81,7 +81,8 @@ EXPORTS = (
     "octgpu_sync", "octgpu_step", "octgpu_sweep", "octgpu_t", "octgpu_phase", "octgpu_master_seed",
     "octgpu_get_planes", "octgpu_get_states", "octgpu_field_checksum", "octgpu_measure", "octgpu_heights",
     "octgpu_last_error", "octgpu_version", "octgpu_launch_count", "octgpu_create_stripe", "octgpu_stripe_sizes",
-    "octgpu_halo_pack", "octgpu_halo_unpack", "octgpu_stripe_mcs", "octgpu_stripe_finish", "octgpu_measure_stripe",
+    "octgpu_halo_pack", "octgpu_halo_unpack", "octgpu_stripe_mcs", "octgpu_stripe_mcs_n", "octgpu_stripe_max_mcs",
+    "octgpu_stripe_finish", "octgpu_measure_stripe",
     "octgpu_stripe_y0", "octgpu_stripe_rows", "octgpu_height_moments",
 )
 
@@ -128,6 +129,8 @@ def lib() -> C.CDLL:
         "octgpu_halo_pack": (i32, [vp, vp, vp]),
         "octgpu_halo_unpack": (i32, [vp, vp, vp]),
         "octgpu_stripe_mcs": (i32, [vp, P(OctParams), vp]),
+        "octgpu_stripe_mcs_n": (i32, [vp, P(OctParams), u32, vp]),
+        "octgpu_stripe_max_mcs": (i32, [vp, P(OctParams)]),
         "octgpu_stripe_finish": (i32, [vp, vp]),
         "octgpu_measure_stripe": (i32, [vp, P(OctStripeMoments)]),
         "octgpu_stripe_y0": (u32, [vp]),

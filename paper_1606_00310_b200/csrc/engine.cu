@@ -346,7 +346,8 @@ struct octgpu_engine {
     // k_mcs_deep: the same periodic lattice with core rows starting at virtual row kDeepSweeps - 1
     Geom deep_geom() const { return Geom{Y, n, size_t(n) * Y, kDeepSweeps - 1, L + kDeepSweeps - 1, L, 0, kGhostRows}; }
     Geom geom() const {
-        return stripe ? Geom{Y, n, size_t(n) * Y, 1, L + 1, 0, (y0 + 1) & 1u, 0}  // local row 0 = global y0 - 1
+        // stripe: local row 0 = global y0 - kStripeHA (parity of y0 + 1)
+        return stripe ? Geom{Y, n, size_t(n) * Y, kStripeHA, kStripeHA + L, 0, (y0 + 1) & 1u, 0}
                       : Geom{Y, n, size_t(n) * Y, 1, L + 1, L, 0, kGhostRows};
     }
     uint32_t core_rows() const { return L; }
@@ -354,7 +355,7 @@ struct octgpu_engine {
     // every allocated row (stripe; the host slices rows 1..L)
     uint32_t host_rows() const { return stripe ? Y : L; }
     size_t host_bytes() const { return 4 * size_t(n) * host_rows() * word_bytes(); }
-    uint32_t first_row() const { return stripe ? 1 : 0; }  // local index of the first core row
+    uint32_t first_row() const { return stripe ? kStripeHA : 0; }  // local index of the first core row
     size_t word_bytes() const { return w / 8; }
     size_t set_bytes() const { return 4 * size_t(n) * Y * word_bytes(); }
     size_t rng_bytes() const { return 4 * size_t(Y) * sizeof(uint64_t); }
@@ -611,10 +612,10 @@ int make_engine(uint32_t X, uint32_t Ytot, uint32_t w, bool stripe, uint32_t y0,
     auto* e = new octgpu_engine;
     e->X = X; e->w = w; e->n = X / (2 * w); e->device = device; e->master_seed = master_seed;
     e->Ytot = Ytot; e->stripe = stripe; e->y0 = stripe ? y0 : 0; e->L = stripe ? L : Ytot;
-    // stripe: halo row 0, core 1..L, halos L+1, L+2, then >= 34 rows of padding (k_mcs
-    // reads up to 33 rows past a warp's first row; the TMA of k_mcs_bulk zero-fills
-    // past the allocation); even for 16-B alignment
-    e->Y = stripe ? ((L + 3 + 36 + 1) & ~1u) : Ytot + kGhostRows;
+    // stripe: halo rows 0..HA-1, core HA..HA+L-1, halos below HA+L..HA+L+HB-1, then >= 34
+    // rows of padding (k_mcs reads up to 33 rows past a warp's first row; the TMA kernels
+    // zero-fill past the allocation); even for 16-B alignment
+    e->Y = stripe ? ((L + kStripeHA + kStripeHB + 34 + 1) & ~1u) : Ytot + kGhostRows;
     int rc = alloc_engine(e);
     if (rc) {
         std::string keep = g_err;
@@ -636,7 +637,7 @@ int load_planes(octgpu_engine* e, const void* planes) {
     } else {
         std::vector<unsigned char> pad(e->host_bytes(), 0);
         for (int p = 0; p < 4; ++p)
-            std::memcpy(pad.data() + (size_t(p) * e->Y + 1) * row_bytes,
+            std::memcpy(pad.data() + (size_t(p) * e->Y + kStripeHA) * row_bytes,
                         static_cast<const unsigned char*>(planes) + size_t(p) * e->L * row_bytes, e->L * row_bytes);
         CK(cudaMemcpyAsync(e->stage, pad.data(), e->host_bytes(), cudaMemcpyHostToDevice, e->stream));
         CK(cudaStreamSynchronize(e->stream));
@@ -723,9 +724,10 @@ int octgpu_create_stripe(uint32_t X, uint32_t Y, uint32_t w, uint32_t y0, uint32
     *out = nullptr;
     int rc = validate(X, Y, w);
     if (rc) return rc;
-    if (!(y0 < y1 && y1 <= Y) || y1 - y0 < 2)
+    if (!(y0 < y1 && y1 <= Y) || y1 - y0 < kStripeHB)
         return fail(OCTGPU_ERR_CONFIG, "stripe rows [" + std::to_string(y0) + "," + std::to_string(y1) +
-                                           ") must hold at least 2 rows of the lattice");
+                                           ") must hold at least " + std::to_string(kStripeHB) +
+                                           " rows of the lattice");
     if (phase != 0 && phase != 1) return fail(OCTGPU_ERR_CONFIG, "phase must be 0 or 1");
     if ((planes == nullptr) != (states == nullptr))
         return fail(OCTGPU_ERR_CONFIG, "give both planes and states, or neither (flat start)");
@@ -926,7 +928,7 @@ int octgpu_get_planes(octgpu_engine* e, void* out) {
     const size_t row_bytes = size_t(e->n) * e->word_bytes();
     for (int p = 0; p < 4; ++p)
         std::memcpy(static_cast<unsigned char*>(out) + size_t(p) * e->L * row_bytes,
-                    pad.data() + (size_t(p) * e->Y + 1) * row_bytes, e->L * row_bytes);
+                    pad.data() + (size_t(p) * e->Y + kStripeHA) * row_bytes, e->L * row_bytes);
     return OCTGPU_OK;
 }
 
@@ -1064,9 +1066,9 @@ int octgpu_heights(octgpu_engine* e, int32_t* out) {
 
 int octgpu_stripe_sizes(const octgpu_engine* e, uint64_t* to_prev, uint64_t* to_next, uint64_t* boundary) {
     if (!e || !e->stripe) return fail(OCTGPU_ERR_CONFIG, "not a row stripe");
-    const uint64_t row = 4ull * e->n * e->word_bytes();
-    if (to_prev) *to_prev = 2 * row + 32;
-    if (to_next) *to_next = row + 32;
+    const uint64_t row = 4ull * e->n * e->word_bytes() + 32;  // 4 plane-rows + the row's rng state
+    if (to_prev) *to_prev = kStripeHB * row;
+    if (to_next) *to_next = kStripeHA * row;
     if (boundary) *boundary = uint64_t(e->n) * e->word_bytes();
     return OCTGPU_OK;
 }
@@ -1076,10 +1078,10 @@ int octgpu_halo_pack(octgpu_engine* e, void* to_prev, void* to_next) {
     int rc = use_device(e);
     if (rc) return rc;
     const Geom g = e->geom();
-    // rows 1, 2 (+ state of row 1) become the next-lower rank's halo rows L+1, L+2
-    CK(launch_rows_gather(e->w, e->planes[e->pcur], e->rng[e->rcur], g, 1, 2, to_prev, e->stream));
-    // row L (+ state) becomes the next-higher rank's halo row 0
-    CK(launch_rows_gather(e->w, e->planes[e->pcur], e->rng[e->rcur], g, e->L, 1, to_next, e->stream));
+    // first HB core rows (+ states) become the next-lower rank's halo rows below
+    CK(launch_rows_gather(e->w, e->planes[e->pcur], e->rng[e->rcur], g, kStripeHA, kStripeHB, to_prev, e->stream));
+    // last HA core rows (+ states) become the next-higher rank's halo rows above
+    CK(launch_rows_gather(e->w, e->planes[e->pcur], e->rng[e->rcur], g, e->L, kStripeHA, to_next, e->stream));
     e->launches += 2;
     return OCTGPU_OK;
 }
@@ -1089,18 +1091,40 @@ int octgpu_halo_unpack(octgpu_engine* e, const void* from_prev, const void* from
     int rc = use_device(e);
     if (rc) return rc;
     const Geom g = e->geom();
-    CK(launch_rows_scatter(e->w, e->planes[e->pcur], e->rng[e->rcur], g, 0, 1, from_prev, e->stream));
-    CK(launch_rows_scatter(e->w, e->planes[e->pcur], e->rng[e->rcur], g, e->L + 1, 2, from_next, e->stream));
+    CK(launch_rows_scatter(e->w, e->planes[e->pcur], e->rng[e->rcur], g, 0, kStripeHA, from_prev, e->stream));
+    CK(launch_rows_scatter(e->w, e->planes[e->pcur], e->rng[e->rcur], g, kStripeHA + e->L, kStripeHB, from_next,
+                           e->stream));
     e->launches += 2;
     return OCTGPU_OK;
 }
 
-int octgpu_stripe_mcs(octgpu_engine* e, const octgpu_params* prm, void* boundary_out) {
+namespace {
+// k_mcs_deep can carry a stripe through 2 MCS per halo exchange (constant-xi modes)
+bool stripe_deep_ok(const octgpu_engine* e, const ProbDev& p, const ProbDev& q) {
+    return e->deep && e->mcs_impl == 2 && mcs_deep_supported(p.mode, q.mode) && is_const(p) && is_const(q);
+}
+}  // namespace
+
+int octgpu_stripe_max_mcs(octgpu_engine* e, const octgpu_params* prm) {
+    if (!e || !e->stripe) {
+        fail(OCTGPU_ERR_CONFIG, "not a row stripe");
+        return 0;
+    }
+    ProbDev p, q;
+    if (lower_params(prm, p, q)) return 0;
+    return stripe_deep_ok(e, p, q) ? kDeepSweeps / 2 : 1;
+}
+
+int octgpu_stripe_mcs_n(octgpu_engine* e, const octgpu_params* prm, uint32_t n_mcs, void* boundary_out) {
     if (!e || !e->stripe || !boundary_out) return fail(OCTGPU_ERR_CONFIG, "not a row stripe / null buffer");
     ProbDev p, q;
     int rc = lower_params(prm, p, q);
     if (!rc) rc = use_device(e);
     if (rc) return rc;
+    const bool deep = n_mcs == uint32_t(kDeepSweeps / 2);
+    if (n_mcs != 1 && !(deep && stripe_deep_ok(e, p, q)))
+        return fail(OCTGPU_ERR_CONFIG, "a stripe pass covers 1 MCS, or " + std::to_string(kDeepSweeps / 2) +
+                                           " with constant xi (see octgpu_stripe_max_mcs)");
     const bool live = !(is_const(p) && is_const(q));
     const uint64_t D = draws(prm->p, e->w) + (q.mode != M_ZERO ? draws(prm->q, e->w) : 0);
     const uint64_t per_sweep = uint64_t(e->n) * D;
@@ -1112,7 +1136,12 @@ int octgpu_stripe_mcs(octgpu_engine* e, const octgpu_params* prm, void* boundary
     }
     const Geom g = e->geom();
     const int ps = e->pcur, rs = e->rcur;
-    if (e->mcs_impl == 2) {
+    if (deep) {
+        rc = ensure_tmaps_deep(e);
+        if (rc) return rc;
+        CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
+                           e->deep_S, &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
+    } else if (e->mcs_impl == 2) {
         rc = plan_bulk(e, p, q);
         if (rc) return rc;
         CK(launch_mcs_bulk(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
@@ -1120,24 +1149,30 @@ int octgpu_stripe_mcs(octgpu_engine* e, const octgpu_params* prm, void* boundary
     } else
         CK(launch_mcs(e->w, e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, live,
                       jtab, e->stream));
-    // Y(f) of halo row L+1 is final here (first sweep of row L+1, second of row L): the next rank's row 1
-    CK(launch_planerow_copy(e->w, e->planes[ps ^ 1], 2 + e->phase, g, e->L + 1, boundary_out, true, e->stream));
+    // Y(f) of the first halo row below is final here (its own f sweeps + the s sweeps of
+    // our last core row): the next rank's first core row, which its own pass never writes
+    CK(launch_planerow_copy(e->w, e->planes[ps ^ 1], 2 + e->phase, g, kStripeHA + e->L, boundary_out, true,
+                            e->stream));
     e->launches += 2;
     e->pcur ^= 1;
     if (live)
         e->rcur ^= 1;
     else
-        e->pending += 2 * per_sweep;
-    ++e->t;
+        e->pending += 2 * uint64_t(n_mcs) * per_sweep;
+    e->t += n_mcs;
     return OCTGPU_OK;
+}
+
+int octgpu_stripe_mcs(octgpu_engine* e, const octgpu_params* prm, void* boundary_out) {
+    return octgpu_stripe_mcs_n(e, prm, 1, boundary_out);
 }
 
 int octgpu_stripe_finish(octgpu_engine* e, const void* boundary_in) {
     if (!e || !e->stripe || !boundary_in) return fail(OCTGPU_ERR_CONFIG, "not a row stripe / null buffer");
     int rc = use_device(e);
     if (rc) return rc;
-    CK(launch_planerow_copy(e->w, e->planes[e->pcur], 2 + e->phase, e->geom(), 1, const_cast<void*>(boundary_in),
-                            false, e->stream));
+    CK(launch_planerow_copy(e->w, e->planes[e->pcur], 2 + e->phase, e->geom(), kStripeHA,
+                            const_cast<void*>(boundary_in), false, e->stream));
     ++e->launches;
     return OCTGPU_OK;
 }

@@ -437,8 +437,9 @@ __global__ void k_rows_gather(const Word* __restrict__ planes, const uint64_t* _
         const uint32_t p = i / per, rem = i % per, r = rem / n, k = rem % n;
         buf[i] = planes[size_t(p) * g.plane_stride + size_t(k) * g.Y + r0 + r];
     }
-    if (rng && blockIdx.x == 0 && threadIdx.x < 4)
-        reinterpret_cast<uint64_t*>(buf + total)[threadIdx.x] = rng[size_t(threadIdx.x) * g.Y + r0];
+    if (rng && blockIdx.x == 0)
+        for (uint32_t t = threadIdx.x; t < 4 * nrows; t += blockDim.x)  // [row][j]
+            reinterpret_cast<uint64_t*>(buf + total)[t] = rng[size_t(t & 3) * g.Y + r0 + (t >> 2)];
 }
 
 template <typename Word>
@@ -449,8 +450,9 @@ __global__ void k_rows_scatter(Word* __restrict__ planes, uint64_t* __restrict__
         const uint32_t p = i / per, rem = i % per, r = rem / n, k = rem % n;
         planes[size_t(p) * g.plane_stride + size_t(k) * g.Y + r0 + r] = buf[i];
     }
-    if (rng && blockIdx.x == 0 && threadIdx.x < 4)
-        rng[size_t(threadIdx.x) * g.Y + r0] = reinterpret_cast<const uint64_t*>(buf + total)[threadIdx.x];
+    if (rng && blockIdx.x == 0)
+        for (uint32_t t = threadIdx.x; t < 4 * nrows; t += blockDim.x)
+            rng[size_t(t & 3) * g.Y + r0 + (t >> 2)] = reinterpret_cast<const uint64_t*>(buf + total)[t];
 }
 
 template <typename Word>

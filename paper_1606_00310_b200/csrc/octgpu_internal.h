@@ -55,6 +55,12 @@ constexpr int kDeepWarps = OCTGPU_DEEP_WARPS;
 constexpr int kDeepMinBlocks = kDeepWarps >= 8 ? 2 : 3;  // resident blocks per SM the register budget targets
 constexpr int deep_box_rows(int L) { return ((34 - 2 * L) * (kDeepWarps - 1) + 34) / 2 * 2; }
 
+// Row stripes: halo rows above / below the core rows (local rows 0..HA-1 and
+// HA+L..HA+L+HB-1): enough for k_mcs_deep's 2-MCS pass (3 rows of shrinking
+// lanes each side + stage 1's Y(s)[y+1]); the one-MCS kernels use 1 / 2 of them.
+constexpr uint32_t kStripeHA = uint32_t(kDeepSweeps) - 1;
+constexpr uint32_t kStripeHB = uint32_t(kDeepSweeps);
+
 // periodic lattices keep this many ghost rows (>= every TMA window) so windows never wrap
 constexpr uint32_t kGhostRows = deep_box_rows(kDeepSweeps) <= 192 ? 192 : 256;
 static_assert(kTmaBoxRows <= kGhostRows && uint32_t(deep_box_rows(kDeepSweeps)) <= kGhostRows, "ghost rows");
@@ -113,8 +119,8 @@ cudaError_t launch_measure(int w, const void* planes, Geom g, uint32_t X, void* 
                            cudaStream_t st);
 
 // Row-stripe halo exchange: gather rows [r0, r0+nrows) of all 4 planes (and
-// the rng state of row r0 when rng != null) into a contiguous buffer laid
-// out [plane][row][word] + [4] state words, or scatter such a buffer back.
+// their rng states when rng != null) into a contiguous buffer laid out
+// [plane][row][word] + [row][4] state words, or scatter such a buffer back.
 cudaError_t launch_rows_gather(int w, const void* planes, const uint64_t* rng, Geom g, uint32_t r0, uint32_t nrows,
                                void* buf, cudaStream_t st);
 cudaError_t launch_rows_scatter(int w, void* planes, uint64_t* rng, Geom g, uint32_t r0, uint32_t nrows,

@@ -2,18 +2,19 @@
 
 Partition: contiguous row blocks exactly as the reference's SweepPlan
 (params.hpp:107-127; the result is partition-independent, like the
-reference's worker count). Per MCS, stripe r (rows [y0, y1)):
+reference's worker count). Per pass of k MCS (k = 2 for constant-xi
+parameters: the temporally blocked kernel; else 1), stripe r (rows [y0, y1),
+at least 4):
 
-  1. pack      rows y0, y0+1 (+ rng state of y0) -> to_prev; row y1-1 (+ state) -> to_next
+  1. pack      rows y0..y0+3 (+ rng states) -> to_prev; rows y1-3..y1-1 (+ states) -> to_next
   2. exchange  shift-up   (to_prev -> rank r-1, from_next <- rank r+1)
                shift-down (to_next -> rank r+1, from_prev <- rank r-1)
-  3. unpack    halo rows y0-1 (from_prev) and y1, y1+1 (from_next)
-  4. mcs       fused sweep f / sweep f^1 over the stripe's rows (k_mcs_bulk)
+  3. unpack    halo rows y0-3..y0-1 (from_prev) and y1..y1+3 (from_next)
+  4. mcs       k fused MCS over the stripe's rows (k_mcs_deep / k_mcs_bulk)
   5. boundary  y-plane f of row y1 -> rank r+1, which completes its row y0 (finish)
 
-The halo traffic is 3 plane-rows x 4 planes + one plane-row per stripe
-boundary per MCS (X/16 bytes per plane-row), independent of the stripe
-height. Measurement: every stripe reduces its own rows in a local height
+The halo traffic is 7 x 4 plane-rows + one plane-row per stripe boundary
+per pass (X/16 bytes per plane-row), independent of the stripe height. Measurement: every stripe reduces its own rows in a local height
 gauge; the exact int128 power sums are shifted binomially by the column-0
 prefix of the stripes above and summed (``combine``).
 
@@ -158,9 +159,17 @@ class StripeEngine:
     def unpack(self, from_prev, from_next) -> None:
         check(lib().octgpu_halo_unpack(self._h, self._p(from_prev), self._p(from_next)))
 
-    def mcs(self, prm: UpdateParams, boundary_out) -> None:
+    def mcs(self, prm: UpdateParams, boundary_out, n: int = 1) -> None:
         c = prm.to_c()
-        check(lib().octgpu_stripe_mcs(self._h, C.byref(c), self._p(boundary_out)))
+        check(lib().octgpu_stripe_mcs_n(self._h, C.byref(c), n, self._p(boundary_out)))
+
+    def max_mcs(self, prm: UpdateParams) -> int:
+        """MCS one halo exchange can cover for these parameters (1, or 2 with constant xi)."""
+        c = prm.to_c()
+        k = int(lib().octgpu_stripe_max_mcs(self._h, C.byref(c)))
+        if k < 1:
+            check(1)
+        return k
 
     def finish(self, boundary_in) -> None:
         check(lib().octgpu_stripe_finish(self._h, self._p(boundary_in)))
@@ -284,11 +293,14 @@ class StripeGroup:
         self.tr, self.X, self.Y = transport, X, Y
 
     def step(self, prm: UpdateParams, n: int = 1) -> None:
-        for _ in range(n):
+        kmax = self.tr.engines[0].max_mcs(prm)  # the same on every rank (depends on params and X only)
+        while n > 0:
+            k = min(n, kmax)
             self.tr.halos()
             for e, b in zip(self.tr.engines, self.tr.bufs):
-                e.mcs(prm, b.bo)
+                e.mcs(prm, b.bo, k)
             self.tr.boundary()
+            n -= k
 
     def measure(self) -> MeasurementRecord:
         self.tr.halos()  # the curl check of each stripe's first row reads the row above

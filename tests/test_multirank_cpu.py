@@ -112,7 +112,7 @@ def test_combine_reproduces_global_moments(oracle):
     parts = []
     for (y0, y1) in [(0, 7), (7, 19), (19, 30)]:
         st = OracleStripe(oracle, X, Y, y0, y1, 3)
-        st.buf[:, 1:y1 - y0 + 1] = L.planes[:, y0:y1]
+        st.buf[:, st.HA:st.HA + y1 - y0] = L.planes[:, y0:y1]
         parts.append(st.measure_local())
     rec = combine(parts, X, Y)
     h, _ = oracle.reconstruct(L.planes)

@@ -23,8 +23,10 @@ def _group(cfg, parts, seed, stream):
     return StripeGroup(LocalTransport(engines, alloc), cfg.X, cfg.Y), engines
 
 
-@pytest.mark.parametrize("X,Y,parts", [(1024, 128, 2), (1024, 130, 4), (2048, 96, 3), (256, 40, 2), (8192, 512, 8)])
-@pytest.mark.parametrize("pq", [(0.5, 0.0), (0.98, 0.02), (1.0, 0.0), (0.75, 0.5)])
+# (1024, 32, 8): 4-row stripes, the minimum (the 2-MCS pass reads 4 rows of the next stripe)
+@pytest.mark.parametrize("X,Y,parts", [(1024, 128, 2), (1024, 130, 4), (2048, 96, 3), (256, 40, 2), (8192, 512, 8),
+                                       (1024, 32, 8)])
+@pytest.mark.parametrize("pq", [(0.5, 0.0), (0.98, 0.02), (1.0, 0.0), (0.75, 0.5), (0.0, 0.0)])
 def test_stripes_match_single_engine(X, Y, parts, pq):
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
@@ -67,3 +69,14 @@ def test_stripe_curl_violation_reported_globally():
         with pytest.raises(octgpu.InvariantError) as e2:
             grp.measure()
         assert str(e1.value) == str(e2.value)
+
+
+def test_stripe_pass_sizes():
+    cfg = octgpu.LatticeConfig(1024, 64)
+    e = StripeEngine(cfg, 0, 32, 3)
+    assert e.max_mcs(octgpu.UpdateParams.make(1.0, 0.0)) == 2  # constant xi: 2-MCS passes (k_mcs_deep)
+    assert e.max_mcs(octgpu.UpdateParams.make(0.5, 0.0)) == 1
+    with pytest.raises(octgpu.ConfigError):
+        e.mcs(octgpu.UpdateParams.make(0.5, 0.0), torch.zeros(e.boundary_bytes, dtype=torch.uint8, device="cuda"), 2)
+    with pytest.raises(octgpu.ConfigError):
+        StripeEngine(cfg, 0, 3, 3)  # fewer rows than the halo a pass reads

@@ -33,7 +33,8 @@ CONFIGS = {
     "c3": dict(X=1 << 16, Y=1 << 16, p=0.5, q=0.5, workload="2^16x2^16 EW-like p=q=1/2 (BASELINE configs[2])"),
     "c4": dict(X=1 << 16, Y=1 << 16, p=0.98, q=0.02,
                workload="2^16x2^16 arbitrary p=0.98 q=0.02 (BASELINE configs[3])"),
-    "c5": dict(X=1 << 17, Y=1 << 17, p=1.0, q=0.0, workload="2^17x2^17 KPZ p=1 q=0 (BASELINE configs[4])"),
+    "c5": dict(X=1 << 17, Y=1 << 17, p=1.0, q=0.0, workload="2^17x2^17 KPZ p=1 q=0 (BASELINE configs[4])",
+               multi="strong"),
 }
 METRIC = "site updates/ns"
 SCHEDULE_TMAX, SCHEDULE_PPD = 10000, 8
@@ -160,9 +161,15 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
     ws, rank, local = _dist()
     K, W = args.steps, max(3, args.warmup)
+    # N > 1: c5 is one fixed 2^17 x 2^17 lattice striped over the GPUs (strong scaling, BASELINE configs[4]);
+    # the 2^16 x 2^16 configs keep 2^16 x 2^16 sites per GPU: an X x (N * 2^16) lattice in N row stripes (weak)
+    scaling = cfg.get("multi", "weak")
+    if ws > 1 and scaling == "weak":
+        cfg["Y"] = cfg["Y"] * ws
+        cfg["workload"] += f"; {ws} GPUs: {cfg['X']}x{cfg['Y']} lattice, one 2^16-row stripe per GPU"
 
     config_key = {"workload": cfg["workload"], "X": cfg["X"], "Y": cfg["Y"], "p": cfg["p"], "q": cfg["q"],
                   "w": 64, "seed": 1, "schedule": f"log_schedule({SCHEDULE_TMAX},{SCHEDULE_PPD}) within steps",
@@ -174,8 +181,8 @@ def main():
         v, cores, done, el = cpu_reference_run(cfg, K, W, args.cpu_budget)
         sample = f"{done} MCS of {cfg['X']}x{cfg['Y']} (steps only, no W2), {el:.1f} s"
         print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": "updates/ns",
-                          "n_gpus": 0, "steps": done, "warmup": min(W, 1), "ms_per_step": el * 1e3 / done,
-                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+                          "n_gpus": ws, "steps": done, "warmup": min(W, 1), "ms_per_step": el * 1e3 / done,
+                          "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u64",
                           "data": "synthetic (flat start, seed 1)", "config": config_key,
                           "cpu_baseline": {"value": v, "unit": "updates/ns", "cores": cores, "kind": "reference",
                                            "sample": sample},
@@ -339,7 +346,7 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "updates/ns", "n_gpus": ws, "steps": K, "warmup": W,
-            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": "u64", "data": "synthetic (flat start h=(x+y) mod 2, seed 1)", "config": config_key,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": _traffic(kname, args.config), "kernel": f"{kname} ({mcs_per_launch} MCS per launch)",

@@ -266,8 +266,15 @@ class DistTransport:
     def halos(self):
         e, b = self.engines[0], self.bufs[0]
         e.pack(b.tp, b.tn)
-        self._shift(b.tp, self.prev, b.rn, self.next)  # shift up
-        self._shift(b.tn, self.next, b.rp, self.prev)  # shift down
+        if self.size == 1:
+            b.rn.copy_(b.tp)
+            b.rp.copy_(b.tn)
+        else:  # shift up and shift down in one batch (per-peer order matches sends to receives)
+            d = self.dist
+            ops = [d.P2POp(d.isend, b.tp, self.prev), d.P2POp(d.irecv, b.rn, self.next),
+                   d.P2POp(d.isend, b.tn, self.next), d.P2POp(d.irecv, b.rp, self.prev)]
+            for req in d.batch_isend_irecv(ops):
+                req.wait()
         e.unpack(b.rp, b.rn)
 
     def boundary(self):

@@ -111,13 +111,13 @@ def _traffic(kernel: str, config: str):
 def _mcs_kernel(prm, Y: int, n: int, ws: int) -> tuple[str, int]:
     """The fused MCS kernel the engine runs for these parameters and the MCS per launch
     (engine.cu octgpu_step: k_mcs_deep, 2 MCS per pass, for constant-xi modes on periodic
-    lattices with n >= 8 words and >= 192 rows; otherwise k_mcs_bulk, 1 MCS per pass)."""
+    lattices with n >= 8 words and >= 256 rows, and row stripes; otherwise k_mcs_bulk, 1 MCS per pass)."""
     from paper_1606_00310_b200.params import ProbMode
 
     const = all(ps.mode == ProbMode.Zero or (ps.mode == ProbMode.Arbitrary and ps.value == 1.0)
                 for ps in (prm.p, prm.q))
-    if ws == 1 and const and n >= 8 and Y >= 192 and os.environ.get("OCTGPU_DEEP", "1") != "0":
-        return "k_mcs_deep", 2
+    if const and n >= 8 and (ws > 1 or Y >= 256) and os.environ.get("OCTGPU_DEEP", "1") != "0":
+        return "k_mcs_deep", 2  # periodic lattice, or each rank's row stripe (2-MCS passes)
     return "k_mcs_bulk", 1
 
 
@@ -195,11 +195,18 @@ def main():
 
     import paper_1606_00310_b200 as octgpu
 
+    # OCTGPU_BENCH_ONE_GPU=1 (protocol check only, timings meaningless): every rank on cuda:0, gloo
+    one_gpu = os.environ.get("OCTGPU_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.Stream(dev)  # a real (non-default) stream shared by the engine and the timing events
     torch.cuda.set_stream(stream)
 
@@ -222,20 +229,44 @@ def main():
                 eng = octgpu.GpuEngine(octgpu.SlopeField(lat, planes), octgpu.RngStreamSet(1, states), device=local)
             eng.set_stream(stream.cuda_stream)
             return eng, [eng]
-        from paper_1606_00310_b200.stripes import DistTransport, StripeEngine, StripeGroup, stripe_bounds
+        from paper_1606_00310_b200.stripes import (DistTransport, PeerDistTransport, StripeEngine, StripeGroup,
+                                                   stripe_bounds)
         y0, y1 = stripe_bounds(Y, ws, rank)
-        e = StripeEngine(lat, y0, y1, 1, device=local,
-                         planes=None if planes is None else planes[:, y0:y1],
-                         states=None if states is None else states[y0:y1])
+        e = StripeEngine(lat, y0, y1, 1, device=local, planes=planes, states=states)  # this rank's rows only
         e.set_stream(stream.cuda_stream)
         alloc = lambda nb: torch.zeros(nb, dtype=torch.uint8, device=dev)  # noqa: E731
-        return StripeGroup(DistTransport(e, alloc), X, Y), [e]
+        return StripeGroup(_transport(e, alloc, PeerDistTransport, DistTransport), X, Y), [e]
+
+    transport_used = []
+
+    def _close(job):
+        tr = getattr(job, "tr", None)
+        if tr is not None and hasattr(tr, "close"):
+            tr.close()
+
+    def _transport(e, alloc, peer_cls, nccl_cls):
+        """Device-side peer-memory halo exchange (csrc/p2p.cu) unless OCTGPU_TRANSPORT=nccl or any rank
+        cannot map its neighbours (then every rank falls back to the NCCL host protocol)."""
+        ok, tr = 0, None
+        if os.environ.get("OCTGPU_TRANSPORT", "p2p") == "p2p":
+            try:
+                tr, ok = peer_cls(e), 1
+            except Exception as ex:  # noqa: BLE001 - reported in the JSON line
+                transport_used.append(f"p2p unavailable: {ex}")
+        flag = torch.tensor([ok], device=dev)
+        torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)
+        if int(flag[0]) == 1:
+            transport_used.append("p2p (device-side halo exchange over peer memory)")
+            return tr
+        transport_used.append("nccl (host-driven isend/irecv)")
+        return nccl_cls(e, alloc)
 
     # ---- warm-up (separate engine; the timed run starts from the flat state) ----
     job, engs = make()
     job.step(prm, W)
     job.measure()
     torch.cuda.synchronize()
+    _close(job)
     del job, engs
     torch.cuda.synchronize()
 
@@ -285,17 +316,25 @@ def main():
     launch_ms = kernel_ms * mcs_per_launch
     achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
     final_checksum = engs[0].checksum() if ws == 1 and X * Y <= (1 << 32) else None
+    _close(job)
     del job, engs
 
     # ---- e2e through the C-ABI with host buffers ----
     e2e = None
     if not args.no_e2e:
-        flat = octgpu.new_flat(lat)
-        states0 = octgpu.RngStreamSet.derive(1, Y).states
-        host_planes = torch.from_numpy(flat.planes.view(np.int64)).pin_memory()
-        host_states = torch.from_numpy(states0.view(np.int64)).pin_memory()
+        # this rank's input (the whole lattice, or its row stripe) in pinned host memory, and pinned
+        # result buffers, prepared before the timed region
+        if ws == 1:
+            r0, r1 = 0, Y
+        else:
+            from paper_1606_00310_b200.stripes import stripe_bounds
+            r0, r1 = stripe_bounds(Y, ws, rank)
+        flat = np.zeros((4, r1 - r0, X // 128), np.uint64)  # new_flat (slope_field.hpp:110-118): rows do not
+        flat[1] = flat[3] = np.iinfo(np.uint64).max         # depend on y, so any row range is a flat stripe
+        states0 = octgpu.RngStreamSet.derive(1, r1).states[r0:r1]
+        host_planes = torch.from_numpy(np.ascontiguousarray(flat).view(np.int64)).pin_memory()
+        host_states = torch.from_numpy(np.ascontiguousarray(states0).view(np.int64)).pin_memory()
         import ctypes as C
-        # pinned result buffers (allocated before the timed region, like the pinned inputs)
         pin_planes = torch.empty(host_planes.shape, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
         pin_states = torch.empty(host_states.shape, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
         barrier()
@@ -313,24 +352,22 @@ def main():
             if target in sched:
                 job.measure()
                 n_meas += 1
-        if ws > 1:
-            out_planes = engs[0].planes()
-            out_states = engs[0].states()
-        else:
-            out_planes = engs[0].planes(out=pin_planes)
-            out_states = engs[0].streams(out=pin_states).states
+        out_planes = engs[0].planes(out=pin_planes)
+        out_states = (engs[0].states(out=pin_states) if ws > 1 else engs[0].streams(out=pin_states).states)
         el = time.perf_counter() - t0
+        _close(job)
         del job, engs
         if ws > 1:
             tt = torch.tensor([el], device=dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             el = float(tt[0])
         e2e = {"value": X * Y * K / (el * 1e9), "unit": "updates/ns",
-               "h2d_bytes_per_step": (hp.nbytes + hs.nbytes) / K,
+               "h2d_bytes_per_step": ws * (hp.nbytes + hs.nbytes) / K,
                "d2h_bytes_per_step": (ws * (out_planes.nbytes + out_states.nbytes)
                                       + n_meas * C.sizeof(octgpu._lib.OctMoments)) / K,
                "wall_s": el,
-               "note": "engine created from pinned host planes+states, K MCS + measurements, planes/states D2H"}
+               "note": "engine(s) created from pinned host planes+states (each rank its stripe), K MCS + "
+                       "measurements, planes/states D2H into pinned buffers; max over ranks"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -356,6 +393,7 @@ def main():
                                  "kernels move ~0.5 B (k_mcs_bulk) / ~0.25 B (k_mcs_deep) of DRAM traffic per update, "
                                  "so frac exceeds 1; traffic = ncu dram bytes per launch (profiles/ncu_summary.json)"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+            "transport": transport_used[-1] if transport_used else None,
             "measurements": len(records),
             "W2_last": records[-1].W2 if records else None,
             "final_checksum": hex(final_checksum) if final_checksum is not None else None,

@@ -191,6 +191,42 @@ int octgpu_measure_stripe(octgpu_engine* e, octgpu_stripe_moments* out);
 uint32_t octgpu_stripe_y0(const octgpu_engine* e);
 uint32_t octgpu_stripe_rows(const octgpu_engine* e);
 
+/* ---- device-side halo exchange over peer memory (NVLink P2P / same GPU) ----
+ * Replaces pack -> NCCL -> unpack -> boundary -> finish with kernels that read
+ * the neighbours' rows and write the boundary plane-row directly in their
+ * memory, synchronised by per-stripe "passes done" counters in device memory
+ * (no host round trip, no NCCL). Stripes must step in lockstep (same number of
+ * passes with the same k). Needs w = 64 and X >= 1024 (the TMA kernels).
+ *   octgpu_stripe_peer        this stripe's device memory, as seen by this process
+ *   octgpu_stripe_ipc_export  the same as a CUDA IPC blob (OCTGPU_IPC_BYTES) for another process
+ *   octgpu_stripe_ipc_open    map a neighbour's blob into this process
+ *   octgpu_stripe_connect     set the ring neighbours (the same peer twice for 2 stripes) and pull the
+ *                             initial halo rows with their xoshiro states
+ *   octgpu_stripe_pass        one pass of n_mcs (1, or 2 with constant xi): pull -> MCS -> push + signal
+ *   octgpu_stripe_pull        refresh the halo rows (before octgpu_measure_stripe)
+ *   octgpu_stripe_disconnect  unmap the neighbours (every rank, then a barrier, before any rank frees its stripe)
+ * A neighbour that stops stepping makes the waits time out (~10 s): the next
+ * octgpu_measure_stripe / octgpu_sync reports OCTGPU_ERR_CUDA. */
+#define OCTGPU_IPC_BYTES 512
+typedef struct {
+    uint64_t planes[2]; /* device addresses of the two plane sets */
+    uint64_t rng[2];    /* device addresses of the two rng-state sets */
+    uint64_t done;      /* device address of the passes-done counter */
+    uint32_t alloc_rows;
+    uint32_t rows;
+    uint32_t n;
+    uint32_t w;
+    int32_t device;
+    int32_t pad;
+} octgpu_peer;
+int octgpu_stripe_peer(const octgpu_engine* e, octgpu_peer* out);
+int octgpu_stripe_ipc_export(const octgpu_engine* e, void* out);
+int octgpu_stripe_ipc_open(octgpu_engine* e, const void* blob, octgpu_peer* out);
+int octgpu_stripe_connect(octgpu_engine* e, const octgpu_peer* prev, const octgpu_peer* next);
+int octgpu_stripe_pass(octgpu_engine* e, const octgpu_params* prm, uint32_t n_mcs);
+int octgpu_stripe_pull(octgpu_engine* e);
+int octgpu_stripe_disconnect(octgpu_engine* e);
+
 /* ---- diagnostics ---- */
 const char* octgpu_last_error(void);
 const char* octgpu_version(void);

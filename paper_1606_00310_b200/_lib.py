@@ -74,6 +74,22 @@ class OctStripeMoments(C.Structure):
     ]
 
 
+class OctPeer(C.Structure):
+    _fields_ = [
+        ("planes", C.c_uint64 * 2),
+        ("rng", C.c_uint64 * 2),
+        ("done", C.c_uint64),
+        ("alloc_rows", C.c_uint32),
+        ("rows", C.c_uint32),
+        ("n", C.c_uint32),
+        ("w", C.c_uint32),
+        ("device", C.c_int32),
+        ("pad", C.c_int32),
+    ]
+
+
+IPC_BYTES = 512  # OCTGPU_IPC_BYTES
+
 # Every symbol include/octgpu.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "octgpu_resolve", "octgpu_draws_per_word", "octgpu_validate_lattice", "octgpu_stream_states",
@@ -82,7 +98,9 @@ EXPORTS = (
     "octgpu_get_planes", "octgpu_get_states", "octgpu_field_checksum", "octgpu_measure", "octgpu_heights",
     "octgpu_last_error", "octgpu_version", "octgpu_launch_count", "octgpu_create_stripe", "octgpu_stripe_sizes",
     "octgpu_halo_pack", "octgpu_halo_unpack", "octgpu_stripe_mcs", "octgpu_stripe_mcs_n", "octgpu_stripe_max_mcs",
-    "octgpu_stripe_finish", "octgpu_measure_stripe",
+    "octgpu_stripe_finish", "octgpu_measure_stripe", "octgpu_stripe_peer", "octgpu_stripe_ipc_export",
+    "octgpu_stripe_ipc_open", "octgpu_stripe_connect", "octgpu_stripe_pass", "octgpu_stripe_pull",
+    "octgpu_stripe_disconnect",
     "octgpu_stripe_y0", "octgpu_stripe_rows", "octgpu_height_moments",
 )
 
@@ -131,6 +149,13 @@ def lib() -> C.CDLL:
         "octgpu_stripe_mcs": (i32, [vp, P(OctParams), vp]),
         "octgpu_stripe_mcs_n": (i32, [vp, P(OctParams), u32, vp]),
         "octgpu_stripe_max_mcs": (i32, [vp, P(OctParams)]),
+        "octgpu_stripe_peer": (i32, [vp, P(OctPeer)]),
+        "octgpu_stripe_ipc_export": (i32, [vp, vp]),
+        "octgpu_stripe_ipc_open": (i32, [vp, vp, P(OctPeer)]),
+        "octgpu_stripe_connect": (i32, [vp, P(OctPeer), P(OctPeer)]),
+        "octgpu_stripe_pass": (i32, [vp, P(OctParams), u32]),
+        "octgpu_stripe_pull": (i32, [vp]),
+        "octgpu_stripe_disconnect": (i32, [vp]),
         "octgpu_stripe_finish": (i32, [vp, vp]),
         "octgpu_measure_stripe": (i32, [vp, P(OctStripeMoments)]),
         "octgpu_stripe_y0": (u32, [vp]),

@@ -342,6 +342,14 @@ struct octgpu_engine {
     // count. Periodic mode: Y = Ytot, y0 = 0, L = Ytot.
     bool stripe = false;
     uint32_t Ytot = 0, y0 = 0, L = 0;
+    // device-side P2P halo exchange (p2p.cu): passes completed (device counter,
+    // exposed to the neighbours), timeout flag, and the neighbours' memory
+    uint64_t* done = nullptr;
+    uint32_t* p2p_err = nullptr;
+    uint64_t passes = 0;
+    bool p2p = false;
+    octgpu_peer prev{}, next{};
+    std::vector<void*> ipc_opened;  // peer allocations mapped with cudaIpcOpenMemHandle
 
     // k_mcs_deep: the same periodic lattice with core rows starting at virtual row kDeepSweeps - 1
     Geom deep_geom() const { return Geom{Y, n, size_t(n) * Y, kDeepSweeps - 1, L + kDeepSweeps - 1, L, 0, kGhostRows}; }
@@ -502,6 +510,15 @@ int plan_bulk(octgpu_engine* e, const ProbDev& p, const ProbDev& q) {
     return ensure_tmaps(e);
 }
 
+int alloc_p2p(octgpu_engine* e) {
+    // separate allocations: each is exported on its own with cudaIpcGetMemHandle
+    CK(cudaMalloc(reinterpret_cast<void**>(&e->done), 256));
+    CK(cudaMalloc(reinterpret_cast<void**>(&e->p2p_err), 256));
+    CK(cudaMemset(e->done, 0, 256));
+    CK(cudaMemset(e->p2p_err, 0, 256));
+    return OCTGPU_OK;
+}
+
 int alloc_engine(octgpu_engine* e) {
     CK(cudaSetDevice(e->device));
     CK(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
@@ -617,6 +634,7 @@ int make_engine(uint32_t X, uint32_t Ytot, uint32_t w, bool stripe, uint32_t y0,
     // zero-fill past the allocation); even for 16-B alignment
     e->Y = stripe ? ((L + kStripeHA + kStripeHB + 34 + 1) & ~1u) : Ytot + kGhostRows;
     int rc = alloc_engine(e);
+    if (!rc && stripe) rc = alloc_p2p(e);
     if (rc) {
         std::string keep = g_err;
         octgpu_destroy(e);
@@ -778,6 +796,9 @@ void octgpu_destroy(octgpu_engine* e) {
         if (e->rng[i]) cudaFree(e->rng[i]);
     }
     for (auto& kv : e->jtabs) cudaFree(kv.second);
+    for (void* ptr : e->ipc_opened) cudaIpcCloseMemHandle(ptr);
+    if (e->done) cudaFree(e->done);
+    if (e->p2p_err) cudaFree(e->p2p_err);
     if (e->stage) cudaFree(e->stage);
     if (e->scratch) cudaFree(e->scratch);
     if (e->res_dev) cudaFree(e->res_dev);
@@ -801,6 +822,11 @@ int octgpu_sync(octgpu_engine* e) {
     if (rc) return rc;
     CK(cudaStreamSynchronize(e->stream));
     CK(cudaGetLastError());
+    if (e->p2p) {  // a peer-memory halo wait that timed out (p2p.cu)
+        uint32_t err = 0;
+        CK(cudaMemcpy(&err, e->p2p_err, sizeof(err), cudaMemcpyDeviceToHost));
+        if (err) return fail(OCTGPU_ERR_CUDA, "peer halo exchange timed out waiting for a neighbour stripe");
+    }
     return OCTGPU_OK;
 }
 
@@ -1185,6 +1211,8 @@ int octgpu_measure_stripe(octgpu_engine* e, octgpu_stripe_moments* out) {
     e->launches += 3;
     CK(cudaMemcpyAsync(e->res_host, e->res_dev, sizeof(MeasureResult), cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
+    rc = octgpu_sync(e);  // reports a timed-out peer halo wait
+    if (rc) return rc;
     const MeasureResult& r = *e->res_host;
     out->t = e->t;
     out->n_sites = uint64_t(e->X) * e->L;
@@ -1197,6 +1225,181 @@ int octgpu_measure_stripe(octgpu_engine* e, octgpu_stripe_moments* out) {
     out->row_first_sum = r.row0_sum;
     out->curl_count = r.curl_count;
     out->curl_first = r.curl_count ? r.curl_first + uint64_t(e->y0) * e->X : ~0ull;
+    return OCTGPU_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Device-side halo exchange over peer memory (p2p.cu)
+
+namespace {
+struct IpcBlob {
+    cudaIpcMemHandle_t h[5];  // planes[0], planes[1], rng[0], rng[1], done
+    uint32_t alloc_rows, rows, n, w;
+    int32_t device;
+};
+static_assert(sizeof(IpcBlob) <= OCTGPU_IPC_BYTES, "IPC blob");
+
+PeerView peer_view(const octgpu_engine* e, const octgpu_peer& p) {
+    return PeerView{reinterpret_cast<const void*>(p.planes[e->pcur]), reinterpret_cast<const uint64_t*>(p.rng[e->rcur]),
+                    reinterpret_cast<const uint64_t*>(p.done), p.alloc_rows, p.rows};
+}
+
+int p2p_pull(octgpu_engine* e, bool with_rng) {
+    CK(launch_halo_pull(e->w, e->planes[e->pcur], e->rng[e->rcur], e->geom(), peer_view(e, e->prev),
+                        peer_view(e, e->next), e->passes, e->p2p_err, with_rng, e->stream));
+    ++e->launches;
+    return OCTGPU_OK;
+}
+
+}  // namespace
+
+int octgpu_stripe_peer(const octgpu_engine* e, octgpu_peer* out) {
+    if (!e || !e->stripe || !out) return fail(OCTGPU_ERR_CONFIG, "not a row stripe / null output");
+    *out = octgpu_peer{};
+    for (int i = 0; i < 2; ++i) {
+        out->planes[i] = reinterpret_cast<uint64_t>(e->planes[i]);
+        out->rng[i] = reinterpret_cast<uint64_t>(e->rng[i]);
+    }
+    out->done = reinterpret_cast<uint64_t>(e->done);
+    out->alloc_rows = e->Y;
+    out->rows = e->L;
+    out->n = e->n;
+    out->w = e->w;
+    out->device = e->device;
+    return OCTGPU_OK;
+}
+
+int octgpu_stripe_ipc_export(const octgpu_engine* e, void* out) {
+    if (!e || !e->stripe || !out) return fail(OCTGPU_ERR_CONFIG, "not a row stripe / null output");
+    IpcBlob b{};
+    CK(cudaSetDevice(e->device));
+    void* ptrs[5] = {e->planes[0], e->planes[1], e->rng[0], e->rng[1], e->done};
+    for (int i = 0; i < 5; ++i) CK(cudaIpcGetMemHandle(&b.h[i], ptrs[i]));
+    b.alloc_rows = e->Y;
+    b.rows = e->L;
+    b.n = e->n;
+    b.w = e->w;
+    b.device = e->device;
+    std::memset(out, 0, OCTGPU_IPC_BYTES);
+    std::memcpy(out, &b, sizeof(b));
+    return OCTGPU_OK;
+}
+
+int octgpu_stripe_ipc_open(octgpu_engine* e, const void* blob, octgpu_peer* out) {
+    if (!e || !e->stripe || !blob || !out) return fail(OCTGPU_ERR_CONFIG, "not a row stripe / null argument");
+    IpcBlob b;
+    std::memcpy(&b, blob, sizeof(b));
+    CK(cudaSetDevice(e->device));
+    void* ptrs[5];
+    for (int i = 0; i < 5; ++i) {
+        CK(cudaIpcOpenMemHandle(&ptrs[i], b.h[i], cudaIpcMemLazyEnablePeerAccess));
+        e->ipc_opened.push_back(ptrs[i]);
+    }
+    *out = octgpu_peer{};
+    for (int i = 0; i < 2; ++i) {
+        out->planes[i] = reinterpret_cast<uint64_t>(ptrs[i]);
+        out->rng[i] = reinterpret_cast<uint64_t>(ptrs[2 + i]);
+    }
+    out->done = reinterpret_cast<uint64_t>(ptrs[4]);
+    out->alloc_rows = b.alloc_rows;
+    out->rows = b.rows;
+    out->n = b.n;
+    out->w = b.w;
+    out->device = b.device;
+    return OCTGPU_OK;
+}
+
+int octgpu_stripe_connect(octgpu_engine* e, const octgpu_peer* prev, const octgpu_peer* next) {
+    if (!e || !e->stripe || !prev || !next) return fail(OCTGPU_ERR_CONFIG, "not a row stripe / null peer");
+    if (e->mcs_impl != 2)
+        return fail(OCTGPU_ERR_CONFIG, "the peer-memory halo exchange needs w = 64 and X >= 1024 (TMA kernels)");
+    for (const octgpu_peer* p : {prev, next}) {
+        if (p->n != e->n || p->w != e->w) return fail(OCTGPU_ERR_CONFIG, "peer stripe has a different row width");
+        if (p->rows < kStripeHB) return fail(OCTGPU_ERR_CONFIG, "peer stripe holds fewer rows than the halo");
+    }
+    int rc = use_device(e);
+    if (rc) return rc;
+    for (const octgpu_peer* p : {prev, next})
+        if (p->device != e->device) {
+            const cudaError_t pe = cudaDeviceEnablePeerAccess(p->device, 0);
+            if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) CK(pe);
+            cudaGetLastError();
+        }
+    if (e->pending) return fail(OCTGPU_ERR_CONFIG, "connect stripes before stepping them");
+    e->prev = *prev;
+    e->next = *next;
+    e->p2p = true;
+    return p2p_pull(e, true);  // halo rows with their streams; later passes advance those streams locally
+}
+
+int octgpu_stripe_disconnect(octgpu_engine* e) {
+    if (!e || !e->stripe) return fail(OCTGPU_ERR_CONFIG, "not a row stripe");
+    int rc = use_device(e);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(e->stream));
+    for (void* ptr : e->ipc_opened) CK(cudaIpcCloseMemHandle(ptr));
+    e->ipc_opened.clear();
+    e->p2p = false;
+    e->prev = e->next = octgpu_peer{};
+    return OCTGPU_OK;
+}
+
+int octgpu_stripe_pull(octgpu_engine* e) {
+    if (!e || !e->stripe || !e->p2p) return fail(OCTGPU_ERR_CONFIG, "not a connected row stripe");
+    int rc = use_device(e);
+    if (rc) return rc;
+    return p2p_pull(e, false);
+}
+
+int octgpu_stripe_pass(octgpu_engine* e, const octgpu_params* prm, uint32_t n_mcs) {
+    if (!e || !e->stripe || !e->p2p) return fail(OCTGPU_ERR_CONFIG, "not a connected row stripe");
+    ProbDev p, q;
+    int rc = lower_params(prm, p, q);
+    if (!rc) rc = use_device(e);
+    if (rc) return rc;
+    const bool deep = n_mcs == uint32_t(kDeepSweeps / 2);
+    if (n_mcs != 1 && !(deep && stripe_deep_ok(e, p, q)))
+        return fail(OCTGPU_ERR_CONFIG, "a stripe pass covers 1 MCS, or " + std::to_string(kDeepSweeps / 2) +
+                                           " with constant xi (see octgpu_stripe_max_mcs)");
+    const bool live = !(is_const(p) && is_const(q));
+    const uint64_t D = draws(prm->p, e->w) + (q.mode != M_ZERO ? draws(prm->q, e->w) : 0);
+    const uint64_t per_sweep = uint64_t(e->n) * D;
+    // 1. wait for the neighbours' previous pass, pull their boundary rows
+    rc = p2p_pull(e, false);
+    if (rc) return rc;
+    // 2. lazy stream advance (after the wait: no neighbour reads our states any more)
+    uint64_t* jtab = nullptr;
+    if (live) {
+        rc = materialize(e);
+        if (!rc) rc = get_table(e, per_sweep, &jtab);
+        if (rc) return rc;
+    }
+    // 3. the MCS kernel
+    const Geom g = e->geom();
+    const int ps = e->pcur, rs = e->rcur;
+    if (deep) {
+        rc = ensure_tmaps_deep(e);
+        if (rc) return rc;
+        CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
+                           e->deep_S, &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
+    } else {
+        rc = plan_bulk(e, p, q);
+        if (rc) return rc;
+        CK(launch_mcs_bulk(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
+                           e->bulk_ks, e->bulk_S, &e->tm[ps][0], &e->tm[ps][1], e->stream));
+    }
+    e->pcur ^= 1;
+    if (live)
+        e->rcur ^= 1;
+    else
+        e->pending += 2 * uint64_t(n_mcs) * per_sweep;
+    e->t += n_mcs;
+    ++e->passes;
+    // 4. the boundary plane-row into the next stripe's new plane set, then publish the pass
+    CK(launch_push_signal(e->w, e->planes[e->pcur], 2 + e->phase, g,
+                          reinterpret_cast<void*>(e->next.planes[e->pcur]), e->next.alloc_rows, e->done, e->passes,
+                          e->stream));
+    e->launches += 2;
     return OCTGPU_OK;
 }
 

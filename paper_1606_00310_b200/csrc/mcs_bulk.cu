@@ -322,10 +322,11 @@ __global__ void __launch_bounds__(32 * (kP + 1), 4) k_mcs_bulk(const uint64_t* _
         put(dXf + Y, xf1 ^ (sh2 ? Word(m2 >> (W - 1)) : Word(0)), core);
     }
     if constexpr (LIVE) {
-        if (core) {
-            store_state(rd, Y, y, s2);
-            if (ghost_row) store_state(rd, Y, y + g.wrap, s2);
-        }
+        // a row stripe also advances the streams of the halo rows next to its core rows
+        // (the peer-memory halo exchange pulls neighbour states only once, p2p.cu)
+        const bool halo_state = g.wrap == 0 && (v + 1 == g.c0 || v == g.c1);
+        if (core || halo_state) store_state(rd, Y, y, s2);
+        if (core && ghost_row) store_state(rd, Y, y + g.wrap, s2);
     }
 }
 

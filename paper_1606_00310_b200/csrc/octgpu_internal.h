@@ -128,6 +128,25 @@ cudaError_t launch_rows_scatter(int w, void* planes, uint64_t* rng, Geom g, uint
 // one plane-row (word k = 0..n-1 of row r) <-> contiguous n words
 cudaError_t launch_planerow_copy(int w, void* planes, int plane, Geom g, uint32_t r, void* buf, bool to_buf,
                                  cudaStream_t st);
+// Device-side halo exchange over peer memory (p2p.cu). A neighbour stripe as
+// this device sees it: its current plane / rng set (pass parity), allocated
+// rows, core rows and its "passes done" counter.
+struct PeerView {
+    const void* planes;
+    const uint64_t* rng;
+    const uint64_t* done;
+    uint32_t Y;  // allocated rows (row stride)
+    uint32_t L;  // core rows
+};
+constexpr long long kP2PTimeoutCycles = 20'000'000'000ll;  // ~10 s at 2 GHz: a dead neighbour is an error, not a hang
+// wait for prev.done >= need && next.done >= need, then copy the neighbours' boundary core rows (+ states)
+// into the local halo rows (kStripeHA above, kStripeHB below)
+cudaError_t launch_halo_pull(int w, void* planes, uint64_t* rng, Geom g, const PeerView& prev, const PeerView& next,
+                             uint64_t need, uint32_t* err, bool with_rng, cudaStream_t st);
+// copy plane-row (plane, local row kStripeHA + L) into the next stripe's row kStripeHA, then publish *done = value
+cudaError_t launch_push_signal(int w, const void* planes, int plane, Geom g, void* next_planes, uint32_t next_Y,
+                               uint64_t* done, uint64_t value, cudaStream_t st);
+
 // Heights (reference HeightMap layout, row-major int32), after launch_measure.
 cudaError_t launch_heights(int w, const void* planes, Geom g, uint32_t X, const void* scratch, int32_t* out,
                            cudaStream_t st);

@@ -21,7 +21,14 @@ prefix of the stripes above and summed (``combine``).
 Transports: ``LocalTransport`` (all stripes in this process, e.g. several
 stripes on one GPU — used to prove bit-exactness on one device) and
 ``DistTransport`` (one stripe per rank over torch.distributed: NCCL on GPUs,
-gloo on CPU for the protocol tests).
+gloo on CPU for the protocol tests) run steps 1-5 from the host.
+``PeerLocalTransport`` / ``PeerDistTransport`` replace them with the
+device-side exchange over peer memory (csrc/p2p.cu): each pass is one halo
+pull kernel that reads the neighbours' rows over NVLink (waiting on their
+"passes done" counters), the MCS kernel, and one kernel that writes the
+boundary plane-row into the next stripe and publishes the pass — no NCCL, no
+host synchronisation between passes. Peers are mapped with CUDA IPC across
+processes.
 """
 from __future__ import annotations
 
@@ -32,7 +39,7 @@ from math import comb
 
 import numpy as np
 
-from ._lib import ConfigError, InvariantError, OctStripeMoments, check, lib
+from ._lib import IPC_BYTES, ConfigError, InvariantError, OctPeer, OctStripeMoments, check, lib
 from .engine import MeasurementRecord, _i128, _word_dtype
 from .params import LatticeConfig, UpdateParams
 
@@ -174,6 +181,35 @@ class StripeEngine:
     def finish(self, boundary_in) -> None:
         check(lib().octgpu_stripe_finish(self._h, self._p(boundary_in)))
 
+    # ---- device-side exchange over peer memory ----
+    def peer(self) -> OctPeer:
+        out = OctPeer()
+        check(lib().octgpu_stripe_peer(self._h, C.byref(out)))
+        return out
+
+    def ipc_export(self) -> bytes:
+        buf = C.create_string_buffer(IPC_BYTES)
+        check(lib().octgpu_stripe_ipc_export(self._h, buf))
+        return buf.raw
+
+    def ipc_open(self, blob: bytes) -> OctPeer:
+        out = OctPeer()
+        check(lib().octgpu_stripe_ipc_open(self._h, C.create_string_buffer(blob, IPC_BYTES), C.byref(out)))
+        return out
+
+    def connect(self, prev: OctPeer, nxt: OctPeer) -> None:
+        check(lib().octgpu_stripe_connect(self._h, C.byref(prev), C.byref(nxt)))
+
+    def pass_(self, prm: UpdateParams, n: int = 1) -> None:
+        c = prm.to_c()
+        check(lib().octgpu_stripe_pass(self._h, C.byref(c), n))
+
+    def pull(self) -> None:
+        check(lib().octgpu_stripe_pull(self._h))
+
+    def disconnect(self) -> None:
+        check(lib().octgpu_stripe_disconnect(self._h))
+
     def measure_local(self) -> StripeMoments:
         m = OctStripeMoments()
         check(lib().octgpu_measure_stripe(self._h, C.byref(m)))
@@ -190,13 +226,20 @@ class StripeEngine:
     def launches(self) -> int:
         return int(lib().octgpu_launch_count(self._h))
 
-    def planes(self) -> np.ndarray:
-        out = np.zeros((4, self.y1 - self.y0, self.cfg.words_per_row()), _word_dtype(self.cfg.w))
+    def planes(self, out: np.ndarray | None = None) -> np.ndarray:
+        shape, dt = (4, self.y1 - self.y0, self.cfg.words_per_row()), _word_dtype(self.cfg.w)
+        if out is None:
+            out = np.zeros(shape, dt)
+        elif out.shape != shape or out.dtype != dt or not out.flags.c_contiguous:
+            raise ConfigError(f"planes buffer must be a C-contiguous {dt.__name__} array of shape {shape}")
         check(lib().octgpu_get_planes(self._h, out.ctypes.data_as(C.c_void_p)))
         return out
 
-    def states(self) -> np.ndarray:
-        out = np.zeros((self.y1 - self.y0, 4), np.uint64)
+    def states(self, out: np.ndarray | None = None) -> np.ndarray:
+        if out is None:
+            out = np.zeros((self.y1 - self.y0, 4), np.uint64)
+        elif out.shape != (self.y1 - self.y0, 4) or out.dtype != np.uint64 or not out.flags.c_contiguous:
+            raise ConfigError(f"states buffer must be a C-contiguous uint64 array of shape ({self.y1 - self.y0}, 4)")
         check(lib().octgpu_get_states(self._h, out.ctypes.data_as(C.c_void_p)))
         return out
 
@@ -293,6 +336,58 @@ class DistTransport:
         return [StripeMoments.from_array(o.cpu().numpy()) for o in out]
 
 
+class PeerLocalTransport:
+    """All stripes in this process, exchanging halos device-side over peer memory."""
+
+    peer = True
+
+    def __init__(self, engines: list):
+        self.engines = engines
+        peers = [e.peer() for e in engines]
+        n = len(engines)
+        for r, e in enumerate(engines):
+            e.connect(peers[(r - 1) % n], peers[(r + 1) % n])
+
+    def gather(self, parts: list[StripeMoments]) -> list[StripeMoments]:
+        return parts
+
+
+class PeerDistTransport:
+    """One stripe per rank; the ring neighbours' device memory is mapped with CUDA
+    IPC (handles exchanged once over torch.distributed), then every pass runs
+    device-side (csrc/p2p.cu). torch.distributed only gathers the moments."""
+
+    peer = True
+
+    def __init__(self, engine, device=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.engines = [engine]
+        self.rank, self.size = dist.get_rank(), dist.get_world_size()
+        self.device = device
+        blobs = [None] * self.size
+        dist.all_gather_object(blobs, engine.ipc_export())
+        prev, nxt = (self.rank - 1) % self.size, (self.rank + 1) % self.size
+        if self.size == 1:
+            p = q = engine.peer()
+        else:
+            p = engine.ipc_open(blobs[prev])
+            q = p if nxt == prev else engine.ipc_open(blobs[nxt])
+        engine.connect(p, q)
+        dist.barrier()
+
+    def close(self) -> None:
+        """Unmap the neighbours on every rank before any rank frees its stripe."""
+        self.engines[0].disconnect()
+        self.dist.barrier()
+
+    def gather(self, parts: list[StripeMoments]) -> list[StripeMoments]:
+        out = [None] * self.size
+        self.dist.all_gather_object(out, parts[0].to_array().tolist())
+        return [StripeMoments.from_array(np.array(o, np.int64)) for o in out]
+
+
 class StripeGroup:
     """Drives stripe engines through the per-MCS protocol above."""
 
@@ -301,16 +396,26 @@ class StripeGroup:
 
     def step(self, prm: UpdateParams, n: int = 1) -> None:
         kmax = self.tr.engines[0].max_mcs(prm)  # the same on every rank (depends on params and X only)
+        peer = getattr(self.tr, "peer", False)
         while n > 0:
             k = min(n, kmax)
-            self.tr.halos()
-            for e, b in zip(self.tr.engines, self.tr.bufs):
-                e.mcs(prm, b.bo, k)
-            self.tr.boundary()
+            if peer:
+                for e in self.tr.engines:
+                    e.pass_(prm, k)
+            else:
+                self.tr.halos()
+                for e, b in zip(self.tr.engines, self.tr.bufs):
+                    e.mcs(prm, b.bo, k)
+                self.tr.boundary()
             n -= k
 
     def measure(self) -> MeasurementRecord:
-        self.tr.halos()  # the curl check of each stripe's first row reads the row above
+        # the curl check of each stripe's first row reads the row above
+        if getattr(self.tr, "peer", False):
+            for e in self.tr.engines:
+                e.pull()
+        else:
+            self.tr.halos()
         parts = self.tr.gather([e.measure_local() for e in self.tr.engines])
         return combine(parts, self.X, self.Y)
 

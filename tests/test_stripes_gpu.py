@@ -7,18 +7,20 @@ import pytest
 import torch
 
 import paper_1606_00310_b200 as octgpu
-from paper_1606_00310_b200.stripes import LocalTransport, StripeEngine, StripeGroup, stripe_bounds
+from paper_1606_00310_b200.stripes import LocalTransport, PeerLocalTransport, StripeEngine, StripeGroup, stripe_bounds
 
 pytestmark = pytest.mark.gpu
 
 
-def _group(cfg, parts, seed, stream):
+def _group(cfg, parts, seed, stream, transport="host"):
     engines = []
     for r in range(parts):
         y0, y1 = stripe_bounds(cfg.Y, parts, r)
         e = StripeEngine(cfg, y0, y1, seed)
         e.set_stream(stream.cuda_stream)
         engines.append(e)
+    if transport == "peer":
+        return StripeGroup(PeerLocalTransport(engines), cfg.X, cfg.Y), engines
     alloc = lambda nb: torch.zeros(nb, dtype=torch.uint8, device="cuda")  # noqa: E731
     return StripeGroup(LocalTransport(engines, alloc), cfg.X, cfg.Y), engines
 
@@ -27,12 +29,15 @@ def _group(cfg, parts, seed, stream):
 @pytest.mark.parametrize("X,Y,parts", [(1024, 128, 2), (1024, 130, 4), (2048, 96, 3), (256, 40, 2), (8192, 512, 8),
                                        (1024, 32, 8)])
 @pytest.mark.parametrize("pq", [(0.5, 0.0), (0.98, 0.02), (1.0, 0.0), (0.75, 0.5), (0.0, 0.0)])
-def test_stripes_match_single_engine(X, Y, parts, pq):
+@pytest.mark.parametrize("transport", ["host", "peer"])
+def test_stripes_match_single_engine(X, Y, parts, pq, transport):
+    if transport == "peer" and X < 1024:
+        pytest.skip("the peer-memory exchange runs the TMA kernels (X >= 1024)")
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         cfg = octgpu.LatticeConfig(X, Y)
         prm = octgpu.UpdateParams.make(*pq)
-        grp, engines = _group(cfg, parts, 21, stream)
+        grp, engines = _group(cfg, parts, 21, stream, transport)
         grp.step(prm, 7)
         ref = octgpu.GpuEngine(cfg, 21)
         ref.step(prm, 7)

@@ -264,6 +264,20 @@ __device__ __forceinline__ void gen_xi_pair(Xo& a, Xo& b, const ProbDev& p, cons
     }
 }
 
+// x+ neighbour alignment and its inverse as branch-free funnel shifts, with
+// s = 1 on rows whose sites sit at odd packed positions (engine_vec.hpp:34-88):
+//   rot_sel(x0, x1, s)     = s ? (x0 >> 1) | (x1 << 63) : x0     (gather_xplus, word k and k+1)
+//   carry_sel(m, mp, s)    = s ? (m << 1) | (mp >> 63) : m       (scatter_xplus, word k and k-1)
+// Two SHF.R.W / SHF.L.W per 64-bit result instead of shift + shift + or + 2 selects.
+__device__ __forceinline__ uint64_t rot_sel(uint64_t x0, uint64_t x1, uint32_t s) {
+    const uint32_t l0 = uint32_t(x0), h0 = uint32_t(x0 >> 32), l1 = uint32_t(x1);
+    return (uint64_t(__funnelshift_r(h0, l1, s)) << 32) | __funnelshift_r(l0, h0, s);
+}
+__device__ __forceinline__ uint64_t carry_sel(uint64_t m, uint64_t mp, uint32_t s) {
+    const uint32_t l = uint32_t(m), h = uint32_t(m >> 32), hp = uint32_t(mp >> 32);
+    return (uint64_t(__funnelshift_l(l, h, s)) << 32) | __funnelshift_l(hp, l, s);
+}
+
 // engine_vec.hpp:25-30
 template <typename Word>
 __device__ __forceinline__ Word update_mask(Word sxm, Word sym, Word sxp, Word syp, Word xp, Word xq) {

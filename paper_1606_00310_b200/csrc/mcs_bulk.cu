@@ -19,6 +19,7 @@
 #include <cuda.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "device_common.cuh"
 #include "octgpu_internal.h"
@@ -182,8 +183,8 @@ __global__ void __launch_bounds__(32 * (kP + 1), 4) k_mcs_bulk(const uint64_t* _
     Word* dYf = dst + size_t(2 + f) * PS + y;
     Word* dXs = dst + size_t(0 + s) * PS + y;
     Word* dYs = dst + size_t(2 + s) * PS + y;
-    const bool sh1 = ((uint32_t(f) ^ y ^ g.ypar) & 1u) != 0;
-    const bool sh2 = !sh1;
+    const uint32_t sf1 = (uint32_t(f) ^ y ^ g.ypar) & 1u;  // first sweep: x+ neighbour shifted by one bit
+    const uint32_t sf2 = sf1 ^ 1u;
 
     // Periodic lattices keep ghost rows wrap..wrap+ghost-1 equal to rows
     // 0..ghost-1, so a block window never wraps; warps that store rows
@@ -191,37 +192,45 @@ __global__ void __launch_bounds__(32 * (kP + 1), 4) k_mcs_bulk(const uint64_t* _
     const bool ghostw = g.ghost && (r0 + 1 < g.ghost || r0 + 31 >= g.wrap);  // warp-uniform
     const bool ghost_row = ghostw && y < g.ghost;
 
-    Xo s1{0, 0, 0, 0}, s2{0, 0, 0, 0};
+    Xo st1{0, 0, 0, 0}, st2{0, 0, 0, 0};  // first / second sweep streams
     if constexpr (LIVE) {
-        s1 = load_state(rs, Y, y);
-        s2 = apply_table(jtab, s1);
+        st1 = load_state(rs, Y, y);
+        st2 = apply_table(jtab, st1);
     }
     Word xi2p0, xi2q0;
-    gen_xi<PM, QM, Word>(s2, p, q, xi2p0, xi2q0);
+    gen_xi<PM, QM, Word>(st2, p, q, xi2p0, xi2q0);
 
     Word A0 = 0, B0 = 0, C0 = 0, R0 = 0, A1 = 0;
     Word pA = 0, pB = 0, pC = 0, pR = 0;
-    Word carry1 = 0, m2last = 0, xf1 = 0;
+    Word m1last = 0, m2last = 0, xf1 = 0;
     Word cur = 0, raw0 = 0;
 
-    // predicated store, mirrored into the ghost row when this is one of rows 0..33
+    // predicated store, mirrored into the ghost row when this is one of rows 0..ghost-1;
+    // gh = integral_constant: 0 / 1 = warp-uniform ghostw hoisted out of the loop, 2 = checked here
+    auto putg = [&](auto gh, Word* ptr, Word val, bool pred) {
+        st_pred(ptr, val, pred);
+        if constexpr (decltype(gh)::value == 1) st_pred(ptr + g.wrap, val, pred && ghost_row);
+        if constexpr (decltype(gh)::value == 2)
+            if (ghostw) st_pred(ptr + g.wrap, val, pred && ghost_row);
+    };
     auto put = [&](Word* ptr, Word val, bool pred) {
         st_pred(ptr, val, pred);
         if (ghostw) st_pred(ptr + g.wrap, val, pred && ghost_row);
     };
 
-    auto second = [&](uint32_t j, Word Aj, Word Ajn, Word Bj, Word Cj, Word Rj, Word x2p, Word x2q) {
+    auto second = [&](auto gh, uint32_t j, Word Aj, Word Ajn, Word Bj, Word Cj, Word Rj, Word x2p, Word x2q) {
         const Word Cup = __shfl_up_sync(0xffffffffu, Cj, 1);
         const Word Bdn = __shfl_down_sync(0xffffffffu, Bj, 1);
-        const Word sxp2 = sh2 ? Word((Aj >> 1) | (Ajn << (W - 1))) : Aj;
+        const Word sxp2 = rot_sel(Aj, Ajn, sf2);
         const Word m2 = update_mask<Word>(Rj, Cup, sxp2, Bdn, x2p, x2q);
         const Word mup = __shfl_up_sync(0xffffffffu, m2, 1);
         const uint32_t o = j * Y;  // < 2^32: n * Y words per plane
-        put(dXs + o, Rj ^ m2, core);
-        put(dYs + o, Cup ^ m2, core);
-        put(dYf + o, Bj ^ mup, wyf);
+        putg(gh, dXs + o, Rj ^ m2, core);
+        putg(gh, dYs + o, Cup ^ m2, core);
+        putg(gh, dYf + o, Bj ^ mup, wyf);
         return m2;
     };
+    const std::integral_constant<int, 2> GHOST{};
 
     uint32_t st = 0, ph = 0;  // ring stage and the parity of its current fill
     for (uint32_t b = 0; b < nblocks; ++b) {
@@ -236,26 +245,34 @@ __global__ void __launch_bounds__(32 * (kP + 1), 4) k_mcs_bulk(const uint64_t* _
         constexpr int kUnroll = (PM == M_ARB || QM == M_ARB) ? 1 : KS;
         if (kb >= 3 && kb + KS <= n) {
             // steady state: words k >= 3, second sweep of word k-1 >= 2, no special cases
+            auto steady = [&](auto gh) {
 #pragma unroll kUnroll
-            for (int jj = 0; jj < KS; ++jj) {
-                const uint32_t k = kb + jj;
-                const Word A = sb[LY::kXf + jj * kWin + wrow];
-                const Word B = sb[LY::kYf + jj * kWin + wrow];
-                const Word Cn = sb[LY::kYs + jj * kWin + wrow + 1];
-                const Word nxt = (k + 1 == n) ? raw0 : sb[LY::kXs + (jj + 1) * kWin + wrow];
-                Word x1p, x1q, x2p, x2q;
-                gen_xi_pair<PM, QM, Word>(s1, s2, p, q, x1p, x1q, x2p, x2q);
-                const Word sxp = sh1 ? Word((cur >> 1) | (nxt << (W - 1))) : cur;
-                const Word m1 = update_mask<Word>(A, B, sxp, Cn, x1p, x1q);
-                const Word Ap = A ^ m1, Bp = B ^ m1, Cp = Cn ^ m1;
-                const Word sc1 = sh1 ? Word((m1 << 1) | carry1) : m1;
-                carry1 = Word(m1 >> (W - 1));
-                const Word Rp = cur ^ sc1;
-                cur = nxt;
-                const Word m2 = second(k - 1, pA, Ap, pB, pC, pR, x2p, x2q);
-                put(dXf + (k - 1) * Y, pA ^ (sh2 ? Word((m2 << 1) | (m2last >> (W - 1))) : m2), core);
-                m2last = m2;
-                pA = Ap; pB = Bp; pC = Cp; pR = Rp;
+                for (int jj = 0; jj < KS; ++jj) {
+                    const uint32_t k = kb + jj;
+                    const Word A = sb[LY::kXf + jj * kWin + wrow];
+                    const Word B = sb[LY::kYf + jj * kWin + wrow];
+                    const Word Cn = sb[LY::kYs + jj * kWin + wrow + 1];
+                    const Word nxt = (k + 1 == n) ? raw0 : sb[LY::kXs + (jj + 1) * kWin + wrow];
+                    Word x1p, x1q, x2p, x2q;
+                    gen_xi_pair<PM, QM, Word>(st1, st2, p, q, x1p, x1q, x2p, x2q);
+                    const Word sxp = rot_sel(cur, nxt, sf1);
+                    const Word m1 = update_mask<Word>(A, B, sxp, Cn, x1p, x1q);
+                    const Word Ap = A ^ m1, Bp = B ^ m1, Cp = Cn ^ m1;
+                    const Word Rp = cur ^ carry_sel(m1, m1last, sf1);
+                    m1last = m1;
+                    cur = nxt;
+                    const Word m2 = second(gh, k - 1, pA, Ap, pB, pC, pR, x2p, x2q);
+                    putg(gh, dXf + (k - 1) * Y, pA ^ carry_sel(m2, m2last, sf2), core);
+                    m2last = m2;
+                    pA = Ap; pB = Bp; pC = Cp; pR = Rp;
+                }
+            };
+            if constexpr (kUnroll == 1) {  // arbitrary-p bodies: one copy (instruction cache)
+                steady(std::integral_constant<int, 2>{});
+            } else if (ghostw) {
+                steady(std::integral_constant<int, 1>{});
+            } else {
+                steady(std::integral_constant<int, 0>{});
             }
         } else {
 #pragma unroll kUnroll
@@ -269,16 +286,15 @@ __global__ void __launch_bounds__(32 * (kP + 1), 4) k_mcs_bulk(const uint64_t* _
                 // ---- xi for first sweep word k and (k >= 2) second sweep word k-1, interleaved ----
                 Word x1p, x1q, x2p = 0, x2q = 0;
                 if (k >= 2)
-                    gen_xi_pair<PM, QM, Word>(s1, s2, p, q, x1p, x1q, x2p, x2q);
+                    gen_xi_pair<PM, QM, Word>(st1, st2, p, q, x1p, x1q, x2p, x2q);
                 else
-                    gen_xi<PM, QM, Word>(s1, p, q, x1p, x1q);
+                    gen_xi<PM, QM, Word>(st1, p, q, x1p, x1q);
                 // ---- first sweep, word k ----
-                const Word sxp = sh1 ? Word((cur >> 1) | (nxt << (W - 1))) : cur;
+                const Word sxp = rot_sel(cur, nxt, sf1);
                 const Word m1 = update_mask<Word>(A, B, sxp, Cn, x1p, x1q);
                 const Word Ap = A ^ m1, Bp = B ^ m1, Cp = Cn ^ m1;
-                const Word sc1 = sh1 ? Word((m1 << 1) | carry1) : m1;
-                carry1 = Word(m1 >> (W - 1));
-                const Word Rp = cur ^ sc1;
+                const Word Rp = cur ^ carry_sel(m1, m1last, sf1);  // word 0: m1last = 0, carry of word n-1 added last
+                m1last = m1;
                 cur = nxt;
                 if (k == 0) {
                     A0 = Ap; B0 = Bp; C0 = Cp; R0 = Rp;
@@ -286,12 +302,11 @@ __global__ void __launch_bounds__(32 * (kP + 1), 4) k_mcs_bulk(const uint64_t* _
                     if (k == 1) A1 = Ap;
                     if (k >= 2) {
                         const uint32_t j = k - 1;
-                        const Word m2 = second(j, pA, Ap, pB, pC, pR, x2p, x2q);
-                        const Word xfj = pA ^ (sh2 ? Word(m2 << 1) : m2);
+                        const Word m2 = second(GHOST, j, pA, Ap, pB, pC, pR, x2p, x2q);
                         if (j == 1)
-                            xf1 = xfj;
+                            xf1 = pA ^ carry_sel(m2, 0, sf2);  // word 0's carry comes last
                         else
-                            put(dXf + j * Y, xfj ^ (sh2 ? Word(m2last >> (W - 1)) : Word(0)), core);
+                            put(dXf + j * Y, pA ^ carry_sel(m2, m2last, sf2), core);
                         m2last = m2;
                     }
                 }
@@ -305,28 +320,26 @@ __global__ void __launch_bounds__(32 * (kP + 1), 4) k_mcs_bulk(const uint64_t* _
             ph ^= 1u;
         }
     }
-    if (sh1) R0 ^= carry1;
+    R0 ^= carry_sel(0, m1last, sf1);  // periodic seam: carry of word n-1 into word 0
     {
         const uint32_t j = n - 1;  // n >= 8 here
         Word x2p, x2q;
-        gen_xi<PM, QM, Word>(s2, p, q, x2p, x2q);
-        const Word m2 = second(j, pA, A0, pB, pC, pR, x2p, x2q);
-        const Word xfj = pA ^ (sh2 ? Word(m2 << 1) : m2);
-        put(dXf + j * Y, xfj ^ (sh2 ? Word(m2last >> (W - 1)) : Word(0)), core);
+        gen_xi<PM, QM, Word>(st2, p, q, x2p, x2q);
+        const Word m2 = second(GHOST, j, pA, A0, pB, pC, pR, x2p, x2q);
+        put(dXf + j * Y, pA ^ carry_sel(m2, m2last, sf2), core);
         m2last = m2;
     }
     {
-        const Word m2 = second(0, A0, A1, B0, C0, R0, xi2p0, xi2q0);
-        const Word xf0 = A0 ^ (sh2 ? Word((m2 << 1) | (m2last >> (W - 1))) : m2);
-        put(dXf, xf0, core);
-        put(dXf + Y, xf1 ^ (sh2 ? Word(m2 >> (W - 1)) : Word(0)), core);
+        const Word m2 = second(GHOST, 0, A0, A1, B0, C0, R0, xi2p0, xi2q0);
+        put(dXf, A0 ^ carry_sel(m2, m2last, sf2), core);
+        put(dXf + Y, xf1 ^ carry_sel(0, m2, sf2), core);
     }
     if constexpr (LIVE) {
         // a row stripe also advances the streams of the halo rows next to its core rows
         // (the peer-memory halo exchange pulls neighbour states only once, p2p.cu)
         const bool halo_state = g.wrap == 0 && (v + 1 == g.c0 || v == g.c1);
-        if (core || halo_state) store_state(rd, Y, y, s2);
-        if (core && ghost_row) store_state(rd, Y, y + g.wrap, s2);
+        if (core || halo_state) store_state(rd, Y, y, st2);
+        if (core && ghost_row) store_state(rd, Y, y + g.wrap, st2);
     }
 }
 

@@ -39,6 +39,10 @@ namespace octgpu {
 
 namespace {
 
+#ifndef OCTGPU_DEEP_GHOST_HOIST
+#define OCTGPU_DEEP_GHOST_HOIST 0  // hoisting duplicates the steady state: +regs, spills, measured 4% slower
+#endif
+
 constexpr int kDP = kDeepWarps;  // compute warps per block (+1 producer)
 constexpr int kKS = 2;                  // words per ring stage
 constexpr int kSMax = 8;                // ring stages: runtime S <= kSMax (barrier slots)
@@ -132,7 +136,8 @@ struct DeepCtx {
     uint64_t* dXs;
     uint64_t* dYs;
     uint32_t wrap;
-    bool sh1, sh2, core, wyf, ghostw, ghost_row;
+    uint32_t sf1, sf2;  // x+ neighbour shifted by one packed bit in sweeps of parity f / s
+    bool core, wyf, ghostw, ghost_row;
     uint64_t* save;  // this lane's parking slots: save[slot * kLanes]
 };
 
@@ -144,14 +149,19 @@ struct DeepState {
     uint64_t cur, raw0;                   // sweep 1: original X(s)[y][j], X(s)[y][0]
 };
 
+// GH: the warp stores rows 0..ghost-1 of a periodic lattice and mirrors them into the ghost rows
+// (warp-uniform; 0 / 1 hoisted out of the steady state, 2 = decide at run time)
+template <int GH>
 __device__ __forceinline__ void put(const DeepCtx& c, uint64_t* ptr, uint64_t val, bool pred) {
     st_pred(ptr, val, pred);
-    if (c.ghostw) st_pred(ptr + c.wrap, val, pred && c.ghost_row);
+    if constexpr (GH == 1) st_pred(ptr + c.wrap, val, pred && c.ghost_row);
+    if constexpr (GH == 2)
+        if (c.ghostw) st_pred(ptr + c.wrap, val, pred && c.ghost_row);
 }
 
 // One iteration i: sweep l on word (i-(l-1)) mod n for every active l.
 // STEADY: all sweeps active, no first/second/last words, no wrap (i in [2L, n-1]).
-template <int PM, int QM, int L, bool STEADY>
+template <int PM, int QM, int L, bool STEADY, int GH>
 __device__ __forceinline__ void deep_iter(DeepState<L>& S, const DeepCtx& c, uint32_t i, const uint64_t* sb, int jj,
                                           const ProbDev& p, const ProbDev& q) {
     using ST = DeepStage<L>;
@@ -223,14 +233,14 @@ __device__ __forceinline__ void deep_iter(DeepState<L>& S, const DeepCtx& c, uin
             x0 = qA;
             x1 = nxa;
         }
-        const bool sh = (l & 1) ? c.sh1 : c.sh2;
-        const uint64_t rot = sh ? ((x0 >> 1) | (x1 << (W - 1))) : x0;
+        const uint32_t sh = (l & 1) ? c.sf1 : c.sf2;
+        const uint64_t rot = rot_sel(x0, x1, sh);
         const uint64_t m = update_mask<uint64_t>(xo, yo, rot, yn, xp, xq);
         const uint64_t mprev = first ? uint64_t(0) : S.ml[li];
         nA[li] = xo ^ m;
         nB[li] = yo ^ m;
         nC[li] = yn ^ m;
-        nR[li] = x0 ^ (sh ? ((m << 1) | (mprev >> (W - 1))) : m);
+        nR[li] = x0 ^ carry_sel(m, mprev, sh);
         S.ml[li] = m;
 
         if constexpr (!STEADY) {
@@ -247,22 +257,22 @@ __device__ __forceinline__ void deep_iter(DeepState<L>& S, const DeepCtx& c, uin
             }
             if (second && l < L) c.save[(sv + 4) * kLanes] = nA[li];
             if (last) {  // the x carry of the last word completes X(other) of the first word
-                const uint64_t carry = sh ? (m >> (W - 1)) : uint64_t(0);
+                const uint64_t carry = carry_sel(0, m, sh);
                 if (l < L) {
                     c.save[(sv + 3) * kLanes] ^= carry;
                 } else {
                     const uint64_t xf = c.save[sv * kLanes] ^ carry;
-                    put(c, ((L & 1) ? c.dXs : c.dXf) + size_t(l - 1) * c.Y, xf, c.core);
+                    put<GH>(c, ((L & 1) ? c.dXs : c.dXf) + size_t(l - 1) * c.Y, xf, c.core);
                 }
             }
         }
         if (l == L) {
             // sweep L has parity s (L even): X(s), Y(s) own; Y(f)[y] = B^{L-1}[y] ^ m^L[y-1]; X(f) via the carry
             const uint32_t o = j * c.Y;
-            put(c, c.dXs + o, nA[li], c.core);
-            put(c, c.dYs + o, nB[li], c.core);
-            put(c, c.dYf + o, qB ^ shup(m), c.wyf);
-            if (!first) put(c, c.dXf + o, nR[li], c.core);
+            put<GH>(c, c.dXs + o, nA[li], c.core);
+            put<GH>(c, c.dYs + o, nB[li], c.core);
+            put<GH>(c, c.dYf + o, qB ^ shup(m), c.wyf);
+            if (!first) put<GH>(c, c.dXf + o, nR[li], c.core);
         }
     }
 #pragma unroll
@@ -349,8 +359,8 @@ __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
     c.dYf = dst + size_t(2 + f) * PS + y;
     c.dXs = dst + size_t(0 + s) * PS + y;
     c.dYs = dst + size_t(2 + s) * PS + y;
-    c.sh1 = ((uint32_t(f) ^ y ^ g.ypar) & 1u) != 0;
-    c.sh2 = !c.sh1;
+    c.sf1 = (uint32_t(f) ^ y ^ g.ypar) & 1u;
+    c.sf2 = c.sf1 ^ 1u;
     c.core = lane >= L - 1 && lane <= 32 - L && v < g.c1;
     c.wyf = lane >= L && lane <= 33 - L && v - 1 < g.c1;
     c.ghostw = g.ghost && (r0 + uint32_t(L - 1) < g.ghost || r0 + uint32_t(33 - L) >= g.wrap);
@@ -391,13 +401,23 @@ __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
             R.raw0 = R.cur;
         }
         if (kb >= uint32_t(2 * L) && kb + kKS < n) {  // i = n-1 is sweep 1's last word: generic
+#if OCTGPU_DEEP_GHOST_HOIST
+            if (c.ghostw) {
 #pragma unroll
-            for (int jj = 0; jj < kKS; ++jj) deep_iter<PM, QM, L, true>(R, c, kb + jj, sb, jj, p, q);
+                for (int jj = 0; jj < kKS; ++jj) deep_iter<PM, QM, L, true, 1>(R, c, kb + jj, sb, jj, p, q);
+            } else {
+#pragma unroll
+                for (int jj = 0; jj < kKS; ++jj) deep_iter<PM, QM, L, true, 0>(R, c, kb + jj, sb, jj, p, q);
+            }
+#else
+#pragma unroll
+            for (int jj = 0; jj < kKS; ++jj) deep_iter<PM, QM, L, true, 2>(R, c, kb + jj, sb, jj, p, q);
+#endif
         } else {
 #pragma unroll 1
             for (int jj = 0; jj < kKS; ++jj) {
                 if (kb + jj >= n) break;
-                deep_iter<PM, QM, L, false>(R, c, kb + jj, sb, jj, p, q);
+                deep_iter<PM, QM, L, false, 2>(R, c, kb + jj, sb, jj, p, q);
             }
         }
         __syncwarp();
@@ -409,7 +429,7 @@ __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
     }
     // drain: sweeps 2..L finish their wrapped words
 #pragma unroll 1
-    for (uint32_t i = n; i < n + uint32_t(2 * L - 2); ++i) deep_iter<PM, QM, L, false>(R, c, i, nullptr, 0, p, q);
+    for (uint32_t i = n; i < n + uint32_t(2 * L - 2); ++i) deep_iter<PM, QM, L, false, 2>(R, c, i, nullptr, 0, p, q);
 
     if constexpr (LIVE) {
         if (c.core) {

@@ -343,6 +343,8 @@ def main():
         hp = host_planes.numpy().view(np.uint64)
         hs = host_states.numpy().view(np.uint64)
         job, engs = make(hp, hs)
+        engs[0].sync()
+        t_create = time.perf_counter() - t0
         t = 0
         n_meas = 0
         for target in targets:
@@ -352,6 +354,8 @@ def main():
             if target in sched:
                 job.measure()
                 n_meas += 1
+        engs[0].sync()
+        t_run = time.perf_counter() - t0 - t_create
         out_planes = engs[0].planes(out=pin_planes)
         out_states = (engs[0].states(out=pin_states) if ws > 1 else engs[0].streams(out=pin_states).states)
         el = time.perf_counter() - t0
@@ -365,7 +369,7 @@ def main():
                "h2d_bytes_per_step": ws * (hp.nbytes + hs.nbytes) / K,
                "d2h_bytes_per_step": (ws * (out_planes.nbytes + out_states.nbytes)
                                       + n_meas * C.sizeof(octgpu._lib.OctMoments)) / K,
-               "wall_s": el,
+               "wall_s": el, "create_s": t_create, "run_s": t_run, "d2h_s": el - t_create - t_run,
                "note": "engine(s) created from pinned host planes+states (each rank its stripe), K MCS + "
                        "measurements, planes/states D2H into pinned buffers; max over ranks"}
 

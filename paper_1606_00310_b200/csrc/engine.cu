@@ -376,8 +376,18 @@ int use_device(octgpu_engine* e) {
     return OCTGPU_OK;
 }
 
-int ensure_stage(octgpu_engine* e) {
+// Reference-layout staging buffer for import / export transposes. A periodic
+// engine uses its idle ping-pong plane set (the next MCS rewrites every row of
+// it), saving a 1-GiB allocation at 2^16^2; a stripe keeps its own buffer,
+// since a neighbour may push its boundary row into the idle set at any time
+// (p2p.cu).
+int ensure_stage(octgpu_engine* e, void** out) {
+    if (!e->stripe) {
+        *out = e->planes[e->pcur ^ 1];
+        return OCTGPU_OK;
+    }
     if (!e->stage) CK(cudaMalloc(&e->stage, e->set_bytes()));
+    *out = e->stage;
     return OCTGPU_OK;
 }
 
@@ -647,20 +657,21 @@ int make_engine(uint32_t X, uint32_t Ytot, uint32_t w, bool stripe, uint32_t y0,
 
 // Upload core-row planes given in the reference layout ([4][core rows][n]).
 int load_planes(octgpu_engine* e, const void* planes) {
-    int rc = ensure_stage(e);
+    void* stage = nullptr;
+    int rc = ensure_stage(e, &stage);
     if (rc) return rc;
     const size_t wb = e->word_bytes(), row_bytes = size_t(e->n) * wb;
     if (!e->stripe) {
-        CK(cudaMemcpyAsync(e->stage, planes, e->host_bytes(), cudaMemcpyHostToDevice, e->stream));
+        CK(cudaMemcpyAsync(stage, planes, e->host_bytes(), cudaMemcpyHostToDevice, e->stream));
     } else {
         std::vector<unsigned char> pad(e->host_bytes(), 0);
         for (int p = 0; p < 4; ++p)
             std::memcpy(pad.data() + (size_t(p) * e->Y + kStripeHA) * row_bytes,
                         static_cast<const unsigned char*>(planes) + size_t(p) * e->L * row_bytes, e->L * row_bytes);
-        CK(cudaMemcpyAsync(e->stage, pad.data(), e->host_bytes(), cudaMemcpyHostToDevice, e->stream));
+        CK(cudaMemcpyAsync(stage, pad.data(), e->host_bytes(), cudaMemcpyHostToDevice, e->stream));
         CK(cudaStreamSynchronize(e->stream));
     }
-    CK(launch_import(e->w, e->stage, e->planes[e->pcur], e->geom(), e->host_rows(), e->stream));
+    CK(launch_import(e->w, stage, e->planes[e->pcur], e->geom(), e->host_rows(), e->stream));
     ++e->launches;
     rc = refresh_ghosts(e);
     if (rc) return rc;
@@ -939,17 +950,18 @@ uint64_t octgpu_launch_count(const octgpu_engine* e) { return e ? e->launches : 
 int octgpu_get_planes(octgpu_engine* e, void* out) {
     if (!e || !out) return fail(OCTGPU_ERR_CONFIG, "null argument");
     int rc = use_device(e);
-    if (!rc) rc = ensure_stage(e);
+    void* stage = nullptr;
+    if (!rc) rc = ensure_stage(e, &stage);
     if (rc) return rc;
-    CK(launch_export(e->w, e->planes[e->pcur], e->stage, e->geom(), e->host_rows(), e->stream));
+    CK(launch_export(e->w, e->planes[e->pcur], stage, e->geom(), e->host_rows(), e->stream));
     ++e->launches;
     if (!e->stripe) {
-        CK(cudaMemcpyAsync(out, e->stage, e->host_bytes(), cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaMemcpyAsync(out, stage, e->host_bytes(), cudaMemcpyDeviceToHost, e->stream));
         CK(cudaStreamSynchronize(e->stream));
         return OCTGPU_OK;
     }
     std::vector<unsigned char> pad(e->host_bytes());
-    CK(cudaMemcpyAsync(pad.data(), e->stage, e->host_bytes(), cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaMemcpyAsync(pad.data(), stage, e->host_bytes(), cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
     const size_t row_bytes = size_t(e->n) * e->word_bytes();
     for (int p = 0; p < 4; ++p)

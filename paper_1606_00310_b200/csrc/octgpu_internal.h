@@ -50,7 +50,10 @@ constexpr uint32_t kTmaBoxRows = 30 * kMcsConsumerWarps + 4;  // k_mcs_bulk wind
 #ifndef OCTGPU_DEEP_WARPS
 #define OCTGPU_DEEP_WARPS 9
 #endif
-constexpr int kDeepSweeps = 4;
+#ifndef OCTGPU_DEEP_SWEEPS
+#define OCTGPU_DEEP_SWEEPS 4
+#endif
+constexpr int kDeepSweeps = OCTGPU_DEEP_SWEEPS;  // sweeps per k_mcs_deep pass (even)
 constexpr int kDeepWarps = OCTGPU_DEEP_WARPS;
 constexpr int kDeepMinBlocks = kDeepWarps >= 8 ? 2 : 3;  // resident blocks per SM the register budget targets
 constexpr int deep_box_rows(int L) { return ((34 - 2 * L) * (kDeepWarps - 1) + 34) / 2 * 2; }

@@ -230,3 +230,19 @@ def test_stripe_sweep_equals_full_sweep(oracle):
         res[2 + (ph ^ 1), y1 % Y] = ghost
     assert np.array_equal(res, L.planes)
     assert np.array_equal(np.concatenate([o[4] for o in outs]), L.states)
+
+
+@pytest.mark.parametrize("r", [0.5, 0.75, 0.95])
+def test_xi_bit_frequencies_4sigma(oracle, r):
+    """SPEC.md acceptance 8: bit frequencies of the xi words at 4 sigma over 10^6 words
+    (the oracle's xi words are pinned to the reference's by test_xi_words)."""
+    import numpy as np
+
+    nwords = 10 ** 6
+    st = oracle.stream_set(2024, 1)[0].copy()
+    words = oracle.xi_words(st, oracle.resolve(r), 64, nwords)
+    bits = np.unpackbits(words.view(np.uint8), bitorder="little").reshape(nwords, 64)
+    per_pos = bits.mean(axis=0)
+    sig_pos = (r * (1 - r) / nwords) ** 0.5
+    assert np.all(np.abs(per_pos - r) <= 4 * sig_pos), per_pos
+    assert abs(bits.mean() - r) <= 4 * sig_pos / 8

@@ -154,9 +154,9 @@ class GpuEngine:
 
     name = "gpu"
 
-    def __del__(self):
+    def __del__(self, _lib=lib):  # the module global may already be gone at interpreter shutdown
         if getattr(self, "_h", None):
-            lib().octgpu_destroy(self._h)
+            _lib().octgpu_destroy(self._h)
             self._h = None
 
     def close(self) -> None:

@@ -148,9 +148,9 @@ class StripeEngine:
         check(lib().octgpu_stripe_sizes(h, C.byref(a), C.byref(b), C.byref(c)))
         self.to_prev_bytes, self.to_next_bytes, self.boundary_bytes = a.value, b.value, c.value
 
-    def __del__(self):
+    def __del__(self, _lib=lib):  # the module global may already be gone at interpreter shutdown
         if getattr(self, "_h", None):
-            lib().octgpu_destroy(self._h)
+            _lib().octgpu_destroy(self._h)
             self._h = None
 
     @staticmethod

@@ -14,12 +14,17 @@ pytestmark = pytest.mark.gpu
 
 def _group(cfg, parts, seed, stream, transport="host"):
     engines = []
+    streams = []
     for r in range(parts):
         y0, y1 = stripe_bounds(cfg.Y, parts, r)
         e = StripeEngine(cfg, y0, y1, seed)
-        e.set_stream(stream.cuda_stream)
+        if transport == "peer-streams":  # one stream per stripe: passes run concurrently, ordered by the counters
+            streams.append(torch.cuda.Stream())
+            e.set_stream(streams[-1].cuda_stream)
+        else:
+            e.set_stream(stream.cuda_stream)
         engines.append(e)
-    if transport == "peer":
+    if transport.startswith("peer"):
         return StripeGroup(PeerLocalTransport(engines), cfg.X, cfg.Y), engines
     alloc = lambda nb: torch.zeros(nb, dtype=torch.uint8, device="cuda")  # noqa: E731
     return StripeGroup(LocalTransport(engines, alloc), cfg.X, cfg.Y), engines
@@ -29,9 +34,9 @@ def _group(cfg, parts, seed, stream, transport="host"):
 @pytest.mark.parametrize("X,Y,parts", [(1024, 128, 2), (1024, 130, 4), (2048, 96, 3), (256, 40, 2), (8192, 512, 8),
                                        (1024, 32, 8)])
 @pytest.mark.parametrize("pq", [(0.5, 0.0), (0.98, 0.02), (1.0, 0.0), (0.75, 0.5), (0.0, 0.0)])
-@pytest.mark.parametrize("transport", ["host", "peer"])
+@pytest.mark.parametrize("transport", ["host", "peer", "peer-streams"])
 def test_stripes_match_single_engine(X, Y, parts, pq, transport):
-    if transport == "peer" and X < 1024:
+    if transport.startswith("peer") and X < 1024:
         pytest.skip("the peer-memory exchange runs the TMA kernels (X >= 1024)")
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
@@ -39,6 +44,8 @@ def test_stripes_match_single_engine(X, Y, parts, pq, transport):
         prm = octgpu.UpdateParams.make(*pq)
         grp, engines = _group(cfg, parts, 21, stream, transport)
         grp.step(prm, 7)
+        for e in engines:
+            e.sync()  # the per-stripe streams, and a timed-out peer wait would raise here
         ref = octgpu.GpuEngine(cfg, 21)
         ref.step(prm, 7)
         torch.cuda.synchronize()

@@ -144,7 +144,7 @@ struct DeepCtx {
 template <int L>
 struct DeepState {
     uint64_t pA[L], pB[L], pC[L], pR[L];  // each sweep's outputs at its previous word
-    uint64_t ml[L];                       // each sweep's mask at its previous word (x carry)
+    uint32_t ml[L];                       // high word of each sweep's mask at its previous word (x carry)
     Xo rs[L];                             // stream of each sweep
     uint64_t cur, raw0;                   // sweep 1: original X(s)[y][j], X(s)[y][0]
 };
@@ -236,12 +236,12 @@ __device__ __forceinline__ void deep_iter(DeepState<L>& S, const DeepCtx& c, uin
         const uint32_t sh = (l & 1) ? c.sf1 : c.sf2;
         const uint64_t rot = rot_sel(x0, x1, sh);
         const uint64_t m = update_mask<uint64_t>(xo, yo, rot, yn, xp, xq);
-        const uint64_t mprev = first ? uint64_t(0) : S.ml[li];
+        const uint64_t mprev = first ? uint64_t(0) : (uint64_t(S.ml[li]) << 32);  // carry_sel reads its high word
         nA[li] = xo ^ m;
         nB[li] = yo ^ m;
         nC[li] = yn ^ m;
         nR[li] = x0 ^ carry_sel(m, mprev, sh);
-        S.ml[li] = m;
+        S.ml[li] = uint32_t(m >> 32);
 
         if constexpr (!STEADY) {
             const int sv = 5 * (l - 1);

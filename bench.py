@@ -108,6 +108,20 @@ def _traffic(kernel: str, config: str):
         return None
 
 
+def _int_pipe(kernel: str, config: str):
+    """Integer-issue evidence for the same kernel from the committed ncu capture (the arbitrary-p
+    configs are ALU-pipe bound, not HBM bound): issue-active and ALU / FMA pipe utilisation in %
+    of the SM's peak."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            k = json.load(f)[kernel][config]
+        return {"issue_active_pct": k["issue_active_pct"], "pipe_alu_pct": k.get("pipe_alu_pct"),
+                "pipe_fma_pct": k.get("pipe_fma_pct"), "dram_pct_peak": k["dram_pct_peak"],
+                "source": "ncu --set full (profiles/ncu_summary.json)"}
+    except Exception:
+        return None
+
+
 def _mcs_kernel(prm, Y: int, n: int, ws: int) -> tuple[str, int]:
     """The fused MCS kernel the engine runs for these parameters and the MCS per launch
     (engine.cu octgpu_step: k_mcs_deep, 2 MCS per pass, for constant-xi modes on periodic
@@ -396,6 +410,7 @@ def main():
                          "note": "alg bytes = 1 B/site-update (2 slope bits x 2 reads + 2 writes per MCS); the fused "
                                  "kernels move ~0.5 B (k_mcs_bulk) / ~0.25 B (k_mcs_deep) of DRAM traffic per update, "
                                  "so frac exceeds 1; traffic = ncu dram bytes per launch (profiles/ncu_summary.json)"},
+            "int_pipe": _int_pipe(kname, args.config),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
             "transport": transport_used[-1] if transport_used else None,
             "measurements": len(records),

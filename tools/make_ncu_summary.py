@@ -16,7 +16,8 @@ for arg in sys.argv[1:]:
         "gpu_time_s": k["gpu__time_duration.sum"],
         "dram_pct_peak": k["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"],
         "issue_active_pct": k["smsp__issue_active.avg.pct_of_peak_sustained_active"],
+        "pipe_alu_pct": k.get("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+        "pipe_fma_pct": k.get("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
         "source": path,
     }
 json.dump(out, open("profiles/ncu_summary.json", "w"), indent=1)
-print(json.dumps(out, indent=1))

@@ -335,6 +335,8 @@ struct octgpu_engine {
     CUtensorMap tmd[2][2];  // the same for k_mcs_deep (deep_box_rows rows x 2 / 3 words)
     bool tmd_ok = false;
     int deep = 1;  // temporally blocked passes (k_mcs_deep) where supported; OCTGPU_DEEP=0 disables
+    bool graphs = true;  // replay CUDA graphs for long step() calls (OCTGPU_GRAPH=0 disables)
+    std::map<std::string, cudaGraphExec_t> graph_cache;
     int deep_S = 3;    // k_mcs_deep ring stages (OCTGPU_DEEP_S; S = 3 measured best, profiles/r1_deep_modes.json)
     // Row-stripe mode (multi-GPU): this engine owns global rows [y0, y0 + L) of
     // a Ytot-row periodic lattice, held at local rows 1..L with one halo row
@@ -440,6 +442,7 @@ int plan_mcs(octgpu_engine* e) {
     e->mcs_impl = (e->w == 64 && e->n >= 8 && (e->stripe || e->L >= kGhostRows)) ? 2 : 1;
     if (const char* v = getenv("OCTGPU_MCS_IMPL")) e->mcs_impl = (atoi(v) == 1) ? 1 : e->mcs_impl;
     if (const char* v = getenv("OCTGPU_DEEP")) e->deep = atoi(v);
+    if (const char* v = getenv("OCTGPU_GRAPH")) e->graphs = atoi(v) != 0;
     if (const char* v = getenv("OCTGPU_DEEP_S")) e->deep_S = std::max(2, std::min(8, atoi(v)));
     return OCTGPU_OK;
 }
@@ -806,6 +809,7 @@ void octgpu_destroy(octgpu_engine* e) {
         if (e->planes[i]) cudaFree(e->planes[i]);
         if (e->rng[i]) cudaFree(e->rng[i]);
     }
+    for (auto& kv : e->graph_cache) cudaGraphExecDestroy(kv.second);
     for (auto& kv : e->jtabs) cudaFree(kv.second);
     for (void* ptr : e->ipc_opened) cudaIpcCloseMemHandle(ptr);
     if (e->done) cudaFree(e->done);
@@ -841,6 +845,49 @@ int octgpu_sync(octgpu_engine* e) {
     return OCTGPU_OK;
 }
 
+namespace {
+
+// One fused pass (k_mcs_deep: kDeepSweeps/2 MCS; else 1 MCS) from the current plane / rng set into the other,
+// with the host-side bookkeeping of what the pass does.
+int step_pass(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool live, bool deep, const uint64_t* jtab,
+              uint64_t per_sweep) {
+    const int ps = e->pcur, rs = e->rcur;
+    if (deep) {
+        int rc = ensure_tmaps_deep(e);
+        if (rc) return rc;
+        CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, e->deep_geom(), p,
+                           q, jtab, e->deep_S, &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
+    } else if (e->mcs_impl == 2) {
+        int rc = plan_bulk(e, p, q);
+        if (rc) return rc;
+        CK(launch_mcs_bulk(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, e->geom(), p, q,
+                           jtab, e->bulk_ks, e->bulk_S, &e->tm[ps][0], &e->tm[ps][1], e->stream));
+    } else {
+        CK(launch_mcs(e->w, e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, e->geom(), p, q,
+                      live, jtab, e->stream));
+    }
+    const uint32_t mcs = deep ? kDeepSweeps / 2 : 1;
+    ++e->launches;
+    e->pcur ^= 1;
+    if (live)
+        e->rcur ^= 1;
+    else
+        e->pending += 2 * uint64_t(mcs) * per_sweep;  // constant xi: streams advance lazily
+    e->t += mcs;  // whole MCS: the phase returns to its value (engine_vec.hpp:172-177)
+    return OCTGPU_OK;
+}
+
+std::string graph_key(const octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool deep, const uint64_t* jtab) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf, "%d/%u/%llx/%llx|%d/%u/%llx/%llx|%d|%d%d%d|%p|%d%d%d", p.mode, p.k,
+                  (unsigned long long)p.m, (unsigned long long)p.T, q.mode, q.k, (unsigned long long)q.m,
+                  (unsigned long long)q.T, int(deep), e->pcur, e->rcur, e->phase, static_cast<const void*>(jtab),
+                  e->deep_S, e->bulk_ks, e->bulk_S);
+    return buf;
+}
+
+}  // namespace
+
 int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
     if (!e) return fail(OCTGPU_ERR_CONFIG, "null engine");
     if (e->stripe) return fail(OCTGPU_ERR_CONFIG, "octgpu_step is not available on a row stripe (use the octgpu_stripe_* calls)");
@@ -860,45 +907,67 @@ int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
         rc = get_table(e, per_sweep, &jtab);
         if (rc) return rc;
     }
-    const Geom g = e->geom();
     // Temporal blocking pays where the one-MCS kernel is DRAM-bound and the
-    // deep kernel fits in 80 registers without spills: constant xi (zero /
-    // one). With live streams it spills (4 xoshiro states) and measured slower
+    // deep kernel runs without spills: constant xi (zero / one). With live
+    // streams it needs four xoshiro states per lane and measured slower
     // (profiles/r1_deep_modes.json); OCTGPU_DEEP=2 forces it for experiments.
     const bool deep = e->deep && e->mcs_impl == 2 && mcs_deep_supported(p.mode, q.mode) && (!live || e->deep == 2);
-    for (uint64_t i = 0; i < n_mcs; ++i) {
-        const int ps = e->pcur, rs = e->rcur;
-        if (deep && n_mcs - i >= uint64_t(kDeepSweeps / 2)) {  // kDeepSweeps/2 MCS in one pass
-            rc = ensure_tmaps_deep(e);
-            if (rc) return rc;
-            CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase,
-                               e->deep_geom(), p, q, jtab, e->deep_S, &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
-            ++e->launches;
-            e->pcur ^= 1;
-            if (live)
-                e->rcur ^= 1;
-            else
-                e->pending += uint64_t(kDeepSweeps) * per_sweep;
-            e->t += kDeepSweeps / 2;
-            i += kDeepSweeps / 2 - 1;
-            continue;
+    const uint64_t mpp = deep ? kDeepSweeps / 2 : 1;  // MCS per pass
+    uint64_t left = n_mcs;
+    // Long runs on small / medium lattices replay a CUDA graph of kGraphPasses passes
+    // (an even number, so the plane / rng sets end where they started and the captured
+    // arguments repeat): no per-launch CPU work, which is what bounds small lattices.
+    // Measured steady state (tools/step_timer.py, KWARM=300): 1024^2 p=1/2 10.3 -> 7.7 us/MCS,
+    // 4096^2 p=1 10.0 -> 9.0, 16384^2 p=1 27.7 -> 26.7 us. The first capture + instantiate
+    // in a process costs tens of ms, so lattices whose passes are long anyway (> 2^28
+    // sites, where a pass is >= 0.1 ms) keep plain launches.
+    const uint64_t period = mpp * kGraphPasses;
+    const bool graph_ok = e->graphs && uint64_t(e->X) * e->L <= (uint64_t(1) << 28) &&
+                          e->stream != cudaStreamLegacy && e->stream != cudaStreamPerThread;
+    if (graph_ok && left >= 2 * period) {
+        // first pass outside any capture: plans, tensor maps and kernel attributes exist afterwards
+        rc = step_pass(e, p, q, live, deep, jtab, per_sweep);
+        if (rc) return rc;
+        left -= mpp;
+        const std::string key = graph_key(e, p, q, deep, jtab);
+        auto it = e->graph_cache.find(key);
+        if (it == e->graph_cache.end()) {
+            const int pc = e->pcur, rcs = e->rcur;
+            const uint64_t pend = e->pending, t0 = e->t, l0 = e->launches;
+            cudaGraph_t graph = nullptr;
+            CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+            int crc = OCTGPU_OK;
+            for (int k = 0; k < kGraphPasses && !crc; ++k) crc = step_pass(e, p, q, live, deep, jtab, per_sweep);
+            const cudaError_t ce = cudaStreamEndCapture(e->stream, &graph);
+            e->pcur = pc;  // capturing enqueued nothing: undo the bookkeeping
+            e->rcur = rcs;
+            e->pending = pend;
+            e->t = t0;
+            e->launches = l0;
+            if (crc) {
+                if (graph) cudaGraphDestroy(graph);
+                return crc;
+            }
+            CK(ce);
+            cudaGraphExec_t exec = nullptr;
+            const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+            cudaGraphDestroy(graph);
+            CK(ie);
+            it = e->graph_cache.emplace(key, exec).first;
         }
-        if (e->mcs_impl == 2) {
-            rc = plan_bulk(e, p, q);
-            if (rc) return rc;
-            CK(launch_mcs_bulk(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
-                               e->bulk_ks, e->bulk_S, &e->tm[ps][0], &e->tm[ps][1], e->stream));
+        while (left >= period) {
+            CK(cudaGraphLaunch(it->second, e->stream));
+            if (!live) e->pending += 2 * period * per_sweep;
+            e->t += period;
+            e->launches += kGraphPasses;
+            left -= period;
         }
-        else
-            CK(launch_mcs(e->w, e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q,
-                          live, jtab, e->stream));
-        ++e->launches;
-        e->pcur ^= 1;
-        if (live)
-            e->rcur ^= 1;
-        else
-            e->pending += 2 * per_sweep;  // constant xi: streams advance lazily
-        ++e->t;  // two sweeps: phase returns to its value (engine_vec.hpp:172-177)
+    }
+    while (left > 0) {
+        const bool d = deep && left >= mpp;
+        rc = step_pass(e, p, q, live, d, jtab, per_sweep);
+        if (rc) return rc;
+        left -= d ? mpp : 1;
     }
     return OCTGPU_OK;
 }

@@ -58,6 +58,8 @@ constexpr int kDeepWarps = OCTGPU_DEEP_WARPS;
 constexpr int kDeepMinBlocks = kDeepWarps >= 8 ? 2 : 3;  // resident blocks per SM the register budget targets
 constexpr int deep_box_rows(int L) { return ((34 - 2 * L) * (kDeepWarps - 1) + 34) / 2 * 2; }
 
+constexpr int kGraphPasses = 16;  // passes per CUDA graph replayed by octgpu_step (even)
+
 // Row stripes: halo rows above / below the core rows (local rows 0..HA-1 and
 // HA+L..HA+L+HB-1): enough for k_mcs_deep's 2-MCS pass (3 rows of shrinking
 // lanes each side + stage 1's Y(s)[y+1]); the one-MCS kernels use 1 / 2 of them.

@@ -11,7 +11,7 @@ eng = octgpu.GpuEngine(octgpu.LatticeConfig(X, Y), 1)
 st = torch.cuda.Stream()
 eng.set_stream(st.cuda_stream)
 prm = octgpu.UpdateParams.make(p, q)
-eng.step(prm, 6)
+eng.step(prm, int(os.environ.get("KWARM", 6)))
 eng.sync()
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 a.record(st)

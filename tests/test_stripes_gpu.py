@@ -92,3 +92,25 @@ def test_stripe_pass_sizes():
         e.mcs(octgpu.UpdateParams.make(0.5, 0.0), torch.zeros(e.boundary_bytes, dtype=torch.uint8, device="cuda"), 2)
     with pytest.raises(octgpu.ConfigError):
         StripeEngine(cfg, 0, 3, 3)  # fewer rows than the halo a pass reads
+
+
+@pytest.mark.parametrize("transport", ["host", "peer-streams"])
+def test_stripes_mixed_modes_lazy_streams(transport):
+    """Constant-xi passes (2 MCS, streams owed lazily) followed by live passes: the halo rows'
+    streams (advanced locally on the peer path) must stay exact."""
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        cfg = octgpu.LatticeConfig(2048, 200)
+        grp, engines = _group(cfg, 4, 9, stream, transport)
+        ref = octgpu.GpuEngine(cfg, 9)
+        for pq, n in [((1.0, 0.0), 5), ((0.5, 0.25), 4), ((0.0, 0.0), 3), ((0.75, 0.0), 3)]:
+            prm = octgpu.UpdateParams.make(*pq)
+            grp.step(prm, n)
+            ref.step(prm, n)
+        for e in engines:
+            e.sync()
+        planes = np.concatenate([e.planes() for e in engines], axis=1)
+        states = np.concatenate([e.states() for e in engines], axis=0)
+        assert np.array_equal(planes, ref.planes())
+        assert np.array_equal(states, ref.streams().states)
+        assert grp.measure().power_sums == ref.measure().power_sums

@@ -121,7 +121,6 @@ __global__ void __launch_bounds__(32 * (kP + 1), 4) k_mcs_bulk(const uint64_t* _
                                                             const __grid_constant__ CUtensorMap tmK1) {
     using Word = uint64_t;
     using LY = StageLayout<KS>;
-    constexpr int W = 64;
     constexpr bool LIVE = Plan<PM, QM>::live;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t Y = g.Y, n = g.n;

@@ -74,11 +74,12 @@ template <int L, int PM, int QM>
 struct DeepSlots {
     static constexpr bool kPreP = !(PM == M_ZERO || PM == M_ONE);
     static constexpr bool kPreQ = !(QM == M_ZERO || QM == M_ONE);
-    static constexpr int kSave = 5 * (L - 1) + 1;  // stages 1..L-1: A,B,C,R,A1 of their first two words; stage L: R
-    static constexpr int kPre = L * (L - 1) / 2;   // xi words 0..l-2 of streams l = 2..L
-    static constexpr int kPreP0 = kSave;
-    static constexpr int kPreQ0 = kSave + (kPreP ? kPre : 0);
-    static constexpr int kCount = kPreQ0 + (kPreQ ? kPre : 0);
+    // stages 1..L-1: A,B,C,R,A1 of their first two words; stage L: R
+    __host__ __device__ static constexpr int save() { return 5 * (L - 1) + 1; }
+    // xi words 0..l-2 of streams l = 2..L
+    __host__ __device__ static constexpr int npre() { return L * (L - 1) / 2; }
+    __host__ __device__ static constexpr int preP0() { return save(); }
+    __host__ __device__ static constexpr int preQ0() { return save() + (kPreP ? npre() : 0); }
     __host__ __device__ static constexpr int pre(int l, int j) { return (l - 1) * (l - 2) / 2 + j; }
 };
 
@@ -166,7 +167,6 @@ __device__ __forceinline__ void deep_iter(DeepState<L>& S, const DeepCtx& c, uin
                                           const ProbDev& p, const ProbDev& q) {
     using ST = DeepStage<L>;
     using SL = DeepSlots<L, PM, QM>;
-    constexpr int W = 64;
     const uint32_t n = c.n;
     uint64_t nA[L] = {}, nB[L] = {}, nC[L] = {}, nR[L] = {};
     bool act[L];
@@ -191,9 +191,9 @@ __device__ __forceinline__ void deep_iter(DeepState<L>& S, const DeepCtx& c, uin
             gen_xi<PM, QM, uint64_t>(S.rs[li], p, q, xp, xq);
         } else {
             const int k = SL::pre(l, int(j));
-            if constexpr (SL::kPreP) xp = c.save[(SL::kPreP0 + k) * kLanes];
+            if constexpr (SL::kPreP) xp = c.save[(SL::preP0() + k) * kLanes];
             else xp = (PM == M_ONE) ? ~uint64_t(0) : 0;
-            if constexpr (SL::kPreQ) xq = c.save[(SL::kPreQ0 + k) * kLanes];
+            if constexpr (SL::kPreQ) xq = c.save[(SL::preQ0() + k) * kLanes];
             else xq = (QM == M_ONE) ? ~uint64_t(0) : 0;
         }
 
@@ -385,8 +385,8 @@ __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
             for (int jw = 0; jw <= l - 2; ++jw) {
                 uint64_t xp, xq;
                 gen_xi<PM, QM, uint64_t>(R.rs[l - 1], p, q, xp, xq);
-                if constexpr (SL::kPreP) c.save[(SL::kPreP0 + SL::pre(l, jw)) * kLanes] = xp;
-                if constexpr (SL::kPreQ) c.save[(SL::kPreQ0 + SL::pre(l, jw)) * kLanes] = xq;
+                if constexpr (SL::kPreP) c.save[(SL::preP0() + SL::pre(l, jw)) * kLanes] = xp;
+                if constexpr (SL::kPreQ) c.save[(SL::preQ0() + SL::pre(l, jw)) * kLanes] = xq;
             }
         }
     }

@@ -124,14 +124,21 @@ def _int_pipe(kernel: str, config: str):
 
 def _mcs_kernel(prm, Y: int, n: int, ws: int) -> tuple[str, int]:
     """The fused MCS kernel the engine runs for these parameters and the MCS per launch
-    (engine.cu octgpu_step: k_mcs_deep, 2 MCS per pass, for constant-xi modes on periodic
-    lattices with n >= 8 words and >= 256 rows, and row stripes; otherwise k_mcs_bulk, 1 MCS per pass)."""
+    (engine.cu octgpu_step: k_mcs_deep, 2 MCS per pass, for constant-xi modes (periodic lattices with
+    n >= 8 words and >= 256 rows, and row stripes) and for one-draw-per-word modes (periodic);
+    otherwise k_mcs_bulk, 1 MCS per pass)."""
     from paper_1606_00310_b200.params import ProbMode
 
     const = all(ps.mode == ProbMode.Zero or (ps.mode == ProbMode.Arbitrary and ps.value == 1.0)
                 for ps in (prm.p, prm.q))
-    if const and n >= 8 and (ws > 1 or Y >= 256) and os.environ.get("OCTGPU_DEEP", "1") != "0":
+    deep_env = os.environ.get("OCTGPU_DEEP", "1")
+    sites = 128 * n * Y // ws  # per engine (stripe)
+    big = deep_env == "2" or sites >= 1 << 28
+    if const and n >= 8 and (ws > 1 or Y >= 256) and deep_env != "0" and big:
         return "k_mcs_deep", 2  # periodic lattice, or each rank's row stripe (2-MCS passes)
+    if (ws == 1 and prm.draws_per_word(64) == 1 and n >= 8 and Y >= 256 and deep_env != "0"
+            and (deep_env == "2" or sites >= 1 << 30)):
+        return "k_mcs_deep", 2  # one live stream draw per word (p = 1/2, q = 0), large lattices
     return "k_mcs_bulk", 1
 
 

@@ -847,6 +847,17 @@ int octgpu_sync(octgpu_engine* e) {
 
 namespace {
 
+// k_mcs_deep ring depth: deep_S (3) unless two blocks per SM would no longer fit
+// in shared memory (live passes park xoshiro states and pre-drawn xi there) -> 2.
+int deep_ring(octgpu_engine* e, const ProbDev& p, const ProbDev& q) {
+    int smem_sm = 0;
+    if (cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, e->device) != cudaSuccess)
+        return 2;
+    int S = e->deep_S;
+    while (S > 2 && 2 * (mcs_deep_smem(p.mode, q.mode, kDeepSweeps, S) + 1024) > size_t(smem_sm)) --S;
+    return S;
+}
+
 // One fused pass (k_mcs_deep: kDeepSweeps/2 MCS; else 1 MCS) from the current plane / rng set into the other,
 // with the host-side bookkeeping of what the pass does.
 int step_pass(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool live, bool deep, const uint64_t* jtab,
@@ -856,7 +867,7 @@ int step_pass(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool live, b
         int rc = ensure_tmaps_deep(e);
         if (rc) return rc;
         CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, e->deep_geom(), p,
-                           q, jtab, e->deep_S, &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
+                           q, jtab, deep_ring(e, p, q), &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
     } else if (e->mcs_impl == 2) {
         int rc = plan_bulk(e, p, q);
         if (rc) return rc;
@@ -882,7 +893,7 @@ std::string graph_key(const octgpu_engine* e, const ProbDev& p, const ProbDev& q
     std::snprintf(buf, sizeof buf, "%d/%u/%llx/%llx|%d/%u/%llx/%llx|%d|%d%d%d|%p|%d%d%d", p.mode, p.k,
                   (unsigned long long)p.m, (unsigned long long)p.T, q.mode, q.k, (unsigned long long)q.m,
                   (unsigned long long)q.T, int(deep), e->pcur, e->rcur, e->phase, static_cast<const void*>(jtab),
-                  e->deep_S, e->bulk_ks, e->bulk_S);
+                  deep_ring(const_cast<octgpu_engine*>(e), p, q), e->bulk_ks, e->bulk_S);
     return buf;
 }
 
@@ -907,11 +918,19 @@ int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
         rc = get_table(e, per_sweep, &jtab);
         if (rc) return rc;
     }
-    // Temporal blocking pays where the one-MCS kernel is DRAM-bound and the
-    // deep kernel runs without spills: constant xi (zero / one). With live
-    // streams it needs four xoshiro states per lane and measured slower
-    // (profiles/r1_deep_modes.json); OCTGPU_DEEP=2 forces it for experiments.
-    const bool deep = e->deep && e->mcs_impl == 2 && mcs_deep_supported(p.mode, q.mode) && (!live || e->deep == 2);
+    // Temporal blocking pays where the one-MCS kernel is DRAM-bound: constant xi
+    // (zero / one) and one draw per word (p = 1/2 with q = 0, the paper's benchmark
+    // case: 0.367 -> 0.316 ms/MCS at 2^16^2). With more draws per word the four
+    // streams per lane make it issue-bound and slower than k_mcs_bulk (p = q = 1/2:
+    // 0.41 -> 0.47; p = 3/4: 0.40 -> 0.51; profiles/r1_deep_modes.json).
+    // OCTGPU_DEEP=2 forces it for every cheap mode, OCTGPU_DEEP=0 disables it.
+    // Small lattices underfill the GPU and are latency-bound, where the longer 2-MCS
+    // pipeline loses (tools/step_timer.py: constant xi wins from 2^28 sites, p = 1/2
+    // from 2^30); OCTGPU_DEEP=2 forces the deep pass for any size (tests).
+    const uint64_t sites = uint64_t(e->X) * e->L;
+    const bool deep = e->mcs_impl == 2 && mcs_deep_supported(p.mode, q.mode) &&
+                      (e->deep == 2 || (e->deep == 1 && (live ? (D == 1 && sites >= (uint64_t(1) << 30))
+                                                               : sites >= (uint64_t(1) << 28))));
     const uint64_t mpp = deep ? kDeepSweeps / 2 : 1;  // MCS per pass
     uint64_t left = n_mcs;
     // Long runs on small / medium lattices replay a CUDA graph of kGraphPasses passes
@@ -1208,7 +1227,9 @@ int octgpu_halo_unpack(octgpu_engine* e, const void* from_prev, const void* from
 namespace {
 // k_mcs_deep can carry a stripe through 2 MCS per halo exchange (constant-xi modes)
 bool stripe_deep_ok(const octgpu_engine* e, const ProbDev& p, const ProbDev& q) {
-    return e->deep && e->mcs_impl == 2 && mcs_deep_supported(p.mode, q.mode) && is_const(p) && is_const(q);
+    // constant xi only: a live deep pass would not advance the halo rows' streams (p2p.cu relies on that)
+    const bool size_ok = e->deep == 2 || uint64_t(e->X) * e->L >= (uint64_t(1) << 28);
+    return e->deep && size_ok && e->mcs_impl == 2 && mcs_deep_supported(p.mode, q.mode) && is_const(p) && is_const(q);
 }
 }  // namespace
 

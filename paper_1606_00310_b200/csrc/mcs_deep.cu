@@ -47,6 +47,12 @@ constexpr int kDP = kDeepWarps;  // compute warps per block (+1 producer)
 constexpr int kKS = 2;                  // words per ring stage
 constexpr int kSMax = 8;                // ring stages: runtime S <= kSMax (barrier slots)
 constexpr int kLanes = 32 * kDP;        // parking-slot stride (compute lanes per block)
+// xoshiro streams kept in registers in a live pass; the others live in parking slots
+// (loaded / stored around each use): four 256-bit states per lane do not fit 96 registers
+#ifndef OCTGPU_DEEP_REG_STREAMS
+#define OCTGPU_DEEP_REG_STREAMS 2
+#endif
+constexpr int kRegStreams = OCTGPU_DEEP_REG_STREAMS;
 
 template <int L>
 struct DeepGeo {
@@ -80,6 +86,11 @@ struct DeepSlots {
     __host__ __device__ static constexpr int npre() { return L * (L - 1) / 2; }
     __host__ __device__ static constexpr int preP0() { return save(); }
     __host__ __device__ static constexpr int preQ0() { return save() + (kPreP ? npre() : 0); }
+    // streams kRegStreams..L-1 (0-based) of a live pass are parked in shared memory (4 slots each)
+    static constexpr bool kLive = kPreP || kPreQ || !(PM == M_ZERO || PM == M_ONE) || !(QM == M_ZERO || QM == M_ONE);
+    __host__ __device__ static constexpr int parked() { return kLive && L > kRegStreams ? L - kRegStreams : 0; }
+    __host__ __device__ static constexpr int st0() { return preQ0() + (kPreQ ? npre() : 0); }
+    __host__ __device__ static constexpr int count() { return st0() + 4 * parked(); }
     __host__ __device__ static constexpr int pre(int l, int j) { return (l - 1) * (l - 2) / 2 + j; }
 };
 
@@ -127,6 +138,16 @@ __device__ __forceinline__ void st_pred(uint64_t* p, uint64_t v, bool pred) {
 }
 
 __device__ __forceinline__ uint64_t shup(uint64_t v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+
+__device__ __forceinline__ Xo slot_state(const uint64_t* save, int slot) {
+    return Xo{save[(slot + 0) * kLanes], save[(slot + 1) * kLanes], save[(slot + 2) * kLanes], save[(slot + 3) * kLanes]};
+}
+__device__ __forceinline__ void slot_store(uint64_t* save, int slot, const Xo& s) {
+    save[(slot + 0) * kLanes] = s.a;
+    save[(slot + 1) * kLanes] = s.b;
+    save[(slot + 2) * kLanes] = s.c;
+    save[(slot + 3) * kLanes] = s.d;
+}
 __device__ __forceinline__ uint64_t shdn(uint64_t v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 
 // Lane context shared by every iteration.
@@ -188,7 +209,14 @@ __device__ __forceinline__ void deep_iter(DeepState<L>& S, const DeepCtx& c, uin
         // ---- xi of word j of stream l (stream order: pre-drawn words 0..l-2 come first) ----
         uint64_t xp, xq;
         if (STEADY || l == 1 || j >= uint32_t(l - 1)) {
-            gen_xi<PM, QM, uint64_t>(S.rs[li], p, q, xp, xq);
+            if (SL::parked() > 0 && li >= kRegStreams) {  // li is a constant after unrolling
+                const int sl = SL::st0() + 4 * (li - kRegStreams);
+                Xo st = slot_state(c.save, sl);
+                gen_xi<PM, QM, uint64_t>(st, p, q, xp, xq);
+                slot_store(c.save, sl, st);
+            } else {
+                gen_xi<PM, QM, uint64_t>(S.rs[li], p, q, xp, xq);
+            }
         } else {
             const int k = SL::pre(l, int(j));
             if constexpr (SL::kPreP) xp = c.save[(SL::preP0() + k) * kLanes];
@@ -375,18 +403,26 @@ __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
         R.rs[l] = Xo{0, 0, 0, 0};
     }
     if constexpr (LIVE) {
-        R.rs[0] = load_state(rs, g.Y, y);
+        Xo base = load_state(rs, g.Y, y);
 #pragma unroll
-        for (int l = 1; l < L; ++l) R.rs[l] = apply_table(jtab, R.rs[l - 1]);
-        // words 0..l-2 of streams l >= 2 are processed last but drawn first
-#pragma unroll
-        for (int l = 2; l <= L; ++l) {
+        for (int l = 1; l <= L; ++l) {
+            if (l > 1) base = apply_table(jtab, base);  // stream l starts (l-1) n D draws after stream 1
+            Xo cur = base;
+            // words 0..l-2 of streams l >= 2 are processed last but drawn first
 #pragma unroll
             for (int jw = 0; jw <= l - 2; ++jw) {
                 uint64_t xp, xq;
-                gen_xi<PM, QM, uint64_t>(R.rs[l - 1], p, q, xp, xq);
+                gen_xi<PM, QM, uint64_t>(cur, p, q, xp, xq);
                 if constexpr (SL::kPreP) c.save[(SL::preP0() + SL::pre(l, jw)) * kLanes] = xp;
                 if constexpr (SL::kPreQ) c.save[(SL::preQ0() + SL::pre(l, jw)) * kLanes] = xq;
+            }
+            if constexpr (SL::parked() > 0) {
+                if (l - 1 >= kRegStreams)
+                    slot_store(c.save, SL::st0() + 4 * (l - 1 - kRegStreams), cur);
+                else
+                    R.rs[l - 1] = cur;
+            } else {
+                R.rs[l - 1] = cur;
             }
         }
     }
@@ -432,9 +468,11 @@ __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
     for (uint32_t i = n; i < n + uint32_t(2 * L - 2); ++i) deep_iter<PM, QM, L, false, 2>(R, c, i, nullptr, 0, p, q);
 
     if constexpr (LIVE) {
+        Xo fin = R.rs[L - 1];
+        if constexpr (SL::parked() > 0) fin = slot_state(c.save, SL::st0() + 4 * (L - 1 - kRegStreams));
         if (c.core) {
-            store_state(rd, g.Y, y, R.rs[L - 1]);
-            if (c.ghost_row) store_state(rd, g.Y, y + g.wrap, R.rs[L - 1]);
+            store_state(rd, g.Y, y, fin);
+            if (c.ghost_row) store_state(rd, g.Y, y + g.wrap, fin);
         }
     }
 }
@@ -472,7 +510,8 @@ cudaError_t deep_q(const void* src, void* dst, const uint64_t* rs, uint64_t* rd,
 template <int L>
 size_t deep_smem_l(int pm, int qm, int S) {
     const bool pp = !(pm == M_ZERO || pm == M_ONE), pq = !(qm == M_ZERO || qm == M_ONE);
-    const int slots = 5 * (L - 1) + 1 + (pp ? L * (L - 1) / 2 : 0) + (pq ? L * (L - 1) / 2 : 0);
+    const int parked = (pp || pq) && L > kRegStreams ? L - kRegStreams : 0;
+    const int slots = 5 * (L - 1) + 1 + (pp ? L * (L - 1) / 2 : 0) + (pq ? L * (L - 1) / 2 : 0) + 4 * parked;
     return 128 + size_t(S) * DeepStage<L>::kWords * 8 + size_t(slots) * kLanes * 8;
 }
 

@@ -33,6 +33,7 @@ def _worker(rank, world, port, X, Y, seed, pq, mcs, out):
         sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    os.environ["OCTGPU_DEEP"] = "2"  # 2-MCS passes at test sizes (constant xi)
     import torch
     import torch.distributed as dist
     dist.init_process_group("gloo", rank=rank, world_size=world)

@@ -12,6 +12,13 @@ from paper_1606_00310_b200.stripes import LocalTransport, PeerLocalTransport, St
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _deep_passes_at_test_sizes(monkeypatch):
+    """The 2-MCS stripe passes are the default only from 2^28 sites per stripe; force them at
+    test sizes (constant-xi modes; odd MCS counts still run one-MCS passes)."""
+    monkeypatch.setenv("OCTGPU_DEEP", "2")
+
+
 def _group(cfg, parts, seed, stream, transport="host"):
     engines = []
     streams = []

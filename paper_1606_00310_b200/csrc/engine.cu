@@ -336,6 +336,7 @@ struct octgpu_engine {
     bool tmd_ok = false;
     int deep = 1;  // temporally blocked passes (k_mcs_deep) where supported; OCTGPU_DEEP=0 disables
     bool graphs = true;  // replay CUDA graphs for long step() calls (OCTGPU_GRAPH=0 disables)
+    uint64_t tile_shift = 0;  // != 0: random per-pass row origin of the block tiling (DTr-style, result-neutral)
     std::map<std::string, cudaGraphExec_t> graph_cache;
     int deep_S = 3;    // k_mcs_deep ring stages (OCTGPU_DEEP_S; S = 3 measured best, profiles/r1_deep_modes.json)
     // Row-stripe mode (multi-GPU): this engine owns global rows [y0, y0 + L) of
@@ -443,6 +444,7 @@ int plan_mcs(octgpu_engine* e) {
     if (const char* v = getenv("OCTGPU_MCS_IMPL")) e->mcs_impl = (atoi(v) == 1) ? 1 : e->mcs_impl;
     if (const char* v = getenv("OCTGPU_DEEP")) e->deep = atoi(v);
     if (const char* v = getenv("OCTGPU_GRAPH")) e->graphs = atoi(v) != 0;
+    if (const char* v = getenv("OCTGPU_TILE_SHIFT")) e->tile_shift = strtoull(v, nullptr, 10);
     if (const char* v = getenv("OCTGPU_DEEP_S")) e->deep_S = std::max(2, std::min(8, atoi(v)));
     return OCTGPU_OK;
 }
@@ -860,19 +862,40 @@ int deep_ring(octgpu_engine* e, const ProbDev& p, const ProbDev& q) {
 
 // One fused pass (k_mcs_deep: kDeepSweeps/2 MCS; else 1 MCS) from the current plane / rng set into the other,
 // with the host-side bookkeeping of what the pass does.
+// Random tile-origin shift (the DTr idea of BASELINE.json's north_star, applied to the block tiling): the
+// first core row of the block decomposition moves by s rows, drawn per pass from (tile_shift seed, t).
+// Sites of one sublattice share no slopes (engine_vec.hpp:95-97), so any tiling gives the same result;
+// the shift only moves block / warp / halo boundaries (tested: shifted == unshifted, bit for bit).
+// s is even and keeps every TMA window inside the ghost rows.
+Geom shifted(const octgpu_engine* e, Geom g, uint32_t window) {
+    if (!e->tile_shift || e->stripe || e->mcs_impl != 2) return g;
+    uint64_t z = e->tile_shift + 0x9e3779b97f4a7c15ull * (e->t + 1);  // splitmix64 finaliser
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    // even shifts: a TMA box must start 16-B aligned in its innermost (row) dimension
+    const uint32_t smax = (kGhostRows - window - 2) / 2;
+    const uint32_t s = 2 * uint32_t(z % (smax + 1));
+    g.c0 += s;
+    g.c1 += s;
+    return g;
+}
+
 int step_pass(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool live, bool deep, const uint64_t* jtab,
               uint64_t per_sweep) {
     const int ps = e->pcur, rs = e->rcur;
     if (deep) {
         int rc = ensure_tmaps_deep(e);
         if (rc) return rc;
-        CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, e->deep_geom(), p,
-                           q, jtab, deep_ring(e, p, q), &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
+        CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase,
+                           shifted(e, e->deep_geom(), uint32_t(deep_box_rows(kDeepSweeps))), p, q, jtab,
+                           deep_ring(e, p, q), &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
     } else if (e->mcs_impl == 2) {
         int rc = plan_bulk(e, p, q);
         if (rc) return rc;
-        CK(launch_mcs_bulk(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, e->geom(), p, q,
-                           jtab, e->bulk_ks, e->bulk_S, &e->tm[ps][0], &e->tm[ps][1], e->stream));
+        CK(launch_mcs_bulk(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase,
+                           shifted(e, e->geom(), kTmaBoxRows), p, q, jtab, e->bulk_ks, e->bulk_S, &e->tm[ps][0],
+                           &e->tm[ps][1], e->stream));
     } else {
         CK(launch_mcs(e->w, e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, e->geom(), p, q,
                       live, jtab, e->stream));
@@ -941,7 +964,7 @@ int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
     // in a process costs tens of ms, so lattices whose passes are long anyway (> 2^28
     // sites, where a pass is >= 0.1 ms) keep plain launches.
     const uint64_t period = mpp * kGraphPasses;
-    const bool graph_ok = e->graphs && uint64_t(e->X) * e->L <= (uint64_t(1) << 28) &&
+    const bool graph_ok = e->graphs && !e->tile_shift && uint64_t(e->X) * e->L <= (uint64_t(1) << 28) &&
                           e->stream != cudaStreamLegacy && e->stream != cudaStreamPerThread;
     if (graph_ok && left >= 2 * period) {
         // first pass outside any capture: plans, tensor maps and kernel attributes exist afterwards
@@ -1027,6 +1050,12 @@ int octgpu_sweep(octgpu_engine* e, int parity, const octgpu_params* prm, void* m
         CK(cudaStreamSynchronize(e->stream));
         CK(cudaFree(mlog));
     }
+    return OCTGPU_OK;
+}
+
+int octgpu_set_tile_shift(octgpu_engine* e, uint64_t seed) {
+    if (!e) return fail(OCTGPU_ERR_CONFIG, "null engine");
+    e->tile_shift = seed;
     return OCTGPU_OK;
 }
 

@@ -178,6 +178,10 @@ class GpuEngine:
                                  buf.ctypes.data_as(C.c_void_p) if buf is not None else None))
         return buf
 
+    def set_tile_shift(self, seed: int) -> None:
+        """Random per-pass row origin of the kernels' block tiling (DTr-style); 0 = off. Result-neutral."""
+        check(lib().octgpu_set_tile_shift(self._h, int(seed)))
+
     def set_stream(self, cuda_stream: int | None) -> None:
         check(lib().octgpu_set_stream(self._h, C.c_void_p(cuda_stream) if cuda_stream else None))
 

@@ -336,6 +336,7 @@ struct octgpu_engine {
     bool tmd_ok = false;
     int deep = 1;  // temporally blocked passes (k_mcs_deep) where supported; OCTGPU_DEEP=0 disables
     bool graphs = true;  // replay CUDA graphs for long step() calls (OCTGPU_GRAPH=0 disables)
+    uint32_t prefetch = 0;  // TMA kernels: L2 prefetch distance in ring stages (OCTGPU_PREFETCH)
     uint64_t tile_shift = 0;  // != 0: random per-pass row origin of the block tiling (DTr-style, result-neutral)
     std::map<std::string, cudaGraphExec_t> graph_cache;
     int deep_S = 3;    // k_mcs_deep ring stages (OCTGPU_DEEP_S; S = 3 measured best, profiles/r1_deep_modes.json)
@@ -445,6 +446,7 @@ int plan_mcs(octgpu_engine* e) {
     if (const char* v = getenv("OCTGPU_DEEP")) e->deep = atoi(v);
     if (const char* v = getenv("OCTGPU_GRAPH")) e->graphs = atoi(v) != 0;
     if (const char* v = getenv("OCTGPU_TILE_SHIFT")) e->tile_shift = strtoull(v, nullptr, 10);
+    if (const char* v = getenv("OCTGPU_PREFETCH")) e->prefetch = uint32_t(std::max(0, std::min(64, atoi(v))));
     if (const char* v = getenv("OCTGPU_DEEP_S")) e->deep_S = std::max(2, std::min(8, atoi(v)));
     return OCTGPU_OK;
 }
@@ -868,6 +870,7 @@ int deep_ring(octgpu_engine* e, const ProbDev& p, const ProbDev& q) {
 // the shift only moves block / warp / halo boundaries (tested: shifted == unshifted, bit for bit).
 // s is even and keeps every TMA window inside the ghost rows.
 Geom shifted(const octgpu_engine* e, Geom g, uint32_t window) {
+    g.pf = e->prefetch;
     if (!e->tile_shift || e->stripe || e->mcs_impl != 2) return g;
     uint64_t z = e->tile_shift + 0x9e3779b97f4a7c15ull * (e->t + 1);  // splitmix64 finaliser
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;

@@ -78,6 +78,14 @@ __device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* tm, uint32_t
         : "memory");
 }
 
+// L2 prefetch of a TMA box (no shared memory, no barrier): SASS UTMAPF
+__device__ __forceinline__ void tma3d_prefetch(const CUtensorMap* tm, uint32_t row, uint32_t word, uint32_t plane) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(tm)),
+                 "r"(row), "r"(word), "r"(plane)
+                 : "memory");
+}
+
 __device__ __forceinline__ void st_pred(uint64_t* p, uint64_t v, bool pred) {
     asm volatile(
         "{\n"
@@ -161,6 +169,13 @@ __global__ void __launch_bounds__(32 * (kP + 1), 4) k_mcs_bulk(const uint64_t* _
                 tma3d(base + LY::kYf, &tmK, blk_r0, kb, uint32_t(2 + f), &full[st]);
                 tma3d(base + LY::kYs, &tmK, blk_r0, kb, 2 + s_, &full[st]);
                 tma3d(base + LY::kXs, &tmK1, blk_r0, kb, s_, &full[st]);
+                if (g.pf > 0 && b + g.pf < nblocks) {  // warm L2 pf stages ahead of the ring
+                    const uint32_t kp = (b + g.pf) * KS;
+                    tma3d_prefetch(&tmK, blk_r0, kp, uint32_t(f));
+                    tma3d_prefetch(&tmK, blk_r0, kp, uint32_t(2 + f));
+                    tma3d_prefetch(&tmK, blk_r0, kp, 2 + s_);
+                    tma3d_prefetch(&tmK1, blk_r0, kp, s_);
+                }
                 if (++st == uint32_t(S)) {
                     st = 0;
                     ph ^= 1u;

@@ -41,6 +41,7 @@ struct Geom {
     uint32_t wrap;         // periodic modulus in y, or 0
     uint32_t ypar;         // parity of the global row of physical row 0 (site parity uses global rows)
     uint32_t ghost;        // periodic: rows wrap..wrap+ghost-1 mirror rows (i mod wrap), so block windows never wrap
+    uint32_t pf = 0;       // TMA kernels: L2 prefetch distance in ring stages (0 = off)
 };
 
 constexpr uint32_t kMcsConsumerWarps = 4;                   // k_mcs_bulk: compute warps per block (+1 producer)

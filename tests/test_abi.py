@@ -1,7 +1,6 @@
 """The C-ABI boundary without a GPU: the library loads, exports exactly what
 include/octgpu.h declares, and its host-side logic (parameter resolution,
 validation, stream seeding, schedules) matches the reference goldens."""
-import ctypes as C
 import os
 import re
 

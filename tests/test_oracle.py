@@ -13,7 +13,7 @@ import random
 import numpy as np
 import pytest
 
-from oracle import ARBITRARY, DYADIC, HALF, ZERO, OracleLattice, RefEngine
+from oracle import ARBITRARY, DYADIC, OracleLattice, RefEngine
 
 H = lambda v: int(v, 16)  # noqa: E731
 

@@ -192,6 +192,12 @@ int octgpu_stripe_max_mcs(octgpu_engine* e, const octgpu_params* prm);
 int octgpu_stripe_finish(octgpu_engine* e, const void* boundary_in);
 /* local moments; needs fresh halos (pack/exchange/unpack) for the curl check of row y0 */
 int octgpu_measure_stripe(octgpu_engine* e, octgpu_stripe_moments* out);
+/* Global measure_heights from the stripes' local moments, in row order (parts[0] holds row 0):
+ * reconstruct_heights' checks (curl, row 0, column 0; InvariantError messages as the periodic
+ * engine) and the exact int128 sums shifted binomially by the column-0 prefix of the stripes
+ * above. Host-only (no GPU). */
+int octgpu_stripes_combine(const octgpu_stripe_moments* parts, uint32_t n_parts, uint32_t X, uint32_t Y,
+                           octgpu_moments* out);
 uint32_t octgpu_stripe_y0(const octgpu_engine* e);
 uint32_t octgpu_stripe_rows(const octgpu_engine* e);
 

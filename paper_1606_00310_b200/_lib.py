@@ -100,7 +100,7 @@ EXPORTS = (
     "octgpu_halo_pack", "octgpu_halo_unpack", "octgpu_stripe_mcs", "octgpu_stripe_mcs_n", "octgpu_stripe_max_mcs",
     "octgpu_stripe_finish", "octgpu_measure_stripe", "octgpu_stripe_peer", "octgpu_stripe_ipc_export",
     "octgpu_stripe_ipc_open", "octgpu_stripe_connect", "octgpu_stripe_pass", "octgpu_stripe_pull",
-    "octgpu_stripe_disconnect", "octgpu_set_tile_shift",
+    "octgpu_stripe_disconnect", "octgpu_set_tile_shift", "octgpu_stripes_combine",
     "octgpu_stripe_y0", "octgpu_stripe_rows", "octgpu_height_moments",
 )
 
@@ -157,6 +157,7 @@ def lib() -> C.CDLL:
         "octgpu_stripe_pull": (i32, [vp]),
         "octgpu_stripe_disconnect": (i32, [vp]),
         "octgpu_set_tile_shift": (i32, [vp, u64]),
+        "octgpu_stripes_combine": (i32, [P(OctStripeMoments), u32, u32, u32, P(OctMoments)]),
         "octgpu_stripe_finish": (i32, [vp, vp]),
         "octgpu_measure_stripe": (i32, [vp, P(OctStripeMoments)]),
         "octgpu_stripe_y0": (u32, [vp]),

@@ -1155,25 +1155,19 @@ int run_measure(octgpu_engine* e) {
 
 }  // namespace
 
-int octgpu_measure(octgpu_engine* e, octgpu_moments* out) {
-    if (!e || !out) return fail(OCTGPU_ERR_CONFIG, "null argument");
-    if (e->stripe) return fail(OCTGPU_ERR_CONFIG, "octgpu_measure is not available on a row stripe (use the octgpu_stripe_* calls)");
-    int rc = run_measure(e);
-    if (rc) return rc;
-    const MeasureResult& r = *e->res_host;
-    const uint64_t N = uint64_t(e->X) * e->L;
-    out->t = e->t;
+namespace {
+// MeasurementRecord from the exact sums S_k = sum h^k (measure.cpp:24-56 semantics):
+// mean = S1/N exactly rounded (the reference's double sum is exact here); central
+// moments about the nearest integer c, exact in int128, then one extended-precision
+// correction for d = mean - c (|d| <= 1/2).
+void fill_moments(uint64_t t, uint64_t N, const __int128 S[4], octgpu_moments* out) {
+    out->t = t;
     out->n_sites = N;
-    __int128 S[4];
     for (int k = 0; k < 4; ++k) {
-        out->s_lo[k] = r.s_lo[k];
-        out->s_hi[k] = r.s_hi[k];
-        S[k] = i128_of(r.s_lo[k], r.s_hi[k]);
+        out->s_lo[k] = uint64_t((unsigned __int128)S[k]);
+        out->s_hi[k] = int64_t((unsigned __int128)S[k] >> 64);
     }
-    // mean = S1/N exactly rounded (the reference's double sum is exact here).
     out->mean_h = double(S[0]) / double(N);
-    // Central moments about the nearest integer c, exact in int128, then one
-    // extended-precision correction for d = mean - c (|d| <= 1/2).
     const __int128 NN = N;
     __int128 c = S[0] / NN;
     if (2 * (S[0] - c * NN) > NN) c += 1;
@@ -1198,6 +1192,63 @@ int octgpu_measure(octgpu_engine* e, octgpu_moments* out) {
         out->skew = NAN;
         out->kurt = NAN;
     }
+}
+}  // namespace
+
+int octgpu_stripes_combine(const octgpu_stripe_moments* parts, uint32_t n_parts, uint32_t X, uint32_t Y,
+                           octgpu_moments* out) {
+    // parts in row order (SweepPlan order; parts[0] holds global row 0), as StripeGroup and the C++
+    // GpuStripeGroup pass them; reconstruct_heights' checks in its order (slope_field.hpp:209-226)
+    if (!parts || !out || n_parts == 0) return fail(OCTGPU_ERR_CONFIG, "null argument / no stripes");
+    uint64_t N = 0, curl = 0, first = ~0ull;
+    for (uint32_t i = 0; i < n_parts; ++i) {
+        N += parts[i].n_sites;
+        curl += parts[i].curl_count;
+        if (parts[i].curl_count && parts[i].curl_first < first) first = parts[i].curl_first;
+    }
+    if (N != uint64_t(X) * Y) return fail(OCTGPU_ERR_CONFIG, "stripes do not cover the lattice");
+    if (curl)
+        return fail(OCTGPU_ERR_INVARIANT, "curl violation at plaquette (" + std::to_string(first % X) + "," +
+                                              std::to_string(first / X) + "); " + std::to_string(curl) +
+                                              " plaquettes inconsistent");
+    if (parts[0].row_first_sum != 0) return fail(OCTGPU_ERR_INVARIANT, "row 0 of sigma_x- does not balance to zero");
+    long long col = 0;
+    for (uint32_t i = 0; i < n_parts; ++i) col += parts[i].col_sum;
+    if (col != 0) return fail(OCTGPU_ERR_INVARIANT, "column 0 of sigma_y- does not balance to zero");
+    // h_global = h_local + c on each stripe, c = (sum of col_sum above) - sigma_y-(0, 0)
+    const long long sigma00 = parts[0].sy_first;
+    __int128 S[4] = {0, 0, 0, 0};
+    long long prefix = 0;
+    for (uint32_t i = 0; i < n_parts; ++i) {
+        const octgpu_stripe_moments& m = parts[i];
+        const __int128 c = prefix - sigma00;
+        __int128 loc[5] = {(__int128)m.n_sites, 0, 0, 0, 0};
+        for (int k = 0; k < 4; ++k) loc[k + 1] = i128_of(m.s_lo[k], m.s_hi[k]);
+        static const int C[5][5] = {{1}, {1, 1}, {1, 2, 1}, {1, 3, 3, 1}, {1, 4, 6, 4, 1}};
+        for (int k = 1; k <= 4; ++k) {
+            __int128 acc = 0, cp = 1;  // sum_j C(k,j) c^(k-j) loc_j, j = k..0
+            for (int j = k; j >= 0; --j) {
+                acc += C[k][j] * cp * loc[j];
+                cp *= c;
+            }
+            S[k - 1] += acc;
+        }
+        prefix += m.col_sum;
+    }
+    fill_moments(parts[0].t, N, S, out);
+    return OCTGPU_OK;
+}
+
+int octgpu_measure(octgpu_engine* e, octgpu_moments* out) {
+    if (!e || !out) return fail(OCTGPU_ERR_CONFIG, "null argument");
+    if (e->stripe) return fail(OCTGPU_ERR_CONFIG, "octgpu_measure is not available on a row stripe (use the octgpu_stripe_* calls)");
+    int rc = run_measure(e);
+    if (rc) return rc;
+    const MeasureResult& r = *e->res_host;
+    const uint64_t N = uint64_t(e->X) * e->L;
+    __int128 S[4];
+    for (int k = 0; k < 4; ++k) S[k] = i128_of(r.s_lo[k], r.s_hi[k]);
+    fill_moments(e->t, N, S, out);
     return OCTGPU_OK;
 }
 

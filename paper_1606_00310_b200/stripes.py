@@ -34,12 +34,10 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass
-from fractions import Fraction
-from math import comb
 
 import numpy as np
 
-from ._lib import IPC_BYTES, ConfigError, InvariantError, OctPeer, OctStripeMoments, check, lib
+from ._lib import IPC_BYTES, ConfigError, OctMoments, OctPeer, OctStripeMoments, check, lib
 from .engine import MeasurementRecord, _i128, _word_dtype
 from .params import LatticeConfig, UpdateParams
 
@@ -89,44 +87,25 @@ class StripeMoments:
 
 
 def combine(parts: list[StripeMoments], X: int, Y: int) -> MeasurementRecord:
-    """Global measure_heights from stripe-local sums, with reconstruct_heights'
-    checks in its order (slope_field.hpp:209-226)."""
+    """Global measure_heights from stripe-local sums (octgpu_stripes_combine: reconstruct_heights'
+    checks in its order, slope_field.hpp:209-226, and the binomial shift of the exact int128 sums
+    by the column-0 prefix of the stripes above). Host-only."""
     parts = sorted(parts, key=lambda m: m.y0)
-    N = sum(m.n_sites for m in parts)
-    if N != X * Y:
-        raise ConfigError("stripes do not cover the lattice")
-    curl = sum(m.curl_count for m in parts)
-    if curl:
-        first = min(m.curl_first for m in parts if m.curl_count)
-        raise InvariantError(f"curl violation at plaquette ({first % X},{first // X}); {curl} plaquettes inconsistent")
-    if parts[0].row_first_sum != 0:
-        raise InvariantError("row 0 of sigma_x- does not balance to zero")
-    if sum(m.col_sum for m in parts) != 0:
-        raise InvariantError("column 0 of sigma_y- does not balance to zero")
-    sigma00 = parts[0].sy_first
-    S = [0, 0, 0, 0]
-    prefix = 0
-    for m in parts:
-        c = prefix - sigma00  # h_global = h_local + c on this stripe
-        loc = (m.n_sites,) + tuple(m.sums)
-        for k in range(1, 5):
-            S[k - 1] += sum(comb(k, j) * c ** (k - j) * loc[j] for j in range(k + 1))
-        prefix += m.col_sum
-    return _record(parts[0].t, N, S)
-
-
-def _record(t: int, N: int, S: list[int]) -> MeasurementRecord:
-    S1, S2, S3, S4 = S
-    mean = Fraction(S1, N)
-    m2 = Fraction(S2, N) - mean ** 2
-    m3 = Fraction(S3, N) - 3 * mean * Fraction(S2, N) + 2 * mean ** 3
-    m4 = Fraction(S4, N) - 4 * mean * Fraction(S3, N) + 6 * mean ** 2 * Fraction(S2, N) - 3 * mean ** 4
-    if m2 > 0:
-        skew = float(m3) / float(m2) ** 1.5
-        kurt = float(m4 / (m2 * m2)) - 3.0
-    else:
-        skew = kurt = float("nan")
-    return MeasurementRecord(t, float(m2), float(mean), skew, kurt, N, tuple(S))
+    arr = (OctStripeMoments * len(parts))()
+    mask = (1 << 64) - 1
+    for a, m in zip(arr, parts):
+        a.t, a.n_sites = m.t, m.n_sites
+        for k in range(4):
+            a.s_lo[k] = m.sums[k] & mask
+            hi = (m.sums[k] >> 64) & mask
+            a.s_hi[k] = hi - (1 << 64) if hi >> 63 else hi
+        a.col_sum, a.sy_first, a.row_first_sum = m.col_sum, m.sy_first, m.row_first_sum
+        a.curl_count = m.curl_count
+        a.curl_first = m.curl_first if m.curl_count else mask
+    out = OctMoments()
+    check(lib().octgpu_stripes_combine(arr, len(parts), X, Y, C.byref(out)))
+    sums = tuple(_i128(int(out.s_lo[k]), int(out.s_hi[k])) for k in range(4))
+    return MeasurementRecord(int(out.t), out.W2, out.mean_h, out.skew, out.kurt, int(out.n_sites), sums)
 
 
 class StripeEngine:
@@ -418,6 +397,12 @@ class StripeGroup:
             self.tr.halos()
         parts = self.tr.gather([e.measure_local() for e in self.tr.engines])
         return combine(parts, self.X, self.Y)
+
+    def sync(self) -> None:
+        """Drain every stripe's stream (a stripe's first row is completed by its neighbour's
+        boundary push, so download planes only after syncing the whole group)."""
+        for e in self.tr.engines:
+            e.sync()
 
     @property
     def t(self) -> int:

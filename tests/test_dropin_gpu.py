@@ -51,3 +51,19 @@ def test_resume_from_snapshot_is_bit_exact(goldens, tmp_path):
     full = [l for l in s["csv"].splitlines() if l and l[0].isdigit()]
     tail = [l for l in open(b / "measurements.csv").read().splitlines() if l and l[0].isdigit()]
     assert tail == [l for l in full if int(l.split(",")[0]) >= 316]
+
+
+STRIPES = os.path.join(ROOT, "oracle", "_ref", "stripes_dropin")
+
+
+@pytest.mark.parametrize("X,Y,parts", [(2048, 256, 4), (1024, 130, 3), (4096, 512, 8)])
+def test_cpp_stripe_group_matches_engine(X, Y, parts):
+    """octsca::GpuStripeGroup (C++, peer-memory halos, native combine) == octsca::GpuEngine
+    under the reference's own octsca::run, for constant and live parameter legs."""
+    if not os.path.exists(STRIPES):
+        pytest.skip("oracle/_ref/stripes_dropin not built (needs the reference headers at build time)")
+    env = dict(os.environ, OCTGPU_DEEP="2")  # 2-MCS stripe passes at test sizes
+    r = subprocess.run([STRIPES, str(X), str(Y), str(parts), "11"], capture_output=True, text=True, timeout=600,
+                       env=env)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.startswith("stripes ok")

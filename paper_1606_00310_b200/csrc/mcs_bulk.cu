@@ -120,7 +120,7 @@ size_t mcs_bulk_stage_bytes(int ks) {
 }
 
 template <int PM, int QM, int KS>
-__global__ void __launch_bounds__(32 * (kP + 1), 4) k_mcs_bulk(const uint64_t* __restrict__ src,
+__global__ void __launch_bounds__(32 * (kP + 1), kP >= 8 ? 2 : 4) k_mcs_bulk(const uint64_t* __restrict__ src,
                                                             uint64_t* __restrict__ dst,
                                                             const uint64_t* __restrict__ rs,
                                                             uint64_t* __restrict__ rd, int f, Geom g, ProbDev p,

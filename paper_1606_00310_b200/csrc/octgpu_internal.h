@@ -44,7 +44,10 @@ struct Geom {
     uint32_t pf = 0;       // TMA kernels: L2 prefetch distance in ring stages (0 = off)
 };
 
-constexpr uint32_t kMcsConsumerWarps = 4;                   // k_mcs_bulk: compute warps per block (+1 producer)
+#ifndef OCTGPU_BULK_WARPS
+#define OCTGPU_BULK_WARPS 4
+#endif
+constexpr uint32_t kMcsConsumerWarps = OCTGPU_BULK_WARPS;  // k_mcs_bulk: compute warps per block (+1 producer)
 constexpr uint32_t kTmaBoxRows = 30 * kMcsConsumerWarps + 4;  // k_mcs_bulk window rows (124)
 
 // k_mcs_deep block shape (mcs_deep.cu): kDeepWarps compute warps + 1 producer.

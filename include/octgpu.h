@@ -123,13 +123,13 @@ int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs);
  * (engine_vec.hpp:145-168). mask_log: NULL or host buffer of Y*n words
  * (reference row-major), receives the applied mask of every (row, word). */
 int octgpu_sweep(octgpu_engine* e, int parity, const octgpu_params* prm, void* mask_log);
-
-/* ---- state access ---- */
-
 /* Random tile-origin shifts (DTr-style, BASELINE.json north_star): seed != 0 moves the row origin of the
  * kernels' block tiling by a pseudo-random offset every pass (periodic lattices, TMA kernels); 0 = off.
  * Result-neutral: sites of one sublattice share no slopes (engine_vec.hpp:95-97). */
 int octgpu_set_tile_shift(octgpu_engine* e, uint64_t seed);
+
+/* ---- state access ---- */
+
 uint64_t octgpu_t(const octgpu_engine* e);         /* VecEngine::t (engine_vec.hpp:199) */
 int octgpu_phase(const octgpu_engine* e);          /* SlopeField::phase (slope_field.hpp:44) */
 uint64_t octgpu_master_seed(const octgpu_engine* e); /* RngStreamSet::master_seed (rng.hpp:97) */

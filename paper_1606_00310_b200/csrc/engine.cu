@@ -337,6 +337,7 @@ struct octgpu_engine {
     int deep = 1;  // temporally blocked passes (k_mcs_deep) where supported; OCTGPU_DEEP=0 disables
     bool graphs = true;  // replay CUDA graphs for long step() calls (OCTGPU_GRAPH=0 disables)
     uint32_t prefetch = 0;  // TMA kernels: L2 prefetch distance in ring stages (OCTGPU_PREFETCH)
+    long long p2p_timeout = kP2PTimeoutCycles;  // peer halo wait limit (OCTGPU_P2P_TIMEOUT_MS)
     uint64_t tile_shift = 0;  // != 0: random per-pass row origin of the block tiling (DTr-style, result-neutral)
     std::map<std::string, cudaGraphExec_t> graph_cache;
     int deep_S = 3;    // k_mcs_deep ring stages (OCTGPU_DEEP_S; S = 3 measured best, profiles/r1_deep_modes.json)
@@ -446,6 +447,7 @@ int plan_mcs(octgpu_engine* e) {
     if (const char* v = getenv("OCTGPU_DEEP")) e->deep = atoi(v);
     if (const char* v = getenv("OCTGPU_GRAPH")) e->graphs = atoi(v) != 0;
     if (const char* v = getenv("OCTGPU_TILE_SHIFT")) e->tile_shift = strtoull(v, nullptr, 10);
+    if (const char* v = getenv("OCTGPU_P2P_TIMEOUT_MS")) e->p2p_timeout = std::max(1LL, atoll(v)) * 2'000'000LL;
     if (const char* v = getenv("OCTGPU_PREFETCH")) e->prefetch = uint32_t(std::max(0, std::min(64, atoi(v))));
     if (const char* v = getenv("OCTGPU_DEEP_S")) e->deep_S = std::max(2, std::min(8, atoi(v)));
     return OCTGPU_OK;
@@ -1426,7 +1428,7 @@ static_assert(sizeof(IpcBlob) <= OCTGPU_IPC_BYTES, "IPC blob");
 
 PeerView peer_view(const octgpu_engine* e, const octgpu_peer& p) {
     return PeerView{reinterpret_cast<const void*>(p.planes[e->pcur]), reinterpret_cast<const uint64_t*>(p.rng[e->rcur]),
-                    reinterpret_cast<const uint64_t*>(p.done), p.alloc_rows, p.rows};
+                    reinterpret_cast<const uint64_t*>(p.done), p.alloc_rows, p.rows, e->p2p_timeout};
 }
 
 int p2p_pull(octgpu_engine* e, bool with_rng) {

@@ -146,8 +146,9 @@ struct PeerView {
     const uint64_t* done;
     uint32_t Y;  // allocated rows (row stride)
     uint32_t L;  // core rows
+    long long timeout;  // wait limit in SM clock cycles (the prev view's value is used)
 };
-constexpr long long kP2PTimeoutCycles = 20'000'000'000ll;  // ~10 s at 2 GHz: a dead neighbour is an error, not a hang
+constexpr long long kP2PTimeoutCycles = 20'000'000'000ll;  // default ~10 s at 2 GHz: a dead neighbour is an error, not a hang
 // wait for prev.done >= need && next.done >= need, then copy the neighbours' boundary core rows (+ states)
 // into the local halo rows (kStripeHA above, kStripeHB below)
 cudaError_t launch_halo_pull(int w, void* planes, uint64_t* rng, Geom g, const PeerView& prev, const PeerView& next,

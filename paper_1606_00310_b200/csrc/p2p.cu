@@ -46,13 +46,14 @@ __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
 }
 
 // thread 0 of the block waits for both counters; the block then proceeds
-__device__ __forceinline__ bool block_wait(const uint64_t* a, const uint64_t* b, uint64_t need, uint32_t* err) {
+__device__ __forceinline__ bool block_wait(const uint64_t* a, const uint64_t* b, uint64_t need, uint32_t* err,
+                                           long long limit) {
     __shared__ int ok;
     if (threadIdx.x == 0) {
         const long long t0 = clock64();
         ok = 1;
         while (ld_acquire_sys(a) < need || ld_acquire_sys(b) < need) {
-            if (clock64() - t0 > kP2PTimeoutCycles) {
+            if (clock64() - t0 > limit) {
                 atomicExch(err, 1u);
                 ok = 0;
                 break;
@@ -67,7 +68,7 @@ __device__ __forceinline__ bool block_wait(const uint64_t* a, const uint64_t* b,
 template <typename Word>
 __global__ void k_halo_pull(Word* __restrict__ planes, uint64_t* __restrict__ rng, Geom g, PeerView prev,
                             PeerView next, uint64_t need, uint32_t* err, int with_rng) {
-    if (!block_wait(prev.done, next.done, need, err)) return;
+    if (!block_wait(prev.done, next.done, need, err, prev.timeout)) return;
     const uint32_t n = g.n;
     const uint32_t rows = kStripeHA + kStripeHB;
     const uint32_t per = rows * n, total = 4 * per;

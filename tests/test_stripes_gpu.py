@@ -121,3 +121,18 @@ def test_stripes_mixed_modes_lazy_streams(transport):
         assert np.array_equal(planes, ref.planes())
         assert np.array_equal(states, ref.streams().states)
         assert grp.measure().power_sums == ref.measure().power_sums
+
+
+def test_peer_wait_times_out_instead_of_hanging(monkeypatch):
+    """A neighbour that stops stepping must surface as an error (bounded device wait), not a hang."""
+    monkeypatch.setenv("OCTGPU_P2P_TIMEOUT_MS", "200")
+    cfg = octgpu.LatticeConfig(1024, 64)
+    engines = [StripeEngine(cfg, *stripe_bounds(64, 2, r), 4) for r in range(2)]
+    PeerLocalTransport(engines)
+    prm = octgpu.UpdateParams.make(0.5, 0.0)
+    engines[0].pass_(prm, 1)  # needs the neighbours' pass 0: fine
+    engines[0].pass_(prm, 1)  # needs stripe 1's pass 1, which never comes
+    with pytest.raises(octgpu.CudaError, match="timed out"):
+        engines[0].sync()
+    for e in engines:
+        e.disconnect()

@@ -3,8 +3,11 @@
 
 Workload (default, BASELINE.json configs[1]): a 2^16 x 2^16 lattice from the
 flat start, KPZ p=1 q=0, one MCS per step, W^2(t) measured on the device at
-the points of log_schedule(10^4, 8) that fall inside the K timed steps (the
-first K MCS of the configs[1] job; K = 10^4 runs it whole). Inputs: the slope
+the points of log_schedule(10^4, 8) that fall inside the K timed steps. The
+timed steps are the LAST K MCS of the 10^4-MCS configs[1] job (the state at
+t = 10^4 - K is prepared untimed; K = 10^4 runs the job whole), so a short K
+measures a representative stretch rather than the W^2-dense first MCS;
+--from-flat times MCS 1..K instead (c4 always does: 10 ms/MCS). Inputs: the slope
 planes are 1 GiB, far larger than the 126 MB L2, so no L2 flush is needed.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c2h|c3|c4|c5] [--impl ours|reference]
@@ -31,7 +34,7 @@ CONFIGS = {
     "c2h": dict(X=1 << 16, Y=1 << 16, p=0.5, q=0.0,
                 workload="2^16x2^16 KPZ p=0.5 q=0 (half mode; paper's benchmark case), W^2(t) log-sampled"),
     "c3": dict(X=1 << 16, Y=1 << 16, p=0.5, q=0.5, workload="2^16x2^16 EW-like p=q=1/2 (BASELINE configs[2])"),
-    "c4": dict(X=1 << 16, Y=1 << 16, p=0.98, q=0.02,
+    "c4": dict(X=1 << 16, Y=1 << 16, p=0.98, q=0.02, window=False,  # 10 ms/MCS: no untimed 10^4-MCS prefix
                workload="2^16x2^16 arbitrary p=0.98 q=0.02 (BASELINE configs[3])"),
     "c5": dict(X=1 << 17, Y=1 << 17, p=1.0, q=0.0, workload="2^17x2^17 KPZ p=1 q=0 (BASELINE configs[4])",
                multi="strong"),
@@ -181,6 +184,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU reference work")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--from-flat", action="store_true", help="time MCS 1..K instead of the job's last K MCS")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     ws, rank, local = _dist()
@@ -234,26 +238,34 @@ def main():
     X, Y = cfg["X"], cfg["Y"]
     lat = octgpu.LatticeConfig(X, Y, 64)
     prm = octgpu.UpdateParams.make(cfg["p"], cfg["q"])
-    sched = [t for t in octgpu.log_schedule(SCHEDULE_TMAX, SCHEDULE_PPD) if t <= K]
-    targets = sched + ([K] if not sched or sched[-1] != K else [])
+    # The timed K MCS are the LAST K MCS of the 10^4-MCS job (the state at t_start = 10^4 - K is prepared
+    # untimed), with the job's W^2 points inside that window: K = 10^4 (default) is the whole job; a short
+    # K measures a representative stretch instead of the W^2-dense first MCS. --from-flat times MCS 1..K.
+    t_start = 0 if (args.from_flat or not cfg.get("window", True)) else max(0, SCHEDULE_TMAX - K)
+    sched = [t for t in octgpu.log_schedule(SCHEDULE_TMAX, SCHEDULE_PPD) if t_start < t <= t_start + K]
+    targets = sched + ([t_start + K] if not sched or sched[-1] != t_start + K else [])
+    config_key["window"] = (f"MCS {t_start + 1}..{t_start + K} of the {SCHEDULE_TMAX}-MCS job with its "
+                            f"{len(sched)} W^2 points; "
+                            + (f"state at t={t_start} prepared untimed" if t_start else "from the flat start"))
 
     def barrier():
         if ws > 1:
             torch.distributed.barrier()
 
-    def make(planes=None, states=None):
-        """The job's engine: one GpuEngine, or this rank's row stripe (NCCL halo exchange)."""
+    def make(planes=None, states=None, t=0):
+        """The job's engine: one GpuEngine, or this rank's row stripe (peer-memory / NCCL halo exchange)."""
         if ws == 1:
             if planes is None:
                 eng = octgpu.GpuEngine(lat, 1, device=local)
             else:
-                eng = octgpu.GpuEngine(octgpu.SlopeField(lat, planes), octgpu.RngStreamSet(1, states), device=local)
+                eng = octgpu.GpuEngine(octgpu.SlopeField(lat, planes, t, 0), octgpu.RngStreamSet(1, states),
+                                       device=local)
             eng.set_stream(stream.cuda_stream)
             return eng, [eng]
         from paper_1606_00310_b200.stripes import (DistTransport, PeerDistTransport, StripeEngine, StripeGroup,
                                                    stripe_bounds)
         y0, y1 = stripe_bounds(Y, ws, rank)
-        e = StripeEngine(lat, y0, y1, 1, device=local, planes=planes, states=states)  # this rank's rows only
+        e = StripeEngine(lat, y0, y1, 1, device=local, planes=planes, states=states, t=t)  # this rank's rows
         e.set_stream(stream.cuda_stream)
         alloc = lambda nb: torch.zeros(nb, dtype=torch.uint8, device=dev)  # noqa: E731
         return StripeGroup(_transport(e, alloc, PeerDistTransport, DistTransport), X, Y), [e]
@@ -293,6 +305,10 @@ def main():
 
     # ---- timed region, device-resident ----
     job, engs = make()
+    if t_start:
+        job.step(prm, t_start)  # untimed: the job's state at the start of the timed window
+        for e in engs:
+            e.sync()
     torch.cuda.synchronize()
     seg_events = []
     records = []
@@ -303,7 +319,7 @@ def main():
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        t = 0
+        t = t_start
         for target in targets:
             if target > t:
                 a = torch.cuda.Event(enable_timing=True)
@@ -350,9 +366,19 @@ def main():
         else:
             from paper_1606_00310_b200.stripes import stripe_bounds
             r0, r1 = stripe_bounds(Y, ws, rank)
-        flat = np.zeros((4, r1 - r0, X // 128), np.uint64)  # new_flat (slope_field.hpp:110-118): rows do not
-        flat[1] = flat[3] = np.iinfo(np.uint64).max         # depend on y, so any row range is a flat stripe
-        states0 = octgpu.RngStreamSet.derive(1, r1).states[r0:r1]
+        if t_start == 0:
+            flat = np.zeros((4, r1 - r0, X // 128), np.uint64)  # new_flat (slope_field.hpp:110-118): rows do
+            flat[1] = flat[3] = np.iinfo(np.uint64).max         # not depend on y: any row range is a flat stripe
+            states0 = octgpu.RngStreamSet.derive(1, r1).states[r0:r1]
+        else:  # the state at t_start, downloaded untimed
+            prep, pengs = make()
+            prep.step(prm, t_start)
+            for e in pengs:
+                e.sync()
+            flat = pengs[0].planes()
+            states0 = pengs[0].states() if ws > 1 else pengs[0].streams().states
+            _close(prep)
+            del prep, pengs
         host_planes = torch.from_numpy(np.ascontiguousarray(flat).view(np.int64)).pin_memory()
         host_states = torch.from_numpy(np.ascontiguousarray(states0).view(np.int64)).pin_memory()
         import ctypes as C
@@ -363,10 +389,10 @@ def main():
         t0 = time.perf_counter()
         hp = host_planes.numpy().view(np.uint64)
         hs = host_states.numpy().view(np.uint64)
-        job, engs = make(hp, hs)
+        job, engs = make(hp, hs, t_start)
         engs[0].sync()
         t_create = time.perf_counter() - t0
-        t = 0
+        t = t_start
         n_meas = 0
         for target in targets:
             if target > t:

@@ -2,6 +2,7 @@
 // parameter resolution, stream seeding and GF(2) jump-ahead matrices.
 // Device work lives in kernels.cu.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <limits>
@@ -412,6 +413,8 @@ int get_table(octgpu_engine* e, uint64_t draws_n, uint64_t** out) {
     return OCTGPU_OK;
 }
 
+void trace_create(const char* what, bool start);
+
 // Apply owed draws to every row stream (lazy advance of constant-xi sweeps).
 int materialize(octgpu_engine* e) {
     if (!e->pending) return OCTGPU_OK;
@@ -436,6 +439,7 @@ int upload_states(octgpu_engine* e, const uint64_t* aos) {
         ++e->launches;
     }
     CK(cudaStreamSynchronize(e->stream));
+    trace_create("states", false);
     return OCTGPU_OK;
 }
 
@@ -542,6 +546,7 @@ int alloc_p2p(octgpu_engine* e) {
 int alloc_engine(octgpu_engine* e) {
     CK(cudaSetDevice(e->device));
     CK(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
+    trace_create("stream", false);
     e->stream = e->own_stream;
     // Plane sets of a periodic engine come from the device's stream-ordered pool, kept (release threshold
     // = max) across engines: an engine re-created in the same process (resume, e2e runs) reuses the
@@ -561,9 +566,11 @@ int alloc_engine(octgpu_engine* e) {
             CK(cudaMalloc(&e->planes[i], e->set_bytes()));
         CK(cudaMalloc(reinterpret_cast<void**>(&e->rng[i]), e->rng_bytes()));
     }
+    trace_create("planes", false);
     CK(cudaMalloc(&e->scratch, measure_scratch_bytes(e->Y)));
     CK(cudaMalloc(reinterpret_cast<void**>(&e->res_dev), sizeof(MeasureResult)));
     CK(cudaMallocHost(reinterpret_cast<void**>(&e->res_host), sizeof(MeasureResult)));
+    trace_create("small", false);
     return plan_mcs(e);
 }
 
@@ -656,6 +663,17 @@ namespace {
 
 int refresh_ghosts(octgpu_engine* e);
 
+// OCTGPU_TRACE_CREATE=1: stderr timings of the engine-creation phases (diagnostics)
+void trace_create(const char* what, bool start) {
+    static const bool on = getenv("OCTGPU_TRACE_CREATE") != nullptr;
+    static std::chrono::steady_clock::time_point last;
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    if (!start) fprintf(stderr, "[octgpu create] %-10s %8.3f ms\n", what,
+                        std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
+
 // Allocates an engine over global rows [y0, y0 + L) of an X x Ytot lattice
 // (stripe) or the whole periodic lattice (!stripe).
 int make_engine(uint32_t X, uint32_t Ytot, uint32_t w, bool stripe, uint32_t y0, uint32_t L, int device,
@@ -667,7 +685,9 @@ int make_engine(uint32_t X, uint32_t Ytot, uint32_t w, bool stripe, uint32_t y0,
     // rows of padding (k_mcs reads up to 33 rows past a warp's first row; the TMA kernels
     // zero-fill past the allocation); even for 16-B alignment
     e->Y = stripe ? ((L + kStripeHA + kStripeHB + 34 + 1) & ~1u) : Ytot + kGhostRows;
+    trace_create("", true);
     int rc = alloc_engine(e);
+    trace_create("alloc", false);
     if (!rc && stripe) rc = alloc_p2p(e);
     if (rc) {
         std::string keep = g_err;
@@ -695,11 +715,16 @@ int load_planes(octgpu_engine* e, const void* planes) {
         CK(cudaMemcpyAsync(stage, pad.data(), e->host_bytes(), cudaMemcpyHostToDevice, e->stream));
         CK(cudaStreamSynchronize(e->stream));
     }
+    if (getenv("OCTGPU_TRACE_CREATE")) {
+        CK(cudaStreamSynchronize(e->stream));
+        trace_create("upload", false);
+    }
     CK(launch_import(e->w, stage, e->planes[e->pcur], e->geom(), e->host_rows(), e->stream));
     ++e->launches;
     rc = refresh_ghosts(e);
     if (rc) return rc;
     CK(cudaStreamSynchronize(e->stream));
+    trace_create("import", false);
     return OCTGPU_OK;
 }
 

@@ -33,3 +33,17 @@ for rep in range(3):
     torch.cuda.synchronize()
     t5 = time.perf_counter()
     print(f"create {t1-t0:.3f}  100 MCS {t2-t1:.3f}  measure {t3-t2:.4f}  d2h {t4-t3:.3f}  destroy {t5-t4:.3f}")
+
+# raw copy rates of the same pinned buffers, for comparison
+d = torch.empty(hp.shape, dtype=torch.int64, device="cuda")
+src = torch.from_numpy(hp.view(np.int64))
+for rep in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    d.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    torch.from_numpy(pp.view(np.int64)).copy_(d, non_blocking=True)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    print(f"raw H2D {hp.nbytes / (t1 - t0) / 1e9:.1f} GB/s  D2H {hp.nbytes / (t2 - t1) / 1e9:.1f} GB/s")

@@ -67,7 +67,45 @@ __device__ __forceinline__ uint64_t shl64(uint64_t x) {
     return pack64(lo << K, fsl<K, FMA>(lo, hi));
 }
 
+// The xoshiro xor network as four three-input LOP3 per 32-bit half: b' = b ^ c ^ a, c' = c ^ a ^ t,
+// d' = d ^ b, a' = a ^ d' (the sequential statement order of rng.hpp:34-44 compiles to 9.5 LOP3 per step:
+// c ^ a is materialised and reused). OCTGPU_XO_ASM=0 restores the plain C++ statements.
+#ifndef OCTGPU_XO_ASM
+#define OCTGPU_XO_ASM 1
+#endif
+#if OCTGPU_XO_ASM
+#define OCTGPU_XO_STEP_PTX                               \
+    "shl.b32 t0, b0, 17;\n\t" /* t = b << 17 */         \
+    "shf.l.wrap.b32 t1, b0, b1, 17;\n\t"                 \
+    "xor.b32 e0, d0, b0;\n\t" /* d' = d ^ b */          \
+    "xor.b32 e1, d1, b1;\n\t"                           \
+    "lop3.b32 b0, b0, c0, a0, 0x96;\n\t" /* b ^ c ^ a */ \
+    "lop3.b32 b1, b1, c1, a1, 0x96;\n\t"                \
+    "lop3.b32 c0, c0, a0, t0, 0x96;\n\t" /* c ^ a ^ t */ \
+    "lop3.b32 c1, c1, a1, t1, 0x96;\n\t"                \
+    "xor.b32 a0, a0, e0;\n\t" /* a ^ d' */              \
+    "xor.b32 a1, a1, e1;\n\t"                           \
+    "shf.l.wrap.b32 d0, e0, e1, 13;\n\t" /* rotl 45 */   \
+    "shf.l.wrap.b32 d1, e1, e0, 13;\n\t"
+#define OCTGPU_XO_IN                                          \
+    ".reg .u32 a0, a1, b0, b1, c0, c1, d0, d1, t0, t1, e0, e1;\n\t" \
+    "mov.b64 {a0, a1}, %1;\n\t"                            \
+    "mov.b64 {b0, b1}, %2;\n\t"                            \
+    "mov.b64 {c0, c1}, %3;\n\t"                            \
+    "mov.b64 {d0, d1}, %4;\n\t"
+#define OCTGPU_XO_OUT                \
+    "mov.b64 %1, {a0, a1};\n\t"     \
+    "mov.b64 %2, {b0, b1};\n\t"     \
+    "mov.b64 %3, {c0, c1};\n\t"     \
+    "mov.b64 %4, {d0, d1};\n\t"
+#endif
+
 __device__ __forceinline__ void xo_step(Xo& s) {
+#if OCTGPU_XO_ASM
+    uint32_t dummy = 0;
+    asm("{\n\t" OCTGPU_XO_IN OCTGPU_XO_STEP_PTX OCTGPU_XO_OUT "}"
+        : "+r"(dummy), "+l"(s.a), "+l"(s.b), "+l"(s.c), "+l"(s.d));
+#else
     const uint64_t t = shl64<17, OCTGPU_SHL17_FMA>(s.b);
     s.c ^= s.a;
     s.d ^= s.b;
@@ -75,6 +113,7 @@ __device__ __forceinline__ void xo_step(Xo& s) {
     s.a ^= s.d;
     s.c ^= t;
     s.d = rotl64_hi<45, OCTGPU_ROT45_FMA>(s.d);
+#endif
 }
 
 __device__ __forceinline__ uint64_t xo_next(Xo& s) {
@@ -128,26 +167,54 @@ __device__ __forceinline__ uint32_t acc_ge(uint32_t acc, uint64_t r, uint64_t T)
     return out;
 }
 
+// One draw + compare + xoshiro step, spelled out so that the xor network is four three-input LOP3 per half
+// (b ^ c ^ a, c ^ a ^ t, d ^ b, a ^ d') instead of the 9.5 LOP3 per draw the compiler derives from the
+// sequential xoshiro statement order: the arbitrary-p path is bound by the ALU pipe, which LOP3, SHF and IADD3
+// share. (64-bit adds as mad.wide by a runtime 1, to move them to the FMA pipe, do not survive ptxas: it splits
+// them back into IMAD.WIDE + IADD3 + IMAD.X.) Same values as acc_ge(acc, xo_next(s), T).
+__device__ __forceinline__ uint32_t arb_draw(Xo& s, uint32_t T0, uint32_t T1, uint32_t acc) {
+#if OCTGPU_XO_ASM
+    asm("{\n\t" OCTGPU_XO_IN
+        ".reg .u32 u0, u1, r0, r1, x0, x1, z;\n\t"
+        "add.cc.u32 u0, a0, d0;\n\t"  // u = a + d
+        "addc.u32 u1, a1, d1;\n\t"
+        "shf.l.wrap.b32 r1, u0, u1, 23;\n\t"  // rotl(u, 23)
+        "shf.l.wrap.b32 r0, u1, u0, 23;\n\t"
+        "add.cc.u32 x0, r0, a0;\n\t"  // x = rotl(u, 23) + a
+        "addc.u32 x1, r1, a1;\n\t"
+        "sub.cc.u32 z, x0, %5;\n\t"  // acc = 2 acc + (x >= T)
+        "subc.cc.u32 z, x1, %6;\n\t"
+        "addc.u32 %0, %0, %0;\n\t" OCTGPU_XO_STEP_PTX OCTGPU_XO_OUT "}"
+        : "+r"(acc), "+l"(s.a), "+l"(s.b), "+l"(s.c), "+l"(s.d)
+        : "r"(T0), "r"(T1));
+    return acc;
+#else
+    return acc_ge(acc, xo_next(s), (uint64_t(T1) << 32) | T0);
+#endif
+}
+
 template <typename Word>
-__device__ __forceinline__ uint32_t arb_half(Xo& s, uint64_t T) {
+__device__ __forceinline__ uint32_t arb_half(Xo& s, const ProbDev& pd) {
+    const uint32_t T0 = uint32_t(pd.T), T1 = uint32_t(pd.T >> 32);
     uint32_t acc = 0;
 #pragma unroll 1
     for (int it = 0; it < 4; ++it) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc = acc_ge(acc, xo_next(s), T);
+        for (int j = 0; j < 8; ++j) acc = arb_draw(s, T0, T1, acc);
     }
     return ~__brev(acc);
 }
 
 // two independent streams interleaved draw by draw (instruction-level parallelism)
-__device__ __forceinline__ void arb_half_pair(Xo& a, Xo& b, uint64_t T, uint32_t& ra, uint32_t& rb) {
+__device__ __forceinline__ void arb_half_pair(Xo& a, Xo& b, const ProbDev& pd, uint32_t& ra, uint32_t& rb) {
+    const uint32_t T0 = uint32_t(pd.T), T1 = uint32_t(pd.T >> 32);
     uint32_t acca = 0, accb = 0;
 #pragma unroll 1
     for (int it = 0; it < 4; ++it) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            acca = acc_ge(acca, xo_next(a), T);
-            accb = acc_ge(accb, xo_next(b), T);
+            acca = arb_draw(a, T0, T1, acca);
+            accb = arb_draw(b, T0, T1, accb);
         }
     }
     ra = ~__brev(acca);
@@ -173,11 +240,11 @@ __device__ __forceinline__ Word xi_word(Xo& s, const ProbDev& pd) {
         return acc;
     } else if constexpr (MODE == M_ARB) {
         // xi_arbitrary: bit i = to_unit(draw_i) < r  <=>  draw_i < T (integer threshold)
-        const uint32_t lo = arb_half<Word>(s, pd.T);
+        const uint32_t lo = arb_half<Word>(s, pd);
         if constexpr (W == 32) {
             return Word(lo);
         } else {
-            return Word(pack64(lo, arb_half<Word>(s, pd.T)));
+            return Word(pack64(lo, arb_half<Word>(s, pd)));
         }
     } else {  // M_ONE: every bit accepted, stream still advances w draws
 #pragma unroll 8
@@ -228,13 +295,13 @@ __device__ __forceinline__ void xi_word_pair(Xo& a, Xo& b, const ProbDev& pd, Wo
         wb = rb;
     } else if constexpr (MODE == M_ARB) {
         uint32_t la, lb;
-        arb_half_pair(a, b, pd.T, la, lb);
+        arb_half_pair(a, b, pd, la, lb);
         if constexpr (W == 32) {
             wa = Word(la);
             wb = Word(lb);
         } else {
             uint32_t ha, hb;
-            arb_half_pair(a, b, pd.T, ha, hb);
+            arb_half_pair(a, b, pd, ha, hb);
             wa = Word(pack64(la, ha));
             wb = Word(pack64(lb, hb));
         }

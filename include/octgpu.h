@@ -128,6 +128,20 @@ int octgpu_sweep(octgpu_engine* e, int parity, const octgpu_params* prm, void* m
  * Result-neutral: sites of one sublattice share no slopes (engine_vec.hpp:95-97). */
 int octgpu_set_tile_shift(octgpu_engine* e, uint64_t seed);
 
+/* xi source of octgpu_step. OCTGPU_RNG_XOSHIRO (default): the reference's per-row
+ * xoshiro256++ streams (rng.hpp:17-124), bit-exact with VecEngine. OCTGPU_RNG_COUNTER:
+ * opt-in counter-based streams with NO reference equivalent (BASELINE north_star,
+ * SURVEY.md 8f row 4): draw i of row y in global sweep sigma = 2 t + (0 | 1) is
+ * mix64(o + (i+1) g), o = mix64(mix64(seed + (sigma+1) g) + (y+1) g), g = 0x9E3779B97F4A7C15,
+ * mix64 = the SplitMix64 finaliser; seed = octgpu_master_seed. The xi words are built from
+ * these draws exactly as from xoshiro draws (half / dyadic / arbitrary). Counter steps leave
+ * the xoshiro states untouched; single sweeps (octgpu_sweep) and row stripes are xoshiro-only
+ * (OCTGPU_ERR_CONFIG). Results are pinned by oracle/octoracle.c oo_step_ctr. */
+#define OCTGPU_RNG_XOSHIRO 0
+#define OCTGPU_RNG_COUNTER 1
+int octgpu_set_rng(octgpu_engine* e, int kind);
+int octgpu_get_rng(const octgpu_engine* e);
+
 /* ---- state access ---- */
 
 uint64_t octgpu_t(const octgpu_engine* e);         /* VecEngine::t (engine_vec.hpp:199) */

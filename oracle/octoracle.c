@@ -135,15 +135,37 @@ uint32_t oo_draws_per_word(const oo_prob* p, uint32_t w) {
     }
 }
 
+/* ---- opt-in counter-based streams (NOT in the reference; include/octgpu.h octgpu_set_rng):
+ * SplitMix64's finaliser (the reference's seeding mixer, rng.hpp splitmix64) over a Weyl
+ * sequence whose origin hashes (seed, global sweep sigma, row y). st[0] holds the Weyl value. */
+#define OO_GAMMA 0x9E3779B97F4A7C15ull
+static uint64_t oo_mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static uint64_t ctr_sweep_key(uint64_t seed, uint64_t sigma) { return oo_mix64(seed + (sigma + 1) * OO_GAMMA); }
+static uint64_t ctr_row_origin(uint64_t key, uint32_t y) { return oo_mix64(key + ((uint64_t)y + 1) * OO_GAMMA); }
+uint64_t oo_ctr_draw(uint64_t seed, uint64_t sigma, uint32_t y, uint64_t i) {
+    return oo_mix64(ctr_row_origin(ctr_sweep_key(seed, sigma), y) + (i + 1) * OO_GAMMA);
+}
+
+/* one draw from a row's source: xoshiro state (ctr = 0) or Weyl counter in st[0] (ctr = 1) */
+static uint64_t src_next(uint64_t st[4], int ctr) {
+    if (!ctr) return oo_rng_next(st);
+    st[0] += OO_GAMMA;
+    return oo_mix64(st[0]);
+}
+
 /* ---- rng.hpp:135-179, params.hpp:84-92 (xi words) ---- */
-uint64_t oo_xi_word(uint64_t st[4], const oo_prob* p, uint32_t w) {
+static uint64_t xi_word_src(uint64_t st[4], const oo_prob* p, uint32_t w, int ctr) {
     switch (p->mode) {
     case OO_ZERO: return 0;
-    case OO_HALF: return oo_rng_next(st) & wmask(w);
+    case OO_HALF: return src_next(st, ctr) & wmask(w);
     case OO_DYADIC: {
-        uint64_t acc = oo_rng_next(st) & wmask(w);
+        uint64_t acc = src_next(st, ctr) & wmask(w);
         for (uint32_t i = 1; i < p->k; ++i) {
-            uint64_t xi = oo_rng_next(st) & wmask(w);
+            uint64_t xi = src_next(st, ctr) & wmask(w);
             acc = ((p->m >> i) & 1) ? (acc | xi) : (acc & xi);
         }
         return acc;
@@ -151,13 +173,15 @@ uint64_t oo_xi_word(uint64_t st[4], const oo_prob* p, uint32_t w) {
     default: {
         uint64_t word = 0;
         for (uint32_t i = 0; i < w; ++i) {
-            double u = (double)(oo_rng_next(st) >> 11) * 0x1.0p-53;
+            double u = (double)(src_next(st, ctr) >> 11) * 0x1.0p-53;
             word |= (uint64_t)(u < p->r) << i;
         }
         return word;
     }
     }
 }
+
+uint64_t oo_xi_word(uint64_t st[4], const oo_prob* p, uint32_t w) { return xi_word_src(st, p, w, 0); }
 
 /* ---- slope_field.hpp:110-118 (flat start) ---- */
 void oo_new_flat(uint32_t X, uint32_t Y, uint32_t w, uint64_t* planes) {
@@ -195,15 +219,19 @@ static uint64_t* row_of(const lat_t* L, int plane, uint32_t y) {
 }
 
 /* ---- engine_vec.hpp:98-137 (detail::sweep_rows) ---- */
-static void sweep_range(const lat_t* L, int parity, const oo_prob* p, const oo_prob* q, uint64_t* states,
-                        uint32_t ya, uint32_t yb, uint64_t* mask_log) {
+/* ctr = 0: row y draws from states[y - y0] (xoshiro); ctr = 1: from the counter stream of
+ * sweep key `key` (states unused) */
+static void sweep_range_src(const lat_t* L, int parity, const oo_prob* p, const oo_prob* q, uint64_t* states,
+                            uint32_t ya, uint32_t yb, uint64_t* mask_log, int ctr, uint64_t key) {
     const uint32_t n = L->n, w = L->w;
     const uint64_t M = wmask(w);
     const int with_q = q->mode != OO_ZERO;
     uint64_t* xbuf = malloc(n * sizeof(uint64_t));
     uint64_t* mbuf = malloc(n * sizeof(uint64_t));
     for (uint32_t y = ya; y < yb; ++y) {
-        uint64_t* st = states + 4 * (size_t)(y - L->y0);
+        uint64_t cst[4] = {0, 0, 0, 0};
+        if (ctr) cst[0] = ctr_row_origin(key, y + L->yoff);
+        uint64_t* st = ctr ? cst : states + 4 * (size_t)(y - L->y0);
         uint64_t* px = row_of(L, 0 * 2 + parity, y);
         uint64_t* py = row_of(L, 1 * 2 + parity, y);
         uint64_t* qy1 = row_of(L, 1 * 2 + (parity ^ 1), y + 1);
@@ -217,8 +245,8 @@ static void sweep_range(const lat_t* L, int parity, const oo_prob* p, const oo_p
         else
             memcpy(xbuf, raw, n * sizeof(uint64_t));
         for (uint32_t k = 0; k < n; ++k) {
-            uint64_t xp = oo_xi_word(st, p, w);
-            uint64_t xq = with_q ? oo_xi_word(st, q, w) : 0;
+            uint64_t xp = xi_word_src(st, p, w, ctr);
+            uint64_t xq = with_q ? xi_word_src(st, q, w, ctr) : 0;
             uint64_t m = update_mask(px[k], py[k], xbuf[k], qy1[k], xp, xq) & M;
             mbuf[k] = m;
             px[k] ^= m;
@@ -239,6 +267,11 @@ static void sweep_range(const lat_t* L, int parity, const oo_prob* p, const oo_p
     }
     free(xbuf);
     free(mbuf);
+}
+
+static void sweep_range(const lat_t* L, int parity, const oo_prob* p, const oo_prob* q, uint64_t* states,
+                        uint32_t ya, uint32_t yb, uint64_t* mask_log) {
+    sweep_range_src(L, parity, p, q, states, ya, yb, mask_log, 0, 0);
 }
 
 static void sweep_rows(const lat_t* L, int parity, const oo_prob* p, const oo_prob* q, uint64_t* states,
@@ -262,6 +295,20 @@ int oo_step(uint32_t X, uint32_t Y, uint32_t w, uint64_t* planes, uint64_t* stat
     for (uint64_t i = 0; i < n_mcs; ++i) {
         oo_sweep(X, Y, w, planes, states, phase, *phase, p, q, NULL);
         oo_sweep(X, Y, w, planes, states, phase, *phase, p, q, NULL);
+        ++*t;
+    }
+    return 0;
+}
+
+/* n MCS with the counter-based streams: sweeps phase then !phase, sigma = 2 t + 0 / 1 */
+int oo_step_ctr(uint32_t X, uint32_t Y, uint32_t w, uint64_t* planes, int* phase, uint64_t* t, const oo_prob* p,
+                const oo_prob* q, uint64_t seed, uint64_t n_mcs) {
+    lat_t L = {X, Y, w, X / (2 * w), 0, Y, planes, NULL, 0};
+    for (uint64_t i = 0; i < n_mcs; ++i) {
+        for (int h = 0; h < 2; ++h) {
+            sweep_range_src(&L, *phase, p, q, NULL, 0, Y, NULL, 1, ctr_sweep_key(seed, 2 * *t + (uint64_t)h));
+            *phase ^= 1;
+        }
         ++*t;
     }
     return 0;

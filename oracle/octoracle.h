@@ -51,6 +51,10 @@ void oo_new_flat(uint32_t X, uint32_t Y, uint32_t w, uint64_t* planes);
 /* engine_vec.hpp:98-177. Returns 0, or 2 on phase mismatch. */
 int oo_sweep(uint32_t X, uint32_t Y, uint32_t w, uint64_t* planes, uint64_t* states, int* phase, int parity,
              const oo_prob* p, const oo_prob* q, uint64_t* mask_log);
+/* opt-in counter-based streams (include/octgpu.h octgpu_set_rng; no reference equivalent) */
+uint64_t oo_ctr_draw(uint64_t seed, uint64_t sigma, uint32_t y, uint64_t i);
+int oo_step_ctr(uint32_t X, uint32_t Y, uint32_t w, uint64_t* planes, int* phase, uint64_t* t, const oo_prob* p,
+                const oo_prob* q, uint64_t seed, uint64_t n_mcs);
 int oo_step(uint32_t X, uint32_t Y, uint32_t w, uint64_t* planes, uint64_t* states, int* phase, uint64_t* t,
             const oo_prob* p, const oo_prob* q, uint64_t n_mcs);
 

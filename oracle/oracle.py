@@ -73,6 +73,13 @@ class Oracle:
         L.oo_log_schedule.argtypes = [u64, u32, _u64p, u32]
         L.oo_log_schedule.restype = u32
         L.oo_mcs_stripe.argtypes = [u32, u32, u32, u32, u32, _u64p, _u64p, i32, P(OOProb), P(OOProb)]
+        L.oo_ctr_draw.argtypes = [u64, u64, u32, u64]
+        L.oo_ctr_draw.restype = u64
+        L.oo_step_ctr.argtypes = [u32, u32, u32, _u64p, P(i32), P(u64), P(OOProb), P(OOProb), u64, u64]
+
+    # -- opt-in counter-based streams (include/octgpu.h octgpu_set_rng) ---
+    def ctr_draw(self, seed: int, sigma: int, y: int, i: int) -> int:
+        return int(self.L.oo_ctr_draw(seed, sigma, y, i))
 
     # -- rng -------------------------------------------------------------
     def from_seed(self, seed: int) -> np.ndarray:
@@ -175,6 +182,13 @@ class OracleLattice:
         ph, t = C.c_int(self.phase), C.c_uint64(self.t)
         o.L.oo_step(self.X, self.Y, self.w, self.planes, self.states, C.byref(ph), C.byref(t),
                     C.byref(p), C.byref(q), n)
+        self.phase, self.t = ph.value, t.value
+
+    def step_ctr(self, o: Oracle, p: OOProb, q: OOProb, seed: int, n: int = 1) -> None:
+        """n MCS with the counter-based streams (states untouched)."""
+        ph, t = C.c_int(self.phase), C.c_uint64(self.t)
+        o.L.oo_step_ctr(self.X, self.Y, self.w, self.planes, C.byref(ph), C.byref(t), C.byref(p), C.byref(q),
+                        seed, n)
         self.phase, self.t = ph.value, t.value
 
     def sweep(self, o: Oracle, parity: int, p: OOProb, q: OOProb, mask_log: np.ndarray | None = None) -> None:

@@ -101,6 +101,7 @@ EXPORTS = (
     "octgpu_stripe_finish", "octgpu_measure_stripe", "octgpu_stripe_peer", "octgpu_stripe_ipc_export",
     "octgpu_stripe_ipc_open", "octgpu_stripe_connect", "octgpu_stripe_pass", "octgpu_stripe_pull",
     "octgpu_stripe_disconnect", "octgpu_set_tile_shift", "octgpu_stripes_combine",
+    "octgpu_set_rng", "octgpu_get_rng",
     "octgpu_stripe_y0", "octgpu_stripe_rows", "octgpu_height_moments",
 )
 
@@ -157,6 +158,8 @@ def lib() -> C.CDLL:
         "octgpu_stripe_pull": (i32, [vp]),
         "octgpu_stripe_disconnect": (i32, [vp]),
         "octgpu_set_tile_shift": (i32, [vp, u64]),
+        "octgpu_set_rng": (i32, [vp, i32]),
+        "octgpu_get_rng": (i32, [vp]),
         "octgpu_stripes_combine": (i32, [P(OctStripeMoments), u32, u32, u32, P(OctMoments)]),
         "octgpu_stripe_finish": (i32, [vp, vp]),
         "octgpu_measure_stripe": (i32, [vp, P(OctStripeMoments)]),

@@ -2,6 +2,7 @@
 // the Kawasaki mask. Included by kernels.cu and mcs_bulk.cu only.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "octgpu_internal.h"
 
@@ -122,6 +123,40 @@ __device__ __forceinline__ uint64_t xo_next(Xo& s) {
     return r;
 }
 
+// -------------------------------------------------------------------------
+// Counter-based streams (opt-in rng mode, NOT the reference's generator; see
+// octgpu_set_rng): draw i of row y in global sweep sigma is
+//   mix64(origin(seed, sigma, y) + (i + 1) * gamma),
+//   origin = mix64(mix64(seed + (sigma + 1) * gamma) + (y + 1) * gamma),
+// i.e. SplitMix64 (the reference's seeding mixer, rng.hpp splitmix64) run as a
+// Weyl sequence from a hashed per-(sweep, row) origin. No state is stored: a
+// row's draws are a pure function of (seed, sigma, y, i).
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+struct Ctr {
+    uint64_t x;
+};
+
+__host__ __device__ __forceinline__ uint64_t ctr_sweep_key(uint64_t seed, uint64_t sigma) {
+    return mix64(seed + (sigma + 1) * kGamma);
+}
+
+__device__ __forceinline__ Ctr ctr_row(uint64_t sweep_key, uint32_t y) {
+    return Ctr{mix64(sweep_key + (uint64_t(y) + 1) * kGamma)};
+}
+
+__device__ __forceinline__ uint64_t rng_next(Ctr& s) {
+    s.x += kGamma;
+    return mix64(s.x);
+}
+__device__ __forceinline__ uint64_t rng_next(Xo& s) { return xo_next(s); }
+
 __device__ __forceinline__ Xo load_state(const uint64_t* __restrict__ r, uint32_t Y, uint32_t y) {
     return Xo{r[y], r[size_t(Y) + y], r[2 * size_t(Y) + y], r[3 * size_t(Y) + y]};
 }
@@ -224,31 +259,43 @@ __device__ __forceinline__ void arb_half_pair(Xo& a, Xo& b, const ProbDev& pd, u
 // -------------------------------------------------------------------------
 // xi words (rng.hpp:129-179, params.hpp:84-92)
 
-template <int MODE, typename Word>
-__device__ __forceinline__ Word xi_word(Xo& s, const ProbDev& pd) {
+template <int MODE, typename Word, typename R>
+__device__ __forceinline__ Word xi_word(R& s, const ProbDev& pd) {
     constexpr int W = int(sizeof(Word) * 8);
+    constexpr bool XO = std::is_same<R, Xo>::value;
     if constexpr (MODE == M_ZERO) {
         return Word(0);
     } else if constexpr (MODE == M_HALF) {
-        return Word(xo_next(s));  // xi_half: low w bits of one draw
+        return Word(rng_next(s));  // xi_half: low w bits of one draw
     } else if constexpr (MODE == M_DYADIC) {
-        Word acc = Word(xo_next(s));  // Horner over the digits of m, LSB first
+        Word acc = Word(rng_next(s));  // Horner over the digits of m, LSB first
         for (uint32_t i = 1; i < pd.k; ++i) {
-            const Word x = Word(xo_next(s));
+            const Word x = Word(rng_next(s));
             acc = ((pd.m >> i) & 1) ? Word(acc | x) : Word(acc & x);
         }
         return acc;
     } else if constexpr (MODE == M_ARB) {
         // xi_arbitrary: bit i = to_unit(draw_i) < r  <=>  draw_i < T (integer threshold)
-        const uint32_t lo = arb_half<Word>(s, pd);
-        if constexpr (W == 32) {
-            return Word(lo);
+        if constexpr (XO) {
+            const uint32_t lo = arb_half<Word>(s, pd);
+            if constexpr (W == 32) {
+                return Word(lo);
+            } else {
+                return Word(pack64(lo, arb_half<Word>(s, pd)));
+            }
         } else {
-            return Word(pack64(lo, arb_half<Word>(s, pd)));
+            Word acc = 0;
+#pragma unroll 4
+            for (int i = 0; i < W; ++i) acc |= Word(rng_next(s) < pd.T ? 1 : 0) << i;
+            return acc;
         }
     } else {  // M_ONE: every bit accepted, stream still advances w draws
+        if constexpr (XO) {
 #pragma unroll 8
-        for (int i = 0; i < W; ++i) xo_step(s);
+            for (int i = 0; i < W; ++i) xo_step(s);
+        } else {
+            s.x += uint64_t(W) * kGamma;
+        }
         return Word(~Word(0));
     }
 }
@@ -260,8 +307,8 @@ struct Plan {
     static constexpr bool live = !(p_const && q_const);  // any draw needs a live stream
 };
 
-template <int PM, int QM, typename Word>
-__device__ __forceinline__ void gen_xi(Xo& s, const ProbDev& p, const ProbDev& q, Word& xp, Word& xq) {
+template <int PM, int QM, typename Word, typename R>
+__device__ __forceinline__ void gen_xi(R& s, const ProbDev& p, const ProbDev& q, Word& xp, Word& xq) {
     if constexpr (Plan<PM, QM>::live) {
         xp = xi_word<PM, Word>(s, p);
         xq = (QM == M_ZERO) ? Word(0) : xi_word<QM, Word>(s, q);  // engine_vec.hpp:105,125

@@ -339,6 +339,7 @@ struct octgpu_engine {
     bool graphs = true;  // replay CUDA graphs for long step() calls (OCTGPU_GRAPH=0 disables)
     uint32_t prefetch = 0;  // TMA kernels: L2 prefetch distance in ring stages (OCTGPU_PREFETCH)
     long long p2p_timeout = kP2PTimeoutCycles;  // peer halo wait limit (OCTGPU_P2P_TIMEOUT_MS)
+    int rng_kind = OCTGPU_RNG_XOSHIRO;  // octgpu_set_rng
     uint64_t tile_shift = 0;  // != 0: random per-pass row origin of the block tiling (DTr-style, result-neutral)
     std::map<std::string, cudaGraphExec_t> graph_cache;
     int deep_S = 3;    // k_mcs_deep ring stages (OCTGPU_DEEP_S; S = 3 measured best, profiles/r1_deep_modes.json)
@@ -975,6 +976,29 @@ std::string graph_key(const octgpu_engine* e, const ProbDev& p, const ProbDev& q
 
 }  // namespace
 
+}  // extern "C"
+
+namespace {
+
+// n MCS with counter-based xi (octgpu_set_rng): two in-place sweeps per MCS (k_sweep_ctr, engine_vec.hpp:171-177
+// order: phase, then !phase), global sweep index sigma = 2 t + 0 / 1.
+int step_counter(octgpu_engine* e, const ProbDev& p, const ProbDev& q, uint64_t n_mcs) {
+    for (uint64_t i = 0; i < n_mcs; ++i) {
+        for (int h = 0; h < 2; ++h) {
+            CK(launch_sweep_ctr(e->w, e->planes[e->pcur], e->phase, e->geom(), p, q, e->master_seed, 2 * e->t + h,
+                                e->stream));
+            ++e->launches;
+            e->phase ^= 1;
+        }
+        ++e->t;
+    }
+    return refresh_ghosts(e);  // k_sweep_ctr works in place and does not maintain ghost rows
+}
+
+}  // namespace
+
+extern "C" {
+
 int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
     if (!e) return fail(OCTGPU_ERR_CONFIG, "null engine");
     if (e->stripe) return fail(OCTGPU_ERR_CONFIG, "octgpu_step is not available on a row stripe (use the octgpu_stripe_* calls)");
@@ -984,6 +1008,7 @@ int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
     if (n_mcs == 0) return OCTGPU_OK;
     rc = use_device(e);
     if (rc) return rc;
+    if (e->rng_kind == OCTGPU_RNG_COUNTER) return step_counter(e, p, q, n_mcs);
     const bool live = !(is_const(p) && is_const(q));
     const uint64_t D = draws(prm->p, e->w) + (q.mode != M_ZERO ? draws(prm->q, e->w) : 0);
     const uint64_t per_sweep = uint64_t(e->n) * D;
@@ -1070,6 +1095,9 @@ int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
 int octgpu_sweep(octgpu_engine* e, int parity, const octgpu_params* prm, void* mask_log) {
     if (!e) return fail(OCTGPU_ERR_CONFIG, "null engine");
     if (e->stripe) return fail(OCTGPU_ERR_CONFIG, "octgpu_sweep is not available on a row stripe (use the octgpu_stripe_* calls)");
+    if (e->rng_kind != OCTGPU_RNG_XOSHIRO)
+        return fail(OCTGPU_ERR_CONFIG, "single sweeps draw from the per-row xoshiro streams; the counter-based "
+                                       "rng steps whole MCS only (octgpu_step)");
     if (parity != e->phase)  // engine_vec.hpp:150-152
         return fail(OCTGPU_ERR_INVARIANT, "sweep parity " + std::to_string(parity) +
                                               " does not match field phase " + std::to_string(e->phase));
@@ -1111,6 +1139,18 @@ int octgpu_set_tile_shift(octgpu_engine* e, uint64_t seed) {
     e->tile_shift = seed;
     return OCTGPU_OK;
 }
+
+int octgpu_set_rng(octgpu_engine* e, int kind) {
+    if (!e) return fail(OCTGPU_ERR_CONFIG, "null engine");
+    if (kind != OCTGPU_RNG_XOSHIRO && kind != OCTGPU_RNG_COUNTER)
+        return fail(OCTGPU_ERR_CONFIG, "unknown rng kind " + std::to_string(kind));
+    if (kind == OCTGPU_RNG_COUNTER && e->stripe)
+        return fail(OCTGPU_ERR_CONFIG, "the counter-based rng is not available on a row stripe");
+    e->rng_kind = kind;
+    return OCTGPU_OK;
+}
+
+int octgpu_get_rng(const octgpu_engine* e) { return e ? e->rng_kind : -1; }
 
 uint64_t octgpu_t(const octgpu_engine* e) { return e ? e->t : 0; }
 int octgpu_phase(const octgpu_engine* e) { return e ? e->phase : 0; }

@@ -28,22 +28,19 @@ namespace octgpu {
 // -------------------------------------------------------------------------
 // Single sublattice sweep, in place (sublattice_sweep, engine_vec.hpp:145-168)
 
-template <typename Word, int PM, int QM, int PF>
-__global__ void __launch_bounds__(128) k_sweep(Word* __restrict__ planes, uint64_t* __restrict__ rng, int parity,
-                                               Geom g, ProbDev p, ProbDev q, Word* __restrict__ mask_log) {
+// One row y of the sweep; R is the row's xi source (Xo: the reference's
+// xoshiro stream; Ctr: the opt-in counter-based stream).
+template <typename Word, int PM, int QM, int PF, typename R>
+__device__ __forceinline__ void sweep_row(Word* __restrict__ planes, int parity, const Geom& g, const ProbDev& p,
+                                          const ProbDev& q, Word* __restrict__ mask_log, uint32_t y, R& s) {
     constexpr int W = int(sizeof(Word) * 8);
     const uint32_t Y = g.wrap, LD = g.Y, n = g.n;  // periodic lattice: Y rows, row stride LD
-    const uint32_t y = blockIdx.x * blockDim.x + threadIdx.x;
-    if (y >= Y) return;
     const size_t PS = g.plane_stride;
     Word* px = planes + size_t(0 + parity) * PS + y;                         // X(pi)[y]
     Word* py = planes + size_t(2 + parity) * PS + y;                         // Y(pi)[y]
     Word* qy = planes + size_t(2 + (parity ^ 1)) * PS + (y + 1 == Y ? 0 : y + 1);  // Y(!pi)[y+1]
     Word* xr = planes + size_t(0 + (parity ^ 1)) * PS + y;                   // X(!pi)[y]
     const bool shifted = ((uint32_t(parity) ^ y) & 1u) != 0;                  // engine_vec.hpp:59-61
-
-    Xo s{0, 0, 0, 0};
-    if constexpr (Plan<PM, QM>::live) s = load_state(rng, LD, y);
 
     const Word raw0 = xr[0];
     Word bA[PF], bB[PF], bC[PF], bR[PF];
@@ -93,7 +90,28 @@ __global__ void __launch_bounds__(128) k_sweep(Word* __restrict__ planes, uint64
     }
     if (shifted) new0 ^= carry;
     xr[0] = new0;
-    if constexpr (Plan<PM, QM>::live) store_state(rng, LD, y, s);
+}
+
+template <typename Word, int PM, int QM, int PF>
+__global__ void __launch_bounds__(128) k_sweep(Word* __restrict__ planes, uint64_t* __restrict__ rng, int parity,
+                                               Geom g, ProbDev p, ProbDev q, Word* __restrict__ mask_log) {
+    const uint32_t y = blockIdx.x * blockDim.x + threadIdx.x;
+    if (y >= g.wrap) return;
+    Xo s{0, 0, 0, 0};
+    if constexpr (Plan<PM, QM>::live) s = load_state(rng, g.Y, y);
+    sweep_row<Word, PM, QM, PF>(planes, parity, g, p, q, mask_log, y, s);
+    if constexpr (Plan<PM, QM>::live) store_state(rng, g.Y, y, s);
+}
+
+// The same sweep with counter-based xi (octgpu_set_rng; device_common.cuh Ctr):
+// row y's draws start from ctr_row(key, y), key = ctr_sweep_key(seed, sigma).
+template <typename Word, int PM, int QM, int PF>
+__global__ void __launch_bounds__(128) k_sweep_ctr(Word* __restrict__ planes, int parity, Geom g, ProbDev p,
+                                                   ProbDev q, uint64_t key) {
+    const uint32_t y = blockIdx.x * blockDim.x + threadIdx.x;
+    if (y >= g.wrap) return;
+    Ctr s = ctr_row(key, y);
+    sweep_row<Word, PM, QM, PF>(planes, parity, g, p, q, static_cast<Word*>(nullptr), y, s);
 }
 
 // -------------------------------------------------------------------------
@@ -339,6 +357,14 @@ cudaError_t sweep_pq(void* planes, uint64_t* rng, int parity, Geom g, const Prob
 }
 
 template <typename Word, int PM, int QM>
+cudaError_t sweep_ctr_pq(void* planes, int parity, Geom g, const ProbDev& p, const ProbDev& q, uint64_t key,
+                         cudaStream_t st) {
+    const uint32_t threads = 128, blocks = (g.wrap + threads - 1) / threads;
+    k_sweep_ctr<Word, PM, QM, kPF><<<blocks, threads, 0, st>>>(static_cast<Word*>(planes), parity, g, p, q, key);
+    return cudaGetLastError();
+}
+
+template <typename Word, int PM, int QM>
 cudaError_t mcs_pq(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
                    const ProbDev& q, const uint64_t* jtab, cudaStream_t st) {
     const uint32_t warps = (g.c1 - g.c0 + 29) / 30;
@@ -376,6 +402,16 @@ cudaError_t launch_sweep(int w, void* planes, uint64_t* rng, int parity, Geom g,
         OCT_PQ_CASES(sweep_pq, uint64_t, planes, rng, parity, g, p, q, mask_log, st)
     } else {
         OCT_PQ_CASES(sweep_pq, uint32_t, planes, rng, parity, g, p, q, mask_log, st)
+    }
+}
+
+cudaError_t launch_sweep_ctr(int w, void* planes, int parity, Geom g, const ProbDev& p, const ProbDev& q,
+                             uint64_t seed, uint64_t sigma, cudaStream_t st) {
+    const uint64_t key = ctr_sweep_key(seed, sigma);
+    if (w == 64) {
+        OCT_PQ_CASES(sweep_ctr_pq, uint64_t, planes, parity, g, p, q, key, st)
+    } else {
+        OCT_PQ_CASES(sweep_ctr_pq, uint32_t, planes, parity, g, p, q, key, st)
     }
 }
 

@@ -85,6 +85,9 @@ cudaError_t launch_refresh_ghosts(int w, void* planes, uint64_t* rng, Geom g, cu
 
 // One sublattice sweep in place (engine_vec.hpp:145-168), optional mask log in
 // reference row-major layout.
+// one in-place sweep with counter-based xi (sweep sigma of the run keyed by seed; octgpu_set_rng)
+cudaError_t launch_sweep_ctr(int w, void* planes, int parity, Geom g, const ProbDev& p, const ProbDev& q,
+                             uint64_t seed, uint64_t sigma, cudaStream_t st);
 cudaError_t launch_sweep(int w, void* planes, uint64_t* rng, int parity, Geom g, const ProbDev& p,
                          const ProbDev& q, bool rng_live, void* mask_log, cudaStream_t st);
 

@@ -182,6 +182,21 @@ class GpuEngine:
         """Random per-pass row origin of the kernels' block tiling (DTr-style); 0 = off. Result-neutral."""
         check(lib().octgpu_set_tile_shift(self._h, int(seed)))
 
+    RNG_KINDS = {"xoshiro": 0, "counter": 1}
+
+    def set_rng(self, kind: str) -> None:
+        """xi source of step(): "xoshiro" (default; the reference's per-row streams, bit-exact) or
+        "counter" (opt-in counter-based SplitMix64 streams keyed by (master seed, sweep, row); no
+        reference equivalent, pinned by the oracle's oo_step_ctr). See include/octgpu.h."""
+        if kind not in self.RNG_KINDS:
+            raise ValueError(f"rng kind must be one of {sorted(self.RNG_KINDS)}")
+        check(lib().octgpu_set_rng(self._h, self.RNG_KINDS[kind]))
+
+    @property
+    def rng(self) -> str:
+        k = int(lib().octgpu_get_rng(self._h))
+        return {v: n for n, v in self.RNG_KINDS.items()}[k]
+
     def set_stream(self, cuda_stream: int | None) -> None:
         check(lib().octgpu_set_stream(self._h, C.c_void_p(cuda_stream) if cuda_stream else None))
 

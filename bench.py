@@ -185,6 +185,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--from-flat", action="store_true", help="time MCS 1..K instead of the job's last K MCS")
+    ap.add_argument("--rng", default="xoshiro", choices=["xoshiro", "counter"],
+                    help="xi source: the reference's xoshiro streams, or the opt-in counter-based mode "
+                         "(not bit-compatible with the reference; single GPU)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     ws, rank, local = _dist()
@@ -196,9 +199,13 @@ def main():
         cfg["Y"] = cfg["Y"] * ws
         cfg["workload"] += f"; {ws} GPUs: {cfg['X']}x{cfg['Y']} lattice, one 2^16-row stripe per GPU"
 
+    if args.rng != "xoshiro" and (ws > 1 or args.impl == "reference"):
+        raise SystemExit("--rng counter: single GPU, our implementation only (the reference has no counter rng)")
     config_key = {"workload": cfg["workload"], "X": cfg["X"], "Y": cfg["Y"], "p": cfg["p"], "q": cfg["q"],
                   "w": 64, "seed": 1, "schedule": f"log_schedule({SCHEDULE_TMAX},{SCHEDULE_PPD}) within steps",
                   "l2": "planes (>=1 GiB) exceed L2 (126 MB); no flush needed", "parallelism": f"row stripes x{ws}" if ws > 1 else "single GPU"}
+    if args.rng != "xoshiro":
+        config_key["rng"] = "counter (opt-in SplitMix64 streams, octgpu_set_rng; not the reference's generator)"
 
     if args.impl == "reference":
         if rank != 0:
@@ -261,6 +268,8 @@ def main():
                 eng = octgpu.GpuEngine(octgpu.SlopeField(lat, planes, t, 0), octgpu.RngStreamSet(1, states),
                                        device=local)
             eng.set_stream(stream.cuda_stream)
+            if args.rng != "xoshiro":
+                eng.set_rng(args.rng)
             return eng, [eng]
         from paper_1606_00310_b200.stripes import (DistTransport, PeerDistTransport, StripeEngine, StripeGroup,
                                                    stripe_bounds)
@@ -347,7 +356,7 @@ def main():
     value = X * Y * K / (ms * 1e6)
     kernel_ms = step_ms / K  # per MCS, all launches of the step calls
     peak, peak_src = _peaks()
-    kname, mcs_per_launch = _mcs_kernel(prm, Y, X // 128, ws)
+    kname, mcs_per_launch = _mcs_kernel(prm, Y, X // 128, ws) if args.rng == "xoshiro" else ("k_sweep_ctr", 0.5)
     # paper identity: 1 byte of slope traffic per site update, per GPU, per launch
     alg_bytes = X * Y // ws * mcs_per_launch
     launch_ms = kernel_ms * mcs_per_launch

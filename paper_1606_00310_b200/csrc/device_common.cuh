@@ -362,6 +362,14 @@ __device__ __forceinline__ void xi_word_pair(Xo& a, Xo& b, const ProbDev& pd, Wo
     }
 }
 
+// counter-based streams: two independent draw chains as they are (no state to interleave)
+template <int PM, int QM, typename Word>
+__device__ __forceinline__ void gen_xi_pair(Ctr& a, Ctr& b, const ProbDev& p, const ProbDev& q, Word& ap, Word& aq,
+                                            Word& bp, Word& bq) {
+    gen_xi<PM, QM, Word>(a, p, q, ap, aq);
+    gen_xi<PM, QM, Word>(b, p, q, bp, bq);
+}
+
 template <int PM, int QM, typename Word>
 __device__ __forceinline__ void gen_xi_pair(Xo& a, Xo& b, const ProbDev& p, const ProbDev& q, Word& ap, Word& aq,
                                             Word& bp, Word& bq) {

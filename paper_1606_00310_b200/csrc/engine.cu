@@ -980,9 +980,25 @@ std::string graph_key(const octgpu_engine* e, const ProbDev& p, const ProbDev& q
 
 namespace {
 
-// n MCS with counter-based xi (octgpu_set_rng): two in-place sweeps per MCS (k_sweep_ctr, engine_vec.hpp:171-177
-// order: phase, then !phase), global sweep index sigma = 2 t + 0 / 1.
+// n MCS with counter-based xi (octgpu_set_rng), sweeps in the engine_vec.hpp:171-177 order (phase, then !phase),
+// global sweep index sigma = 2 t + 0 / 1: the fused TMA kernel (k_mcs_bulk<CTR>, 1 MCS per pass) where the
+// lattice takes it, else two in-place k_sweep_ctr sweeps per MCS.
 int step_counter(octgpu_engine* e, const ProbDev& p, const ProbDev& q, uint64_t n_mcs) {
+    if (e->mcs_impl == 2) {
+        int rc = plan_bulk(e, p, q);
+        if (rc) return rc;
+    }
+    if (e->mcs_impl == 2 && e->bulk_ks == 2) {
+        for (uint64_t i = 0; i < n_mcs; ++i) {
+            const int ps = e->pcur;
+            CK(launch_mcs_bulk_ctr(e->planes[ps], e->planes[ps ^ 1], e->phase, shifted(e, e->geom(), kTmaBoxRows), p,
+                                   q, e->master_seed, 2 * e->t, e->bulk_S, &e->tm[ps][0], &e->tm[ps][1], e->stream));
+            ++e->launches;
+            e->pcur ^= 1;
+            ++e->t;
+        }
+        return OCTGPU_OK;
+    }
     for (uint64_t i = 0; i < n_mcs; ++i) {
         for (int h = 0; h < 2; ++h) {
             CK(launch_sweep_ctr(e->w, e->planes[e->pcur], e->phase, e->geom(), p, q, e->master_seed, 2 * e->t + h,

@@ -119,14 +119,17 @@ size_t mcs_bulk_stage_bytes(int ks) {
     return ks == 4 ? StageLayout<4>::kBytes : ks == 2 ? StageLayout<2>::kBytes : StageLayout<1>::kBytes;
 }
 
-template <int PM, int QM, int KS>
+// CTR: xi from the opt-in counter-based streams (octgpu_set_rng): sweep keys ck1 / ck2, no stream state
+// loaded or stored.
+template <int PM, int QM, int KS, bool CTR>
 __global__ void __launch_bounds__(32 * (kP + 1), kP >= 8 ? 2 : 4) k_mcs_bulk(const uint64_t* __restrict__ src,
                                                             uint64_t* __restrict__ dst,
                                                             const uint64_t* __restrict__ rs,
                                                             uint64_t* __restrict__ rd, int f, Geom g, ProbDev p,
                                                             ProbDev q, const uint64_t* __restrict__ jtab, int S,
                                                             const __grid_constant__ CUtensorMap tmK,
-                                                            const __grid_constant__ CUtensorMap tmK1) {
+                                                            const __grid_constant__ CUtensorMap tmK1,
+                                                            uint64_t ck1, uint64_t ck2) {
     using Word = uint64_t;
     using LY = StageLayout<KS>;
     constexpr bool LIVE = Plan<PM, QM>::live;
@@ -206,8 +209,12 @@ __global__ void __launch_bounds__(32 * (kP + 1), kP >= 8 ? 2 : 4) k_mcs_bulk(con
     const bool ghostw = g.ghost && (r0 + 1 < g.ghost || r0 + 31 >= g.wrap);  // warp-uniform
     const bool ghost_row = ghostw && y < g.ghost;
 
-    Xo st1{0, 0, 0, 0}, st2{0, 0, 0, 0};  // first / second sweep streams
-    if constexpr (LIVE) {
+    using Src = typename std::conditional<CTR, Ctr, Xo>::type;
+    Src st1{}, st2{};  // first / second sweep streams
+    if constexpr (CTR) {
+        st1 = ctr_row(ck1, y);
+        st2 = ctr_row(ck2, y);
+    } else if constexpr (LIVE) {
         st1 = load_state(rs, Y, y);
         st2 = apply_table(jtab, st1);
     }
@@ -348,7 +355,7 @@ __global__ void __launch_bounds__(32 * (kP + 1), kP >= 8 ? 2 : 4) k_mcs_bulk(con
         put(dXf, A0 ^ carry_sel(m2, m2last, sf2), core);
         put(dXf + Y, xf1 ^ carry_sel(0, m2, sf2), core);
     }
-    if constexpr (LIVE) {
+    if constexpr (LIVE && !CTR) {
         // a row stripe also advances the streams of the halo rows next to its core rows
         // (the peer-memory halo exchange pulls neighbour states only once, p2p.cu)
         const bool halo_state = g.wrap == 0 && (v + 1 == g.c0 || v == g.c1);
@@ -359,18 +366,18 @@ __global__ void __launch_bounds__(32 * (kP + 1), kP >= 8 ? 2 : 4) k_mcs_bulk(con
 
 namespace {
 
-template <int PM, int QM, int KS>
+template <int PM, int QM, int KS, bool CTR = false>
 cudaError_t bulk_go(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
                     const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK, const CUtensorMap* tmK1,
-                    cudaStream_t st) {
+                    cudaStream_t st, uint64_t ck1 = 0, uint64_t ck2 = 0) {
     const uint32_t warps = (g.c1 - g.c0 + 29) / 30;
     const uint32_t threads = 32 * (kP + 1), blocks = (warps + kP - 1) / kP;
     const size_t smem = mcs_bulk_smem(KS, S);
-    auto kern = k_mcs_bulk<PM, QM, KS>;
+    auto kern = k_mcs_bulk<PM, QM, KS, CTR>;
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     kern<<<blocks, threads, smem, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), rs, rd, f, g,
-                                        p, q, jtab, S, *tmK, *tmK1);
+                                        p, q, jtab, S, *tmK, *tmK1, ck1, ck2);
     return cudaGetLastError();
 }
 
@@ -409,6 +416,31 @@ cudaError_t launch_mcs_bulk(const void* src, void* dst, const uint64_t* rs, uint
     case M_DYADIC: OCT_BQ(M_DYADIC)
     case M_ARB: OCT_BQ(M_ARB)
     case M_ONE: OCT_BQ(M_ONE)
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+// counter-based streams: KS = 2 only (the engine's plan)
+#define OCT_BQC(PM)                                                                                       \
+    switch (q.mode) {                                                                                     \
+    case M_ZERO: return bulk_go<PM, M_ZERO, 2, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, k1, k2);     \
+    case M_HALF: return bulk_go<PM, M_HALF, 2, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, k1, k2);     \
+    case M_DYADIC: return bulk_go<PM, M_DYADIC, 2, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, k1, k2); \
+    case M_ARB: return bulk_go<PM, M_ARB, 2, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, k1, k2);       \
+    case M_ONE: return bulk_go<PM, M_ONE, 2, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, k1, k2);       \
+    default: return cudaErrorInvalidValue;                                                                \
+    }
+
+cudaError_t launch_mcs_bulk_ctr(const void* src, void* dst, int f, Geom g, const ProbDev& p, const ProbDev& q,
+                                uint64_t seed, uint64_t sigma, int S, const CUtensorMap* tmK, const CUtensorMap* tmK1,
+                                cudaStream_t st) {
+    const uint64_t k1 = ctr_sweep_key(seed, sigma), k2 = ctr_sweep_key(seed, sigma + 1);
+    switch (p.mode) {
+    case M_ZERO: OCT_BQC(M_ZERO)
+    case M_HALF: OCT_BQC(M_HALF)
+    case M_DYADIC: OCT_BQC(M_DYADIC)
+    case M_ARB: OCT_BQC(M_ARB)
+    case M_ONE: OCT_BQC(M_ONE)
     default: return cudaErrorInvalidValue;
     }
 }

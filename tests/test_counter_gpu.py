@@ -86,3 +86,21 @@ def test_counter_measure_consistent():
     h = eng.heights().h.astype(np.int64)
     assert [int(v) for v in rec.power_sums[:2]] == [int(h.sum()), int((h * h).sum())]
     assert rec.W2 > 0.5
+
+
+@pytest.mark.parametrize("pq", [(0.5, 0.0), (0.5, 0.5), (0.98, 0.02)])
+def test_fused_counter_kernel_matches_sweeps(monkeypatch, pq):
+    """At sizes the oracle cannot reach: the fused TMA pass (k_mcs_bulk<CTR>) equals two in-place
+    k_sweep_ctr sweeps per MCS (OCTGPU_MCS_IMPL=1), bit for bit."""
+    X = Y = 4096
+    prm = octgpu.UpdateParams.make(*pq)
+    mcs = 3 if pq[0] == 0.98 else 20
+    fused = octgpu.GpuEngine(octgpu.LatticeConfig(X, Y), 11)
+    fused.set_rng("counter")
+    fused.step(prm, mcs)
+    monkeypatch.setenv("OCTGPU_MCS_IMPL", "1")
+    plain = octgpu.GpuEngine(octgpu.LatticeConfig(X, Y), 11)
+    plain.set_rng("counter")
+    plain.step(prm, mcs)
+    assert fused.checksum() == plain.checksum()
+    assert np.array_equal(fused.planes(), plain.planes())

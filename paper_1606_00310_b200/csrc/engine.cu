@@ -708,13 +708,12 @@ int load_planes(octgpu_engine* e, const void* planes) {
     const size_t wb = e->word_bytes(), row_bytes = size_t(e->n) * wb;
     if (!e->stripe) {
         CK(cudaMemcpyAsync(stage, planes, e->host_bytes(), cudaMemcpyHostToDevice, e->stream));
-    } else {
-        std::vector<unsigned char> pad(e->host_bytes(), 0);
+    } else {  // core rows of each plane into their place in the staged layout; halo and padding rows zero
+        CK(cudaMemsetAsync(stage, 0, e->host_bytes(), e->stream));
         for (int p = 0; p < 4; ++p)
-            std::memcpy(pad.data() + (size_t(p) * e->Y + kStripeHA) * row_bytes,
-                        static_cast<const unsigned char*>(planes) + size_t(p) * e->L * row_bytes, e->L * row_bytes);
-        CK(cudaMemcpyAsync(stage, pad.data(), e->host_bytes(), cudaMemcpyHostToDevice, e->stream));
-        CK(cudaStreamSynchronize(e->stream));
+            CK(cudaMemcpyAsync(static_cast<unsigned char*>(stage) + (size_t(p) * e->Y + kStripeHA) * row_bytes,
+                               static_cast<const unsigned char*>(planes) + size_t(p) * e->L * row_bytes,
+                               e->L * row_bytes, cudaMemcpyHostToDevice, e->stream));
     }
     if (getenv("OCTGPU_TRACE_CREATE")) {
         CK(cudaStreamSynchronize(e->stream));
@@ -1186,13 +1185,14 @@ int octgpu_get_planes(octgpu_engine* e, void* out) {
         CK(cudaStreamSynchronize(e->stream));
         return OCTGPU_OK;
     }
-    std::vector<unsigned char> pad(e->host_bytes());
-    CK(cudaMemcpyAsync(pad.data(), stage, e->host_bytes(), cudaMemcpyDeviceToHost, e->stream));
-    CK(cudaStreamSynchronize(e->stream));
+    // a stripe's core rows of each plane are contiguous in the staged reference layout: one copy per plane
+    // straight into the caller's buffer (pinned buffers take the DMA path at full PCIe rate)
     const size_t row_bytes = size_t(e->n) * e->word_bytes();
     for (int p = 0; p < 4; ++p)
-        std::memcpy(static_cast<unsigned char*>(out) + size_t(p) * e->L * row_bytes,
-                    pad.data() + (size_t(p) * e->Y + kStripeHA) * row_bytes, e->L * row_bytes);
+        CK(cudaMemcpyAsync(static_cast<unsigned char*>(out) + size_t(p) * e->L * row_bytes,
+                           static_cast<const unsigned char*>(stage) + (size_t(p) * e->Y + kStripeHA) * row_bytes,
+                           e->L * row_bytes, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
     return OCTGPU_OK;
 }
 

@@ -132,9 +132,13 @@ def _mcs_kernel(prm, Y: int, n: int, ws: int) -> tuple[str, int]:
     otherwise k_mcs_bulk, 1 MCS per pass)."""
     from paper_1606_00310_b200.params import ProbMode
 
-    const = all(ps.mode == ProbMode.Zero or (ps.mode == ProbMode.Arbitrary and ps.value == 1.0)
-                for ps in (prm.p, prm.q))
+    one = [ps.mode == ProbMode.Arbitrary and ps.value == 1.0 for ps in (prm.p, prm.q)]
+    const = all(ps.mode == ProbMode.Zero or o for ps, o in zip((prm.p, prm.q), one))
     deep_env = os.environ.get("OCTGPU_DEEP", "1")
+    # mcs_deep_supported (mcs_deep.cu): zero / half / dyadic / r = 1 modes, r = 1 only next to constant xi
+    cheap = all(ps.mode in (ProbMode.Zero, ProbMode.Half, ProbMode.Dyadic) or o for ps, o in zip((prm.p, prm.q), one))
+    if deep_env == "2" and n >= 8 and (ws > 1 or Y >= 256) and cheap and (const or (ws == 1 and not any(one))):
+        return "k_mcs_deep", 2  # forced (tests / experiments)
     sites = 128 * n * Y // ws  # per engine (stripe)
     big = deep_env == "2" or sites >= 1 << 28
     if const and n >= 8 and (ws > 1 or Y >= 256) and deep_env != "0" and big:

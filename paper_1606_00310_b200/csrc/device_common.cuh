@@ -1,5 +1,6 @@
-// Device helpers shared by the sm_100a kernels: xoshiro256++, xi words,
-// the Kawasaki mask. Included by kernels.cu and mcs_bulk.cu only.
+// Device helpers shared by the sm_100a kernels: xoshiro256++ and the opt-in
+// counter-based streams, xi words, the Kawasaki mask. Included by kernels.cu,
+// mcs_bulk.cu and mcs_deep.cu.
 #pragma once
 #include <cstdint>
 #include <type_traits>

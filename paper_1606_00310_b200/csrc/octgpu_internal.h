@@ -59,7 +59,10 @@ constexpr uint32_t kTmaBoxRows = 30 * kMcsConsumerWarps + 4;  // k_mcs_bulk wind
 #endif
 constexpr int kDeepSweeps = OCTGPU_DEEP_SWEEPS;  // sweeps per k_mcs_deep pass (even)
 constexpr int kDeepWarps = OCTGPU_DEEP_WARPS;
-constexpr int kDeepMinBlocks = kDeepWarps >= 8 ? 2 : 3;  // resident blocks per SM the register budget targets
+#ifndef OCTGPU_DEEP_MINB
+#define OCTGPU_DEEP_MINB (OCTGPU_DEEP_WARPS >= 8 ? 2 : 3)
+#endif
+constexpr int kDeepMinBlocks = OCTGPU_DEEP_MINB;  // resident blocks per SM the register budget targets
 constexpr int deep_box_rows(int L) { return ((34 - 2 * L) * (kDeepWarps - 1) + 34) / 2 * 2; }
 
 constexpr int kGraphPasses = 16;  // passes per CUDA graph replayed by octgpu_step (even)
@@ -71,7 +74,9 @@ constexpr uint32_t kStripeHA = uint32_t(kDeepSweeps) - 1;
 constexpr uint32_t kStripeHB = uint32_t(kDeepSweeps);
 
 // periodic lattices keep this many ghost rows (>= every TMA window) so windows never wrap
-constexpr uint32_t kGhostRows = deep_box_rows(kDeepSweeps) <= 192 ? 192 : 256;
+constexpr uint32_t kGhostRows = deep_box_rows(kDeepSweeps) <= 192   ? 192
+                                : deep_box_rows(kDeepSweeps) <= 256 ? 256
+                                                                    : (uint32_t(deep_box_rows(kDeepSweeps)) + 63) / 64 * 64;
 static_assert(kTmaBoxRows <= kGhostRows && uint32_t(deep_box_rows(kDeepSweeps)) <= kGhostRows, "ghost rows");
 
 // Per-row RNG states are stored SoA: s[j * Y + y], j = 0..3.

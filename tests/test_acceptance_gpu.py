@@ -29,11 +29,12 @@ def _linfit(xs, ys):
     return slope, icpt, r2
 
 
-def _mean_w2(L, p, q, seeds, t_max=2000):
+def _mean_w2(L, p, q, seeds, t_max=2000, rng="xoshiro"):
     sched = octgpu.log_schedule(t_max, 8)
     acc = np.zeros(len(sched))
     for s in seeds:
         eng = octgpu.GpuEngine(octgpu.LatticeConfig(L, L), s)
+        eng.set_rng(rng)
         recs = run(eng, octgpu.UpdateParams.make(p, q), sched)
         acc += np.array([r.W2 for r in recs])
     return np.array(sched), acc / len(seeds)
@@ -48,15 +49,19 @@ def test_invariants_after_1e4_mcs(seed):
     assert sum(rec.power_sums[:1]) == round(rec.mean_h * 512 * 512)
 
 
-def test_kpz_growth_exponent():
-    t, w2 = _mean_w2(1024, 0.5, 0.0, range(1, 11))
+@pytest.mark.parametrize("rng", ["xoshiro", "counter"])
+def test_kpz_growth_exponent(rng):
+    """Criterion 3; with rng="counter" it is the statistical validation of the opt-in counter-based
+    streams (they have no reference to be bit-compared with)."""
+    t, w2 = _mean_w2(1024, 0.5, 0.0, range(1, 11), rng=rng)
     sel = (t >= 50) & (t <= 2000)
     beta, _, _ = _linfit(np.log(t[sel]), 0.5 * np.log(w2[sel]))
     assert abs(beta - 0.24) <= 0.03, beta
 
 
-def test_ew_logarithmic_growth():
-    t, w2 = _mean_w2(1024, 0.5, 0.5, range(1, 11))
+@pytest.mark.parametrize("rng", ["xoshiro", "counter"])
+def test_ew_logarithmic_growth(rng):
+    t, w2 = _mean_w2(1024, 0.5, 0.5, range(1, 11), rng=rng)
     sel = (t >= 50) & (t <= 2000)
     _, _, r2 = _linfit(np.log(t[sel]), w2[sel])
     beta, _, _ = _linfit(np.log(t[sel]), 0.5 * np.log(w2[sel]))

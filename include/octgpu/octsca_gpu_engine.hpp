@@ -86,6 +86,11 @@ class GpuEngine {
 
     uint64_t t() const { return octgpu_t(h_); }
 
+    // opt-in extras outside the reference's behaviour (include/octgpu.h): counter-based xi streams
+    // (OCTGPU_RNG_COUNTER; results differ from VecEngine by design) and random tile origins (result-neutral)
+    void set_rng(int kind) { gpu_detail::check(octgpu_set_rng(h_, kind)); }
+    void set_tile_shift(uint64_t seed) { gpu_detail::check(octgpu_set_tile_shift(h_, seed)); }
+
     const SlopeField<Word>& field() const {
         pull();
         return mirror_;

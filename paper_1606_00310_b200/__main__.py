@@ -42,6 +42,8 @@ def _common(ap):
     ap.add_argument("--workers", type=int, default=int(_env("workers", 1)))
     ap.add_argument("--engine", default=_env("engine", "gpu"))
     ap.add_argument("--device", type=int, default=int(_env("device", 0)))
+    ap.add_argument("--rng", default=_env("rng", "xoshiro"), choices=["xoshiro", "counter"],
+                    help="xi source: the reference's xoshiro256++ streams, or opt-in counter-based streams")
 
 
 def _dims(a):
@@ -56,7 +58,7 @@ def cmd_run(a) -> int:
     X, Y = _dims(a)
     cfg = RunConfig(X=X, Y=Y, w=a.w, p=a.p, q=a.q, pmode=_mode(a.pmode), qmode=_mode(a.qmode), seed=a.seed,
                     workers=a.workers, t_max=a.tmax, ppd=a.ppd, engine=a.engine, out_dir=a.out, resume=a.resume,
-                    moments=a.moments, device=a.device,
+                    moments=a.moments, device=a.device, rng=a.rng,
                     fit_window=(a.fit_tmin, a.fit_tmax) if a.fit_tmin is not None else None)
     res = run_session(cfg)
     print(json.dumps({"records": len(res.records), "csv": res.csv_path, "snapshot": res.snapshot_path,
@@ -72,6 +74,7 @@ def cmd_bench(a) -> int:
     X, Y = _dims(a)
     prm = UpdateParams.make(a.p, a.q, _mode(a.pmode), _mode(a.qmode))
     eng = GpuEngine(LatticeConfig(X, Y, a.w), a.seed, device=a.device)
+    eng.set_rng(a.rng)
     warm = max(1, a.mcs // 10)  # first 10% discarded
     eng.step(prm, warm)
     eng.sync()
@@ -80,7 +83,8 @@ def cmd_bench(a) -> int:
     eng.sync()
     wall = time.perf_counter() - t0
     ups = X * Y * a.mcs / (wall * 1e9)
-    row = {"engine": "gpu", "L": X if X == Y else f"{X}x{Y}", "p": a.p, "q": a.q,
+    row = {"engine": "gpu" if a.rng == "xoshiro" else "gpu-counter-rng", "L": X if X == Y else f"{X}x{Y}",
+           "p": a.p, "q": a.q,
            "mode": f"{prm.p.mode.label}/{prm.q.mode.label}", "workers": a.workers, "mcs": a.mcs,
            "updates_per_ns": ups, "net_GBps": ups * 1.0, "wall_s": wall}
     if a.csv:

@@ -48,6 +48,7 @@ class RunConfig:
     fit_window: tuple | None = None
     moments: str = "auto"  # "reference" | "exact" | "auto"
     device: int = 0
+    rng: str = "xoshiro"  # "xoshiro" (the reference's streams) | "counter" (opt-in, GpuEngine.set_rng)
 
     def update_params(self) -> UpdateParams:
         return UpdateParams.make(self.p, self.q, self.pmode, self.qmode)
@@ -171,6 +172,7 @@ def run_session(cfg: RunConfig) -> SessionResult:
         eng = GpuEngine(f, streams, device=cfg.device)
     else:
         eng = GpuEngine(cfg.lattice(), cfg.seed, device=cfg.device)
+    eng.set_rng(cfg.rng)
     records = []
     for target in schedule:  # run.hpp:18-38
         if target < eng.t:
@@ -193,7 +195,10 @@ def run_session(cfg: RunConfig) -> SessionResult:
         "params": {"p": cfg.p, "pmode": prm.p.mode.label, "p_words": prm.p.draws_per_word(cfg.w),
                    "q": cfg.q, "qmode": prm.q.mode.label, "q_words": prm.q.draws_per_word(cfg.w)},
         "schedule": {"t_max": cfg.t_max, "points_per_decade": cfg.ppd, "times": schedule},
-        "rng": {"generator": "xoshiro256++", "streams": cfg.Y, "assignment": "one stream per lattice row"},
+        "rng": ({"generator": "xoshiro256++", "streams": cfg.Y, "assignment": "one stream per lattice row"}
+                if cfg.rng == "xoshiro" else
+                {"generator": "splitmix64-counter", "streams": cfg.Y,
+                 "assignment": "one counter stream per (sweep, row), keyed by the seed (opt-in, not the reference's)"}),
         "resume": cfg.resume,
         "outputs": {"measurements": res.csv_path, "snapshot": res.snapshot_path},
         "moments": moments,

@@ -120,3 +120,23 @@ def test_cli_run_matches_reference_session(goldens, tmp_path, capsys):
     assert rc == 0
     assert open(tmp_path / "measurements.csv").read() == s["csv"]
     assert main(["bench", "--size", "4096", "--p", "0.5", "--mcs", "20"]) == 0
+
+
+@pytest.mark.gpu
+def test_counter_rng_session_resume(tmp_path):
+    """Opt-in counter rng through the session driver and CLI: a resumed run continues bit-exactly
+    (the counter streams depend only on (seed, t, row)) and the metadata names the generator."""
+    import json
+
+    from paper_1606_00310_b200.__main__ import main
+    kw = dict(X=512, Y=256, p=0.5, q=0.0, seed=3, ppd=4, rng="counter")
+    whole = run_session(RunConfig(t_max=200, out_dir=str(tmp_path / "whole"), **kw))
+    run_session(RunConfig(t_max=60, out_dir=str(tmp_path / "a"), **kw))
+    resumed = run_session(RunConfig(t_max=200, out_dir=str(tmp_path / "b"), resume=str(tmp_path / "a" / "final.snap"),
+                                    **kw))
+    assert open(whole.snapshot_path, "rb").read() == open(resumed.snapshot_path, "rb").read()
+    meta = json.load(open(whole.metadata_path))
+    assert meta["rng"]["generator"] == "splitmix64-counter"
+    xo = run_session(RunConfig(t_max=200, out_dir=str(tmp_path / "xo"), **{**kw, "rng": "xoshiro"}))
+    assert open(xo.snapshot_path, "rb").read() != open(whole.snapshot_path, "rb").read()
+    assert main(["bench", "--size", "4096", "--p", "0.5", "--mcs", "20", "--rng", "counter"]) == 0

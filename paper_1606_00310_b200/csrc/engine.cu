@@ -975,8 +975,6 @@ std::string graph_key(const octgpu_engine* e, const ProbDev& p, const ProbDev& q
 
 }  // namespace
 
-}  // extern "C"
-
 namespace {
 
 // n MCS with counter-based xi (octgpu_set_rng), sweeps in the engine_vec.hpp:171-177 order (phase, then !phase),
@@ -1011,8 +1009,6 @@ int step_counter(octgpu_engine* e, const ProbDev& p, const ProbDev& q, uint64_t 
 }
 
 }  // namespace
-
-extern "C" {
 
 int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
     if (!e) return fail(OCTGPU_ERR_CONFIG, "null engine");

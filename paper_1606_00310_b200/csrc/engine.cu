@@ -903,12 +903,12 @@ namespace {
 
 // k_mcs_deep ring depth: deep_S (3) unless two blocks per SM would no longer fit
 // in shared memory (live passes park xoshiro states and pre-drawn xi there) -> 2.
-int deep_ring(octgpu_engine* e, const ProbDev& p, const ProbDev& q) {
+int deep_ring(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool ctr = false) {
     int smem_sm = 0;
     if (cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, e->device) != cudaSuccess)
         return 2;
     int S = e->deep_S;
-    while (S > 2 && 2 * (mcs_deep_smem(p.mode, q.mode, kDeepSweeps, S) + 1024) > size_t(smem_sm)) --S;
+    while (S > 2 && 2 * (mcs_deep_smem(p.mode, q.mode, kDeepSweeps, S, ctr) + 1024) > size_t(smem_sm)) --S;
     return S;
 }
 
@@ -984,6 +984,26 @@ int step_counter(octgpu_engine* e, const ProbDev& p, const ProbDev& q, uint64_t 
     if (e->mcs_impl == 2) {
         int rc = plan_bulk(e, p, q);
         if (rc) return rc;
+    }
+    // 2-MCS passes (k_mcs_deep<CTR>): no stream state to park, so every cheap mode qualifies; same size
+    // threshold as the constant-xi xoshiro passes
+    const bool deep = e->mcs_impl == 2 && mcs_deep_supported(p.mode, q.mode) &&
+                      (e->deep == 2 || (e->deep == 1 && uint64_t(e->X) * e->L >= (uint64_t(1) << 28)));
+    if (deep) {
+        int rc = ensure_tmaps_deep(e);
+        if (rc) return rc;
+        const uint64_t mpp = kDeepSweeps / 2;
+        while (n_mcs >= mpp) {
+            const int ps = e->pcur;
+            CK(launch_mcs_deep_ctr(e->planes[ps], e->planes[ps ^ 1], e->phase,
+                                   shifted(e, e->deep_geom(), uint32_t(deep_box_rows(kDeepSweeps))), p, q,
+                                   e->master_seed, 2 * e->t, deep_ring(e, p, q, true), &e->tmd[ps][0], &e->tmd[ps][1],
+                                   e->stream));
+            ++e->launches;
+            e->pcur ^= 1;
+            e->t += mpp;
+            n_mcs -= mpp;
+        }
     }
     if (e->mcs_impl == 2 && e->bulk_ks == 2) {
         for (uint64_t i = 0; i < n_mcs; ++i) {

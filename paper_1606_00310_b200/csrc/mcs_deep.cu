@@ -76,7 +76,7 @@ struct DeepStage {  // ring stage: Xf[KS][W] | Yf[KS][W] | Ys[KS][W] | Xs[KS+1][
 };
 
 // Per-lane parking slots in shared memory ([slot][kLanes] u64).
-template <int L, int PM, int QM>
+template <int L, int PM, int QM, bool CTR = false>
 struct DeepSlots {
     static constexpr bool kPreP = !(PM == M_ZERO || PM == M_ONE);
     static constexpr bool kPreQ = !(QM == M_ZERO || QM == M_ONE);
@@ -88,7 +88,8 @@ struct DeepSlots {
     __host__ __device__ static constexpr int preQ0() { return save() + (kPreP ? npre() : 0); }
     // streams kRegStreams..L-1 (0-based) of a live pass are parked in shared memory (4 slots each)
     static constexpr bool kLive = kPreP || kPreQ || !(PM == M_ZERO || PM == M_ONE) || !(QM == M_ZERO || QM == M_ONE);
-    __host__ __device__ static constexpr int parked() { return kLive && L > kRegStreams ? L - kRegStreams : 0; }
+    // (counter-based streams are one word each: all of them stay in registers)
+    __host__ __device__ static constexpr int parked() { return !CTR && kLive && L > kRegStreams ? L - kRegStreams : 0; }
     __host__ __device__ static constexpr int st0() { return preQ0() + (kPreQ ? npre() : 0); }
     __host__ __device__ static constexpr int count() { return st0() + 4 * parked(); }
     __host__ __device__ static constexpr int pre(int l, int j) { return (l - 1) * (l - 2) / 2 + j; }
@@ -171,11 +172,11 @@ struct DeepCtx {
     uint64_t* save;  // this lane's parking slots: save[slot * kLanes]
 };
 
-template <int L>
+template <int L, typename Src = Xo>
 struct DeepState {
     uint64_t pA[L], pB[L], pC[L], pR[L];  // each sweep's outputs at its previous word
     uint32_t ml[L];                       // high word of each sweep's mask at its previous word (x carry)
-    Xo rs[L];                             // stream of each sweep
+    Src rs[L];                            // stream of each sweep (xoshiro, or the opt-in counter stream)
     uint64_t cur, raw0;                   // sweep 1: original X(s)[y][j], X(s)[y][0]
 };
 
@@ -191,11 +192,12 @@ __device__ __forceinline__ void put(const DeepCtx& c, uint64_t* ptr, uint64_t va
 
 // One iteration i: sweep l on word (i-(l-1)) mod n for every active l.
 // STEADY: all sweeps active, no first/second/last words, no wrap (i in [2L, n-1]).
-template <int PM, int QM, int L, bool STEADY, int GH>
-__device__ __forceinline__ void deep_iter(DeepState<L>& S, const DeepCtx& c, uint32_t i, const uint64_t* sb, int jj,
+template <int PM, int QM, int L, bool STEADY, int GH, bool CTR = false>
+__device__ __forceinline__ void deep_iter(DeepState<L, typename std::conditional<CTR, Ctr, Xo>::type>& S,
+                                          const DeepCtx& c, uint32_t i, const uint64_t* sb, int jj,
                                           const ProbDev& p, const ProbDev& q) {
     using ST = DeepStage<L>;
-    using SL = DeepSlots<L, PM, QM>;
+    using SL = DeepSlots<L, PM, QM, CTR>;
     const uint32_t n = c.n;
     uint64_t nA[L] = {}, nB[L] = {}, nC[L] = {}, nR[L] = {};
     bool act[L];
@@ -217,11 +219,15 @@ __device__ __forceinline__ void deep_iter(DeepState<L>& S, const DeepCtx& c, uin
         // ---- xi of word j of stream l (stream order: pre-drawn words 0..l-2 come first) ----
         uint64_t xp, xq;
         if (STEADY || l == 1 || j >= uint32_t(l - 1)) {
-            if (SL::parked() > 0 && li >= kRegStreams) {  // li is a constant after unrolling
-                const int sl = SL::st0() + 4 * (li - kRegStreams);
-                Xo st = slot_state(c.save, sl);
-                gen_xi<PM, QM, uint64_t>(st, p, q, xp, xq);
-                slot_store(c.save, sl, st);
+            if constexpr (SL::parked() > 0) {
+                if (li >= kRegStreams) {  // li is a constant after unrolling
+                    const int sl = SL::st0() + 4 * (li - kRegStreams);
+                    Xo st = slot_state(c.save, sl);
+                    gen_xi<PM, QM, uint64_t>(st, p, q, xp, xq);
+                    slot_store(c.save, sl, st);
+                } else {
+                    gen_xi<PM, QM, uint64_t>(S.rs[li], p, q, xp, xq);
+                }
             } else {
                 gen_xi<PM, QM, uint64_t>(S.rs[li], p, q, xp, xq);
             }
@@ -324,15 +330,19 @@ __device__ __forceinline__ void deep_iter(DeepState<L>& S, const DeepCtx& c, uin
 
 }  // namespace
 
-template <int PM, int QM, int L>
+// CTR: xi from the opt-in counter-based streams (octgpu_set_rng): sweep l of the pass is global sweep
+// sigma0 + l - 1 of seed's streams; no stream state is loaded, parked or stored.
+template <int PM, int QM, int L, bool CTR>
 __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
     k_mcs_deep(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, const uint64_t* __restrict__ rs,
                uint64_t* __restrict__ rd, int f, Geom g, ProbDev p, ProbDev q, const uint64_t* __restrict__ jtab, int S,
-               const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmK1) {
+               const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmK1, uint64_t ctr_seed,
+               uint64_t sigma0) {
     static_assert(L % 2 == 0 && L >= 2, "whole MCS only");
     using GEO = DeepGeo<L>;
     using ST = DeepStage<L>;
-    using SL = DeepSlots<L, PM, QM>;
+    using SL = DeepSlots<L, PM, QM, CTR>;
+    using Src = typename std::conditional<CTR, Ctr, Xo>::type;
     constexpr bool LIVE = Plan<PM, QM>::live;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t n = g.n;
@@ -410,14 +420,28 @@ __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
     c.ghost_row = c.ghostw && y < g.ghost;
     c.save = slots + threadIdx.x;
 
-    DeepState<L> R;
+    DeepState<L, Src> R;
 #pragma unroll
     for (int l = 0; l < L; ++l) {
         R.pA[l] = R.pB[l] = R.pC[l] = R.pR[l] = 0;
         R.ml[l] = 0;
-        R.rs[l] = Xo{0, 0, 0, 0};
+        R.rs[l] = Src{};
     }
-    if constexpr (LIVE) {
+    if constexpr (CTR && LIVE) {
+#pragma unroll
+        for (int l = 1; l <= L; ++l) {
+            Ctr cur = ctr_row(ctr_sweep_key(ctr_seed, sigma0 + uint64_t(l - 1)), y);
+            // words 0..l-2 of streams l >= 2 are processed last: drawn first into their slots, as for xoshiro
+#pragma unroll
+            for (int jw = 0; jw <= l - 2; ++jw) {
+                uint64_t xp, xq;
+                gen_xi<PM, QM, uint64_t>(cur, p, q, xp, xq);
+                if constexpr (SL::kPreP) c.save[(SL::preP0() + SL::pre(l, jw)) * kLanes] = xp;
+                if constexpr (SL::kPreQ) c.save[(SL::preQ0() + SL::pre(l, jw)) * kLanes] = xq;
+            }
+            R.rs[l - 1] = cur;
+        }
+    } else if constexpr (LIVE) {
         Xo base = load_state(rs, g.Y, y);
 #pragma unroll
         for (int l = 1; l <= L; ++l) {
@@ -455,20 +479,20 @@ __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
 #if OCTGPU_DEEP_GHOST_HOIST
             if (c.ghostw) {
 #pragma unroll
-                for (int jj = 0; jj < kKS; ++jj) deep_iter<PM, QM, L, true, 1>(R, c, kb + jj, sb, jj, p, q);
+                for (int jj = 0; jj < kKS; ++jj) deep_iter<PM, QM, L, true, 1, CTR>(R, c, kb + jj, sb, jj, p, q);
             } else {
 #pragma unroll
-                for (int jj = 0; jj < kKS; ++jj) deep_iter<PM, QM, L, true, 0>(R, c, kb + jj, sb, jj, p, q);
+                for (int jj = 0; jj < kKS; ++jj) deep_iter<PM, QM, L, true, 0, CTR>(R, c, kb + jj, sb, jj, p, q);
             }
 #else
 #pragma unroll
-            for (int jj = 0; jj < kKS; ++jj) deep_iter<PM, QM, L, true, 2>(R, c, kb + jj, sb, jj, p, q);
+            for (int jj = 0; jj < kKS; ++jj) deep_iter<PM, QM, L, true, 2, CTR>(R, c, kb + jj, sb, jj, p, q);
 #endif
         } else {
 #pragma unroll 1
             for (int jj = 0; jj < kKS; ++jj) {
                 if (kb + jj >= n) break;
-                deep_iter<PM, QM, L, false, 2>(R, c, kb + jj, sb, jj, p, q);
+                deep_iter<PM, QM, L, false, 2, CTR>(R, c, kb + jj, sb, jj, p, q);
             }
         }
         __syncwarp();
@@ -480,9 +504,9 @@ __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
     }
     // drain: sweeps 2..L finish their wrapped words
 #pragma unroll 1
-    for (uint32_t i = n; i < n + uint32_t(2 * L - 2); ++i) deep_iter<PM, QM, L, false, 2>(R, c, i, nullptr, 0, p, q);
+    for (uint32_t i = n; i < n + uint32_t(2 * L - 2); ++i) deep_iter<PM, QM, L, false, 2, CTR>(R, c, i, nullptr, 0, p, q);
 
-    if constexpr (LIVE) {
+    if constexpr (LIVE && !CTR) {
         Xo fin = R.rs[L - 1];
         if constexpr (SL::parked() > 0) fin = slot_state(c.save, SL::st0() + 4 * (L - 1 - kRegStreams));
         if (c.core) {
@@ -494,18 +518,18 @@ __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
 
 namespace {
 
-template <int PM, int QM, int L>
+template <int PM, int QM, int L, bool CTR = false>
 cudaError_t deep_go(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
                     const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK, const CUtensorMap* tmK1,
-                    cudaStream_t st) {
+                    cudaStream_t st, uint64_t ctr_seed = 0, uint64_t sigma0 = 0) {
     using GEO = DeepGeo<L>;
     const uint32_t blocks = (g.c1 - g.c0 + GEO::kRows - 1) / GEO::kRows;
-    const size_t smem = mcs_deep_smem(p.mode, q.mode, L, S);
-    auto kern = k_mcs_deep<PM, QM, L>;
+    const size_t smem = mcs_deep_smem(p.mode, q.mode, L, S, CTR);
+    auto kern = k_mcs_deep<PM, QM, L, CTR>;
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     kern<<<blocks, 32 * (kDP + 1), smem, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), rs,
-                                               rd, f, g, p, q, jtab, S, *tmK, *tmK1);
+                                               rd, f, g, p, q, jtab, S, *tmK, *tmK1, ctr_seed, sigma0);
     return cudaGetLastError();
 }
 
@@ -523,9 +547,9 @@ cudaError_t deep_q(const void* src, void* dst, const uint64_t* rs, uint64_t* rd,
 }
 
 template <int L>
-size_t deep_smem_l(int pm, int qm, int S) {
+size_t deep_smem_l(int pm, int qm, int S, bool ctr) {
     const bool pp = !(pm == M_ZERO || pm == M_ONE), pq = !(qm == M_ZERO || qm == M_ONE);
-    const int parked = (pp || pq) && L > kRegStreams ? L - kRegStreams : 0;
+    const int parked = !ctr && (pp || pq) && L > kRegStreams ? L - kRegStreams : 0;
     const int slots = 5 * (L - 1) + 1 + (pp ? L * (L - 1) / 2 : 0) + (pq ? L * (L - 1) / 2 : 0) + 4 * parked;
     return 128 + size_t(S) * DeepStage<L>::kWords * 8 + size_t(slots) * kLanes * 8;
 }
@@ -539,7 +563,9 @@ bool mcs_deep_supported(int pm, int qm) {
     return cheap(pm) && cheap(qm) && !(live && (pm == M_ONE || qm == M_ONE));
 }
 
-size_t mcs_deep_smem(int pm, int qm, int L, int S) { return L == kDeepSweeps ? deep_smem_l<kDeepSweeps>(pm, qm, S) : 0; }
+size_t mcs_deep_smem(int pm, int qm, int L, int S, bool ctr) {
+    return L == kDeepSweeps ? deep_smem_l<kDeepSweeps>(pm, qm, S, ctr) : 0;
+}
 
 cudaError_t launch_mcs_deep(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g,
                             const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK,
@@ -550,6 +576,29 @@ cudaError_t launch_mcs_deep(const void* src, void* dst, const uint64_t* rs, uint
     case M_HALF: return deep_q<M_HALF>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
     case M_DYADIC: return deep_q<M_DYADIC>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
     case M_ONE: return deep_q<M_ONE>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+// counter-based streams (octgpu_set_rng): sweeps sigma .. sigma + kDeepSweeps - 1 of seed's streams
+#define OCT_DQC(PM)                                                                                                \
+    switch (q.mode) {                                                                                              \
+    case M_ZERO: return deep_go<PM, M_ZERO, kDeepSweeps, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, seed, sigma);     \
+    case M_HALF: return deep_go<PM, M_HALF, kDeepSweeps, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, seed, sigma);     \
+    case M_DYADIC: return deep_go<PM, M_DYADIC, kDeepSweeps, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, seed, sigma); \
+    case M_ONE: return deep_go<PM, M_ONE, kDeepSweeps, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, seed, sigma);       \
+    default: return cudaErrorInvalidValue;                                                                         \
+    }
+
+cudaError_t launch_mcs_deep_ctr(const void* src, void* dst, int f, Geom g, const ProbDev& p, const ProbDev& q,
+                                uint64_t seed, uint64_t sigma, int S, const CUtensorMap* tmK, const CUtensorMap* tmK1,
+                                cudaStream_t st) {
+    if (S < 2 || S > kSMax) return cudaErrorInvalidValue;
+    switch (p.mode) {
+    case M_ZERO: OCT_DQC(M_ZERO)
+    case M_HALF: OCT_DQC(M_HALF)
+    case M_DYADIC: OCT_DQC(M_DYADIC)
+    case M_ONE: OCT_DQC(M_ONE)
     default: return cudaErrorInvalidValue;
     }
 }

@@ -123,7 +123,11 @@ size_t mcs_bulk_smem(int ks, int S);  // dynamic smem of a block (kMcsConsumerWa
 // engine.cu deep_geom). tmK / tmK1: tensor maps with boxes of
 // deep_box_rows(kDeepSweeps) rows x 2 and x 3 words.
 bool mcs_deep_supported(int p_mode, int q_mode);
-size_t mcs_deep_smem(int p_mode, int q_mode, int L, int S);  // S ring stages
+size_t mcs_deep_smem(int p_mode, int q_mode, int L, int S, bool ctr = false);  // S ring stages
+// k_mcs_deep with counter-based xi: sweeps sigma .. sigma + kDeepSweeps - 1 of seed's streams (octgpu_set_rng)
+cudaError_t launch_mcs_deep_ctr(const void* src, void* dst, int f, Geom g, const ProbDev& p, const ProbDev& q,
+                                uint64_t seed, uint64_t sigma, int S, const CUtensorMap* tmK, const CUtensorMap* tmK1,
+                                cudaStream_t st);
 cudaError_t launch_mcs_deep(const void* src, void* dst, const uint64_t* rng_src, uint64_t* rng_dst, int f, Geom g,
                             const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK,
                             const CUtensorMap* tmK1, cudaStream_t st);

@@ -20,9 +20,12 @@ def _pair(oracle, X, Y, w, seed):
     return eng, OracleLattice.flat(oracle, X, Y, seed, w)
 
 
+@pytest.mark.parametrize("deep", ["1", "2"], ids=["policy", "deep"])
 @pytest.mark.parametrize("geom", GEOMS, ids=lambda g: f"{g[0]}x{g[1]}w{g[2]}")
 @pytest.mark.parametrize("pq", MODES, ids=lambda m: f"p{m[0]}q{m[1]}")
-def test_counter_vs_oracle(oracle, geom, pq):
+def test_counter_vs_oracle(oracle, monkeypatch, deep, geom, pq):
+    """deep=2 forces the 2-MCS pass (k_mcs_deep<CTR>) wherever the lattice takes it (n >= 8, >= 256 rows)."""
+    monkeypatch.setenv("OCTGPU_DEEP", deep)
     X, Y, w = geom
     p, q = pq
     seed = 77 + X + Y
@@ -30,7 +33,7 @@ def test_counter_vs_oracle(oracle, geom, pq):
     st0 = eng.streams().states.copy()
     prm = octgpu.UpdateParams.make(p, q)
     op, oq = oracle.resolve(p), oracle.resolve(q)
-    for chunk in (1, 3):
+    for chunk in (1, 3, 4):
         eng.step(prm, chunk)
         L.step_ctr(oracle, op, oq, seed, chunk)
         assert np.array_equal(eng.planes(), L.planes.astype(eng.planes().dtype)), (chunk, eng.t)
@@ -39,10 +42,12 @@ def test_counter_vs_oracle(oracle, geom, pq):
     assert eng.rng == "counter"
 
 
+@pytest.mark.parametrize("deep", ["1", "2"], ids=["policy", "deep"])
 @pytest.mark.parametrize("pq", [(0.5, 0.0), (1.0, 0.0), (0.98, 0.02)])
-def test_mode_switch_mid_run(oracle, pq):
+def test_mode_switch_mid_run(oracle, monkeypatch, deep, pq):
     """xoshiro -> counter -> xoshiro on a lattice the TMA kernels run (ghost rows refreshed after the
     in-place counter sweeps; constant-xi draws owed to the streams survive the switch)."""
+    monkeypatch.setenv("OCTGPU_DEEP", deep)
     X, Y, seed = 1024, 262, 5
     p, q = pq
     eng = octgpu.GpuEngine(octgpu.LatticeConfig(X, Y), seed)
@@ -88,13 +93,15 @@ def test_counter_measure_consistent():
     assert rec.W2 > 0.5
 
 
-@pytest.mark.parametrize("pq", [(0.5, 0.0), (0.5, 0.5), (0.98, 0.02)])
-def test_fused_counter_kernel_matches_sweeps(monkeypatch, pq):
-    """At sizes the oracle cannot reach: the fused TMA pass (k_mcs_bulk<CTR>) equals two in-place
-    k_sweep_ctr sweeps per MCS (OCTGPU_MCS_IMPL=1), bit for bit."""
+@pytest.mark.parametrize("deep", ["0", "2"], ids=["bulk", "deep"])
+@pytest.mark.parametrize("pq", [(0.5, 0.0), (0.5, 0.5), (0.98, 0.02), (0.75, 0.25)])
+def test_fused_counter_kernel_matches_sweeps(monkeypatch, deep, pq):
+    """At sizes the oracle cannot reach: the fused TMA passes (k_mcs_bulk<CTR>, and k_mcs_deep<CTR> with
+    deep=2 where the modes allow) equal two in-place k_sweep_ctr sweeps per MCS (OCTGPU_MCS_IMPL=1)."""
     X = Y = 4096
     prm = octgpu.UpdateParams.make(*pq)
-    mcs = 3 if pq[0] == 0.98 else 20
+    mcs = 3 if pq[0] == 0.98 else 21
+    monkeypatch.setenv("OCTGPU_DEEP", deep)
     fused = octgpu.GpuEngine(octgpu.LatticeConfig(X, Y), 11)
     fused.set_rng("counter")
     fused.step(prm, mcs)

@@ -421,14 +421,15 @@ cudaError_t launch_mcs_bulk(const void* src, void* dst, const uint64_t* rs, uint
 }
 
 // counter-based streams: KS = 2 only (the engine's plan)
-#define OCT_BQC(PM)                                                                                       \
-    switch (q.mode) {                                                                                     \
-    case M_ZERO: return bulk_go<PM, M_ZERO, 2, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, k1, k2);     \
-    case M_HALF: return bulk_go<PM, M_HALF, 2, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, k1, k2);     \
-    case M_DYADIC: return bulk_go<PM, M_DYADIC, 2, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, k1, k2); \
-    case M_ARB: return bulk_go<PM, M_ARB, 2, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, k1, k2);       \
-    case M_ONE: return bulk_go<PM, M_ONE, 2, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, k1, k2);       \
-    default: return cudaErrorInvalidValue;                                                                \
+#define OCT_CTR_ARGS src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, k1, k2
+#define OCT_BQC(PM)                                                           \
+    switch (q.mode) {                                                         \
+    case M_ZERO: return bulk_go<PM, M_ZERO, 2, true>(OCT_CTR_ARGS);         \
+    case M_HALF: return bulk_go<PM, M_HALF, 2, true>(OCT_CTR_ARGS);         \
+    case M_DYADIC: return bulk_go<PM, M_DYADIC, 2, true>(OCT_CTR_ARGS);     \
+    case M_ARB: return bulk_go<PM, M_ARB, 2, true>(OCT_CTR_ARGS);           \
+    case M_ONE: return bulk_go<PM, M_ONE, 2, true>(OCT_CTR_ARGS);           \
+    default: return cudaErrorInvalidValue;                                    \
     }
 
 cudaError_t launch_mcs_bulk_ctr(const void* src, void* dst, int f, Geom g, const ProbDev& p, const ProbDev& q,

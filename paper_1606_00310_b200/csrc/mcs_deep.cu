@@ -504,7 +504,8 @@ __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
     }
     // drain: sweeps 2..L finish their wrapped words
 #pragma unroll 1
-    for (uint32_t i = n; i < n + uint32_t(2 * L - 2); ++i) deep_iter<PM, QM, L, false, 2, CTR>(R, c, i, nullptr, 0, p, q);
+    for (uint32_t i = n; i < n + uint32_t(2 * L - 2); ++i)
+        deep_iter<PM, QM, L, false, 2, CTR>(R, c, i, nullptr, 0, p, q);
 
     if constexpr (LIVE && !CTR) {
         Xo fin = R.rs[L - 1];
@@ -581,13 +582,14 @@ cudaError_t launch_mcs_deep(const void* src, void* dst, const uint64_t* rs, uint
 }
 
 // counter-based streams (octgpu_set_rng): sweeps sigma .. sigma + kDeepSweeps - 1 of seed's streams
-#define OCT_DQC(PM)                                                                                                \
-    switch (q.mode) {                                                                                              \
-    case M_ZERO: return deep_go<PM, M_ZERO, kDeepSweeps, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, seed, sigma);     \
-    case M_HALF: return deep_go<PM, M_HALF, kDeepSweeps, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, seed, sigma);     \
-    case M_DYADIC: return deep_go<PM, M_DYADIC, kDeepSweeps, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, seed, sigma); \
-    case M_ONE: return deep_go<PM, M_ONE, kDeepSweeps, true>(src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, seed, sigma);       \
-    default: return cudaErrorInvalidValue;                                                                         \
+#define OCT_CTR_ARGS src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, seed, sigma
+#define OCT_DQC(PM)                                                               \
+    switch (q.mode) {                                                             \
+    case M_ZERO: return deep_go<PM, M_ZERO, kDeepSweeps, true>(OCT_CTR_ARGS);     \
+    case M_HALF: return deep_go<PM, M_HALF, kDeepSweeps, true>(OCT_CTR_ARGS);     \
+    case M_DYADIC: return deep_go<PM, M_DYADIC, kDeepSweeps, true>(OCT_CTR_ARGS); \
+    case M_ONE: return deep_go<PM, M_ONE, kDeepSweeps, true>(OCT_CTR_ARGS);       \
+    default: return cudaErrorInvalidValue;                                        \
     }
 
 cudaError_t launch_mcs_deep_ctr(const void* src, void* dst, int f, Geom g, const ProbDev& p, const ProbDev& q,

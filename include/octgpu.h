@@ -134,9 +134,11 @@ int octgpu_set_tile_shift(octgpu_engine* e, uint64_t seed);
  * SURVEY.md 8f row 4): draw i of row y in global sweep sigma = 2 t + (0 | 1) is
  * mix64(o + (i+1) g), o = mix64(mix64(seed + (sigma+1) g) + (y+1) g), g = 0x9E3779B97F4A7C15,
  * mix64 = the SplitMix64 finaliser; seed = octgpu_master_seed. The xi words are built from
- * these draws exactly as from xoshiro draws (half / dyadic / arbitrary). Counter steps leave
- * the xoshiro states untouched; single sweeps (octgpu_sweep) and row stripes are xoshiro-only
- * (OCTGPU_ERR_CONFIG). Results are pinned by oracle/octoracle.c oo_step_ctr. */
+ * these draws exactly as from xoshiro draws (half / dyadic / arbitrary); y is the GLOBAL row,
+ * so row stripes (w = 64, >= 8 words per row; set the same kind on every stripe) reproduce the
+ * periodic engine. Counter steps leave the xoshiro states untouched; single sweeps
+ * (octgpu_sweep) are xoshiro-only (OCTGPU_ERR_CONFIG). Results are pinned by
+ * oracle/octoracle.c oo_step_ctr. */
 #define OCTGPU_RNG_XOSHIRO 0
 #define OCTGPU_RNG_COUNTER 1
 int octgpu_set_rng(octgpu_engine* e, int kind);

@@ -152,6 +152,11 @@ __device__ __forceinline__ Ctr ctr_row(uint64_t sweep_key, uint32_t y) {
     return Ctr{mix64(sweep_key + (uint64_t(y) + 1) * kGamma)};
 }
 
+// the lattice row whose counter stream physical row y uses (row stripes: local rows -> global rows)
+__device__ __forceinline__ uint32_t ctr_global_row(const Geom& g, uint32_t y) {
+    return g.gytot ? (y + g.gy0) % g.gytot : y;
+}
+
 __device__ __forceinline__ uint64_t rng_next(Ctr& s) {
     s.x += kGamma;
     return mix64(s.x);

@@ -363,8 +363,11 @@ struct octgpu_engine {
     Geom deep_geom() const { return Geom{Y, n, size_t(n) * Y, kDeepSweeps - 1, L + kDeepSweeps - 1, L, 0, kGhostRows}; }
     Geom geom() const {
         // stripe: local row 0 = global y0 - kStripeHA (parity of y0 + 1)
-        return stripe ? Geom{Y, n, size_t(n) * Y, kStripeHA, kStripeHA + L, 0, (y0 + 1) & 1u, 0}
-                      : Geom{Y, n, size_t(n) * Y, 1, L + 1, L, 0, kGhostRows};
+        if (!stripe) return Geom{Y, n, size_t(n) * Y, 1, L + 1, L, 0, kGhostRows};
+        Geom g{Y, n, size_t(n) * Y, kStripeHA, kStripeHA + L, 0, (y0 + 1) & 1u, 0};
+        g.gy0 = (y0 + Ytot - kStripeHA % Ytot) % Ytot;
+        g.gytot = Ytot;
+        return g;
     }
     uint32_t core_rows() const { return L; }
     // rows of the reference-layout staging buffer: the lattice rows (periodic) or
@@ -1175,8 +1178,8 @@ int octgpu_set_rng(octgpu_engine* e, int kind) {
     if (!e) return fail(OCTGPU_ERR_CONFIG, "null engine");
     if (kind != OCTGPU_RNG_XOSHIRO && kind != OCTGPU_RNG_COUNTER)
         return fail(OCTGPU_ERR_CONFIG, "unknown rng kind " + std::to_string(kind));
-    if (kind == OCTGPU_RNG_COUNTER && e->stripe)
-        return fail(OCTGPU_ERR_CONFIG, "the counter-based rng is not available on a row stripe");
+    if (kind == OCTGPU_RNG_COUNTER && e->stripe && e->mcs_impl != 2)
+        return fail(OCTGPU_ERR_CONFIG, "the counter-based rng on a row stripe needs w = 64 and >= 8 words per row");
     e->rng_kind = kind;
     return OCTGPU_OK;
 }
@@ -1432,9 +1435,30 @@ int octgpu_halo_unpack(octgpu_engine* e, const void* from_prev, const void* from
 namespace {
 // k_mcs_deep can carry a stripe through 2 MCS per halo exchange (constant-xi modes)
 bool stripe_deep_ok(const octgpu_engine* e, const ProbDev& p, const ProbDev& q) {
-    // constant xi only: a live deep pass would not advance the halo rows' streams (p2p.cu relies on that)
+    // xoshiro: constant xi only (a live deep pass would not advance the halo rows' streams, which p2p.cu
+    // relies on); counter streams have no state, so every cheap mode qualifies
     const bool size_ok = e->deep == 2 || uint64_t(e->X) * e->L >= (uint64_t(1) << 28);
-    return e->deep && size_ok && e->mcs_impl == 2 && mcs_deep_supported(p.mode, q.mode) && is_const(p) && is_const(q);
+    const bool xi_ok = e->rng_kind == OCTGPU_RNG_COUNTER || (is_const(p) && is_const(q));
+    return e->deep && size_ok && e->mcs_impl == 2 && mcs_deep_supported(p.mode, q.mode) && xi_ok;
+}
+
+// one fused stripe pass with counter-based xi (n_mcs = 1: k_mcs_bulk<CTR>, else k_mcs_deep<CTR>)
+int stripe_kernel_ctr(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool deep) {
+    const Geom g = e->geom();
+    const int ps = e->pcur;
+    if (deep) {
+        int rc = ensure_tmaps_deep(e);
+        if (rc) return rc;
+        CK(launch_mcs_deep_ctr(e->planes[ps], e->planes[ps ^ 1], e->phase, g, p, q, e->master_seed, 2 * e->t,
+                               deep_ring(e, p, q, true), &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
+    } else {
+        int rc = plan_bulk(e, p, q);
+        if (rc) return rc;
+        if (e->bulk_ks != 2) return fail(OCTGPU_ERR_CONFIG, "the counter-based rng needs OCTGPU_MCS_KS=2");
+        CK(launch_mcs_bulk_ctr(e->planes[ps], e->planes[ps ^ 1], e->phase, g, p, q, e->master_seed, 2 * e->t,
+                               e->bulk_S, &e->tm[ps][0], &e->tm[ps][1], e->stream));
+    }
+    return OCTGPU_OK;
 }
 }  // namespace
 
@@ -1458,7 +1482,8 @@ int octgpu_stripe_mcs_n(octgpu_engine* e, const octgpu_params* prm, uint32_t n_m
     if (n_mcs != 1 && !(deep && stripe_deep_ok(e, p, q)))
         return fail(OCTGPU_ERR_CONFIG, "a stripe pass covers 1 MCS, or " + std::to_string(kDeepSweeps / 2) +
                                            " with constant xi (see octgpu_stripe_max_mcs)");
-    const bool live = !(is_const(p) && is_const(q));
+    const bool ctr = e->rng_kind == OCTGPU_RNG_COUNTER;
+    const bool live = !ctr && !(is_const(p) && is_const(q));
     const uint64_t D = draws(prm->p, e->w) + (q.mode != M_ZERO ? draws(prm->q, e->w) : 0);
     const uint64_t per_sweep = uint64_t(e->n) * D;
     uint64_t* jtab = nullptr;
@@ -1469,7 +1494,10 @@ int octgpu_stripe_mcs_n(octgpu_engine* e, const octgpu_params* prm, uint32_t n_m
     }
     const Geom g = e->geom();
     const int ps = e->pcur, rs = e->rcur;
-    if (deep) {
+    if (ctr) {
+        rc = stripe_kernel_ctr(e, p, q, deep);
+        if (rc) return rc;
+    } else if (deep) {
         rc = ensure_tmaps_deep(e);
         if (rc) return rc;
         CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
@@ -1490,7 +1518,7 @@ int octgpu_stripe_mcs_n(octgpu_engine* e, const octgpu_params* prm, uint32_t n_m
     e->pcur ^= 1;
     if (live)
         e->rcur ^= 1;
-    else
+    else if (!ctr)
         e->pending += 2 * uint64_t(n_mcs) * per_sweep;
     e->t += n_mcs;
     return OCTGPU_OK;
@@ -1668,7 +1696,8 @@ int octgpu_stripe_pass(octgpu_engine* e, const octgpu_params* prm, uint32_t n_mc
     if (n_mcs != 1 && !(deep && stripe_deep_ok(e, p, q)))
         return fail(OCTGPU_ERR_CONFIG, "a stripe pass covers 1 MCS, or " + std::to_string(kDeepSweeps / 2) +
                                            " with constant xi (see octgpu_stripe_max_mcs)");
-    const bool live = !(is_const(p) && is_const(q));
+    const bool ctr = e->rng_kind == OCTGPU_RNG_COUNTER;
+    const bool live = !ctr && !(is_const(p) && is_const(q));
     const uint64_t D = draws(prm->p, e->w) + (q.mode != M_ZERO ? draws(prm->q, e->w) : 0);
     const uint64_t per_sweep = uint64_t(e->n) * D;
     // 1. wait for the neighbours' previous pass, pull their boundary rows
@@ -1684,7 +1713,10 @@ int octgpu_stripe_pass(octgpu_engine* e, const octgpu_params* prm, uint32_t n_mc
     // 3. the MCS kernel
     const Geom g = e->geom();
     const int ps = e->pcur, rs = e->rcur;
-    if (deep) {
+    if (ctr) {
+        rc = stripe_kernel_ctr(e, p, q, deep);
+        if (rc) return rc;
+    } else if (deep) {
         rc = ensure_tmaps_deep(e);
         if (rc) return rc;
         CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
@@ -1698,7 +1730,7 @@ int octgpu_stripe_pass(octgpu_engine* e, const octgpu_params* prm, uint32_t n_mc
     e->pcur ^= 1;
     if (live)
         e->rcur ^= 1;
-    else
+    else if (!ctr)
         e->pending += 2 * uint64_t(n_mcs) * per_sweep;
     e->t += n_mcs;
     ++e->passes;

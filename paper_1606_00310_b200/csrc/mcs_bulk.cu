@@ -212,8 +212,9 @@ __global__ void __launch_bounds__(32 * (kP + 1), kP >= 8 ? 2 : 4) k_mcs_bulk(con
     using Src = typename std::conditional<CTR, Ctr, Xo>::type;
     Src st1{}, st2{};  // first / second sweep streams
     if constexpr (CTR) {
-        st1 = ctr_row(ck1, y);
-        st2 = ctr_row(ck2, y);
+        const uint32_t gy = ctr_global_row(g, y);
+        st1 = ctr_row(ck1, gy);
+        st2 = ctr_row(ck2, gy);
     } else if constexpr (LIVE) {
         st1 = load_state(rs, Y, y);
         st2 = apply_table(jtab, st1);

@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
     if constexpr (CTR && LIVE) {
 #pragma unroll
         for (int l = 1; l <= L; ++l) {
-            Ctr cur = ctr_row(ctr_sweep_key(ctr_seed, sigma0 + uint64_t(l - 1)), y);
+            Ctr cur = ctr_row(ctr_sweep_key(ctr_seed, sigma0 + uint64_t(l - 1)), ctr_global_row(g, y));
             // words 0..l-2 of streams l >= 2 are processed last: drawn first into their slots, as for xoshiro
 #pragma unroll
             for (int jw = 0; jw <= l - 2; ++jw) {

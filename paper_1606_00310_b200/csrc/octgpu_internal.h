@@ -42,6 +42,8 @@ struct Geom {
     uint32_t ypar;         // parity of the global row of physical row 0 (site parity uses global rows)
     uint32_t ghost;        // periodic: rows wrap..wrap+ghost-1 mirror rows (i mod wrap), so block windows never wrap
     uint32_t pf = 0;       // TMA kernels: L2 prefetch distance in ring stages (0 = off)
+    // counter-based rng: global row of physical row r = (r + gy0) mod gytot (gytot = 0: r itself)
+    uint32_t gy0 = 0, gytot = 0;
 };
 
 #ifndef OCTGPU_BULK_WARPS

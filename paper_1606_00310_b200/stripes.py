@@ -139,6 +139,14 @@ class StripeEngine:
     def set_stream(self, cuda_stream: int | None) -> None:
         check(lib().octgpu_set_stream(self._h, C.c_void_p(cuda_stream) if cuda_stream else None))
 
+    def set_rng(self, kind: str) -> None:
+        """GpuEngine.set_rng for this stripe: every stripe of a group must use the same kind (the counter
+        streams are keyed by the master seed and the GLOBAL row, so a striped run equals the periodic one)."""
+        from .engine import GpuEngine
+        if kind not in GpuEngine.RNG_KINDS:
+            raise ValueError(f"rng kind must be one of {sorted(GpuEngine.RNG_KINDS)}")
+        check(lib().octgpu_set_rng(self._h, GpuEngine.RNG_KINDS[kind]))
+
     def pack(self, to_prev, to_next) -> None:
         check(lib().octgpu_halo_pack(self._h, self._p(to_prev), self._p(to_next)))
 

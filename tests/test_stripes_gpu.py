@@ -66,6 +66,41 @@ def test_stripes_match_single_engine(X, Y, parts, pq, transport):
         assert abs(rec.W2 - rref.W2) <= 2 ** -50 * rref.W2
 
 
+@pytest.mark.parametrize("X,Y,parts", [(1024, 128, 2), (1024, 130, 4), (2048, 96, 3), (8192, 512, 8), (1024, 32, 8)])
+@pytest.mark.parametrize("pq", [(0.5, 0.0), (0.5, 0.5), (0.98, 0.02), (1.0, 0.0), (0.75, 0.25)])
+@pytest.mark.parametrize("transport", ["host", "peer"])
+def test_counter_rng_stripes_match_single_engine(X, Y, parts, pq, transport):
+    """Opt-in counter streams on row stripes (k_mcs_bulk<CTR> / k_mcs_deep<CTR> with local -> global rows):
+    the striped run equals the periodic engine's (itself pinned to the oracle's oo_step_ctr)."""
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        cfg = octgpu.LatticeConfig(X, Y)
+        prm = octgpu.UpdateParams.make(*pq)
+        engines = []
+        for r in range(parts):
+            y0, y1 = stripe_bounds(Y, parts, r)
+            e = StripeEngine(cfg, y0, y1, 21)
+            e.set_stream(stream.cuda_stream)
+            e.set_rng("counter")
+            engines.append(e)
+        if transport == "peer":
+            grp = StripeGroup(PeerLocalTransport(engines), X, Y)
+        else:
+            grp = StripeGroup(LocalTransport(engines, lambda nb: torch.zeros(nb, dtype=torch.uint8, device="cuda")),
+                              X, Y)
+        grp.step(prm, 7)
+        for e in engines:
+            e.sync()
+        ref = octgpu.GpuEngine(cfg, 21)
+        ref.set_rng("counter")
+        ref.step(prm, 7)
+        torch.cuda.synchronize()
+        planes = np.concatenate([e.planes() for e in engines], axis=1)
+        assert np.array_equal(planes, ref.planes())
+        rec, rref = grp.measure(), ref.measure()
+        assert rec.power_sums == rref.power_sums
+
+
 def test_stripe_curl_violation_reported_globally():
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):

@@ -149,6 +149,23 @@ def _mcs_kernel(prm, Y: int, n: int, ws: int) -> tuple[str, int]:
     return "k_mcs_bulk", 1
 
 
+def _ctr_kernel(prm, Y: int, n: int, ws: int) -> tuple[str, float]:
+    """The kernel of a counter-rng step (engine.cu step_counter / stripe_kernel_ctr): 2-MCS passes for the
+    cheap modes from 2^28 sites per engine, the one-MCS TMA pass otherwise, in-place sweeps on lattices the
+    TMA kernels do not take."""
+    from paper_1606_00310_b200.params import ProbMode
+
+    one = [ps.mode == ProbMode.Arbitrary and ps.value == 1.0 for ps in (prm.p, prm.q)]
+    const = all(ps.mode == ProbMode.Zero or o for ps, o in zip((prm.p, prm.q), one))
+    cheap = all(ps.mode in (ProbMode.Zero, ProbMode.Half, ProbMode.Dyadic) or o for ps, o in zip((prm.p, prm.q), one))
+    deep_env = os.environ.get("OCTGPU_DEEP", "1")
+    tma = n >= 8 and (ws > 1 or Y >= 256)
+    big = deep_env == "2" or 128 * n * Y // ws >= 1 << 28
+    if tma and cheap and (const or not any(one)) and deep_env != "0" and big:
+        return "k_mcs_deep", 2
+    return ("k_mcs_bulk", 1) if tma else ("k_sweep_ctr", 0.5)
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -203,8 +220,8 @@ def main():
         cfg["Y"] = cfg["Y"] * ws
         cfg["workload"] += f"; {ws} GPUs: {cfg['X']}x{cfg['Y']} lattice, one 2^16-row stripe per GPU"
 
-    if args.rng != "xoshiro" and (ws > 1 or args.impl == "reference"):
-        raise SystemExit("--rng counter: single GPU, our implementation only (the reference has no counter rng)")
+    if args.rng != "xoshiro" and args.impl == "reference":
+        raise SystemExit("--rng counter: our implementation only (the reference has no counter rng)")
     config_key = {"workload": cfg["workload"], "X": cfg["X"], "Y": cfg["Y"], "p": cfg["p"], "q": cfg["q"],
                   "w": 64, "seed": 1, "schedule": f"log_schedule({SCHEDULE_TMAX},{SCHEDULE_PPD}) within steps",
                   "l2": "planes (>=1 GiB) exceed L2 (126 MB); no flush needed", "parallelism": f"row stripes x{ws}" if ws > 1 else "single GPU"}
@@ -280,6 +297,8 @@ def main():
         y0, y1 = stripe_bounds(Y, ws, rank)
         e = StripeEngine(lat, y0, y1, 1, device=local, planes=planes, states=states, t=t)  # this rank's rows
         e.set_stream(stream.cuda_stream)
+        if args.rng != "xoshiro":
+            e.set_rng(args.rng)
         alloc = lambda nb: torch.zeros(nb, dtype=torch.uint8, device=dev)  # noqa: E731
         return StripeGroup(_transport(e, alloc, PeerDistTransport, DistTransport), X, Y), [e]
 
@@ -360,7 +379,8 @@ def main():
     value = X * Y * K / (ms * 1e6)
     kernel_ms = step_ms / K  # per MCS, all launches of the step calls
     peak, peak_src = _peaks()
-    kname, mcs_per_launch = _mcs_kernel(prm, Y, X // 128, ws) if args.rng == "xoshiro" else ("k_sweep_ctr", 0.5)
+    kname, mcs_per_launch = (_mcs_kernel(prm, Y, X // 128, ws) if args.rng == "xoshiro"
+                             else _ctr_kernel(prm, Y, X // 128, ws))
     # paper identity: 1 byte of slope traffic per site update, per GPU, per launch
     alg_bytes = X * Y // ws * mcs_per_launch
     launch_ms = kernel_ms * mcs_per_launch

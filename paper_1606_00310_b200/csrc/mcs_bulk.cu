@@ -91,7 +91,7 @@ __device__ __forceinline__ void st_pred(uint64_t* p, uint64_t v, bool pred) {
         "{\n"
         ".reg .pred q;\n"
         "setp.ne.b32 q, %2, 0;\n"
-        "@q st.global.b64 [%0], %1;\n"
+        "@q st.global" OCTGPU_ST_HINT ".b64 [%0], %1;\n"
         "}\n" ::"l"(p),
         "l"(v), "r"(int(pred)));
 }

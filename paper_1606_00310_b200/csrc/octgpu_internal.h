@@ -46,6 +46,11 @@ struct Geom {
     uint32_t gy0 = 0, gytot = 0;
 };
 
+// cache operator of the fused kernels' plane stores ("" = default write-back, ".cs" = streaming / evict-first)
+#ifndef OCTGPU_ST_HINT
+#define OCTGPU_ST_HINT ""
+#endif
+
 #ifndef OCTGPU_BULK_WARPS
 #define OCTGPU_BULK_WARPS 4
 #endif

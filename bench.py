@@ -272,9 +272,9 @@ def main():
     t_start = 0 if (args.from_flat or not cfg.get("window", True)) else max(0, SCHEDULE_TMAX - K)
     sched = [t for t in octgpu.log_schedule(SCHEDULE_TMAX, SCHEDULE_PPD) if t_start < t <= t_start + K]
     targets = sched + ([t_start + K] if not sched or sched[-1] != t_start + K else [])
-    job = (f"the {SCHEDULE_TMAX}-MCS job" if t_start + K <= SCHEDULE_TMAX
-           else f"the {SCHEDULE_TMAX}-MCS job and {t_start + K - SCHEDULE_TMAX} MCS more")
-    config_key["window"] = (f"MCS {t_start + 1}..{t_start + K} of {job} with its {len(sched)} W^2 points; "
+    span = (f"the {SCHEDULE_TMAX}-MCS job" if t_start + K <= SCHEDULE_TMAX
+            else f"the {SCHEDULE_TMAX}-MCS job and {t_start + K - SCHEDULE_TMAX} MCS more")
+    config_key["window"] = (f"MCS {t_start + 1}..{t_start + K} of {span} with its {len(sched)} W^2 points; "
                             + (f"state at t={t_start} prepared untimed" if t_start else "from the flat start"))
 
     def barrier():

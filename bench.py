@@ -149,6 +149,21 @@ def _mcs_kernel(prm, Y: int, n: int, ws: int) -> tuple[str, int]:
     return "k_mcs_bulk", 1
 
 
+def timed_window(K: int, from_flat: bool, schedule: list[int]):
+    """The timed K MCS are the LAST K MCS of the 10^4-MCS job (the state at t_start = 10^4 - K is prepared
+    untimed), with the job's W^2 points inside that window: K = 10^4 (default) is the whole job; a short K
+    measures a representative stretch instead of the W^2-dense first MCS. from_flat: MCS 1..K.
+    Returns (t_start, W^2 points in the window, step targets, description)."""
+    t_start = 0 if from_flat else max(0, SCHEDULE_TMAX - K)
+    sched = [t for t in schedule if t_start < t <= t_start + K]
+    targets = sched + ([t_start + K] if not sched or sched[-1] != t_start + K else [])
+    span = (f"the {SCHEDULE_TMAX}-MCS job" if t_start + K <= SCHEDULE_TMAX
+            else f"the {SCHEDULE_TMAX}-MCS job and {t_start + K - SCHEDULE_TMAX} MCS more")
+    desc = (f"MCS {t_start + 1}..{t_start + K} of {span} with its {len(sched)} W^2 points; "
+            + (f"state at t={t_start} prepared untimed" if t_start else "from the flat start"))
+    return t_start, sched, targets, desc
+
+
 def _ctr_kernel(prm, Y: int, n: int, ws: int) -> tuple[str, float]:
     """The kernel of a counter-rng step (engine.cu step_counter / stripe_kernel_ctr): 2-MCS passes for the
     cheap modes from 2^28 sites per engine, the one-MCS TMA pass otherwise, in-place sweeps on lattices the
@@ -266,16 +281,8 @@ def main():
     X, Y = cfg["X"], cfg["Y"]
     lat = octgpu.LatticeConfig(X, Y, 64)
     prm = octgpu.UpdateParams.make(cfg["p"], cfg["q"])
-    # The timed K MCS are the LAST K MCS of the 10^4-MCS job (the state at t_start = 10^4 - K is prepared
-    # untimed), with the job's W^2 points inside that window: K = 10^4 (default) is the whole job; a short
-    # K measures a representative stretch instead of the W^2-dense first MCS. --from-flat times MCS 1..K.
-    t_start = 0 if (args.from_flat or not cfg.get("window", True)) else max(0, SCHEDULE_TMAX - K)
-    sched = [t for t in octgpu.log_schedule(SCHEDULE_TMAX, SCHEDULE_PPD) if t_start < t <= t_start + K]
-    targets = sched + ([t_start + K] if not sched or sched[-1] != t_start + K else [])
-    span = (f"the {SCHEDULE_TMAX}-MCS job" if t_start + K <= SCHEDULE_TMAX
-            else f"the {SCHEDULE_TMAX}-MCS job and {t_start + K - SCHEDULE_TMAX} MCS more")
-    config_key["window"] = (f"MCS {t_start + 1}..{t_start + K} of {span} with its {len(sched)} W^2 points; "
-                            + (f"state at t={t_start} prepared untimed" if t_start else "from the flat start"))
+    t_start, sched, targets, config_key["window"] = timed_window(
+        K, args.from_flat or not cfg.get("window", True), octgpu.log_schedule(SCHEDULE_TMAX, SCHEDULE_PPD))
 
     def barrier():
         if ws > 1:

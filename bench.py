@@ -149,6 +149,13 @@ def _mcs_kernel(prm, Y: int, n: int, ws: int) -> tuple[str, int]:
     return "k_mcs_bulk", 1
 
 
+def _sync_all(engines) -> None:
+    """Drain every engine's stream (a helper, so no loop variable keeps an engine - and its plane sets -
+    alive after the caller drops it: the next engine then reuses the pooled memory)."""
+    for eng in engines:
+        eng.sync()
+
+
 def timed_window(K: int, from_flat: bool, schedule: list[int]):
     """The timed K MCS are the LAST K MCS of the 10^4-MCS job (the state at t_start = 10^4 - K is prepared
     untimed), with the job's W^2 points inside that window: K = 10^4 (default) is the whole job; a short K
@@ -347,8 +354,7 @@ def main():
     job, engs = make()
     if t_start:
         job.step(prm, t_start)  # untimed: the job's state at the start of the timed window
-        for e in engs:
-            e.sync()
+        _sync_all(engs)
     torch.cuda.synchronize()
     seg_events = []
     records = []
@@ -414,8 +420,7 @@ def main():
         else:  # the state at t_start, downloaded untimed
             prep, pengs = make()
             prep.step(prm, t_start)
-            for e in pengs:
-                e.sync()
+            _sync_all(pengs)
             flat = pengs[0].planes()
             states0 = pengs[0].states() if ws > 1 else pengs[0].streams().states
             _close(prep)

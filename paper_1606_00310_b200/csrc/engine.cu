@@ -342,7 +342,7 @@ struct octgpu_engine {
     int rng_kind = OCTGPU_RNG_XOSHIRO;  // octgpu_set_rng
     uint64_t tile_shift = 0;  // != 0: random per-pass row origin of the block tiling (DTr-style, result-neutral)
     std::map<std::string, cudaGraphExec_t> graph_cache;
-    int deep_S = 3;    // k_mcs_deep ring stages (OCTGPU_DEEP_S; S = 3 measured best, profiles/r1_deep_modes.json)
+    int deep_S = 5;    // k_mcs_deep ring stages (OCTGPU_DEEP_S): with one word per stage (kDeepKS) S = 5 measured best
     // Row-stripe mode (multi-GPU): this engine owns global rows [y0, y0 + L) of
     // a Ytot-row periodic lattice, held at local rows 1..L with one halo row
     // above (0), two below (L+1, L+2) and padding; Y is then the allocated row
@@ -505,7 +505,7 @@ int ensure_tmaps_deep(octgpu_engine* e) {
         for (int v = 0; v < 2; ++v) {
             const cuuint64_t dims[3] = {e->Y, e->n, 4};
             const cuuint64_t strides[2] = {cuuint64_t(e->Y) * 8, cuuint64_t(e->n) * e->Y * 8};
-            const cuuint32_t box[3] = {cuuint32_t(deep_box_rows(kDeepSweeps)), cuuint32_t(2 + v), 1};
+            const cuuint32_t box[3] = {cuuint32_t(deep_box_rows(kDeepSweeps)), cuuint32_t(kDeepKS + v), 1};
             const cuuint32_t estr[3] = {1, 1, 1};
             const CUresult r = enc(&e->tmd[b][v], CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, e->planes[b], dims, strides, box,
                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

@@ -44,7 +44,7 @@ namespace {
 #endif
 
 constexpr int kDP = kDeepWarps;  // compute warps per block (+1 producer)
-constexpr int kKS = 2;                  // words per ring stage
+constexpr int kKS = kDeepKS;            // words per ring stage
 constexpr int kSMax = 8;                // ring stages: runtime S <= kSMax (barrier slots)
 constexpr int kLanes = 32 * kDP;        // parking-slot stride (compute lanes per block)
 // xoshiro streams kept in registers in a live pass; the others live in parking slots

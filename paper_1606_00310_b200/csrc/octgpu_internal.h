@@ -64,7 +64,13 @@ constexpr uint32_t kTmaBoxRows = 30 * kMcsConsumerWarps + 4;  // k_mcs_bulk wind
 #ifndef OCTGPU_DEEP_SWEEPS
 #define OCTGPU_DEEP_SWEEPS 4
 #endif
+// k_mcs_deep words per ring stage: 1 word x 5 stages beat 2 words x 3 stages (c2 0.1778 vs 0.1839 ms/MCS,
+// c2' 0.3105 vs 0.3234, c5 0.723 vs 0.725; tools/sweep_deep_ks*.sh)
+#ifndef OCTGPU_DEEP_KS
+#define OCTGPU_DEEP_KS 1
+#endif
 constexpr int kDeepSweeps = OCTGPU_DEEP_SWEEPS;  // sweeps per k_mcs_deep pass (even)
+constexpr int kDeepKS = OCTGPU_DEEP_KS;          // k_mcs_deep words per ring stage
 constexpr int kDeepWarps = OCTGPU_DEEP_WARPS;
 #ifndef OCTGPU_DEEP_MINB
 #define OCTGPU_DEEP_MINB (OCTGPU_DEEP_WARPS >= 8 ? 2 : 3)

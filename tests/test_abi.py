@@ -28,6 +28,20 @@ def test_library_exports_every_declared_symbol():
     assert b"sm_100a" in L.octgpu_version()
 
 
+def test_header_is_plain_c(tmp_path):
+    """include/octgpu.h is the FFI boundary (ctypes, cgo, JNI): it must compile as strict C99."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    src = tmp_path / "t.c"
+    src.write_text('#include "octgpu.h"\nint main(void) { octgpu_engine* e = 0; (void)e; '
+                   'return OCTGPU_RNG_COUNTER - 1; }\n')
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-fsyntax-only",
+                        "-I" + os.path.join(ROOT, "include"), str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
 def test_library_is_sm100a_cubin():
     so = _lib.LIB_PATH
     data = open(so, "rb").read()

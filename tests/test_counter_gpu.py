@@ -111,3 +111,21 @@ def test_fused_counter_kernel_matches_sweeps(monkeypatch, deep, pq):
     plain.step(prm, mcs)
     assert fused.checksum() == plain.checksum()
     assert np.array_equal(fused.planes(), plain.planes())
+
+
+@pytest.mark.parametrize("deep", ["1", "2"], ids=["policy", "deep"])
+@pytest.mark.parametrize("pq", [(0.5, 0.0), (0.5, 0.5), (1.0, 0.0)])
+def test_counter_tile_shift_neutral(monkeypatch, deep, pq):
+    """DTr-style tile-origin shifts move block / warp / halo boundaries; the counter streams are keyed by the
+    lattice row, so the trajectory is unchanged."""
+    monkeypatch.setenv("OCTGPU_DEEP", deep)
+    cfg = octgpu.LatticeConfig(2048, 482)
+    prm = octgpu.UpdateParams.make(*pq)
+    a = octgpu.GpuEngine(cfg, 4)
+    b = octgpu.GpuEngine(cfg, 4)
+    for e in (a, b):
+        e.set_rng("counter")
+    b.set_tile_shift(12345)
+    a.step(prm, 9)
+    b.step(prm, 9)
+    assert np.array_equal(a.planes(), b.planes())

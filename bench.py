@@ -40,6 +40,10 @@ CONFIGS = {
                multi="strong"),
 }
 METRIC = "site updates/ns"
+# The other BASELINE configs, timed in short windows after the headline (single GPU): MCS per window. Each
+# window is the job's last K MCS like the headline (c4, 10 ms/MCS: MCS 1..K from the flat start).
+CONFIG_WINDOWS = {"c2h": 50, "c3": 50, "c4": 10, "c5": 20}
+CONFIG_CPU_BUDGET = 6.0  # seconds of reference CPU work per config
 SCHEDULE_TMAX, SCHEDULE_PPD = 10000, 8
 
 
@@ -140,7 +144,8 @@ def _mcs_kernel(prm, Y: int, n: int, ws: int) -> tuple[str, int]:
     if deep_env == "2" and n >= 8 and (ws > 1 or Y >= 256) and cheap and (const or (ws == 1 and not any(one))):
         return "k_mcs_deep", 2  # forced (tests / experiments)
     sites = 128 * n * Y // ws  # per engine (stripe)
-    big = deep_env == "2" or sites >= 1 << 28
+    # stripes test the whole lattice (engine.cu stripe_deep_ok), so every rank picks the same pass length
+    big = deep_env == "2" or (128 * n * Y if ws > 1 else sites) >= 1 << 28
     if const and n >= 8 and (ws > 1 or Y >= 256) and deep_env != "0" and big:
         return "k_mcs_deep", 2  # periodic lattice, or each rank's row stripe (2-MCS passes)
     if (ws == 1 and prm.draws_per_word(64) == 1 and n >= 8 and Y >= 256 and deep_env != "0"
@@ -182,7 +187,7 @@ def _ctr_kernel(prm, Y: int, n: int, ws: int) -> tuple[str, float]:
     cheap = all(ps.mode in (ProbMode.Zero, ProbMode.Half, ProbMode.Dyadic) or o for ps, o in zip((prm.p, prm.q), one))
     deep_env = os.environ.get("OCTGPU_DEEP", "1")
     tma = n >= 8 and (ws > 1 or Y >= 256)
-    big = deep_env == "2" or 128 * n * Y // ws >= 1 << 28
+    big = deep_env == "2" or 128 * n * Y >= 1 << 28  # the whole lattice, for stripes too (stripe_deep_ok)
     if tma and cheap and (const or not any(one)) and deep_env != "0" and big:
         return "k_mcs_deep", 2
     return ("k_mcs_bulk", 1) if tma else ("k_sweep_ctr", 0.5)
@@ -195,14 +200,76 @@ def _dist():
     return ws, rank, local
 
 
-def cpu_reference_run(cfg: dict, steps: int, warmup: int, budget_s: float):
-    """Time the reference's VecEngine<uint64_t> (oracle/_ref) on this host."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from oracle import RefEngine, RefLib
+_REF = {}
 
-    lib = RefLib()
-    cores = os.cpu_count() or 1
-    os.environ.setdefault("OMP_PROC_BIND", "close")
+
+def _cpu_info() -> tuple[str, int]:
+    """(CPU model of this host, usable hardware threads), taken once before the reference library loads:
+    libgomp with OMP_PROC_BIND=close pins the loading thread to one CPU, which would shrink the affinity mask."""
+    if "cpu" in _REF:
+        return _REF["cpu"]
+    model = "unknown CPU"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = os.cpu_count() or 1
+    _REF["cpu"] = (model, cores)
+    return model, cores
+
+
+def _ref_lib():
+    """The reference's own VecEngine for the CPU arm: built on THIS host with -march=native from the
+    reference sources shipped in baseline/_ref/proj (oracle/Makefile `native`, once per host), else the
+    prebuilt oracle/_ref/libocref.so (-march=x86-64-v3). Returns (RefLib, build description)."""
+    if "lib" in _REF:
+        return _REF["lib"], _REF["build"]
+    _cpu_info()
+    os.environ.setdefault("OMP_PROC_BIND", "close")  # read by libgomp when the library loads
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import REF_SO, RefLib
+
+    native = os.path.join(ROOT, "baseline", "_ref", "libocref_native.so")
+    src = os.path.join(ROOT, "baseline", "_ref", "proj", "include", "octsca", "engine_vec.hpp")
+    note = ""
+    if not os.path.exists(native) and os.path.exists(src):
+        import fcntl
+        import subprocess
+
+        with open(os.path.join(ROOT, "baseline", "_ref", ".build.lock"), "w") as lk:
+            fcntl.flock(lk, fcntl.LOCK_EX)  # the driver may start both arms back to back
+            if not os.path.exists(native):
+                r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "native"],
+                                   capture_output=True, text=True, timeout=600)
+                if r.returncode:
+                    note = f" (native build failed: {r.stderr.strip().splitlines()[-1:] or r.returncode})"
+    lib, build = None, None
+    if os.path.exists(native):
+        try:
+            lib, build = RefLib(native), "reference sources compiled on this host: g++ -std=c++20 -O3 -march=native -fopenmp"
+        except OSError as ex:
+            note = f" (native library failed to load: {ex})"
+    if lib is None:
+        lib, build = RefLib(REF_SO), "prebuilt oracle/_ref/libocref.so: g++ -std=c++20 -O3 -march=x86-64-v3 -fopenmp" + note
+    _REF["lib"], _REF["build"] = lib, build
+    return lib, build
+
+
+def cpu_reference_run(cfg: dict, steps: int, warmup: int, budget_s: float):
+    """Time the reference's VecEngine<uint64_t> (engine_vec.hpp:184-213) on this host's cores: `warmup`
+    (at most 1) untimed MCS, then MCS until `steps` or the time budget (at least one).
+    Returns (updates/ns, threads, MCS timed, seconds, description)."""
+    lib, build = _ref_lib()  # puts oracle/ on sys.path
+    from oracle import RefEngine
+
+    model, cores = _cpu_info()
     X, Y = cfg["X"], cfg["Y"]
     eng = RefEngine(lib, X, Y, 1, workers=cores)
     for _ in range(max(0, min(warmup, 1))):
@@ -214,7 +281,9 @@ def cpu_reference_run(cfg: dict, steps: int, warmup: int, budget_s: float):
         if time.perf_counter() - t0 > budget_s:
             break
     el = time.perf_counter() - t0
-    return X * Y * done / (el * 1e9), cores, done, el
+    desc = (f"{done} MCS of {X}x{Y} p={cfg['p']} q={cfg['q']} after {min(warmup, 1)} warm-up MCS, steps only "
+            f"(no W2), {el:.1f} s; VecEngine<uint64_t> workers={cores} OMP_PROC_BIND=close on {model}; {build}")
+    return X * Y * done / (el * 1e9), cores, done, el, desc
 
 
 def main():
@@ -224,9 +293,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU reference work")
+    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of CPU reference work")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the short windows of the other BASELINE configs (c2h, c3, c4, c5) in the c2 line")
     ap.add_argument("--from-flat", action="store_true", help="time MCS 1..K instead of the job's last K MCS")
     ap.add_argument("--rng", default="xoshiro", choices=["xoshiro", "counter"],
                     help="xi source: the reference's xoshiro streams, or the opt-in counter-based mode "
@@ -253,16 +324,22 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        v, cores, done, el = cpu_reference_run(cfg, K, W, args.cpu_budget)
-        sample = f"{done} MCS of {cfg['X']}x{cfg['Y']} (steps only, no W2), {el:.1f} s"
-        print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": "updates/ns",
-                          "n_gpus": ws, "steps": done, "warmup": min(W, 1), "ms_per_step": el * 1e3 / done,
-                          "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u64",
-                          "data": "synthetic (flat start, seed 1)", "config": config_key,
-                          "cpu_baseline": {"value": v, "unit": "updates/ns", "cores": cores, "kind": "reference",
-                                           "sample": sample},
-                          "e2e": {"value": v, "unit": "updates/ns", "h2d_bytes_per_step": 0,
-                                  "d2h_bytes_per_step": 0}}))
+        v, cores, done, el, sample = cpu_reference_run(cfg, K, W, args.cpu_budget)
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "updates/ns",
+                "n_gpus": ws, "steps": done, "warmup": min(W, 1), "ms_per_step": el * 1e3 / done,
+                "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u64",
+                "data": "synthetic (flat start, seed 1)", "config": config_key,
+                "cpu_baseline": {"value": v, "unit": "updates/ns", "cores": cores, "kind": "reference",
+                                 "sample": sample},
+                "e2e": {"value": v, "unit": "updates/ns", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        if ws == 1 and args.config == "c2" and not args.no_configs:
+            line["configs"] = {}
+            for name in CONFIG_WINDOWS:
+                c = CONFIGS[name]
+                cv, cc, cd, cel, cs = cpu_reference_run(c, 1000, 1, CONFIG_CPU_BUDGET)
+                line["configs"][name] = {"workload": c["workload"], "value": cv, "unit": "updates/ns",
+                                         "ms_per_mcs": cel * 1e3 / cd, "cores": cc, "sample": cs}
+        print(json.dumps(line))
         return
 
     import numpy as np
@@ -350,46 +427,56 @@ def main():
     del job, engs
     torch.cuda.synchronize()
 
+    def timed(job, engs, prm_, t0_, sched_, targets_, clk_device=None):
+        """The K timed MCS (targets_) of a prepared job: CUDA events on the engines' stream around the whole
+        window and around each step() segment, W^2 measured at the schedule points inside the window.
+        Returns (window ms, step ms, records, launches, clocks summary), max over ranks."""
+        seg_events, records = [], []
+        launches0 = sum(e.launches for e in engs)
+        barrier()
+        torch.cuda.synchronize()
+        clk = ClockSampler(clk_device) if clk_device is not None else None
+        if clk:
+            clk.__enter__()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        t = t0_
+        for target in targets_:
+            if target > t:
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                job.step(prm_, target - t)
+                b.record(stream)
+                seg_events.append((a, b))
+                t = target
+            if target in sched_:
+                records.append(job.measure())
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if clk:
+            clk.__exit__(None, None, None)
+        barrier()
+        ms_ = ev0.elapsed_time(ev1)
+        step_ms_ = sum(a.elapsed_time(b) for a, b in seg_events)
+        launches_ = sum(e.launches for e in engs) - launches0
+        if ws > 1:
+            tt = torch.tensor([ms_, step_ms_], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            ms_, step_ms_ = float(tt[0]), float(tt[1])
+            lt = torch.tensor([launches_], device=dev)
+            torch.distributed.all_reduce(lt)
+            launches_ = int(lt[0])
+        return ms_, step_ms_, records, launches_, (clk.summary() if clk else None)
+
     # ---- timed region, device-resident ----
     job, engs = make()
     if t_start:
         job.step(prm, t_start)  # untimed: the job's state at the start of the timed window
         _sync_all(engs)
     torch.cuda.synchronize()
-    seg_events = []
-    records = []
-    launches0 = sum(e.launches for e in engs)
-    barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        t = t_start
-        for target in targets:
-            if target > t:
-                a = torch.cuda.Event(enable_timing=True)
-                b = torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                job.step(prm, target - t)
-                b.record(stream)
-                seg_events.append((a, b))
-                t = target
-            if target in sched:
-                records.append(job.measure())
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    barrier()
-    ms = ev0.elapsed_time(ev1)
-    step_ms = sum(a.elapsed_time(b) for a, b in seg_events)
-    launches = sum(e.launches for e in engs) - launches0
-    if ws > 1:
-        tt = torch.tensor([ms, step_ms, float(launches)], device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms, step_ms = float(tt[0]), float(tt[1])
-        lt = torch.tensor([launches], device=dev)
-        torch.distributed.all_reduce(lt)
-        launches = int(lt[0])
+    ms, step_ms, records, launches, clocks = timed(job, engs, prm, t_start, sched, targets, clk_device=local)
     value = X * Y * K / (ms * 1e6)
     kernel_ms = step_ms / K  # per MCS, all launches of the step calls
     peak, peak_src = _peaks()
@@ -399,7 +486,24 @@ def main():
     alg_bytes = X * Y // ws * mcs_per_launch
     launch_ms = kernel_ms * mcs_per_launch
     achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
-    final_checksum = engs[0].checksum() if ws == 1 and X * Y <= (1 << 32) else None
+    final_checksum = engs[0].checksum() if ws == 1 else None
+    # Correctness digest of the timed job (every N): the exact global power sums S_k = sum h^k at the
+    # window's last W^2 point and each stripe's field_checksum (its own rows as a field; N = 1: the
+    # lattice's). Weak-scaled c2 from the flat start with p = 1 is deterministic and invariant under even
+    # row shifts, so every 2^16-row stripe at N GPUs must equal the N = 1 lattice (stripe checksum = the N = 1
+    # final_checksum) and S_k(N) = N * S_k(1).
+    job.sync()
+    rec = records[-1] if records else job.measure()
+    mine = engs[0].checksum()
+    allc = [hex(mine)]
+    if ws > 1:
+        allc = [None] * ws
+        torch.distributed.all_gather_object(allc, hex(mine))
+    digest = {"t": rec.t, "power_sums": [str(v) for v in rec.power_sums], "W2": rec.W2, "mean_h": rec.mean_h,
+              "stripe_checksums": allc}
+    if ws > 1 and scaling == "weak" and cfg["p"] == 1.0 and cfg["q"] == 0.0:
+        digest["expected"] = ("p=1 from the flat start: every stripe checksum equals the N=1 c2 final_checksum; "
+                              "power_sums equal N x the N=1 power_sums")
     _close(job)
     del job, engs
 
@@ -469,13 +573,65 @@ def main():
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            v, cores, done, el = cpu_reference_run(cfg, 1000, 1, args.cpu_budget)
-            cpu = {"value": v, "unit": "updates/ns", "cores": cores, "kind": "reference",
-                   "sample": f"{done} MCS of {X}x{Y} p={cfg['p']} q={cfg['q']} after 1 warm-up MCS, "
-                             f"steps only (no W2), {el:.1f} s, VecEngine<uint64_t> workers={cores}"}
+            v, cores, done, el, sample = cpu_reference_run(cfg, 1000, 1, args.cpu_budget)
+            cpu = {"value": v, "unit": "updates/ns", "cores": cores, "kind": "reference", "sample": sample}
         except Exception as ex:  # reported, never fatal
             cpu = {"value": None, "unit": "updates/ns", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {ex}"}
+
+    def dram(kn: str, cname: str, lms: float):
+        """ncu DRAM bytes per launch (profiles/ncu_summary.json) over this run's event time per launch."""
+        tr = _traffic(kn, cname)
+        if not tr:
+            return None, None, tr
+        gbs = tr / (lms * 1e-3) / 1e9
+        return gbs, gbs / peak, tr
+
+    # ---- the other BASELINE configs in short windows (single GPU, the c2 line only) ----
+    configs = None
+    if ws == 1 and args.config == "c2" and args.rng == "xoshiro" and not args.no_configs:
+        configs = {}
+        sched_all = octgpu.log_schedule(SCHEDULE_TMAX, SCHEDULE_PPD)
+        for name, Kc in CONFIG_WINDOWS.items():
+            c = CONFIGS[name]
+            latc = octgpu.LatticeConfig(c["X"], c["Y"], 64)
+            prmc = octgpu.UpdateParams.make(c["p"], c["q"])
+            t0c, schedc, targetsc, windowc = timed_window(Kc, not c.get("window", True), sched_all)
+            eng = octgpu.GpuEngine(latc, 1, device=local)
+            eng.set_stream(stream.cuda_stream)
+            eng.step(prmc, 2)  # warm-up of this config's kernels (plans, tensor maps), then the window's start
+            eng.sync()
+            eng = None
+            eng = octgpu.GpuEngine(latc, 1, device=local)
+            eng.set_stream(stream.cuda_stream)
+            if t0c:
+                eng.step(prmc, t0c)
+                eng.sync()
+            msc, stepc, recc, lc, clkc = timed(eng, [eng], prmc, t0c, schedc, targetsc, clk_device=local)
+            kc, mplc = _mcs_kernel(prmc, c["Y"], c["X"] // 128, 1)
+            kmsc = stepc / Kc
+            lmsc = kmsc * mplc
+            gbs, dfrac, trc = dram(kc, name, lmsc)
+            endrec = recc[-1] if recc and recc[-1].t == t0c + Kc else eng.measure()  # W^2 at the window's end
+            entry = {"workload": c["workload"], "value": c["X"] * c["Y"] * Kc / (msc * 1e6), "unit": "updates/ns",
+                     "steps": Kc, "window": windowc, "ms_per_step": msc / Kc, "ms_per_mcs": kmsc,
+                     "kernel": f"{kc} ({mplc} MCS per launch)", "launch_ms": lmsc,
+                     "roofline_frac": c["X"] * c["Y"] * mplc / (lmsc * 1e-3) / 1e9 / peak,
+                     "dram_gbs": gbs, "dram_frac": dfrac, "dram_bytes_per_launch": trc,
+                     "int_pipe": _int_pipe(kc, name) if name == "c4" else None,
+                     "gpu_launches": lc, "clocks": clkc, "measurements": len(recc),
+                     "final_checksum": hex(eng.checksum()), "t_end": eng.t, "W2": endrec.W2,
+                     "power_sums": [str(v) for v in endrec.power_sums]}
+            eng = None
+            if rank == 0 and not args.no_cpu_baseline:
+                try:
+                    cv, cc, cd, cel, cs = cpu_reference_run(c, 1000, 1, CONFIG_CPU_BUDGET)
+                    entry["cpu_baseline"] = {"value": cv, "unit": "updates/ns", "cores": cc, "kind": "reference",
+                                             "sample": cs}
+                    entry["vs_cpu"] = entry["value"] / cv
+                except Exception as ex:  # reported, never fatal
+                    entry["cpu_baseline"] = {"value": None, "sample": f"unavailable: {ex}"}
+            configs[name] = entry
 
     if rank == 0:
         line = {
@@ -485,16 +641,18 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": _traffic(kname, args.config), "kernel": f"{kname} ({mcs_per_launch} MCS per launch)",
                          "alg_bytes_per_launch": alg_bytes, "launch_ms": launch_ms, "kernel_ms": kernel_ms,
-                         "peak_source": peak_src,
+                         "peak_source": peak_src, "dram_gbs": dram(kname, args.config, launch_ms)[0],
+                         "dram_frac": dram(kname, args.config, launch_ms)[1],
                          "note": "alg bytes = 1 B/site-update (2 slope bits x 2 reads + 2 writes per MCS); the fused "
                                  "kernels move ~0.5 B (k_mcs_bulk) / ~0.25 B (k_mcs_deep) of DRAM traffic per update, "
                                  "so frac exceeds 1; traffic = ncu dram bytes per launch (profiles/ncu_summary.json)"},
             "int_pipe": _int_pipe(kname, args.config),
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "digest": digest,
             "transport": transport_used[-1] if transport_used else None,
             "measurements": len(records),
             "W2_last": records[-1].W2 if records else None,
             "final_checksum": hex(final_checksum) if final_checksum is not None else None,
+            "configs": configs,
         }
         print(json.dumps(line))
     if ws > 1:

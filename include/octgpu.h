@@ -114,6 +114,11 @@ int octgpu_set_state(octgpu_engine* e, uint64_t t_mcs, int phase, const void* pl
 int octgpu_set_stream(octgpu_engine* e, void* cuda_stream);
 /* Block until all enqueued work finished; surfaces asynchronous CUDA errors. */
 int octgpu_sync(octgpu_engine* e);
+/* Periodic engines take their two plane sets from a library-private stream-ordered pool
+ * (cudaMemPoolCreate) that keeps freed memory for the next engine of the process (no
+ * re-mapping on resume / re-creation). This returns the pool's unused memory on `device`
+ * to the driver (for cudaMalloc, PyTorch, NCCL). No reference counterpart. */
+int octgpu_release_pool(int device);
 
 /* ---- the hot path ---- */
 
@@ -153,7 +158,9 @@ uint64_t octgpu_master_seed(const octgpu_engine* e); /* RngStreamSet::master_see
 int octgpu_get_planes(octgpu_engine* e, void* out);
 /* VecEngine::streams().states() (rng.hpp:102-108), Y*4 words */
 int octgpu_get_states(octgpu_engine* e, uint64_t* out);
-/* field_checksum(field()) (slope_field.hpp:232-246) */
+/* field_checksum(field()) (slope_field.hpp:232-246). On a row stripe: the same FNV-1a over the
+ * stripe's own rows (4 planes x L rows, reference layout) then t, i.e. the checksum of the stripe as an
+ * L-row field (a per-stripe correctness digest; sync the whole group first). */
 int octgpu_field_checksum(octgpu_engine* e, uint64_t* out);
 
 /* ---- measurement ---- */
@@ -166,6 +173,11 @@ int octgpu_measure(octgpu_engine* e, octgpu_moments* out);
 /* VecEngine::heights() = reconstruct_heights(field) (engine_vec.hpp:207):
  * out[y*X + x] int32, h(0,0) = 0. */
 int octgpu_heights(octgpu_engine* e, int32_t* out);
+/* row_balances(field) / col_balances(field) (slope_field.hpp:177-202): rows_out[y] =
+ * sum_x sigma_x-(x,y) (Y entries), cols_out[x] = sum_y sigma_y-(x,y) (X entries); either
+ * pointer may be NULL. On a row stripe: its own rows (rows_out: L entries, global rows
+ * y0..y0+L-1) and column sums over them (the lattice's col_balances = the sum over stripes). */
+int octgpu_balances(octgpu_engine* e, int64_t* rows_out, int64_t* cols_out);
 
 /* ---- row stripes (multi-GPU) ----
  * A stripe engine owns global rows [y0, y1) (at least 4) of an X x Y periodic

@@ -422,6 +422,96 @@ void oo_power_sums(uint32_t X, uint32_t Y, const int32_t* h, uint64_t* out8) {
     }
 }
 
+/* ---- slope_field.hpp:159-229 + measure.cpp:24-51 at scale: the same reconstruction (curl_check, row 0
+ * by its sigma_x- prefix and closure, every column by its sigma_y- walk from row 0 and closure), reduced
+ * to the exact power sums without materialising the HeightMap; OpenMP over rows (curl) and over column
+ * blocks (the column walks keep the reference's y order). For the at-scale parity tests (2^32+ sites),
+ * where the scalar oo_reconstruct + oo_power_sums would need 16+ GiB and minutes. Returns 0, or 2 with
+ * *kind = 1 curl (*where = y * X + x of the first bad plaquette, *count), 2 row 0, 3 column (*where). */
+int oo_measure_planes_mt(uint32_t X, uint32_t Y, uint32_t w, const uint64_t* planes, uint64_t* out8, int* kind,
+                         uint64_t* where, uint64_t* count) {
+    uint64_t bad = 0, first = ~(uint64_t)0;
+#pragma omp parallel for schedule(static) reduction(+ : bad) reduction(min : first)
+    for (uint32_t y = 0; y < Y; ++y) {
+        uint32_t ym = y == 0 ? Y - 1 : y - 1;
+        for (uint32_t x = 0; x < X; ++x) {
+            uint32_t xm = x == 0 ? X - 1 : x - 1;
+            int lhs = pm(minus_bit(planes, X, Y, w, 0, x, y)) - pm(minus_bit(planes, X, Y, w, 0, x, ym));
+            int rhs = pm(minus_bit(planes, X, Y, w, 1, x, y)) - pm(minus_bit(planes, X, Y, w, 1, xm, y));
+            if (lhs != rhs) {
+                uint64_t idx = (uint64_t)y * X + x;
+                if (idx < first) first = idx;
+                ++bad;
+            }
+        }
+    }
+    *count = bad;
+    if (bad) {
+        *kind = 1;
+        *where = first;
+        return 2;
+    }
+    int64_t* row0 = (int64_t*)malloc((size_t)X * sizeof(int64_t));
+    row0[0] = 0;
+    for (uint32_t x = 1; x < X; ++x) row0[x] = row0[x - 1] + pm(minus_bit(planes, X, Y, w, 0, x, 0));
+    if (row0[X - 1] + pm(minus_bit(planes, X, Y, w, 0, 0, 0)) != row0[0]) {
+        free(row0);
+        *kind = 2;
+        *where = 0;
+        return 2;
+    }
+    const uint32_t CB = 256;  /* columns per task */
+    const uint32_t nblk = (X + CB - 1) / CB;
+    i128 S[4] = {0, 0, 0, 0};
+    uint64_t col_bad = ~(uint64_t)0;
+#pragma omp parallel
+    {
+        i128 s[4] = {0, 0, 0, 0};
+        int64_t h[256];
+        uint64_t cb = ~(uint64_t)0;
+#pragma omp for schedule(dynamic, 1)
+        for (uint32_t b = 0; b < nblk; ++b) {
+            uint32_t xa = b * CB, xb = xa + CB < X ? xa + CB : X;
+            for (uint32_t x = xa; x < xb; ++x) h[x - xa] = row0[x];
+            for (uint32_t y = 0; y < Y; ++y) {
+                int64_t s1 = 0;
+                i128 s2 = 0, s3 = 0, s4 = 0;
+                for (uint32_t x = xa; x < xb; ++x) {
+                    if (y) h[x - xa] += pm(minus_bit(planes, X, Y, w, 1, x, y));
+                    i128 v = h[x - xa], v2 = v * v;
+                    s1 += h[x - xa];
+                    s2 += v2;
+                    s3 += v2 * v;
+                    s4 += v2 * v2;
+                }
+                s[0] += s1;
+                s[1] += s2;
+                s[2] += s3;
+                s[3] += s4;
+            }
+            for (uint32_t x = xa; x < xb; ++x)
+                if (h[x - xa] + pm(minus_bit(planes, X, Y, w, 1, x, 0)) != row0[x] && x < cb) cb = x;
+        }
+#pragma omp critical
+        {
+            for (int k = 0; k < 4; ++k) S[k] += s[k];
+            if (cb < col_bad) col_bad = cb;
+        }
+    }
+    free(row0);
+    if (col_bad != ~(uint64_t)0) {
+        *kind = 3;
+        *where = col_bad;
+        return 2;
+    }
+    for (int k = 0; k < 4; ++k) {
+        out8[2 * k] = (uint64_t)S[k];
+        out8[2 * k + 1] = (uint64_t)((unsigned __int128)S[k] >> 64);
+    }
+    *kind = 0;
+    return 0;
+}
+
 /* ---- measure.cpp:24-51 (height_moments, sequential double) ---- */
 void oo_height_moments(uint32_t X, uint32_t Y, const int32_t* h, double* out6) {
     size_t N = (size_t)X * Y;

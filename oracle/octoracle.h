@@ -83,6 +83,9 @@ int oo_reconstruct(uint32_t X, uint32_t Y, uint32_t w, const uint64_t* planes, i
 
 /* Exact integer power sums S_k = sum h^k, k = 1..4, as (lo, hi) int128 halves */
 void oo_power_sums(uint32_t X, uint32_t Y, const int32_t* h, uint64_t* out8);
+/* reconstruct_heights + the exact power sums at scale (OpenMP; no HeightMap): see .c */
+int oo_measure_planes_mt(uint32_t X, uint32_t Y, uint32_t w, const uint64_t* planes, uint64_t* out8, int* kind,
+                         uint64_t* where, uint64_t* count);
 /* measure.cpp:24-51 restated: {mean, m2, m3, m4, skew, kurt} in sequential double */
 void oo_height_moments(uint32_t X, uint32_t Y, const int32_t* h, double* out6);
 /* measure.cpp:143-165 */

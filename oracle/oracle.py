@@ -69,6 +69,7 @@ class Oracle:
         L.oo_curl_check.restype = u64
         L.oo_reconstruct.argtypes = [u32, u32, u32, _u64p, _i32p, P(i32), P(u32)]
         L.oo_power_sums.argtypes = [u32, u32, _i32p, _u64p]
+        L.oo_measure_planes_mt.argtypes = [u32, u32, u32, _u64p, _u64p, P(i32), P(u64), P(u64)]
         L.oo_height_moments.argtypes = [u32, u32, _i32p, _f64p]
         L.oo_log_schedule.argtypes = [u64, u32, _u64p, u32]
         L.oo_log_schedule.restype = u32
@@ -150,6 +151,19 @@ class Oracle:
         self.L.oo_power_sums(X, Y, np.ascontiguousarray(h, np.int32), out)
         return [_i128(int(out[2 * k]), int(out[2 * k + 1])) for k in range(4)]
 
+    def measure_planes(self, planes: np.ndarray, w: int = 64):
+        """reconstruct_heights + exact power sums straight from reference-layout planes (OpenMP, no
+        HeightMap; for lattices of 2^32+ sites). Returns ([S1..S4], None) or (None, (kind, where, count))."""
+        _, Y, n = planes.shape
+        X = n * 2 * w
+        out = np.zeros(8, np.uint64)
+        kind, where, count = C.c_int(), C.c_uint64(), C.c_uint64()
+        p = planes if (planes.dtype == np.uint64 and planes.flags.c_contiguous) else np.ascontiguousarray(planes, np.uint64)
+        rc = self.L.oo_measure_planes_mt(X, Y, w, p, out, C.byref(kind), C.byref(where), C.byref(count))
+        if rc:
+            return None, (kind.value, where.value, count.value)
+        return [_i128(int(out[2 * k]), int(out[2 * k + 1])) for k in range(4)], None
+
     def height_moments(self, h: np.ndarray) -> np.ndarray:
         Y, X = h.shape
         out = np.zeros(6, np.float64)
@@ -227,6 +241,7 @@ class RefLib:
         L.ocref_checksum.argtypes = [vp]
         L.ocref_checksum.restype = u64
         L.ocref_heights.argtypes = [vp, _i32p]
+        L.ocref_balances.argtypes = [vp, vp, vp]
         L.ocref_measure.argtypes = [vp, _f64p]
         L.ocref_height_moments.argtypes = [u32, u32, _i32p, _f64p]
         L.ocref_run.argtypes = [vp, dbl, dbl, i32, i32, u64, u32, _f64p, u32, P(u32)]
@@ -313,6 +328,12 @@ class RefEngine:
         out = np.zeros((self.Y, self.X), np.int32)
         self.lib.check(self.lib.L.ocref_heights(self.h, out))
         return out
+
+    def balances(self) -> tuple[np.ndarray, np.ndarray]:
+        """(row_balances, col_balances) of the reference field (slope_field.hpp:177-202)."""
+        rows, cols = np.zeros(self.Y, np.int64), np.zeros(self.X, np.int64)
+        self.lib.L.ocref_balances(self.h, rows.ctypes.data_as(C.c_void_p), cols.ctypes.data_as(C.c_void_p))
+        return rows, cols
 
     def measure(self) -> np.ndarray:
         out = np.zeros(4, np.float64)

@@ -55,7 +55,20 @@ struct EngineBase {
     virtual uint64_t checksum() const = 0;
     virtual HeightMap heights() const = 0;
     virtual const LatticeConfig& cfg() const = 0;
+    virtual void balances(int64_t* rows, int64_t* cols) const = 0;  // slope_field.hpp:177-202
 };
+
+template <typename Word>
+void copy_balances(const SlopeField<Word>& f, int64_t* rows, int64_t* cols) {
+    if (rows) {
+        auto r = row_balances(f);
+        std::memcpy(rows, r.data(), r.size() * sizeof(int64_t));
+    }
+    if (cols) {
+        auto c = col_balances(f);
+        std::memcpy(cols, c.data(), c.size() * sizeof(int64_t));
+    }
+}
 
 template <typename Word>
 struct VecBox final : EngineBase {
@@ -86,6 +99,7 @@ struct VecBox final : EngineBase {
     uint64_t checksum() const override { return field_checksum(eng.field()); }
     HeightMap heights() const override { return eng.heights(); }
     const LatticeConfig& cfg() const override { return c; }
+    void balances(int64_t* rows, int64_t* cols) const override { copy_balances(eng.field(), rows, cols); }
 };
 
 struct RefBox final : EngineBase {
@@ -121,6 +135,12 @@ struct RefBox final : EngineBase {
     }
     HeightMap heights() const override { return eng.heights(); }
     const LatticeConfig& cfg() const override { return c; }
+    void balances(int64_t* rows, int64_t* cols) const override {
+        if (c.w == 32)
+            copy_balances(eng.slope_field<uint32_t>(), rows, cols);
+        else
+            copy_balances(eng.slope_field<uint64_t>(), rows, cols);
+    }
 };
 
 template <typename Word>
@@ -197,6 +217,9 @@ int ocref_phase(void* h) { return static_cast<EngineBase*>(h)->phase(); }
 void ocref_planes(void* h, uint64_t* out) { static_cast<EngineBase*>(h)->planes(out); }
 void ocref_states(void* h, uint64_t* out) { static_cast<EngineBase*>(h)->states(out); }
 uint64_t ocref_checksum(void* h) { return static_cast<EngineBase*>(h)->checksum(); }
+
+// row_balances / col_balances (slope_field.hpp:177-202) of the engine's field; either pointer may be null
+void ocref_balances(void* h, int64_t* rows, int64_t* cols) { static_cast<EngineBase*>(h)->balances(rows, cols); }
 
 int ocref_heights(void* h, int32_t* out) {
     try {

@@ -7,13 +7,13 @@ package is the host-side mirror of the reference interface.
 """
 from ._lib import ConfigError, CudaError, InvariantError, IoError, OctError
 from .engine import (GpuEngine, HeightMap, MeasurementRecord, RngStreamSet, SlopeField, field_checksum,
-                     new_flat)
+                     new_flat, release_pool)
 from .params import DyadicPlan, LatticeConfig, ProbMode, ProbSpec, UpdateParams, log_schedule
 from .run import run
 
 __all__ = [
     "ConfigError", "CudaError", "InvariantError", "IoError", "OctError", "GpuEngine", "HeightMap",
-    "MeasurementRecord", "RngStreamSet", "SlopeField", "field_checksum", "new_flat", "DyadicPlan",
+    "MeasurementRecord", "RngStreamSet", "SlopeField", "field_checksum", "new_flat", "release_pool", "DyadicPlan",
     "LatticeConfig", "ProbMode", "ProbSpec", "UpdateParams", "log_schedule", "run",
 ]
 __version__ = "0.1.0"

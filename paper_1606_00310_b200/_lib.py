@@ -102,7 +102,8 @@ EXPORTS = (
     "octgpu_stripe_ipc_open", "octgpu_stripe_connect", "octgpu_stripe_pass", "octgpu_stripe_pull",
     "octgpu_stripe_disconnect", "octgpu_set_tile_shift", "octgpu_stripes_combine",
     "octgpu_set_rng", "octgpu_get_rng",
-    "octgpu_stripe_y0", "octgpu_stripe_rows", "octgpu_height_moments",
+    "octgpu_stripe_y0", "octgpu_stripe_rows", "octgpu_height_moments", "octgpu_release_pool",
+    "octgpu_balances",
 )
 
 _lib = None
@@ -166,6 +167,8 @@ def lib() -> C.CDLL:
         "octgpu_stripe_y0": (u32, [vp]),
         "octgpu_stripe_rows": (u32, [vp]),
         "octgpu_height_moments": (None, [u32, u32, vp, vp]),
+        "octgpu_release_pool": (i32, [i32]),
+        "octgpu_balances": (i32, [vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -325,7 +325,10 @@ struct octgpu_engine {
     void* scratch = nullptr;
     MeasureResult* res_dev = nullptr;
     MeasureResult* res_host = nullptr;
-    std::map<uint64_t, uint64_t*> jtabs;  // draws -> device 4-bit table of T^draws
+    std::map<uint64_t, uint64_t*> jtabs;  // draws per sweep -> device 4-bit table of T^draws
+    uint64_t* pend_tab = nullptr;          // table of T^pending (materialize), device
+    uint64_t* pend_host = nullptr;         // ... and its pinned upload buffer
+    cudaEvent_t pend_ev = nullptr;         // the last jump that read them
     uint64_t launches = 0;
     // fused-MCS implementation: 2 = bulk-copy staged (k_mcs_bulk), 1 = register-prefetch (k_mcs)
     int mcs_impl = 2;
@@ -419,13 +422,24 @@ int get_table(octgpu_engine* e, uint64_t draws_n, uint64_t** out) {
 
 void trace_create(const char* what, bool start);
 
-// Apply owed draws to every row stream (lazy advance of constant-xi sweeps).
+// Apply owed draws to every row stream (lazy advance of constant-xi sweeps). The table of T^pending is
+// not cached (every pending count is different): it goes through one engine-owned pinned + device buffer
+// pair, reused once the previous jump that read it has completed (pend_ev).
 int materialize(octgpu_engine* e) {
     if (!e->pending) return OCTGPU_OK;
-    uint64_t* tab = nullptr;
-    int rc = get_table(e, e->pending, &tab);
-    if (rc) return rc;
-    CK(launch_apply_jump(e->rng[e->rcur], e->Y, tab, e->stream));
+    const size_t bytes = size_t(64) * 16 * 4 * sizeof(uint64_t);
+    if (!e->pend_tab) {
+        CK(cudaMalloc(reinterpret_cast<void**>(&e->pend_tab), bytes));
+        CK(cudaMallocHost(reinterpret_cast<void**>(&e->pend_host), bytes));
+        CK(cudaEventCreateWithFlags(&e->pend_ev, cudaEventDisableTiming));
+    } else {
+        CK(cudaEventSynchronize(e->pend_ev));
+    }
+    const std::vector<uint64_t> tab = power_table(e->pending);
+    std::memcpy(e->pend_host, tab.data(), bytes);
+    CK(cudaMemcpyAsync(e->pend_tab, e->pend_host, bytes, cudaMemcpyHostToDevice, e->stream));
+    CK(launch_apply_jump(e->rng[e->rcur], e->Y, e->pend_tab, e->stream));
+    CK(cudaEventRecord(e->pend_ev, e->stream));
     ++e->launches;
     e->pending = 0;
     return OCTGPU_OK;
@@ -547,6 +561,31 @@ int alloc_p2p(octgpu_engine* e) {
     return OCTGPU_OK;
 }
 
+// The library's stream-ordered pool for periodic plane sets, one per device, created on first use with a
+// release threshold of "keep everything": an engine re-created in the same process (resume, e2e runs) reuses
+// the memory instead of paying cudaMalloc's page mapping again (40-130 ms for 2 GiB at 2^16^2).
+std::mutex g_pool_mu;
+std::map<int, cudaMemPool_t> g_pools;
+
+int engine_pool(int device, cudaMemPool_t* out) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto it = g_pools.find(device);
+    if (it == g_pools.end()) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        cudaMemPool_t pool = nullptr;
+        CK(cudaMemPoolCreate(&pool, &props));
+        uint64_t keep = ~uint64_t(0);
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        it = g_pools.emplace(device, pool).first;
+    }
+    *out = it->second;
+    return OCTGPU_OK;
+}
+
 int alloc_engine(octgpu_engine* e) {
     CK(cudaSetDevice(e->device));
     CK(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
@@ -556,17 +595,27 @@ int alloc_engine(octgpu_engine* e) {
     // = max) across engines: an engine re-created in the same process (resume, e2e runs) reuses the
     // memory instead of paying cudaMalloc's page mapping again (40-130 ms for 2 GiB at 2^16^2). Stripes
     // keep cudaMalloc: their plane sets are exported with cudaIpcGetMemHandle (p2p.cu).
+    // The pool is the library's own (cudaMemPoolCreate), not the device's default pool, so the keep-all
+    // release threshold does not leak into other users of cudaMallocAsync (PyTorch, NCCL). Memory a freed
+    // engine leaves in it is returned with octgpu_release_pool(device), and automatically when a later
+    // plane-set allocation of this library would otherwise fail.
     e->pooled = !e->stripe;
+    cudaMemPool_t pool = nullptr;
     if (e->pooled) {
-        cudaMemPool_t pool;
-        CK(cudaDeviceGetDefaultMemPool(&pool, e->device));
-        uint64_t keep = ~uint64_t(0);
-        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        int rc = engine_pool(e->device, &pool);
+        if (rc) return rc;
     }
     for (int i = 0; i < 2; ++i) {
-        if (e->pooled)
-            CK(cudaMallocAsync(&e->planes[i], e->set_bytes(), e->stream));
-        else
+        if (e->pooled) {
+            cudaError_t ae = cudaMallocFromPoolAsync(&e->planes[i], e->set_bytes(), pool, e->stream);
+            if (ae == cudaErrorMemoryAllocation) {  // trim what earlier engines left and retry once
+                cudaGetLastError();
+                CK(cudaStreamSynchronize(e->stream));
+                CK(cudaMemPoolTrimTo(pool, 0));
+                ae = cudaMallocFromPoolAsync(&e->planes[i], e->set_bytes(), pool, e->stream);
+            }
+            CK(ae);
+        } else
             CK(cudaMalloc(&e->planes[i], e->set_bytes()));
         CK(cudaMalloc(reinterpret_cast<void**>(&e->rng[i]), e->rng_bytes()));
     }
@@ -865,6 +914,9 @@ void octgpu_destroy(octgpu_engine* e) {
     }
     for (auto& kv : e->graph_cache) cudaGraphExecDestroy(kv.second);
     for (auto& kv : e->jtabs) cudaFree(kv.second);
+    if (e->pend_tab) cudaFree(e->pend_tab);
+    if (e->pend_host) cudaFreeHost(e->pend_host);
+    if (e->pend_ev) cudaEventDestroy(e->pend_ev);
     for (void* ptr : e->ipc_opened) cudaIpcCloseMemHandle(ptr);
     if (e->done) cudaFree(e->done);
     if (e->p2p_err) cudaFree(e->p2p_err);
@@ -877,6 +929,20 @@ void octgpu_destroy(octgpu_engine* e) {
         cudaStreamDestroy(e->own_stream);
     }
     delete e;
+}
+
+int octgpu_release_pool(int device) {
+    cudaMemPool_t pool = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        auto it = g_pools.find(device);
+        if (it == g_pools.end()) return OCTGPU_OK;
+        pool = it->second;
+    }
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceSynchronize());  // frees of destroyed engines are stream-ordered
+    CK(cudaMemPoolTrimTo(pool, 0));
+    return OCTGPU_OK;
 }
 
 int octgpu_set_stream(octgpu_engine* e, void* s) {
@@ -1231,7 +1297,6 @@ int octgpu_get_states(octgpu_engine* e, uint64_t* out) {
 
 int octgpu_field_checksum(octgpu_engine* e, uint64_t* out) {
     if (!e || !out) return fail(OCTGPU_ERR_CONFIG, "null argument");
-    if (e->stripe) return fail(OCTGPU_ERR_CONFIG, "octgpu_field_checksum is not available on a row stripe (use the octgpu_stripe_* calls)");
     std::vector<unsigned char> buf(e->host_bytes());
     int rc = octgpu_get_planes(e, buf.data());
     if (rc) return rc;
@@ -1394,6 +1459,28 @@ int octgpu_heights(octgpu_engine* e, int32_t* out) {
     return OCTGPU_OK;
 }
 
+int octgpu_balances(octgpu_engine* e, int64_t* rows_out, int64_t* cols_out) {
+    if (!e || (!rows_out && !cols_out)) return fail(OCTGPU_ERR_CONFIG, "null argument");
+    int rc = use_device(e);
+    if (rc) return rc;
+    // periodic: rows 0..Y-1 in order; stripe: its core rows (global rows y0 .. y0 + L - 1)
+    const uint32_t r0 = e->first_row(), R = e->L;
+    const Geom g = e->geom();
+    long long* d = nullptr;
+    const size_t nr = rows_out ? R : 0, nc = cols_out ? e->X : 0;
+    CK(cudaMalloc(&d, (nr + 2 * nc) * sizeof(long long)));
+    cudaError_t le = launch_balances(e->w, e->planes[e->pcur], g, r0, R, e->X, rows_out ? d : nullptr,
+                                     cols_out ? d + nr : nullptr, d + nr + nc, e->stream);
+    e->launches += (rows_out ? 1 : 0) + (cols_out ? 2 : 0);
+    if (le == cudaSuccess && rows_out)
+        le = cudaMemcpyAsync(rows_out, d, nr * sizeof(long long), cudaMemcpyDeviceToHost, e->stream);
+    if (le == cudaSuccess && cols_out)
+        le = cudaMemcpyAsync(cols_out, d + nr, nc * sizeof(long long), cudaMemcpyDeviceToHost, e->stream);
+    if (le == cudaSuccess) le = cudaStreamSynchronize(e->stream);
+    cudaFree(d);
+    if (le != cudaSuccess) return cuda_fail(le, "balances");
+    return OCTGPU_OK;
+}
 
 // ---------------------------------------------------------------------------
 // Row stripes (multi-GPU): see include/octgpu.h
@@ -1437,7 +1524,10 @@ namespace {
 bool stripe_deep_ok(const octgpu_engine* e, const ProbDev& p, const ProbDev& q) {
     // xoshiro: constant xi only (a live deep pass would not advance the halo rows' streams, which p2p.cu
     // relies on); counter streams have no state, so every cheap mode qualifies
-    const bool size_ok = e->deep == 2 || uint64_t(e->X) * e->L >= (uint64_t(1) << 28);
+    // The size threshold uses the WHOLE lattice (X * Ytot), a quantity every stripe of a group shares: with
+    // the stripe's own row count, an uneven SweepPlan split straddling the threshold would give ranks
+    // different pass lengths (a hang with NCCL, drifting pass counters over peer memory).
+    const bool size_ok = e->deep == 2 || uint64_t(e->X) * e->Ytot >= (uint64_t(1) << 28);
     const bool xi_ok = e->rng_kind == OCTGPU_RNG_COUNTER || (is_const(p) && is_const(q));
     return e->deep && size_ok && e->mcs_impl == 2 && mcs_deep_supported(p.mode, q.mode) && xi_ok;
 }
@@ -1501,7 +1591,7 @@ int octgpu_stripe_mcs_n(octgpu_engine* e, const octgpu_params* prm, uint32_t n_m
         rc = ensure_tmaps_deep(e);
         if (rc) return rc;
         CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
-                           e->deep_S, &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
+                           deep_ring(e, p, q), &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
     } else if (e->mcs_impl == 2) {
         rc = plan_bulk(e, p, q);
         if (rc) return rc;
@@ -1720,7 +1810,7 @@ int octgpu_stripe_pass(octgpu_engine* e, const octgpu_params* prm, uint32_t n_mc
         rc = ensure_tmaps_deep(e);
         if (rc) return rc;
         CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
-                           e->deep_S, &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
+                           deep_ring(e, p, q), &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
     } else {
         rc = plan_bulk(e, p, q);
         if (rc) return rc;

@@ -395,6 +395,97 @@ __global__ void k_heights(const Word* __restrict__ planes, Geom g, uint32_t X, c
     }
 }
 
+// ---- row / column balances (slope_field.hpp:177-202) ----------------------------
+// Rows r0 .. r0+R-1 (physical); the site parity of physical row r is (r ^ ypar) & 1.
+// row_balances: out[y] = 2 * popcount(sigma_x- bits of row r0+y) - X, lane per row.
+template <typename Word>
+__global__ void k_row_balances(const Word* __restrict__ planes, Geom g, uint32_t r0, uint32_t R, uint32_t X,
+                               long long* __restrict__ out) {
+    const uint32_t y = blockIdx.x * blockDim.x + threadIdx.x;
+    if (y >= R) return;
+    const size_t PS = g.plane_stride;
+    const Word* a = planes + r0 + y;
+    const Word* b = planes + PS + r0 + y;
+    long long pop = 0;
+    for (uint32_t k = 0; k < g.n; ++k)
+        pop += __popcll((unsigned long long)a[size_t(k) * g.Y]) + __popcll((unsigned long long)b[size_t(k) * g.Y]);
+    out[y] = 2 * pop - (long long)X;
+}
+
+// col_balances: out[x] += sum over rows of sigma_y-(x, y) (out zeroed by the caller). Warp per (word k,
+// chunk of rows); lane = row. Column x = 2 (W k + b) + e takes its bit from plane Y((e ^ parity(row)) & 1),
+// so each lane's two y-plane words are the even-x (wa) and odd-x (wb) columns of its row; the per-bit
+// counts over the warp's rows come from ballots.
+template <typename Word>
+__global__ void k_col_balances(const Word* __restrict__ planes, Geom g, uint32_t r0, uint32_t R, uint32_t chunk,
+                               unsigned long long* __restrict__ cnt) {
+    constexpr int W = int(sizeof(Word) * 8);
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t chunks = (R + chunk - 1) / chunk;
+    const uint32_t k = warp / chunks, c = warp % chunks;
+    if (k >= g.n) return;
+    const size_t PS = g.plane_stride;
+    const uint32_t ya = c * chunk, yb = min(R, ya + chunk);
+    unsigned int ce[W / 32] = {}, co[W / 32] = {};  // lane holds bits lane, lane + 32 (w = 64)
+    for (uint32_t y0 = ya; y0 < yb; y0 += 32) {
+        const uint32_t y = y0 + lane;
+        Word wa = 0, wb = 0;
+        if (y < yb) {
+            const uint32_t r = r0 + y;
+            const int par = int((r ^ g.ypar) & 1u);
+            const Word v0 = planes[2 * PS + size_t(k) * g.Y + r], v1 = planes[3 * PS + size_t(k) * g.Y + r];
+            wa = par ? v1 : v0;  // even x: plane parity = row parity
+            wb = par ? v0 : v1;
+        }
+#pragma unroll
+        for (int b = 0; b < W; ++b) {
+            const unsigned int ma = __ballot_sync(0xffffffffu, (wa >> b) & 1);
+            const unsigned int mb = __ballot_sync(0xffffffffu, (wb >> b) & 1);
+            if (lane == (b & 31)) {
+                ce[b >> 5] += __popc(ma);
+                co[b >> 5] += __popc(mb);
+            }
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < W / 32; ++h) {
+        const uint32_t j = uint32_t(W) * k + 32u * h + lane;  // packed index: columns 2j, 2j + 1
+        atomicAdd(cnt + 2 * size_t(j), (unsigned long long)ce[h]);
+        atomicAdd(cnt + 2 * size_t(j) + 1, (unsigned long long)co[h]);
+    }
+}
+
+__global__ void k_counts_to_balance(const unsigned long long* __restrict__ cnt, uint32_t X, uint32_t R,
+                                    long long* __restrict__ out) {
+    const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x < X) out[x] = 2 * (long long)cnt[x] - (long long)R;
+}
+
+cudaError_t launch_balances(int w, const void* planes, Geom g, uint32_t r0, uint32_t R, uint32_t X,
+                            long long* rows_out, long long* cols_out, void* tmp, cudaStream_t st) {
+    if (rows_out) {
+        const uint32_t nb = (R + 255) / 256;
+        if (w == 64)
+            k_row_balances<uint64_t><<<nb, 256, 0, st>>>(static_cast<const uint64_t*>(planes), g, r0, R, X, rows_out);
+        else
+            k_row_balances<uint32_t><<<nb, 256, 0, st>>>(static_cast<const uint32_t*>(planes), g, r0, R, X, rows_out);
+    }
+    if (cols_out) {
+        unsigned long long* cnt = static_cast<unsigned long long*>(tmp);
+        cudaError_t e = cudaMemsetAsync(cnt, 0, size_t(X) * sizeof(unsigned long long), st);
+        if (e != cudaSuccess) return e;
+        const uint32_t chunk = 1024, chunks = (R + chunk - 1) / chunk;
+        const uint32_t warps = g.n * chunks, nb = (warps * 32 + 255) / 256;
+        if (w == 64)
+            k_col_balances<uint64_t><<<nb, 256, 0, st>>>(static_cast<const uint64_t*>(planes), g, r0, R, chunk, cnt);
+        else
+            k_col_balances<uint32_t><<<nb, 256, 0, st>>>(static_cast<const uint32_t*>(planes), g, r0, R, chunk, cnt);
+        k_counts_to_balance<<<(X + 255) / 256, 256, 0, st>>>(cnt, X, R, cols_out);
+    }
+    return cudaGetLastError();
+}
+
 // ---- launchers -----------------------------------------------------------------
 
 cudaError_t launch_measure(int w, const void* planes, Geom g, uint32_t X, void* scratch, void* result_dev,

@@ -186,6 +186,11 @@ cudaError_t launch_halo_pull(int w, void* planes, uint64_t* rng, Geom g, const P
 cudaError_t launch_push_signal(int w, const void* planes, int plane, Geom g, void* next_planes, uint32_t next_Y,
                                uint64_t* done, uint64_t value, cudaStream_t st);
 
+// row_balances / col_balances (slope_field.hpp:177-202) over physical rows r0 .. r0+R-1: rows_out[R] and
+// cols_out[X] (either may be null); tmp: X u64 of device scratch for the column counts.
+cudaError_t launch_balances(int w, const void* planes, Geom g, uint32_t r0, uint32_t R, uint32_t X,
+                            long long* rows_out, long long* cols_out, void* tmp, cudaStream_t st);
+
 // Heights (reference HeightMap layout, row-major int32), after launch_measure.
 cudaError_t launch_heights(int w, const void* planes, Geom g, uint32_t X, const void* scratch, int32_t* out,
                            cudaStream_t st);

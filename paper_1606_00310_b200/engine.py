@@ -125,6 +125,12 @@ def _i128(lo: int, hi: int) -> int:
     return v - (1 << 128) if v >> 127 else v
 
 
+def release_pool(device: int = 0) -> None:
+    """Return the unused memory of the library's plane-set pool on `device` to the driver
+    (octgpu_release_pool): periodic engines keep freed plane sets for the next engine of the process."""
+    check(lib().octgpu_release_pool(device))
+
+
 class GpuEngine:
     """Drop-in for ``VecEngine<Word>``; ``workers`` is accepted and ignored
     (the GPU partition is fixed and results are partition-independent, as the
@@ -253,6 +259,18 @@ class GpuEngine:
         out = np.zeros((c.Y, c.X), np.int32)
         check(lib().octgpu_heights(self._h, out.ctypes.data_as(C.c_void_p)))
         return HeightMap(c.X, c.Y, out, float(out.mean(dtype=np.float64)))
+
+    def row_balances(self) -> np.ndarray:
+        """row_balances(field) (slope_field.hpp:177-189): sum_x sigma_x-(x, y) per row, on the device."""
+        out = np.zeros(self.cfg.Y, np.int64)
+        check(lib().octgpu_balances(self._h, out.ctypes.data_as(C.c_void_p), None))
+        return out
+
+    def col_balances(self) -> np.ndarray:
+        """col_balances(field) (slope_field.hpp:192-202): sum_y sigma_y-(x, y) per column, on the device."""
+        out = np.zeros(self.cfg.X, np.int64)
+        check(lib().octgpu_balances(self._h, None, out.ctypes.data_as(C.c_void_p)))
+        return out
 
     def measure(self) -> MeasurementRecord:
         """measure_heights(t, heights()) without materialising heights."""

@@ -197,6 +197,21 @@ class StripeEngine:
     def disconnect(self) -> None:
         check(lib().octgpu_stripe_disconnect(self._h))
 
+    def checksum(self) -> int:
+        """field_checksum of this stripe's own rows as an (y1 - y0)-row field (slope_field.hpp:232-246);
+        sync the whole group first (the first row is completed by the previous stripe's push)."""
+        v = C.c_uint64()
+        check(lib().octgpu_field_checksum(self._h, C.byref(v)))
+        return int(v.value)
+
+    def balances(self) -> tuple[np.ndarray, np.ndarray]:
+        """(row_balances of this stripe's rows, col_balances summed over them); the lattice's
+        col_balances is the sum over all stripes (slope_field.hpp:177-202)."""
+        rows = np.zeros(self.y1 - self.y0, np.int64)
+        cols = np.zeros(self.cfg.X, np.int64)
+        check(lib().octgpu_balances(self._h, rows.ctypes.data_as(C.c_void_p), cols.ctypes.data_as(C.c_void_p)))
+        return rows, cols
+
     def measure_local(self) -> StripeMoments:
         m = OctStripeMoments()
         check(lib().octgpu_measure_stripe(self._h, C.byref(m)))
@@ -234,6 +249,18 @@ class StripeEngine:
         check(lib().octgpu_sync(self._h))
 
 
+def _bind_current_stream(engines) -> None:
+    """Host-driven transports copy halo buffers with torch (LocalTransport) or NCCL (DistTransport) on the
+    current torch stream, while each stripe enqueues pack / MCS / finish on its own stream. Binding every
+    GPU stripe to the current torch stream at construction orders the two; the caller keeps that stream
+    current while stepping the group (set_stream() afterwards would break the ordering)."""
+    import torch
+
+    for e in engines:
+        if isinstance(e, StripeEngine) and torch.cuda.is_available():
+            e.set_stream(torch.cuda.current_stream(e.device).cuda_stream)
+
+
 class _Buffers:
     def __init__(self, eng, alloc):
         self.tp = alloc(eng.to_prev_bytes)
@@ -249,6 +276,7 @@ class LocalTransport:
 
     def __init__(self, engines: list, alloc):
         self.engines = engines
+        _bind_current_stream(engines)
         self.bufs = [_Buffers(e, alloc) for e in engines]
 
     def halos(self):
@@ -280,6 +308,7 @@ class DistTransport:
 
         self.dist = dist
         self.engines = [engine]
+        _bind_current_stream(self.engines)
         self.bufs = [_Buffers(engine, alloc)]
         self.rank, self.size = dist.get_rank(), dist.get_world_size()
         self.prev, self.next = (self.rank - 1) % self.size, (self.rank + 1) % self.size
@@ -382,7 +411,7 @@ class StripeGroup:
         self.tr, self.X, self.Y = transport, X, Y
 
     def step(self, prm: UpdateParams, n: int = 1) -> None:
-        kmax = self.tr.engines[0].max_mcs(prm)  # the same on every rank (depends on params and X only)
+        kmax = self.tr.engines[0].max_mcs(prm)  # the same on every rank (depends on params and X * Ytot only)
         peer = getattr(self.tr, "peer", False)
         while n > 0:
             k = min(n, kmax)

@@ -246,3 +246,51 @@ def test_xi_bit_frequencies_4sigma(oracle, r):
     sig_pos = (r * (1 - r) / nwords) ** 0.5
     assert np.all(np.abs(per_pos - r) <= 4 * sig_pos), per_pos
     assert abs(bits.mean() - r) <= 4 * sig_pos / 8
+
+
+# ---------------------------------------------------------------------------
+# the at-scale checker (oo_measure_planes_mt) against the scalar reconstruct + power sums, and the
+# reference's own heights; balances against the reference
+
+@pytest.mark.parametrize("geom", [(128, 2, 64), (256, 34, 64), (384, 62, 64), (192, 66, 32), (1024, 64, 64)])
+def test_measure_planes_mt_equals_reconstruct(oracle, geom):
+    X, Y, w = geom
+    L = OracleLattice.flat(oracle, X, Y, 3 + X + Y, w)
+    L.step(oracle, oracle.resolve(0.5), oracle.resolve(0.25), 9)
+    h, err = oracle.reconstruct(L.planes, w)
+    assert err is None
+    sums, err = oracle.measure_planes(L.planes, w)
+    assert err is None
+    assert sums == oracle.power_sums(h)
+
+
+def test_measure_planes_mt_reports_reconstruct_errors(oracle):
+    X, Y = 256, 34
+    L = OracleLattice.flat(oracle, X, Y, 5)
+    L.step(oracle, oracle.resolve(0.75), oracle.resolve(0.0), 4)
+    bad = L.planes.copy()
+    bad[2, 7, 1] ^= np.uint64(1 << 5)  # one y-slope flipped: curl violations
+    n_bad, (fx, fy) = oracle.curl_check(bad)
+    sums, err = oracle.measure_planes(bad)
+    assert sums is None and err[0] == 1 and err[2] == n_bad and err[1] == fy * X + fx
+    # a uniform tilt (every slope +1) is curl-free but breaks the row-0 closure
+    tilt = np.full((4, Y, X // 128), ~np.uint64(0), np.uint64)
+    assert oracle.measure_planes(tilt)[1][0] == 2
+    _, e2 = oracle.reconstruct(tilt)
+    assert e2[0] == 2
+
+
+def test_balances_reference_on_random_field(oracle, reflib):
+    X, Y = 256, 34
+    ref = RefEngine(reflib, X, Y, 11, workers=2)
+    ref.step(0.5, 0.25, 7)
+    rows, cols = ref.balances()
+    assert rows.shape == (Y,) and cols.shape == (X,)
+    assert not rows.any() and not cols.any()  # a valid periodic surface
+    # a broken field: the reference's balances are what the GPU export must reproduce (test_parity_gpu)
+    planes = ref.planes()
+    planes[2, 3, 0] ^= np.uint64(0b101)
+    planes[0, 5, 1] ^= np.uint64(1 << 9)
+    bad = RefEngine.from_state(reflib, X, Y, 64, 7, 0, planes, ref.states())
+    r2, c2 = bad.balances()
+    assert r2[5] != 0 and (c2 != 0).sum() == 2

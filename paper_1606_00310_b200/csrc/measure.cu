@@ -2,18 +2,26 @@
 // (slope_field.hpp:159-229, measure.cpp:24-56) without materialising the
 // HeightMap, in exact integer arithmetic.
 //
-// Heights: h(x,y) = H_y + r(x,y), H_y = sum_{y'=1..y} sigma_y-(0,y') (column
-// 0) and r(x,y) = sum_{x'=1..x} sigma_x-(x',y) (row prefix). This equals the
-// reference's row-0-then-columns integration whenever curl_check passes,
-// which is checked in the same pass. With u(x) = sum_{x'<=x} sigma_x-(x',y)
-// (inclusive from x = 0) we have h = G_y + u(x), G_y = H_y - sigma_x-(0,y),
-// so S_k = sum_y sum_j C(k,j) G_y^(k-j) U_j(y) with U_j(y) = sum_x u(x)^j.
+// Heights: h(x,y) = H_y + r(x,y), H_y = sum sigma_y-(0,y') over the rows from the first
+// scanned row to y (column 0) and r(x,y) = sum_{x'=1..x} sigma_x-(x',y) (row prefix). This
+// equals the reference's row-0-then-columns integration whenever curl_check passes, which is
+// checked in the same pass. With u(x) = sum_{x'<=x} sigma_x-(x',y) (inclusive from x = 0),
+// h = G_y + u(x), G_y = H_y - sigma_x-(0,y), so S_k = sum_y sum_j C(k,j) G_y^(k-j) U_j(y)
+// with U_j(y) = sum_x u(x)^j.
 //
-// Kernels (one measurement = 3 launches):
-//   k_col_scan     single block: G_y for all rows (column-0 prefix) + column closure
-//   k_measure_rows per row: word-parallel curl check, U_j via an 8-site lookup
-//                  table, binomial shift by G_y, int128 block reduction
-//   k_measure_final single block: sums the per-block partials
+// Kernels (one measurement = 2 launches):
+//   k_measure_rows  per block: 4 row groups of 31 rows (lane per row; lane 0 is the row above,
+//                   for the curl check) x 4 x-segments (one warp each). Word-parallel curl
+//                   check; U_j per segment from 16-site units read through two 8-site tables
+//                   (the second indexed by the first's net step, so a unit costs one combine);
+//                   segments and rows combined in int128 in a block-local column-0 gauge.
+//   k_measure_final one block: exclusive prefix of the blocks' column-0 increments, binomial
+//                   shift of each block's sums to the global gauge, reduction, closure data.
+// Scan order = virtual rows c0 .. c1-1 (periodic: physical rows 1 .. Y-1, 0; a stripe: its core
+// rows); the gauge H is 0 at virtual row c0 - 1. For a periodic lattice that is the reference's
+// h(0,0) = 0 whenever the column closes (otherwise the measurement fails with the reference's
+// column error before the sums are used).
+#include <algorithm>
 #include <cstdint>
 
 #include "octgpu_internal.h"
@@ -21,22 +29,24 @@
 namespace octgpu {
 
 struct Partial {
-    __int128 S[4];
+    __int128 S[4];                   // block sums in the block-local gauge (H = 0 before its first row)
     unsigned long long curl_count;
-    unsigned long long curl_first;
-    long long row0;
+    unsigned long long curl_first;   // row_id * X + x, ~0 if none
+    long long row0;                  // sum_x sigma_x- of row_id 0 (the block holding it)
+    long long delta;                 // sum of sigma_y-(0, y) over the block's rows
+    long long sy_first;              // sigma_y-(0, c0) (block 0)
+    long long prefix;                // written by k_measure_final: H offset of the block
+    unsigned long long n_sites;
     long long pad;
 };
 
 namespace {
 
-constexpr int kRowsPerWarp = 31;  // lane 0 is the y-1 halo for the curl check
-constexpr int kThreads = 128;
+constexpr int kRowsPerGroup = 31;  // lane 0 is the y-1 halo for the curl check
+constexpr int kSeg = 8;            // x-segments per row: one warp each; a block = one row group at a time
+constexpr int kMThreads = 32 * kSeg;
 
-uint32_t measure_blocks(uint32_t rows) {
-    const uint32_t warps = (rows + kRowsPerWarp - 1) / kRowsPerWarp;
-    return (warps * 32 + kThreads - 1) / kThreads;
-}
+__host__ __device__ inline uint32_t measure_groups(uint32_t rows) { return (rows + kRowsPerGroup - 1) / kRowsPerGroup; }
 
 __device__ __forceinline__ __int128 shfl_down_i128(__int128 v, int off) {
     unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)((unsigned __int128)v >> 64);
@@ -45,270 +55,356 @@ __device__ __forceinline__ __int128 shfl_down_i128(__int128 v, int off) {
     return (__int128)(((unsigned __int128)hi << 64) | lo);
 }
 
+// ---- 8-site tables ---------------------------------------------------------------
+// A byte = 8 consecutive sites of a row: bits 0..3 the 4 even-x sites (one packed plane's nibble),
+// bits 4..7 the 4 odd-x sites; sites interleave e0 o0 e1 o1 ... (slope_field.hpp:15-53). For an
+// offset o (the height just before the byte, relative to the unit start) the entry holds
+// q_k = sum_i (o + p_i)^k over the byte's inclusive prefix values p_i, k = 1..4, and d = p_7.
+// T0 = offset 0 (first byte of a 16-site unit), T1[o + 8] = offsets -8..8 (second byte, indexed
+// by the first byte's d). Biased fields; the sum of a T0 and a T1 entry is the unit's, without
+// carries between fields:  lo = q3 + B3 (16 bits) | q1 + B1 << 16 (9 bits) | d + 8 << 25,
+// hi = q2 (11 bits) | q4 << 11 (18 bits); unit biases B1 = 136 (36 + 100), B3 = 18496 (1296 + 17200),
+// d: 16.
+constexpr int kUnitB1 = 136, kUnitB3 = 18496, kUnitD = 16;
+
+struct MeasTab {
+    uint2 t0[256];
+    uint2 t1[17 * 256];
+};
+
+__host__ __device__ constexpr uint2 tab_entry(int b, int o, bool second) {
+    int p = 0, q1 = 0, q2 = 0, q3 = 0, q4 = 0;
+    for (int i = 0; i < 8; ++i) {
+        const int bit = (i & 1) ? (b >> (4 + (i >> 1))) & 1 : (b >> (i >> 1)) & 1;
+        p += bit ? 1 : -1;
+        const int v = o + p;
+        q1 += v;
+        q2 += v * v;
+        q3 += v * v * v;
+        q4 += v * v * v * v;
+    }
+    const int b1 = second ? 100 : 36, b3 = second ? 17200 : 1296;
+    const uint32_t lo = uint32_t(q3 + b3) | (uint32_t(q1 + b1) << 16) | (uint32_t(p + 8) << 25);
+    const uint32_t hi = uint32_t(q2) | (uint32_t(q4) << 11);
+    return uint2{lo, hi};
+}
+
+struct MeasTabInit : MeasTab {
+    constexpr MeasTabInit() : MeasTab{} {
+        for (int b = 0; b < 256; ++b) t0[b] = tab_entry(b, 0, false);
+        for (int o = -8; o <= 8; ++o)
+            for (int b = 0; b < 256; ++b) t1[(o + 8) * 256 + b] = tab_entry(b, o, true);
+    }
+};
+
+__device__ const MeasTab g_tab = MeasTabInit();
+
+// shared memory: T0 replicated x16 (entry b at [b][lane & 15]: every warp lookup conflict-free),
+// T1 once; reused for the cross-warp combine after the row pass
+constexpr int kT0Words = 256 * 16;  // uint2
+constexpr int kT1Words = 17 * 256;
+struct SegOut {                      // one lane's segment result (int128 sums, delta, curl)
+    __int128 T[4];
+    long long D;
+    unsigned int rc, rfirst;
+};
+constexpr size_t kMeasSmem = sizeof(uint2) * (kT0Words + kT1Words) + sizeof(SegOut) * kMThreads;
+
 }  // namespace
 
 size_t measure_scratch_bytes(uint32_t Y) {
-    return size_t(Y) * sizeof(long long) + size_t(measure_blocks(Y + 1)) * sizeof(Partial) + 64;
+    return size_t(Y + 1) * sizeof(long long) + size_t(measure_groups(Y + 1) + 1) * sizeof(Partial) + 64;
 }
 
-// ---- column 0: G_y and the column-0 closure ------------------------------
-// Rows [start, start + count) in order; G[row] = sum_{rows <= row} sigma_y-(0,.) - sigma_x-(0,row)
-// (- sigma_y-(0,start) when exclude_first: the periodic gauge h(0,0) = 0).
+namespace {
+
+// signed 32 x 32 -> 64-bit multiply-add in one IMAD.WIDE (the compiler otherwise emits the unsigned form
+// plus a sign correction when it can prove one factor non-negative)
+__device__ __forceinline__ long long madw(int a, int b, long long c) {
+    long long d;
+    asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+    return d;
+}
+
+// Unit accumulators since the last flush; heights relative to the segment base + u.
+struct UnitAcc {
+    int Au1, Au2, Aq1, Aq2, Aq3, X11, X12, units;
+    unsigned int Aq4;
+    long long Au3, Au4, X13, X21, X22, X31;
+    __device__ __forceinline__ void clear() {
+        Au1 = Au2 = Aq1 = Aq2 = Aq3 = X11 = X12 = units = 0;
+        Aq4 = 0;
+        Au3 = Au4 = X13 = X21 = X22 = X31 = 0;
+    }
+};
+
+// T_k += sum_j C(k,j) B^(k-j) t_j for the unit sums t_j of heights B + u (u = offset within the flush)
+__device__ __noinline__ void flush_units(UnitAcc& A, long long B, __int128* T) {
+    const long long K = A.units;
+    const long long t1 = 16ll * A.Au1 + A.Aq1 - kUnitB1 * K;
+    const long long t2 = 16ll * A.Au2 + 2ll * (A.X11 - (long long)kUnitB1 * A.Au1) + A.Aq2;
+    const long long t3 = 16ll * A.Au3 + 3ll * (A.X21 - (long long)kUnitB1 * A.Au2) + 3ll * A.X12 + A.Aq3 -
+                         (long long)kUnitB3 * K;
+    const long long t4 = 16ll * A.Au4 + 4ll * (A.X31 - (long long)kUnitB1 * A.Au3) + 6ll * A.X22 +
+                         4ll * (A.X13 - (long long)kUnitB3 * A.Au1) + (long long)A.Aq4;
+    const __int128 b = B, b2 = b * b, b3 = b2 * b, b4 = b2 * b2, t0 = 16 * K;
+    T[0] += b * t0 + t1;
+    T[1] += b2 * t0 + 2 * b * t1 + t2;
+    T[2] += b3 * t0 + 3 * b2 * t1 + 3 * b * t2 + t3;
+    T[3] += b4 * t0 + 4 * b3 * t1 + 6 * b2 * t2 + 4 * b * t3 + t4;
+    A.clear();
+}
+
+// one 16-site unit: byte b0 (first 8 sites) then b1 (next 8) of the row. t0b = this lane's replica of
+// T0 (entry b at t0b + 16 b), t1b = T1.
+__device__ __forceinline__ void unit(UnitAcc& A, int& u, uint32_t b0, uint32_t b1, const uint2* t0b,
+                                     const uint2* t1b) {
+    const uint2 e0 = t0b[b0 * 16];
+    const uint2 e1 = t1b[(e0.x >> 25) * 256 + b1];
+    const uint32_t lo = e0.x + e1.x, hi = e0.y + e1.y;
+    const int q3b = int(lo & 0xffffu), q1b = int((lo >> 16) & 0x1ffu), Db = int(lo >> 25);
+    const int q2 = int(hi & 0x7ffu);
+    const unsigned int q4 = hi >> 11;
+    const int u2 = u * u, u3 = u2 * u;
+    A.Au1 += u;
+    A.Au2 += u2;
+    A.Au3 = madw(u3, 1, A.Au3);
+    A.Au4 = madw(u2, u2, A.Au4);
+    A.Aq1 += q1b;
+    A.Aq2 += q2;
+    A.Aq3 += q3b;
+    A.Aq4 += q4;
+    A.X11 += u * q1b;
+    A.X12 += u * q2;
+    A.X13 = madw(u, q3b, A.X13);
+    A.X21 = madw(u2, q1b, A.X21);
+    A.X22 = madw(u2, q2, A.X22);
+    A.X31 = madw(u3, q1b, A.X31);
+    u += Db - kUnitD;
+    ++A.units;
+}
+
+}  // namespace
+
+// ---- row pass -------------------------------------------------------------------------
+// Persistent blocks of kSeg warps walk the row groups (31 core rows each, lane 0 = the row above):
+// warp s handles x-segment s (words [s n / kSeg, (s+1) n / kSeg)) of the group's 32 rows, then warp 0
+// combines the segments of each row and the group's rows into one Partial (group-local gauge).
 template <typename Word>
-__global__ void __launch_bounds__(1024) k_col_scan(const Word* __restrict__ planes, Geom g, uint32_t start,
-                                                   uint32_t count, int exclude_first, long long* __restrict__ G,
-                                                   long long* __restrict__ col_sum, long long* __restrict__ sy_first) {
-    __shared__ int warp_tot[32];
-    __shared__ long long carry_sh;
+__global__ void __launch_bounds__(kMThreads, 2) k_measure_rows(const Word* __restrict__ planes, Geom g, uint32_t X,
+                                                               long long* __restrict__ Gout, Partial* __restrict__ part) {
+    constexpr int W = int(sizeof(Word) * 8);
+    extern __shared__ __align__(16) unsigned char msm[];
+    uint2* t0rep = reinterpret_cast<uint2*>(msm);
+    uint2* t1 = t0rep + kT0Words;
+    SegOut* so = reinterpret_cast<SegOut*>(t1 + kT1Words);
+    for (int i = threadIdx.x; i < kT0Words; i += kMThreads) t0rep[i] = g_tab.t0[i >> 4];
+    {
+        const uint4* src1 = reinterpret_cast<const uint4*>(g_tab.t1);
+        uint4* dst1 = reinterpret_cast<uint4*>(t1);
+        for (int i = threadIdx.x; i < kT1Words / 2; i += kMThreads) dst1[i] = src1[i];
+    }
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
+    const uint32_t n = g.n, Y = g.Y;
     const size_t PS = g.plane_stride;
+    const uint32_t kbeg = uint32_t(seg) * n / kSeg, kend = uint32_t(seg + 1) * n / kSeg;
+    const uint32_t ngroups = measure_groups(g.c1 - g.c0);
+    const uint2* t0b = t0rep + (lane & 15);
+
+    for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        const uint32_t first = g.c0 + grp * uint32_t(kRowsPerGroup);  // the group's first core row
+        const uint32_t v = first - 1 + uint32_t(lane);                // lane 0: the row above
+        const uint32_t y = g.wrap ? v % g.wrap : v;
+        const bool core = lane >= 1 && v < g.c1;
+        const uint32_t row_id = g.wrap ? y : v - g.c0;
+        const int ya = int((y ^ g.ypar) & 1u);
+        // even-x sites of row y are in X(ya), odd-x in X(!ya); C = Y(ya), its partner Y(!ya)
+        const Word* pXa = planes + size_t(ya) * PS + y;
+        const Word* pXb = planes + size_t(ya ^ 1) * PS + y;
+        const Word* pCa = planes + size_t(2 + ya) * PS + y;
+        const Word* pCb = planes + size_t(3 - ya) * PS + y;
+
+        __int128 T[4] = {0, 0, 0, 0};
+        long long B = 0;
+        unsigned int rc = 0, rfirst = 0xffffffffu;
+        int sy0 = 0, sx0 = 0;
+        {
+            UnitAcc A;
+            A.clear();
+            int u = 0;
+            Word pcb = kend > kbeg ? pCb[size_t(kbeg == 0 ? n - 1 : kbeg - 1) * Y] : Word(0);
+            for (uint32_t k = kbeg; k < kend; ++k) {
+                const size_t o = size_t(k) * Y;
+                const Word xa = pXa[o], xb = pXb[o], ca = pCa[o], cb = pCb[o];
+                const Word bxa = __shfl_up_sync(0xffffffffu, xa, 1);
+                const Word bxb = __shfl_up_sync(0xffffffffu, xb, 1);
+                if (k == 0) {
+                    sx0 = (xa & 1) ? 1 : -1;  // sigma_x-(0, y)
+                    sy0 = (ca & 1) ? 1 : -1;  // sigma_y-(0, y)
+                }
+                // curl check, word-parallel: parity ya (even-x sites, D rotated up one packed
+                // bit with the previous word's top bit) and parity !ya (odd-x sites, D aligned)
+                const Word D1 = Word((cb << 1) | (pcb >> (W - 1)));
+                const Word V1 = (xa ^ bxa ^ ca ^ D1) | ((xa ^ bxa) & (xa ^ ca));
+                const Word V2 = (xb ^ bxb ^ cb ^ ca) | ((xb ^ bxb) & (xb ^ cb));
+                pcb = cb;
+                if (V1 | V2) {
+                    rc += __popcll((unsigned long long)V1) + __popcll((unsigned long long)V2);
+                    if (V1)
+                        rfirst = min(rfirst, 2u * (k * W + uint32_t(__ffsll((long long)(unsigned long long)V1) - 1)));
+                    if (V2)
+                        rfirst = min(rfirst,
+                                     2u * (k * W + uint32_t(__ffsll((long long)(unsigned long long)V2) - 1)) + 1u);
+                }
+                // rebase before the 32-bit unit accumulators could overflow: |u| <= 1024, <= 1024 units
+                if (u > 1024 - 2 * W || u < -(1024 - 2 * W) || A.units > 1024 - W / 4) {
+                    flush_units(A, B, T);
+                    B += u;
+                    u = 0;
+                }
+#pragma unroll
+                for (int half = 0; half < W / 32; ++half) {
+                    const uint32_t a32 = uint32_t(uint64_t(xa) >> (32 * half));
+                    const uint32_t b32 = uint32_t(uint64_t(xb) >> (32 * half));
+                    const uint32_t evn = (a32 & 0x0F0F0F0Fu) | ((b32 & 0x0F0F0F0Fu) << 4);  // chunks 0,2,4,6
+                    const uint32_t odd = ((a32 >> 4) & 0x0F0F0F0Fu) | (b32 & 0xF0F0F0F0u);  // chunks 1,3,5,7
+#pragma unroll
+                    for (int un = 0; un < 4; ++un)
+                        unit(A, u, __byte_perm(evn, 0, 0x4440 + un), __byte_perm(odd, 0, 0x4440 + un), t0b, t1);
+                }
+            }
+            flush_units(A, B, T);
+            B += u;
+        }
+        {
+            SegOut& m = so[threadIdx.x];
+            for (int k = 0; k < 4; ++k) m.T[k] = T[k];
+            m.D = B;
+            m.rc = rc;
+            m.rfirst = rfirst;
+        }
+        __syncthreads();
+        if (seg == 0) {
+            // column 0 in the group gauge: inclusive prefix of sigma_y-(0, y) over the core rows
+            long long incl = core ? sy0 : 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const long long t = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += t;
+            }
+            __int128 S[4] = {0, 0, 0, 0};
+            unsigned long long ccount = 0, cfirst = ~0ull;
+            long long row0 = 0;
+            if (core) {
+                const long long G = incl - sx0;  // group-local G_y = H'_y - sigma_x-(0, y)
+                Gout[y] = G;
+                // the row's U_j: segments in order, each shifted by the net step of the segments before it
+                __int128 U[4] = {0, 0, 0, 0};
+                long long off = 0;
+                unsigned int crc = 0, cfst = 0xffffffffu;
+                for (int s2 = 0; s2 < kSeg; ++s2) {
+                    const SegOut& m = so[s2 * 32 + lane];
+                    const __int128 c = off, c2 = c * c, c3 = c2 * c, c4 = c2 * c2;
+                    const __int128 ns = (__int128)(uint32_t(s2 + 1) * n / kSeg - uint32_t(s2) * n / kSeg) * 2 * W;
+                    U[0] += c * ns + m.T[0];
+                    U[1] += c2 * ns + 2 * c * m.T[0] + m.T[1];
+                    U[2] += c3 * ns + 3 * c2 * m.T[0] + 3 * c * m.T[1] + m.T[2];
+                    U[3] += c4 * ns + 4 * c3 * m.T[0] + 6 * c2 * m.T[1] + 4 * c * m.T[2] + m.T[3];
+                    off += m.D;
+                    crc += m.rc;
+                    cfst = min(cfst, m.rfirst);
+                }
+                const __int128 Gq = G, g2 = Gq * Gq, g3 = g2 * Gq, g4 = g2 * g2, U0 = X;
+                S[0] = Gq * U0 + U[0];
+                S[1] = g2 * U0 + 2 * Gq * U[0] + U[1];
+                S[2] = g3 * U0 + 3 * g2 * U[0] + 3 * Gq * U[1] + U[2];
+                S[3] = g4 * U0 + 4 * g3 * U[0] + 6 * g2 * U[1] + 4 * Gq * U[2] + U[3];
+                ccount = crc;
+                if (cfst != 0xffffffffu) cfirst = (unsigned long long)row_id * X + cfst;
+                if (row_id == 0) row0 = off;  // sum_x sigma_x- of the row
+            }
+            const long long delta = __shfl_sync(0xffffffffu, incl, 31);
+            const long long syf = __shfl_sync(0xffffffffu, (long long)sy0, 1);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                for (int off = 16; off > 0; off >>= 1) S[k] += shfl_down_i128(S[k], off);
+            for (int off = 16; off > 0; off >>= 1) {
+                ccount += __shfl_down_sync(0xffffffffu, ccount, off);
+                const unsigned long long o = __shfl_down_sync(0xffffffffu, cfirst, off);
+                cfirst = o < cfirst ? o : cfirst;
+                row0 += __shfl_down_sync(0xffffffffu, row0, off);
+            }
+            if (lane == 0) {
+                Partial pr;
+                for (int k = 0; k < 4; ++k) pr.S[k] = S[k];
+                pr.curl_count = ccount;
+                pr.curl_first = cfirst;
+                pr.row0 = row0;
+                pr.delta = delta;
+                pr.sy_first = syf;
+                pr.prefix = 0;
+                pr.n_sites = (unsigned long long)min(uint32_t(kRowsPerGroup), g.c1 - first) * X;
+                pr.pad = 0;
+                part[grp] = pr;
+            }
+        }
+        __syncthreads();  // the segment buffer is rewritten by the next group
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_measure_final(Partial* __restrict__ part, uint32_t nb,
+                                                        MeasureResult* __restrict__ res) {
+    __shared__ __int128 sh_s[4][32];
+    __shared__ unsigned long long sh_cc[32], sh_cf[32];
+    __shared__ long long sh_r0[32], sh_tot[32];
+    __shared__ long long carry_sh;
     const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
     if (t == 0) carry_sh = 0;
     __syncthreads();
-    const int par0 = int((start ^ g.ypar) & 1u);
-    const int sy00 = (planes[(2 + par0) * PS + start] & 1) ? 1 : -1;
-    const int excl = exclude_first ? sy00 : 0;
-    for (uint32_t base = 0; base < count; base += 1024) {
-        const uint32_t i = base + t;
-        const uint32_t y = start + i;
-        int sy = 0, s0 = 0;
-        if (i < count) {
-            const int par = int((y ^ g.ypar) & 1u);  // site (0,y) has parity (global y)&1
-            sy = (planes[(2 + par) * PS + y] & 1) ? 1 : -1;
-            s0 = (planes[par * PS + y] & 1) ? 1 : -1;
-        }
-        int incl = sy;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int o = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= off) incl += o;
-        }
-        if (lane == 31) warp_tot[wp] = incl;
-        __syncthreads();
-        if (wp == 0) {
-            int v = warp_tot[lane];
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int o = __shfl_up_sync(0xffffffffu, v, off);
-                if (lane >= off) v += o;
-            }
-            warp_tot[lane] = v;  // inclusive over warps
-        }
-        __syncthreads();
-        const long long carry = carry_sh;
-        const long long run = carry + incl + (wp > 0 ? warp_tot[wp - 1] : 0);  // sum_{y'<=y} sy
-        if (i < count) G[y] = (run - excl) - s0;
-        __syncthreads();
-        if (t == 1023) carry_sh = run;
-        __syncthreads();
-    }
-    if (t == 0) {
-        *col_sum = carry_sh;
-        *sy_first = sy00;
-    }
-}
-
-// ---- per-row pass ------------------------------------------------------------
-// 8-site table: index = nibble of the even-x plane | nibble of the odd-x plane << 4
-// (sites interleave a0 b0 a1 b1 ...). Entry = d (net step), q_j = sum_i p_i^j
-// over the chunk's 8 prefix values, packed: lo = q3:12 | q1:7 | d:5 | q2:8, hi = q4.
-// 16 replicas (one per lane mod 16) make every warp lookup conflict-free.
-__device__ __forceinline__ uint64_t lut_entry(uint32_t idx) {
-    int p = 0, q1 = 0, q2 = 0, q3 = 0, q4 = 0;
-    for (int i = 0; i < 8; ++i) {
-        const uint32_t bit = (i & 1) ? (idx >> (4 + (i >> 1))) & 1 : (idx >> (i >> 1)) & 1;
-        p += bit ? 1 : -1;
-        q1 += p;
-        q2 += p * p;
-        q3 += p * p * p;
-        q4 += p * p * p * p;
-    }
-    const uint32_t lo = (uint32_t(q3) & 0xfffu) | ((uint32_t(q1) & 0x7fu) << 12) | ((uint32_t(p) & 0x1fu) << 19) |
-                        (uint32_t(q2) << 24);
-    return (uint64_t(uint32_t(q4)) << 32) | lo;
-}
-
-template <typename Word>
-__global__ void __launch_bounds__(kThreads, 4) k_measure_rows(const Word* __restrict__ planes, Geom g, uint32_t X,
-                                                           const long long* __restrict__ Gv,
-                                                           Partial* __restrict__ part) {
-    constexpr int W = int(sizeof(Word) * 8);
-    __shared__ uint64_t lut[256 * 16];
-    __shared__ __int128 sh_s[4][kThreads / 32];
-    __shared__ unsigned long long sh_cc[kThreads / 32], sh_cf[kThreads / 32];
-    __shared__ long long sh_r0[kThreads / 32];
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-        const uint64_t e = lut_entry(i);
-#pragma unroll
-        for (int r = 0; r < 16; ++r) lut[i * 16 + r] = e;
-    }
-    __syncthreads();
-
-    const uint32_t Y = g.Y, n = g.n;
-    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    __int128 S[4] = {0, 0, 0, 0};
-    unsigned long long ccount = 0, cfirst = ~0ull;
-    long long row0 = 0;
-    if (wid * kRowsPerWarp < g.c1 - g.c0) {  // warp-uniform
-        const uint32_t v = g.c0 - 1 + wid * kRowsPerWarp + lane;  // lane 0: the y-1 halo row
-        const uint32_t y = g.wrap ? v % g.wrap : v;
-        const bool core = lane >= 1 && v < g.c1;
-        const uint32_t row_id = g.wrap ? y : v - g.c0;  // position of this row in the result's scan order
-        const size_t PS = g.plane_stride;
-        const Word* X0 = planes + y;
-        const Word* X1 = planes + PS + y;
-        const Word* Y0 = planes + 2 * PS + y;
-        const Word* Y1 = planes + 3 * PS + y;
-        const int ya = int((y ^ g.ypar) & 1u);
-        const uint64_t* lrep = lut + (lane & 15);
-        const size_t last = size_t(n - 1) * Y;
-        Word pD0 = Y0[last], pD1 = Y1[last];
-        long long U1 = 0, U2 = 0, rowsum = 0;
-        __int128 U3 = 0, U4 = 0;
-        int u0 = 0;
-        unsigned int rc = 0, rfirst = 0xffffffffu;
-        for (uint32_t k = 0; k < n; ++k) {
-            const size_t o = size_t(k) * Y;
-            const Word x0 = X0[o], x1 = X1[o], yy0 = Y0[o], yy1 = Y1[o];
-            const Word bx0 = __shfl_up_sync(0xffffffffu, x0, 1);
-            const Word bx1 = __shfl_up_sync(0xffffffffu, x1, 1);
-#pragma unroll
-            for (int pi = 0; pi < 2; ++pi) {  // curl check, word-parallel
-                const Word A = pi ? x1 : x0;
-                const Word B = pi ? bx0 : bx1;
-                const Word C = pi ? yy1 : yy0;
-                const Word Dr = pi ? yy0 : yy1;
-                const Word Dp = pi ? pD0 : pD1;
-                const bool even_x = ((uint32_t(pi) ^ y ^ g.ypar) & 1u) == 0;
-                const Word D = even_x ? Word((Dr << 1) | (Dp >> (W - 1))) : Dr;
-                const Word Vv = (A ^ B ^ C ^ D) | ((A ^ B) & (A ^ C));
-                if (Vv) {
-                    rc += __popcll((unsigned long long)Vv);
-                    const uint32_t b = __ffsll((long long)(unsigned long long)Vv) - 1;
-                    rfirst = min(rfirst, 2u * (k * W + b) + (even_x ? 0u : 1u));
-                }
-            }
-            pD0 = yy0;
-            pD1 = yy1;
-            const Word xa = ya ? x1 : x0;  // even-x sites of row y
-            const Word xb = ya ? x0 : x1;  // odd-x sites
-            rowsum += 2 * (__popcll((unsigned long long)xa) + __popcll((unsigned long long)xb)) - 2 * W;
-            // 8-site chunk indices, nibble of xa | nibble of xb << 4, gathered per 32-bit half
-            int u = 0, c1 = 0, c2 = 0, c3 = 0;
-            unsigned long long c4 = 0;
-#pragma unroll
-            for (int half = 0; half < W / 32; ++half) {
-                const uint32_t a32 = uint32_t(uint64_t(xa) >> (32 * half));
-                const uint32_t b32 = uint32_t(uint64_t(xb) >> (32 * half));
-                const uint32_t evn = (a32 & 0x0F0F0F0Fu) | ((b32 & 0x0F0F0F0Fu) << 4);  // chunks 0,2,4,6
-                const uint32_t odd = ((a32 >> 4) & 0x0F0F0F0Fu) | (b32 & 0xF0F0F0F0u);  // chunks 1,3,5,7
-#pragma unroll
-                for (int ch = 0; ch < 8; ++ch) {
-                    const uint32_t idx = (((ch & 1) ? odd : evn) >> (8 * (ch >> 1))) & 0xffu;
-                    const uint64_t e = lrep[idx * 16];
-                    const uint32_t lo = uint32_t(e);
-                    const int q3 = int(lo << 20) >> 20;
-                    const int q1 = int(lo << 13) >> 25;
-                    const int d = int(lo << 8) >> 27;
-                    const int q2 = int(lo >> 24);
-                    const int q4 = int(e >> 32);
-                    const int u2 = u * u, u3 = u2 * u, u4 = u2 * u2;  // |u| <= 120: u4 < 2^28
-                    c1 += 8 * u + q1;
-                    c2 += 8 * u2 + 2 * u * q1 + q2;
-                    c3 += 8 * u3 + 3 * u2 * q1 + 3 * u * q2 + q3;
-                    // sum_i (u + p_i)^4 over the chunk: >= 0 and < 2^31 for |u| <= 120
-                    const int t4 = 8 * u4 + 4 * u3 * q1 + 6 * u2 * q2 + 4 * u * q3 + q4;
-                    c4 += (unsigned long long)(unsigned)t4;
-                    u += d;
-                }
-            }
-            constexpr long long NS = 2 * W;
-            if (u0 >= -4096 && u0 <= 4096) {  // 32x32->64 products only, then one int128 add each
-                const int a = u0, aa = a * a;                     // aa <= 2^24
-                const long long aaa = (long long)aa * a;          // <= 2^36
-                const long long a4 = (long long)aa * aa;          // <= 2^48
-                U1 += (long long)(NS * a) + c1;
-                U2 += (long long)aa * NS + (long long)(2 * a) * c1 + c2;
-                U3 += (__int128)(aaa * NS + (long long)(3 * aa) * c1 + (long long)(3 * a) * c2 + c3);
-                U4 += (__int128)(a4 * NS + 4 * aaa * c1 + (long long)(6 * aa) * c2 + (long long)(4 * a) * c3 +
-                                 (long long)c4);
-            } else {
-                const long long uu = (long long)u0 * u0;
-                const __int128 uuu = (__int128)uu * u0;
-                U1 += NS * u0 + c1;
-                U2 += NS * uu + 2ll * u0 * c1 + c2;
-                U3 += (__int128)NS * uuu + (__int128)(3 * uu) * c1 + (__int128)(3ll * u0) * c2 + c3;
-                U4 += (__int128)NS * uuu * u0 + (__int128)4 * uuu * c1 + (__int128)(6 * uu) * c2 +
-                      (__int128)(4ll * u0) * c3 + (__int128)c4;
-            }
-            u0 += u;
-        }
-        if (core) {
-            const __int128 G = Gv[y];
-            const __int128 g2 = G * G, g3 = g2 * G, g4 = g3 * G;
-            const __int128 U0 = X;
-            S[0] = G * U0 + U1;
-            S[1] = g2 * U0 + 2 * G * U1 + U2;
-            S[2] = g3 * U0 + 3 * g2 * U1 + 3 * G * U2 + U3;
-            S[3] = g4 * U0 + 4 * g3 * U1 + 6 * g2 * U2 + 4 * G * U3 + U4;
-            ccount = rc;
-            if (rfirst != 0xffffffffu) cfirst = (unsigned long long)row_id * X + rfirst;
-            if (row_id == 0) row0 = rowsum;
-        }
-    }
-    // block reduction
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        __int128 vs = S[k];
-        for (int off = 16; off > 0; off >>= 1) vs += shfl_down_i128(vs, off);
-        if (lane == 0) sh_s[k][wp] = vs;
-    }
-    for (int off = 16; off > 0; off >>= 1) {
-        ccount += __shfl_down_sync(0xffffffffu, ccount, off);
-        const unsigned long long o = __shfl_down_sync(0xffffffffu, cfirst, off);
-        cfirst = o < cfirst ? o : cfirst;
-        row0 += __shfl_down_sync(0xffffffffu, row0, off);
-    }
-    if (lane == 0) {
-        sh_cc[wp] = ccount;
-        sh_cf[wp] = cfirst;
-        sh_r0[wp] = row0;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        Partial pr;
-        for (int k = 0; k < 4; ++k) pr.S[k] = 0;
-        pr.curl_count = 0;
-        pr.curl_first = ~0ull;
-        pr.row0 = 0;
-        pr.pad = 0;
-        for (int i = 0; i < kThreads / 32; ++i) {
-            for (int k = 0; k < 4; ++k) pr.S[k] += sh_s[k][i];
-            pr.curl_count += sh_cc[i];
-            pr.curl_first = sh_cf[i] < pr.curl_first ? sh_cf[i] : pr.curl_first;
-            pr.row0 += sh_r0[i];
-        }
-        part[blockIdx.x] = pr;
-    }
-}
-
-__global__ void __launch_bounds__(256) k_measure_final(const Partial* __restrict__ part, uint32_t nb,
-                                                       const long long* __restrict__ col_sum,
-                                                       const long long* __restrict__ sy_first,
-                                                       MeasureResult* __restrict__ res) {
-    __shared__ __int128 sh_s[4][8];
-    __shared__ unsigned long long sh_cc[8], sh_cf[8];
-    __shared__ long long sh_r0[8];
-    const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
     __int128 S[4] = {0, 0, 0, 0};
     unsigned long long cc = 0, cf = ~0ull;
     long long r0 = 0;
-    for (uint32_t i = t; i < nb; i += blockDim.x) {
-        const Partial p = part[i];
-        for (int k = 0; k < 4; ++k) S[k] += p.S[k];
-        cc += p.curl_count;
-        cf = p.curl_first < cf ? p.curl_first : cf;
-        r0 += p.row0;
+    for (uint32_t base = 0; base < nb; base += 1024) {
+        const uint32_t i = base + t;
+        Partial p{};
+        if (i < nb) p = part[i];
+        // exclusive prefix of the blocks' column-0 increments (block order = scan order)
+        long long incl = i < nb ? p.delta : 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const long long o = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += o;
+        }
+        if (lane == 31) sh_tot[wp] = incl;
+        __syncthreads();
+        if (wp == 0) {
+            long long v = sh_tot[lane];
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const long long o = __shfl_up_sync(0xffffffffu, v, off);
+                if (lane >= off) v += o;
+            }
+            sh_tot[lane] = v;
+        }
+        __syncthreads();
+        const long long carry = carry_sh;
+        const long long pre = carry + incl - (i < nb ? p.delta : 0) + (wp > 0 ? sh_tot[wp - 1] : 0);
+        if (i < nb) {
+            part[i].prefix = pre;
+            const __int128 c = pre, c2 = c * c, c3 = c2 * c, c4 = c2 * c2, ns = (__int128)p.n_sites;
+            S[0] += c * ns + p.S[0];
+            S[1] += c2 * ns + 2 * c * p.S[0] + p.S[1];
+            S[2] += c3 * ns + 3 * c2 * p.S[0] + 3 * c * p.S[1] + p.S[2];
+            S[3] += c4 * ns + 4 * c3 * p.S[0] + 6 * c2 * p.S[1] + 4 * c * p.S[2] + p.S[3];
+            cc += p.curl_count;
+            cf = p.curl_first < cf ? p.curl_first : cf;
+            r0 += p.row0;
+        }
+        __syncthreads();
+        if (t == 1023) carry_sh = pre + (i < nb ? p.delta : 0);
+        __syncthreads();
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -332,7 +428,7 @@ __global__ void __launch_bounds__(256) k_measure_final(const Partial* __restrict
         __int128 tot[4] = {0, 0, 0, 0};
         unsigned long long tc = 0, tf = ~0ull;
         long long tr = 0;
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < 32; ++i) {
             for (int k = 0; k < 4; ++k) tot[k] += sh_s[k][i];
             tc += sh_cc[i];
             tf = sh_cf[i] < tf ? sh_cf[i] : tf;
@@ -345,17 +441,17 @@ __global__ void __launch_bounds__(256) k_measure_final(const Partial* __restrict
         res->curl_count = tc;
         res->curl_first = tf;
         res->row0_sum = tr;
-        res->col0_sum = *col_sum;
-        res->sy_first = *sy_first;
+        res->col0_sum = carry_sh;
+        res->sy_first = part[0].sy_first;
         res->pad = 0;
     }
 }
 
 // Heights (reference HeightMap layout): one warp per row, lane l owns words
-// l, l+32, ...; h(x,y) = G_y + u(x).
+// l, l+32, ...; h(x,y) = G_y + u(x) with G_y = block-local G + the block's prefix.
 template <typename Word>
 __global__ void k_heights(const Word* __restrict__ planes, Geom g, uint32_t X, const long long* __restrict__ G,
-                          int32_t* __restrict__ out) {
+                          const Partial* __restrict__ part, int32_t* __restrict__ out) {
     constexpr int W = int(sizeof(Word) * 8);
     const uint32_t Y = g.wrap, LD = g.Y, n = g.n;  // periodic only
     const uint32_t y = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -365,7 +461,8 @@ __global__ void k_heights(const Word* __restrict__ planes, Geom g, uint32_t X, c
     const int ya = int(y & 1u);
     const Word* Xa = planes + size_t(ya) * PS + y;
     const Word* Xb = planes + size_t(ya ^ 1) * PS + y;
-    long long carry = G[y];
+    const uint32_t vrow = y < g.c0 ? y + g.wrap : y;  // scan position of physical row y
+    long long carry = G[y] + part[(vrow - g.c0) / kRowsPerGroup].prefix;
     int32_t* row = out + size_t(y) * X;
     for (uint32_t kb = 0; kb < n; kb += 32) {
         const uint32_t k = kb + lane;
@@ -491,35 +588,39 @@ cudaError_t launch_balances(int w, const void* planes, Geom g, uint32_t r0, uint
 cudaError_t launch_measure(int w, const void* planes, Geom g, uint32_t X, void* scratch, void* result_dev,
                            cudaStream_t st) {
     long long* G = static_cast<long long*>(scratch);
-    Partial* part = reinterpret_cast<Partial*>(G + g.Y);
-    const uint32_t rows = g.c1 - g.c0;
-    const uint32_t nb = measure_blocks(rows);
-    long long* col = reinterpret_cast<long long*>(part + measure_blocks(g.Y + 1));
-    long long* syf = col + 1;
-    // periodic: rows 0..Y-1 in the reference's gauge; stripe: its core rows, local gauge
-    const uint32_t start = g.wrap ? 0 : g.c0;
-    const int excl = g.wrap ? 1 : 0;
-    if (w == 64) {
-        k_col_scan<uint64_t><<<1, 1024, 0, st>>>(static_cast<const uint64_t*>(planes), g, start, rows, excl, G, col,
-                                                  syf);
-        k_measure_rows<uint64_t><<<nb, kThreads, 0, st>>>(static_cast<const uint64_t*>(planes), g, X, G, part);
-    } else {
-        k_col_scan<uint32_t><<<1, 1024, 0, st>>>(static_cast<const uint32_t*>(planes), g, start, rows, excl, G, col,
-                                                  syf);
-        k_measure_rows<uint32_t><<<nb, kThreads, 0, st>>>(static_cast<const uint32_t*>(planes), g, X, G, part);
+    Partial* part = reinterpret_cast<Partial*>(G + g.Y + 1);
+    const uint32_t ngroups = measure_groups(g.c1 - g.c0);
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
     }
-    k_measure_final<<<1, 256, 0, st>>>(part, nb, col, syf, static_cast<MeasureResult*>(result_dev));
+    const uint32_t grid = std::min<uint32_t>(ngroups, uint32_t(2 * sms));  // persistent: 2 blocks per SM
+    if (w == 64) {
+        auto kern = k_measure_rows<uint64_t>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMeasSmem));
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kMThreads, kMeasSmem, st>>>(static_cast<const uint64_t*>(planes), g, X, G, part);
+    } else {
+        auto kern = k_measure_rows<uint32_t>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMeasSmem));
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kMThreads, kMeasSmem, st>>>(static_cast<const uint32_t*>(planes), g, X, G, part);
+    }
+    k_measure_final<<<1, 1024, 0, st>>>(part, ngroups, static_cast<MeasureResult*>(result_dev));
     return cudaGetLastError();
 }
 
 cudaError_t launch_heights(int w, const void* planes, Geom g, uint32_t X, const void* scratch, int32_t* out,
                            cudaStream_t st) {
     const long long* G = static_cast<const long long*>(scratch);
+    const Partial* part = reinterpret_cast<const Partial*>(G + g.Y + 1);
     const uint32_t threads = 128, blocks = (g.wrap * 32 + threads - 1) / threads;
     if (w == 64)
-        k_heights<uint64_t><<<blocks, threads, 0, st>>>(static_cast<const uint64_t*>(planes), g, X, G, out);
+        k_heights<uint64_t><<<blocks, threads, 0, st>>>(static_cast<const uint64_t*>(planes), g, X, G, part, out);
     else
-        k_heights<uint32_t><<<blocks, threads, 0, st>>>(static_cast<const uint32_t*>(planes), g, X, G, out);
+        k_heights<uint32_t><<<blocks, threads, 0, st>>>(static_cast<const uint32_t*>(planes), g, X, G, part, out);
     return cudaGetLastError();
 }
 

@@ -113,7 +113,7 @@ constexpr size_t kMeasSmem = sizeof(uint2) * (kT0Words + kT1Words) + sizeof(SegO
 }  // namespace
 
 size_t measure_scratch_bytes(uint32_t Y) {
-    return size_t(Y + 1) * sizeof(long long) + size_t(measure_groups(Y + 1) + 1) * sizeof(Partial) + 64;
+    return size_t(Y + 2) * sizeof(long long) + size_t(measure_groups(Y + 1) + 1) * sizeof(Partial) + 64;
 }
 
 namespace {
@@ -588,7 +588,7 @@ cudaError_t launch_balances(int w, const void* planes, Geom g, uint32_t r0, uint
 cudaError_t launch_measure(int w, const void* planes, Geom g, uint32_t X, void* scratch, void* result_dev,
                            cudaStream_t st) {
     long long* G = static_cast<long long*>(scratch);
-    Partial* part = reinterpret_cast<Partial*>(G + g.Y + 1);
+    Partial* part = reinterpret_cast<Partial*>(G + ((g.Y + 2) & ~1u));  // 16-B aligned (int128)
     const uint32_t ngroups = measure_groups(g.c1 - g.c0);
     static int sms = 0;
     if (!sms) {
@@ -615,7 +615,7 @@ cudaError_t launch_measure(int w, const void* planes, Geom g, uint32_t X, void* 
 cudaError_t launch_heights(int w, const void* planes, Geom g, uint32_t X, const void* scratch, int32_t* out,
                            cudaStream_t st) {
     const long long* G = static_cast<const long long*>(scratch);
-    const Partial* part = reinterpret_cast<const Partial*>(G + g.Y + 1);
+    const Partial* part = reinterpret_cast<const Partial*>(G + ((g.Y + 2) & ~1u));
     const uint32_t threads = 128, blocks = (g.wrap * 32 + threads - 1) / threads;
     if (w == 64)
         k_heights<uint64_t><<<blocks, threads, 0, st>>>(static_cast<const uint64_t*>(planes), g, X, G, part, out);

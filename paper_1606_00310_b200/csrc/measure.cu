@@ -101,7 +101,14 @@ __device__ const MeasTab g_tab = MeasTabInit();
 
 // shared memory: T0 replicated x16 (entry b at [b][lane & 15]: every warp lookup conflict-free),
 // T1 once; reused for the cross-warp combine after the row pass
-constexpr int kT0Words = 256 * 16;  // uint2
+#ifndef OCTGPU_MEAS_REP
+#define OCTGPU_MEAS_REP 16  // T0 replicas: 16 = every lookup conflict-free
+#endif
+#ifndef OCTGPU_MEAS_MINB
+#define OCTGPU_MEAS_MINB 2  // resident blocks per SM the register budget targets
+#endif
+constexpr int kRep = OCTGPU_MEAS_REP;
+constexpr int kT0Words = 256 * kRep;  // uint2
 constexpr int kT1Words = 17 * 256;
 struct SegOut {                      // one lane's segment result (int128 sums, delta, curl)
     __int128 T[4];
@@ -159,7 +166,7 @@ __device__ __noinline__ void flush_units(UnitAcc& A, long long B, __int128* T) {
 // T0 (entry b at t0b + 16 b), t1b = T1.
 __device__ __forceinline__ void unit(UnitAcc& A, int& u, uint32_t b0, uint32_t b1, const uint2* t0b,
                                      const uint2* t1b) {
-    const uint2 e0 = t0b[b0 * 16];
+    const uint2 e0 = t0b[b0 * kRep];
     const uint2 e1 = t1b[(e0.x >> 25) * 256 + b1];
     const uint32_t lo = e0.x + e1.x, hi = e0.y + e1.y;
     const int q3b = int(lo & 0xffffu), q1b = int((lo >> 16) & 0x1ffu), Db = int(lo >> 25);
@@ -168,7 +175,7 @@ __device__ __forceinline__ void unit(UnitAcc& A, int& u, uint32_t b0, uint32_t b
     const int u2 = u * u, u3 = u2 * u;
     A.Au1 += u;
     A.Au2 += u2;
-    A.Au3 = madw(u3, 1, A.Au3);
+    A.Au3 += (long long)u3;
     A.Au4 = madw(u2, u2, A.Au4);
     A.Aq1 += q1b;
     A.Aq2 += q2;
@@ -191,14 +198,14 @@ __device__ __forceinline__ void unit(UnitAcc& A, int& u, uint32_t b0, uint32_t b
 // warp s handles x-segment s (words [s n / kSeg, (s+1) n / kSeg)) of the group's 32 rows, then warp 0
 // combines the segments of each row and the group's rows into one Partial (group-local gauge).
 template <typename Word>
-__global__ void __launch_bounds__(kMThreads, 2) k_measure_rows(const Word* __restrict__ planes, Geom g, uint32_t X,
+__global__ void __launch_bounds__(kMThreads, OCTGPU_MEAS_MINB) k_measure_rows(const Word* __restrict__ planes, Geom g, uint32_t X,
                                                                long long* __restrict__ Gout, Partial* __restrict__ part) {
     constexpr int W = int(sizeof(Word) * 8);
     extern __shared__ __align__(16) unsigned char msm[];
     uint2* t0rep = reinterpret_cast<uint2*>(msm);
     uint2* t1 = t0rep + kT0Words;
     SegOut* so = reinterpret_cast<SegOut*>(t1 + kT1Words);
-    for (int i = threadIdx.x; i < kT0Words; i += kMThreads) t0rep[i] = g_tab.t0[i >> 4];
+    for (int i = threadIdx.x; i < kT0Words; i += kMThreads) t0rep[i] = g_tab.t0[i / kRep];
     {
         const uint4* src1 = reinterpret_cast<const uint4*>(g_tab.t1);
         uint4* dst1 = reinterpret_cast<uint4*>(t1);
@@ -211,7 +218,7 @@ __global__ void __launch_bounds__(kMThreads, 2) k_measure_rows(const Word* __res
     const size_t PS = g.plane_stride;
     const uint32_t kbeg = uint32_t(seg) * n / kSeg, kend = uint32_t(seg + 1) * n / kSeg;
     const uint32_t ngroups = measure_groups(g.c1 - g.c0);
-    const uint2* t0b = t0rep + (lane & 15);
+    const uint2* t0b = t0rep + (lane % kRep);
 
     for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
         const uint32_t first = g.c0 + grp * uint32_t(kRowsPerGroup);  // the group's first core row
@@ -229,21 +236,30 @@ __global__ void __launch_bounds__(kMThreads, 2) k_measure_rows(const Word* __res
         __int128 T[4] = {0, 0, 0, 0};
         long long B = 0;
         unsigned int rc = 0, rfirst = 0xffffffffu;
-        int sy0 = 0, sx0 = 0;
         {
             UnitAcc A;
             A.clear();
             int u = 0;
-            Word pcb = kend > kbeg ? pCb[size_t(kbeg == 0 ? n - 1 : kbeg - 1) * Y] : Word(0);
+            Word pcb = 0, nxa = 0, nxb = 0, nca = 0, ncb = 0;
+            if (kend > kbeg) {
+                pcb = pCb[size_t(kbeg == 0 ? n - 1 : kbeg - 1) * Y];
+                const size_t o = size_t(kbeg) * Y;
+                nxa = pXa[o];
+                nxb = pXb[o];
+                nca = pCa[o];
+                ncb = pCb[o];
+            }
             for (uint32_t k = kbeg; k < kend; ++k) {
-                const size_t o = size_t(k) * Y;
-                const Word xa = pXa[o], xb = pXb[o], ca = pCa[o], cb = pCb[o];
+                const Word xa = nxa, xb = nxb, ca = nca, cb = ncb;
+                if (k + 1 < kend) {  // prefetch the next word (the loads were the top stall)
+                    const size_t o = size_t(k + 1) * Y;
+                    nxa = pXa[o];
+                    nxb = pXb[o];
+                    nca = pCa[o];
+                    ncb = pCb[o];
+                }
                 const Word bxa = __shfl_up_sync(0xffffffffu, xa, 1);
                 const Word bxb = __shfl_up_sync(0xffffffffu, xb, 1);
-                if (k == 0) {
-                    sx0 = (xa & 1) ? 1 : -1;  // sigma_x-(0, y)
-                    sy0 = (ca & 1) ? 1 : -1;  // sigma_y-(0, y)
-                }
                 // curl check, word-parallel: parity ya (even-x sites, D rotated up one packed
                 // bit with the previous word's top bit) and parity !ya (odd-x sites, D aligned)
                 const Word D1 = Word((cb << 1) | (pcb >> (W - 1)));
@@ -288,6 +304,8 @@ __global__ void __launch_bounds__(kMThreads, 2) k_measure_rows(const Word* __res
         __syncthreads();
         if (seg == 0) {
             // column 0 in the group gauge: inclusive prefix of sigma_y-(0, y) over the core rows
+            // sigma_y-(0, y) and sigma_x-(0, y): bit 0 of word 0 of Y(ya) and X(ya)
+            const int sy0 = (pCa[0] & 1) ? 1 : -1, sx0 = (pXa[0] & 1) ? 1 : -1;
             long long incl = core ? sy0 : 0;
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
@@ -590,23 +608,29 @@ cudaError_t launch_measure(int w, const void* planes, Geom g, uint32_t X, void* 
     long long* G = static_cast<long long*>(scratch);
     Partial* part = reinterpret_cast<Partial*>(G + ((g.Y + 2) & ~1u));  // 16-B aligned (int128)
     const uint32_t ngroups = measure_groups(g.c1 - g.c0);
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
-    }
-    const uint32_t grid = std::min<uint32_t>(ngroups, uint32_t(2 * sms));  // persistent: 2 blocks per SM
+    // persistent grid: exactly the blocks that are resident at once (registers / shared memory)
+    auto persistent = [&](auto kern, uint32_t& grid) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMeasSmem));
+        if (e != cudaSuccess) return e;
+        int dev = 0, sms = 0, per_sm = 0;
+        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMThreads, kMeasSmem)) != cudaSuccess)
+            return e;
+        grid = std::max<uint32_t>(1, std::min<uint32_t>(ngroups, uint32_t(std::max(per_sm, 1) * sms)));
+        return cudaSuccess;
+    };
+    uint32_t grid = 1;
     if (w == 64) {
-        auto kern = k_measure_rows<uint64_t>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMeasSmem));
+        cudaError_t e = persistent(k_measure_rows<uint64_t>, grid);
         if (e != cudaSuccess) return e;
-        kern<<<grid, kMThreads, kMeasSmem, st>>>(static_cast<const uint64_t*>(planes), g, X, G, part);
+        k_measure_rows<uint64_t><<<grid, kMThreads, kMeasSmem, st>>>(static_cast<const uint64_t*>(planes), g, X, G,
+                                                                      part);
     } else {
-        auto kern = k_measure_rows<uint32_t>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMeasSmem));
+        cudaError_t e = persistent(k_measure_rows<uint32_t>, grid);
         if (e != cudaSuccess) return e;
-        kern<<<grid, kMThreads, kMeasSmem, st>>>(static_cast<const uint32_t*>(planes), g, X, G, part);
+        k_measure_rows<uint32_t><<<grid, kMThreads, kMeasSmem, st>>>(static_cast<const uint32_t*>(planes), g, X, G,
+                                                                      part);
     }
     k_measure_final<<<1, 1024, 0, st>>>(part, ngroups, static_cast<MeasureResult*>(result_dev));
     return cudaGetLastError();

@@ -129,31 +129,6 @@ def _int_pipe(kernel: str, config: str):
         return None
 
 
-def _mcs_kernel(prm, Y: int, n: int, ws: int) -> tuple[str, int]:
-    """The fused MCS kernel the engine runs for these parameters and the MCS per launch
-    (engine.cu octgpu_step: k_mcs_deep, 2 MCS per pass, for constant-xi modes (periodic lattices with
-    n >= 8 words and >= 256 rows, and row stripes) and for one-draw-per-word modes (periodic);
-    otherwise k_mcs_bulk, 1 MCS per pass)."""
-    from paper_1606_00310_b200.params import ProbMode
-
-    one = [ps.mode == ProbMode.Arbitrary and ps.value == 1.0 for ps in (prm.p, prm.q)]
-    const = all(ps.mode == ProbMode.Zero or o for ps, o in zip((prm.p, prm.q), one))
-    deep_env = os.environ.get("OCTGPU_DEEP", "1")
-    # mcs_deep_supported (mcs_deep.cu): zero / half / dyadic / r = 1 modes, r = 1 only next to constant xi
-    cheap = all(ps.mode in (ProbMode.Zero, ProbMode.Half, ProbMode.Dyadic) or o for ps, o in zip((prm.p, prm.q), one))
-    if deep_env == "2" and n >= 8 and (ws > 1 or Y >= 256) and cheap and (const or (ws == 1 and not any(one))):
-        return "k_mcs_deep", 2  # forced (tests / experiments)
-    sites = 128 * n * Y // ws  # per engine (stripe)
-    # stripes test the whole lattice (engine.cu stripe_deep_ok), so every rank picks the same pass length
-    big = deep_env == "2" or (128 * n * Y if ws > 1 else sites) >= 1 << 28
-    if const and n >= 8 and (ws > 1 or Y >= 256) and deep_env != "0" and big:
-        return "k_mcs_deep", 2  # periodic lattice, or each rank's row stripe (2-MCS passes)
-    if (ws == 1 and prm.draws_per_word(64) == 1 and n >= 8 and Y >= 256 and deep_env != "0"
-            and (deep_env == "2" or sites >= 1 << 30)):
-        return "k_mcs_deep", 2  # one live stream draw per word (p = 1/2, q = 0), large lattices
-    return "k_mcs_bulk", 1
-
-
 def _sync_all(engines) -> None:
     """Drain every engine's stream (a helper, so no loop variable keeps an engine - and its plane sets -
     alive after the caller drops it: the next engine then reuses the pooled memory)."""
@@ -174,23 +149,6 @@ def timed_window(K: int, from_flat: bool, schedule: list[int]):
     desc = (f"MCS {t_start + 1}..{t_start + K} of {span} with its {len(sched)} W^2 points; "
             + (f"state at t={t_start} prepared untimed" if t_start else "from the flat start"))
     return t_start, sched, targets, desc
-
-
-def _ctr_kernel(prm, Y: int, n: int, ws: int) -> tuple[str, float]:
-    """The kernel of a counter-rng step (engine.cu step_counter / stripe_kernel_ctr): 2-MCS passes for the
-    cheap modes from 2^28 sites per engine, the one-MCS TMA pass otherwise, in-place sweeps on lattices the
-    TMA kernels do not take."""
-    from paper_1606_00310_b200.params import ProbMode
-
-    one = [ps.mode == ProbMode.Arbitrary and ps.value == 1.0 for ps in (prm.p, prm.q)]
-    const = all(ps.mode == ProbMode.Zero or o for ps, o in zip((prm.p, prm.q), one))
-    cheap = all(ps.mode in (ProbMode.Zero, ProbMode.Half, ProbMode.Dyadic) or o for ps, o in zip((prm.p, prm.q), one))
-    deep_env = os.environ.get("OCTGPU_DEEP", "1")
-    tma = n >= 8 and (ws > 1 or Y >= 256)
-    big = deep_env == "2" or 128 * n * Y >= 1 << 28  # the whole lattice, for stripes too (stripe_deep_ok)
-    if tma and cheap and (const or not any(one)) and deep_env != "0" and big:
-        return "k_mcs_deep", 2
-    return ("k_mcs_bulk", 1) if tma else ("k_sweep_ctr", 0.5)
 
 
 def _dist():
@@ -477,13 +435,12 @@ def main():
         _sync_all(engs)
     torch.cuda.synchronize()
     ms, step_ms, records, launches, clocks = timed(job, engs, prm, t_start, sched, targets, clk_device=local)
+    kname, mcs_per_launch = engs[0].pass_plan(prm)  # the engine's own dispatch (octgpu_pass_plan)
     value = X * Y * K / (ms * 1e6)
     kernel_ms = step_ms / K  # per MCS, all launches of the step calls
     peak, peak_src = _peaks()
-    kname, mcs_per_launch = (_mcs_kernel(prm, Y, X // 128, ws) if args.rng == "xoshiro"
-                             else _ctr_kernel(prm, Y, X // 128, ws))
     # paper identity: 1 byte of slope traffic per site update, per GPU, per launch
-    alg_bytes = X * Y // ws * mcs_per_launch
+    alg_bytes = int(X * Y // ws * mcs_per_launch)
     launch_ms = kernel_ms * mcs_per_launch
     achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
     final_checksum = engs[0].checksum() if ws == 1 else None
@@ -608,7 +565,7 @@ def main():
                 eng.step(prmc, t0c)
                 eng.sync()
             msc, stepc, recc, lc, clkc = timed(eng, [eng], prmc, t0c, schedc, targetsc, clk_device=local)
-            kc, mplc = _mcs_kernel(prmc, c["Y"], c["X"] // 128, 1)
+            kc, mplc = eng.pass_plan(prmc)
             kmsc = stepc / Kc
             lmsc = kmsc * mplc
             gbs, dfrac, trc = dram(kc, name, lmsc)
@@ -644,7 +601,7 @@ def main():
                          "peak_source": peak_src, "dram_gbs": dram(kname, args.config, launch_ms)[0],
                          "dram_frac": dram(kname, args.config, launch_ms)[1],
                          "note": "alg bytes = 1 B/site-update (2 slope bits x 2 reads + 2 writes per MCS); the fused "
-                                 "kernels move ~0.5 B (k_mcs_bulk) / ~0.25 B (k_mcs_deep) of DRAM traffic per update, "
+                                 "kernels move ~0.5 B (k_mcs_bulk) / ~0.25 or ~0.17 B (k_mcs_deep, 2 or 3 MCS) of DRAM traffic per update, "
                                  "so frac exceeds 1; traffic = ncu dram bytes per launch (profiles/ncu_summary.json)"},
             "int_pipe": _int_pipe(kname, args.config),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "digest": digest,

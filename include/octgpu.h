@@ -149,6 +149,16 @@ int octgpu_set_tile_shift(octgpu_engine* e, uint64_t seed);
 int octgpu_set_rng(octgpu_engine* e, int kind);
 int octgpu_get_rng(const octgpu_engine* e);
 
+/* The fused pass octgpu_step (or, on a row stripe, octgpu_stripe_max_mcs) launches for prm on this engine:
+ * *kernel = OCTGPU_KERNEL_* and *sweeps_per_launch = sublattice sweeps one full-length launch covers (2 per
+ * MCS: 6 for a 3-MCS k_mcs_deep pass, 2 for the one-MCS kernels, 1 for in-place sweeps). No reference
+ * counterpart (the reference's sweeps are OpenMP loops); used by benchmarks to attribute kernel time. */
+#define OCTGPU_KERNEL_MCS 0   /* k_mcs: register-prefetch one-MCS pass */
+#define OCTGPU_KERNEL_BULK 1  /* k_mcs_bulk: TMA one-MCS pass */
+#define OCTGPU_KERNEL_DEEP 2  /* k_mcs_deep: TMA, temporally blocked (2 or 3 MCS per pass) */
+#define OCTGPU_KERNEL_SWEEP 3 /* k_sweep_ctr: one in-place sweep */
+int octgpu_pass_plan(octgpu_engine* e, const octgpu_params* prm, int* kernel, int* sweeps_per_launch);
+
 /* ---- state access ---- */
 
 uint64_t octgpu_t(const octgpu_engine* e);         /* VecEngine::t (engine_vec.hpp:199) */

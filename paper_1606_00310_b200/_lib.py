@@ -103,7 +103,7 @@ EXPORTS = (
     "octgpu_stripe_disconnect", "octgpu_set_tile_shift", "octgpu_stripes_combine",
     "octgpu_set_rng", "octgpu_get_rng",
     "octgpu_stripe_y0", "octgpu_stripe_rows", "octgpu_height_moments", "octgpu_release_pool",
-    "octgpu_balances",
+    "octgpu_balances", "octgpu_pass_plan",
 )
 
 _lib = None
@@ -169,6 +169,7 @@ def lib() -> C.CDLL:
         "octgpu_height_moments": (None, [u32, u32, vp, vp]),
         "octgpu_release_pool": (i32, [i32]),
         "octgpu_balances": (i32, [vp, vp, vp]),
+        "octgpu_pass_plan": (i32, [vp, P(OctParams), P(i32), P(i32)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

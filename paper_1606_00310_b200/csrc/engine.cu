@@ -339,6 +339,7 @@ struct octgpu_engine {
     CUtensorMap tmd[2][2];  // the same for k_mcs_deep (deep_box_rows rows x 2 / 3 words)
     bool tmd_ok = false;
     int deep = 1;  // temporally blocked passes (k_mcs_deep) where supported; OCTGPU_DEEP=0 disables
+    int deep_l = kDeepSweepsConst;  // sweeps of a constant-xi deep pass (OCTGPU_DEEP_L = 4 keeps 2 MCS per pass)
     bool graphs = true;  // replay CUDA graphs for long step() calls (OCTGPU_GRAPH=0 disables)
     uint32_t prefetch = 0;  // TMA kernels: L2 prefetch distance in ring stages (OCTGPU_PREFETCH)
     long long p2p_timeout = kP2PTimeoutCycles;  // peer halo wait limit (OCTGPU_P2P_TIMEOUT_MS)
@@ -362,8 +363,8 @@ struct octgpu_engine {
     octgpu_peer prev{}, next{};
     std::vector<void*> ipc_opened;  // peer allocations mapped with cudaIpcOpenMemHandle
 
-    // k_mcs_deep: the same periodic lattice with core rows starting at virtual row kDeepSweeps - 1
-    Geom deep_geom() const { return Geom{Y, n, size_t(n) * Y, kDeepSweeps - 1, L + kDeepSweeps - 1, L, 0, kGhostRows}; }
+    // k_mcs_deep (ls sweeps per pass): the same periodic lattice with core rows starting at virtual row ls - 1
+    Geom deep_geom(int ls) const { return Geom{Y, n, size_t(n) * Y, uint32_t(ls - 1), L + uint32_t(ls - 1), L, 0, kGhostRows}; }
     Geom geom() const {
         // stripe: local row 0 = global y0 - kStripeHA (parity of y0 + 1)
         if (!stripe) return Geom{Y, n, size_t(n) * Y, 1, L + 1, L, 0, kGhostRows};
@@ -473,6 +474,7 @@ int plan_mcs(octgpu_engine* e) {
     if (const char* v = getenv("OCTGPU_P2P_TIMEOUT_MS")) e->p2p_timeout = std::max(1LL, atoll(v)) * 2'000'000LL;
     if (const char* v = getenv("OCTGPU_PREFETCH")) e->prefetch = uint32_t(std::max(0, std::min(64, atoi(v))));
     if (const char* v = getenv("OCTGPU_DEEP_S")) e->deep_S = std::max(2, std::min(8, atoi(v)));
+    if (const char* v = getenv("OCTGPU_DEEP_L")) e->deep_l = atoi(v) == kDeepSweepsLive ? kDeepSweepsLive : kDeepSweepsConst;
     return OCTGPU_OK;
 }
 
@@ -519,7 +521,7 @@ int ensure_tmaps_deep(octgpu_engine* e) {
         for (int v = 0; v < 2; ++v) {
             const cuuint64_t dims[3] = {e->Y, e->n, 4};
             const cuuint64_t strides[2] = {cuuint64_t(e->Y) * 8, cuuint64_t(e->n) * e->Y * 8};
-            const cuuint32_t box[3] = {cuuint32_t(deep_box_rows(kDeepSweeps)), cuuint32_t(kDeepKS + v), 1};
+            const cuuint32_t box[3] = {cuuint32_t(deep_box_rows()), cuuint32_t(kDeepKS + v), 1};
             const cuuint32_t estr[3] = {1, 1, 1};
             const CUresult r = enc(&e->tmd[b][v], CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, e->planes[b], dims, strides, box,
                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -972,16 +974,37 @@ namespace {
 
 // k_mcs_deep ring depth: deep_S (3) unless two blocks per SM would no longer fit
 // in shared memory (live passes park xoshiro states and pre-drawn xi there) -> 2.
-int deep_ring(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool ctr = false) {
+int deep_ring(octgpu_engine* e, const ProbDev& p, const ProbDev& q, int ls, bool ctr = false) {
     int smem_sm = 0;
     if (cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, e->device) != cudaSuccess)
         return 2;
     int S = e->deep_S;
-    while (S > 2 && 2 * (mcs_deep_smem(p.mode, q.mode, kDeepSweeps, S, ctr) + 1024) > size_t(smem_sm)) --S;
+    while (S > 2 && 2 * (mcs_deep_smem(p.mode, q.mode, ls, S, ctr) + 1024) > size_t(smem_sm)) --S;
     return S;
 }
 
-// One fused pass (k_mcs_deep: kDeepSweeps/2 MCS; else 1 MCS) from the current plane / rng set into the other,
+// sweeps per k_mcs_deep pass: 6 (3 MCS) where the kernel takes it (constant xi on a periodic lattice), else 4;
+// row stripes always 4 (their halo rows are sized for kStripeSweeps)
+int deep_sweeps(const octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool ctr) {
+    if (e->stripe) return kStripeSweeps;
+    return (e->deep_l == kDeepSweepsConst && mcs_deep_supported_l(p.mode, q.mode, kDeepSweepsConst, ctr))
+               ? kDeepSweepsConst
+               : kDeepSweepsLive;
+}
+
+// Periodic lattices: does octgpu_step run k_mcs_deep passes for these parameters? (D = draws per word of a
+// xoshiro sweep; ctr = the counter-based streams)
+bool deep_policy(const octgpu_engine* e, const ProbDev& p, const ProbDev& q, uint64_t D, bool ctr) {
+    if (e->mcs_impl != 2 || !mcs_deep_supported(p.mode, q.mode) || e->deep == 0) return false;
+    if (e->deep == 2) return true;
+    const uint64_t sites = uint64_t(e->X) * e->L;
+    const bool live = !(is_const(p) && is_const(q));
+    // 2-MCS passes with counter streams: no stream state to park, so every cheap mode qualifies from 2^28
+    if (ctr || !live) return sites >= (uint64_t(1) << 28);
+    return D == 1 && sites >= (uint64_t(1) << 30);
+}
+
+// One fused pass (k_mcs_deep: 2 or 3 MCS; else 1 MCS) from the current plane / rng set into the other,
 // with the host-side bookkeeping of what the pass does.
 // Random tile-origin shift (the DTr idea of BASELINE.json's north_star, applied to the block tiling): the
 // first core row of the block decomposition moves by s rows, drawn per pass from (tile_shift seed, t).
@@ -1003,15 +1026,17 @@ Geom shifted(const octgpu_engine* e, Geom g, uint32_t window) {
     return g;
 }
 
-int step_pass(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool live, bool deep, const uint64_t* jtab,
+// ls = sweeps of a k_mcs_deep pass (4 or 6), 0 = one-MCS kernel
+int step_pass(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool live, int ls, const uint64_t* jtab,
               uint64_t per_sweep) {
     const int ps = e->pcur, rs = e->rcur;
+    const bool deep = ls > 0;
     if (deep) {
         int rc = ensure_tmaps_deep(e);
         if (rc) return rc;
         CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase,
-                           shifted(e, e->deep_geom(), uint32_t(deep_box_rows(kDeepSweeps))), p, q, jtab,
-                           deep_ring(e, p, q), &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
+                           shifted(e, e->deep_geom(ls), uint32_t(deep_box_rows())), p, q, jtab, ls,
+                           deep_ring(e, p, q, ls), &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
     } else if (e->mcs_impl == 2) {
         int rc = plan_bulk(e, p, q);
         if (rc) return rc;
@@ -1022,7 +1047,7 @@ int step_pass(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool live, b
         CK(launch_mcs(e->w, e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, e->geom(), p, q,
                       live, jtab, e->stream));
     }
-    const uint32_t mcs = deep ? kDeepSweeps / 2 : 1;
+    const uint32_t mcs = deep ? uint32_t(ls / 2) : 1u;
     ++e->launches;
     e->pcur ^= 1;
     if (live)
@@ -1033,12 +1058,12 @@ int step_pass(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool live, b
     return OCTGPU_OK;
 }
 
-std::string graph_key(const octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool deep, const uint64_t* jtab) {
+std::string graph_key(const octgpu_engine* e, const ProbDev& p, const ProbDev& q, int ls, const uint64_t* jtab) {
     char buf[256];
     std::snprintf(buf, sizeof buf, "%d/%u/%llx/%llx|%d/%u/%llx/%llx|%d|%d%d%d|%p|%d%d%d", p.mode, p.k,
                   (unsigned long long)p.m, (unsigned long long)p.T, q.mode, q.k, (unsigned long long)q.m,
-                  (unsigned long long)q.T, int(deep), e->pcur, e->rcur, e->phase, static_cast<const void*>(jtab),
-                  deep_ring(const_cast<octgpu_engine*>(e), p, q), e->bulk_ks, e->bulk_S);
+                  (unsigned long long)q.T, ls, e->pcur, e->rcur, e->phase, static_cast<const void*>(jtab),
+                  ls ? deep_ring(const_cast<octgpu_engine*>(e), p, q, ls) : 0, e->bulk_ks, e->bulk_S);
     return buf;
 }
 
@@ -1056,17 +1081,18 @@ int step_counter(octgpu_engine* e, const ProbDev& p, const ProbDev& q, uint64_t 
     }
     // 2-MCS passes (k_mcs_deep<CTR>): no stream state to park, so every cheap mode qualifies; same size
     // threshold as the constant-xi xoshiro passes
-    const bool deep = e->mcs_impl == 2 && mcs_deep_supported(p.mode, q.mode) &&
-                      (e->deep == 2 || (e->deep == 1 && uint64_t(e->X) * e->L >= (uint64_t(1) << 28)));
+    const bool deep = deep_policy(e, p, q, 0, true);
     if (deep) {
         int rc = ensure_tmaps_deep(e);
         if (rc) return rc;
-        const uint64_t mpp = kDeepSweeps / 2;
-        while (n_mcs >= mpp) {
+        const int lsmax = deep_sweeps(e, p, q, true);
+        while (n_mcs >= 2) {  // full-length passes, then a 2-MCS pass for a remainder of 2
+            const int ls = n_mcs >= uint64_t(lsmax / 2) ? lsmax : kDeepSweepsLive;
+            const uint64_t mpp = uint64_t(ls / 2);
             const int ps = e->pcur;
             CK(launch_mcs_deep_ctr(e->planes[ps], e->planes[ps ^ 1], e->phase,
-                                   shifted(e, e->deep_geom(), uint32_t(deep_box_rows(kDeepSweeps))), p, q,
-                                   e->master_seed, 2 * e->t, deep_ring(e, p, q, true), &e->tmd[ps][0], &e->tmd[ps][1],
+                                   shifted(e, e->deep_geom(ls), uint32_t(deep_box_rows())), p, q, e->master_seed,
+                                   2 * e->t, ls, deep_ring(e, p, q, ls, true), &e->tmd[ps][0], &e->tmd[ps][1],
                                    e->stream));
             ++e->launches;
             e->pcur ^= 1;
@@ -1128,11 +1154,9 @@ int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
     // Small lattices underfill the GPU and are latency-bound, where the longer 2-MCS
     // pipeline loses (tools/step_timer.py: constant xi wins from 2^28 sites, p = 1/2
     // from 2^30); OCTGPU_DEEP=2 forces the deep pass for any size (tests).
-    const uint64_t sites = uint64_t(e->X) * e->L;
-    const bool deep = e->mcs_impl == 2 && mcs_deep_supported(p.mode, q.mode) &&
-                      (e->deep == 2 || (e->deep == 1 && (live ? (D == 1 && sites >= (uint64_t(1) << 30))
-                                                               : sites >= (uint64_t(1) << 28))));
-    const uint64_t mpp = deep ? kDeepSweeps / 2 : 1;  // MCS per pass
+    const bool deep = deep_policy(e, p, q, D, false);
+    const int lsmax = deep ? deep_sweeps(e, p, q, false) : 0;  // sweeps per full-length pass (0: one-MCS kernel)
+    const uint64_t mpp = deep ? uint64_t(lsmax / 2) : 1;  // MCS per pass
     uint64_t left = n_mcs;
     // Long runs on small / medium lattices replay a CUDA graph of kGraphPasses passes
     // (an even number, so the plane / rng sets end where they started and the captured
@@ -1146,10 +1170,10 @@ int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
                           e->stream != cudaStreamLegacy && e->stream != cudaStreamPerThread;
     if (graph_ok && left >= 2 * period) {
         // first pass outside any capture: plans, tensor maps and kernel attributes exist afterwards
-        rc = step_pass(e, p, q, live, deep, jtab, per_sweep);
+        rc = step_pass(e, p, q, live, lsmax, jtab, per_sweep);
         if (rc) return rc;
         left -= mpp;
-        const std::string key = graph_key(e, p, q, deep, jtab);
+        const std::string key = graph_key(e, p, q, lsmax, jtab);
         auto it = e->graph_cache.find(key);
         if (it == e->graph_cache.end()) {
             const int pc = e->pcur, rcs = e->rcur;
@@ -1157,7 +1181,7 @@ int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
             cudaGraph_t graph = nullptr;
             CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
             int crc = OCTGPU_OK;
-            for (int k = 0; k < kGraphPasses && !crc; ++k) crc = step_pass(e, p, q, live, deep, jtab, per_sweep);
+            for (int k = 0; k < kGraphPasses && !crc; ++k) crc = step_pass(e, p, q, live, lsmax, jtab, per_sweep);
             const cudaError_t ce = cudaStreamEndCapture(e->stream, &graph);
             e->pcur = pc;  // capturing enqueued nothing: undo the bookkeeping
             e->rcur = rcs;
@@ -1184,10 +1208,11 @@ int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
         }
     }
     while (left > 0) {
-        const bool d = deep && left >= mpp;
-        rc = step_pass(e, p, q, live, d, jtab, per_sweep);
+        // full-length passes, then a 2-MCS pass for a remainder of 2 (of a 3-MCS schedule), then one MCS
+        const int ls = !deep ? 0 : left >= mpp ? lsmax : left >= 2 ? kDeepSweepsLive : 0;
+        rc = step_pass(e, p, q, live, ls, jtab, per_sweep);
         if (rc) return rc;
-        left -= d ? mpp : 1;
+        left -= ls ? uint64_t(ls / 2) : 1;
     }
     return OCTGPU_OK;
 }
@@ -1540,7 +1565,8 @@ int stripe_kernel_ctr(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool
         int rc = ensure_tmaps_deep(e);
         if (rc) return rc;
         CK(launch_mcs_deep_ctr(e->planes[ps], e->planes[ps ^ 1], e->phase, g, p, q, e->master_seed, 2 * e->t,
-                               deep_ring(e, p, q, true), &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
+                               kStripeSweeps, deep_ring(e, p, q, kStripeSweeps, true), &e->tmd[ps][0],
+                               &e->tmd[ps][1], e->stream));
     } else {
         int rc = plan_bulk(e, p, q);
         if (rc) return rc;
@@ -1552,6 +1578,33 @@ int stripe_kernel_ctr(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool
 }
 }  // namespace
 
+int octgpu_pass_plan(octgpu_engine* e, const octgpu_params* prm, int* kernel, int* sweeps_per_launch) {
+    if (!e || !kernel || !sweeps_per_launch) return fail(OCTGPU_ERR_CONFIG, "null engine / output");
+    ProbDev p, q;
+    const int rc = lower_params(prm, p, q);
+    if (rc) return rc;
+    const bool ctr = e->rng_kind == OCTGPU_RNG_COUNTER;
+    int k = e->mcs_impl == 2 ? OCTGPU_KERNEL_BULK : OCTGPU_KERNEL_MCS, ls = 2;
+    if (e->stripe) {
+        if (stripe_deep_ok(e, p, q)) {
+            k = OCTGPU_KERNEL_DEEP;
+            ls = kStripeSweeps;
+        }
+    } else {
+        const uint64_t D = draws(prm->p, e->w) + (q.mode != M_ZERO ? draws(prm->q, e->w) : 0);
+        if (deep_policy(e, p, q, D, ctr)) {
+            k = OCTGPU_KERNEL_DEEP;
+            ls = deep_sweeps(e, p, q, ctr);
+        } else if (ctr && !(e->mcs_impl == 2 && e->bulk_ks == 2)) {
+            k = OCTGPU_KERNEL_SWEEP;
+            ls = 1;
+        }
+    }
+    *kernel = k;
+    *sweeps_per_launch = ls;
+    return OCTGPU_OK;
+}
+
 int octgpu_stripe_max_mcs(octgpu_engine* e, const octgpu_params* prm) {
     if (!e || !e->stripe) {
         fail(OCTGPU_ERR_CONFIG, "not a row stripe");
@@ -1559,7 +1612,7 @@ int octgpu_stripe_max_mcs(octgpu_engine* e, const octgpu_params* prm) {
     }
     ProbDev p, q;
     if (lower_params(prm, p, q)) return 0;
-    return stripe_deep_ok(e, p, q) ? kDeepSweeps / 2 : 1;
+    return stripe_deep_ok(e, p, q) ? kStripeSweeps / 2 : 1;
 }
 
 int octgpu_stripe_mcs_n(octgpu_engine* e, const octgpu_params* prm, uint32_t n_mcs, void* boundary_out) {
@@ -1568,9 +1621,9 @@ int octgpu_stripe_mcs_n(octgpu_engine* e, const octgpu_params* prm, uint32_t n_m
     int rc = lower_params(prm, p, q);
     if (!rc) rc = use_device(e);
     if (rc) return rc;
-    const bool deep = n_mcs == uint32_t(kDeepSweeps / 2);
+    const bool deep = n_mcs == uint32_t(kStripeSweeps / 2);
     if (n_mcs != 1 && !(deep && stripe_deep_ok(e, p, q)))
-        return fail(OCTGPU_ERR_CONFIG, "a stripe pass covers 1 MCS, or " + std::to_string(kDeepSweeps / 2) +
+        return fail(OCTGPU_ERR_CONFIG, "a stripe pass covers 1 MCS, or " + std::to_string(kStripeSweeps / 2) +
                                            " with constant xi (see octgpu_stripe_max_mcs)");
     const bool ctr = e->rng_kind == OCTGPU_RNG_COUNTER;
     const bool live = !ctr && !(is_const(p) && is_const(q));
@@ -1591,7 +1644,8 @@ int octgpu_stripe_mcs_n(octgpu_engine* e, const octgpu_params* prm, uint32_t n_m
         rc = ensure_tmaps_deep(e);
         if (rc) return rc;
         CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
-                           deep_ring(e, p, q), &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
+                           kStripeSweeps, deep_ring(e, p, q, kStripeSweeps), &e->tmd[ps][0], &e->tmd[ps][1],
+                           e->stream));
     } else if (e->mcs_impl == 2) {
         rc = plan_bulk(e, p, q);
         if (rc) return rc;
@@ -1782,9 +1836,9 @@ int octgpu_stripe_pass(octgpu_engine* e, const octgpu_params* prm, uint32_t n_mc
     int rc = lower_params(prm, p, q);
     if (!rc) rc = use_device(e);
     if (rc) return rc;
-    const bool deep = n_mcs == uint32_t(kDeepSweeps / 2);
+    const bool deep = n_mcs == uint32_t(kStripeSweeps / 2);
     if (n_mcs != 1 && !(deep && stripe_deep_ok(e, p, q)))
-        return fail(OCTGPU_ERR_CONFIG, "a stripe pass covers 1 MCS, or " + std::to_string(kDeepSweeps / 2) +
+        return fail(OCTGPU_ERR_CONFIG, "a stripe pass covers 1 MCS, or " + std::to_string(kStripeSweeps / 2) +
                                            " with constant xi (see octgpu_stripe_max_mcs)");
     const bool ctr = e->rng_kind == OCTGPU_RNG_COUNTER;
     const bool live = !ctr && !(is_const(p) && is_const(q));
@@ -1810,7 +1864,8 @@ int octgpu_stripe_pass(octgpu_engine* e, const octgpu_params* prm, uint32_t n_mc
         rc = ensure_tmaps_deep(e);
         if (rc) return rc;
         CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
-                           deep_ring(e, p, q), &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
+                           kStripeSweeps, deep_ring(e, p, q, kStripeSweeps), &e->tmd[ps][0], &e->tmd[ps][1],
+                           e->stream));
     } else {
         rc = plan_bulk(e, p, q);
         if (rc) return rc;

@@ -39,29 +39,29 @@ namespace octgpu {
 
 namespace {
 
-#ifndef OCTGPU_DEEP_GHOST_HOIST
-#define OCTGPU_DEEP_GHOST_HOIST 0  // hoisting duplicates the steady state: +regs, spills, measured 4% slower
-#endif
-
-constexpr int kDP = kDeepWarps;  // compute warps per block (+1 producer)
-constexpr int kKS = kDeepKS;            // words per ring stage
-constexpr int kSMax = 8;                // ring stages: runtime S <= kSMax (barrier slots)
-constexpr int kLanes = 32 * kDP;        // parking-slot stride (compute lanes per block)
-// xoshiro streams kept in registers in a live pass; the others live in parking slots
-// (loaded / stored around each use): four 256-bit states per lane do not fit 96 registers
+constexpr int kDP = kDeepWarps;   // compute warps per block (+1 producer)
+constexpr int kKS = kDeepKS;      // words per ring stage
+constexpr int kSMax = 8;          // ring stages: runtime S <= kSMax (barrier slots)
+constexpr int kLanes = kDeepLanes;  // rows per block = compute lanes = parking-slot stride
+// xoshiro streams kept in registers in a live pass; the others live in parking slots (loaded / stored
+// around each use). With the block-wide lane layout a 4-sweep pass keeps all four in registers.
 #ifndef OCTGPU_DEEP_REG_STREAMS
-#define OCTGPU_DEEP_REG_STREAMS 2
+#define OCTGPU_DEEP_REG_STREAMS 4
 #endif
 constexpr int kRegStreams = OCTGPU_DEEP_REG_STREAMS;
+constexpr int kXchBar = 1;  // named barrier of the compute warps' edge exchange (0 = __syncthreads)
 
 template <int L>
 struct DeepGeo {
-    static constexpr int kCore = 34 - 2 * L;   // core lanes L-1 .. 32-L
-    static constexpr int kRows = kCore * kDP;  // core rows per block
-    // window: every compute warp's 32 lanes + row 32 of the last warp (stage 1's Y(s)[y+1]), even rows
-    static constexpr int kWin = (kCore * (kDP - 1) + 33 + 1) / 2 * 2;
-    static_assert(kWin <= int(kGhostRows), "ghost rows must cover the window overhang");
-    static_assert(kWin == deep_box_rows(L), "host tensor-map box must match");
+    // core lanes L-1 .. kLanes-2-L: lane kLanes-1-L would still be exact, but an even core-row count keeps
+    // every block's window start even (a TMA box must start 16-B aligned in its innermost, row dimension)
+    static constexpr int kFirst = L - 1;           // first core lane
+    static constexpr int kLast = kLanes - 2 - L;   // last core lane
+    static constexpr int kRows = kLast - kFirst + 1;  // core rows per block
+    static constexpr int kWin = kLanes;            // window rows (TMA box)
+    static_assert(kRows == deep_core_rows(L), "host core-row count must match");
+    static_assert(kWin == deep_box_rows(), "host tensor-map box must match");
+    static_assert(kWin + 64 <= int(kGhostRows), "ghost rows must cover the window overhang and tile shifts");
 };
 
 constexpr int align16w(int words) { return (words + 15) / 16 * 16; }
@@ -75,7 +75,7 @@ struct DeepStage {  // ring stage: Xf[KS][W] | Yf[KS][W] | Ys[KS][W] | Xs[KS+1][
     static constexpr uint32_t kTx = (4 * kKS + 1) * W * 8;
 };
 
-// Per-lane parking slots in shared memory ([slot][kLanes] u64).
+// Per-lane parking slots in shared memory ([slot][kLanes] u64), then the edge exchange buffers.
 template <int L, int PM, int QM, bool CTR = false>
 struct DeepSlots {
     static constexpr bool kPreP = !(PM == M_ZERO || PM == M_ONE);
@@ -93,6 +93,8 @@ struct DeepSlots {
     __host__ __device__ static constexpr int st0() { return preQ0() + (kPreQ ? npre() : 0); }
     __host__ __device__ static constexpr int count() { return st0() + 4 * parked(); }
     __host__ __device__ static constexpr int pre(int l, int j) { return (l - 1) * (l - 2) / 2 + j; }
+    // edge exchange: [2 buffers][kDP warps][C of lane 31 | B of lane 0][L-1 sweeps] u64
+    __host__ __device__ static constexpr int xch_words() { return 2 * kDP * 2 * (L - 1); }
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -117,9 +119,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                  "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* tm, uint32_t row, uint32_t word, uint32_t plane,
                                       uint64_t* bar) {
     asm volatile(
@@ -135,6 +134,11 @@ __device__ __forceinline__ void tma3d_prefetch(const CUtensorMap* tm, uint32_t r
                  "r"(row), "r"(word), "r"(plane)
                  : "memory");
 }
+// named barrier of the compute lanes; the non-.aligned form: the lanes reach it from lane-divergent code
+__device__ __forceinline__ void xch_barrier() {
+    __syncwarp();
+    asm volatile("barrier.sync %0, %1;" ::"n"(kXchBar), "n"(kLanes) : "memory");
+}
 
 __device__ __forceinline__ void st_pred(uint64_t* p, uint64_t v, bool pred) {
     asm volatile(
@@ -146,8 +150,6 @@ __device__ __forceinline__ void st_pred(uint64_t* p, uint64_t v, bool pred) {
         "l"(v), "r"(int(pred)));
 }
 
-__device__ __forceinline__ uint64_t shup(uint64_t v) { return __shfl_up_sync(0xffffffffu, v, 1); }
-
 __device__ __forceinline__ Xo slot_state(const uint64_t* save, int slot) {
     return Xo{save[(slot + 0) * kLanes], save[(slot + 1) * kLanes], save[(slot + 2) * kLanes], save[(slot + 3) * kLanes]};
 }
@@ -157,18 +159,18 @@ __device__ __forceinline__ void slot_store(uint64_t* save, int slot, const Xo& s
     save[(slot + 2) * kLanes] = s.c;
     save[(slot + 3) * kLanes] = s.d;
 }
-__device__ __forceinline__ uint64_t shdn(uint64_t v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 
 // Lane context shared by every iteration.
 struct DeepCtx {
     uint32_t n, Y;
     uint64_t* dXf;  // dst planes at this lane's physical row
-    uint64_t* dYf;
     uint64_t* dXs;
     uint64_t* dYs;
+    uint64_t* dYf1;  // Y(f) of the row below (physical row y + 1)
     uint32_t wrap;
-    uint32_t sf1, sf2;  // x+ neighbour shifted by one packed bit in sweeps of parity f / s
-    bool core, wyf, ghostw, ghost_row;
+    uint32_t sf1, sf2;   // x+ neighbour shifted by one packed bit in sweeps of parity f / s
+    int up, dn;          // shuffle source lanes of rows y - 1 / y + 1 (rotating: see edge exchange)
+    bool core, ghostw, ghost_row, ghost_row1;
     uint64_t* save;  // this lane's parking slots: save[slot * kLanes]
 };
 
@@ -181,18 +183,42 @@ struct DeepState {
 };
 
 // GH: the warp stores rows 0..ghost-1 of a periodic lattice and mirrors them into the ghost rows
-// (warp-uniform; 0 / 1 hoisted out of the steady state, 2 = decide at run time)
-template <int GH>
-__device__ __forceinline__ void put(const DeepCtx& c, uint64_t* ptr, uint64_t val, bool pred) {
+// (warp-uniform; 2 = decide at run time)
+__device__ __forceinline__ void put(const DeepCtx& c, uint64_t* ptr, uint64_t val, bool pred, bool ghost_row) {
     st_pred(ptr, val, pred);
-    if constexpr (GH == 1) st_pred(ptr + c.wrap, val, pred && c.ghost_row);
-    if constexpr (GH == 2)
-        if (c.ghostw) st_pred(ptr + c.wrap, val, pred && c.ghost_row);
+    if (c.ghostw) st_pred(ptr + c.wrap, val, pred && ghost_row);
+}
+
+// Edge exchange after every word: lane 31 of warp w publishes its rows' C outputs (row y+1's Y input of the
+// next sweep) and lane 0 its B outputs (row y-1's Y(s)[y+1] input); after the barrier lane 31 of warp w+1
+// takes warp w's C and lane 0 of warp w-1 takes warp w's B. Lane 31's own C and lane 0's own B are consumed
+// only by the neighbouring warp, so they are overwritten in place and the rotating shuffles of the next word
+// (lane 0 <- lane 31, lane 31 <- lane 0) deliver the other warp's row.
+template <int L, typename StateT>
+__device__ __forceinline__ void edge_exchange(StateT& S, uint64_t* xch, uint32_t i, int wib, int lane) {
+    uint64_t* buf = xch + size_t(i & 1u) * (kDP * 2 * (L - 1));
+    if (lane == 31) {
+#pragma unroll
+        for (int l = 0; l < L - 1; ++l) buf[(wib * 2 + 0) * (L - 1) + l] = S.pC[l];
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int l = 0; l < L - 1; ++l) buf[(wib * 2 + 1) * (L - 1) + l] = S.pB[l];
+    }
+    xch_barrier();
+    if (lane == 31 && wib > 0) {
+#pragma unroll
+        for (int l = 0; l < L - 1; ++l) S.pC[l] = buf[((wib - 1) * 2 + 0) * (L - 1) + l];
+    }
+    if (lane == 0 && wib < kDP - 1) {
+#pragma unroll
+        for (int l = 0; l < L - 1; ++l) S.pB[l] = buf[((wib + 1) * 2 + 1) * (L - 1) + l];
+    }
 }
 
 // One iteration i: sweep l on word (i-(l-1)) mod n for every active l.
 // STEADY: all sweeps active, no first/second/last words, no wrap (i in [2L, n-1]).
-template <int PM, int QM, int L, bool STEADY, int GH, bool CTR = false>
+template <int PM, int QM, int L, bool STEADY, bool CTR = false>
 __device__ __forceinline__ void deep_iter(DeepState<L, typename std::conditional<CTR, Ctr, Xo>::type>& S,
                                           const DeepCtx& c, uint32_t i, const uint64_t* sb, int jj,
                                           const ProbDev& p, const ProbDev& q) {
@@ -211,7 +237,7 @@ __device__ __forceinline__ void deep_iter(DeepState<L, typename std::conditional
             if (j >= n) j -= n;
         }
         act[li] = active;
-        if (!active) continue;  // warp-uniform
+        if (!active) continue;  // block-uniform
         const bool first = !STEADY && j == uint32_t(l - 1);
         const bool second = !STEADY && j == uint32_t(l);
         const bool last = !STEADY && j == (l == 1 ? n - 1 : uint32_t(l - 2));
@@ -240,7 +266,7 @@ __device__ __forceinline__ void deep_iter(DeepState<L, typename std::conditional
         }
 
         // ---- inputs: own X, own Y, Y[y+1] of the other parity, x+ neighbour words j, j+1 ----
-        uint64_t xo, yo, yn, x0, x1, qB = 0;
+        uint64_t xo, yo, yn, x0, x1;
         if (l == 1) {
             xo = sb[ST::kXf + jj * ST::W];
             yo = sb[ST::kYf + jj * ST::W];
@@ -250,18 +276,17 @@ __device__ __forceinline__ void deep_iter(DeepState<L, typename std::conditional
             x1 = nxt;
             S.cur = nxt;
         } else {
-            uint64_t qA, qC, qR;
             const int sv = 5 * (l - 2);  // slots of sweep l-1
-            if (!STEADY && j == uint32_t(l - 2)) {  // sweep l-1's first word (parked)
-                qA = c.save[(sv + 0) * kLanes];
-                qB = c.save[(sv + 1) * kLanes];
-                qC = c.save[(sv + 2) * kLanes];
-                qR = c.save[(sv + 3) * kLanes];
+            if (!STEADY && j == uint32_t(l - 2)) {  // sweep l-1's first word (parked; rows y±1 = lanes t±1)
+                x0 = c.save[(sv + 0) * kLanes];
+                yn = c.save[(sv + 1) * kLanes + 1];
+                yo = c.save[(sv + 2) * kLanes - 1];
+                xo = c.save[(sv + 3) * kLanes];
             } else {
-                qA = S.pA[li - 1];
-                qB = S.pB[li - 1];
-                qC = S.pC[li - 1];
-                qR = S.pR[li - 1];
+                x0 = S.pA[li - 1];
+                yn = __shfl_sync(0xffffffffu, S.pB[li - 1], c.dn);
+                yo = __shfl_sync(0xffffffffu, S.pC[li - 1], c.up);
+                xo = S.pR[li - 1];
             }
             uint64_t nxa = nA[li - 1];
             if constexpr (!STEADY) {
@@ -269,10 +294,6 @@ __device__ __forceinline__ void deep_iter(DeepState<L, typename std::conditional
                 if (jn == uint32_t(l - 2)) nxa = c.save[(sv + 0) * kLanes];
                 else if (j == uint32_t(l - 2)) nxa = c.save[(sv + 4) * kLanes];
             }
-            xo = qR;
-            yo = shup(qC);
-            yn = shdn(qB);
-            x0 = qA;
             x1 = nxa;
         }
         const uint32_t sh = (l & 1) ? c.sf1 : c.sf2;
@@ -304,17 +325,17 @@ __device__ __forceinline__ void deep_iter(DeepState<L, typename std::conditional
                     c.save[(sv + 3) * kLanes] ^= carry;
                 } else {
                     const uint64_t xf = c.save[sv * kLanes] ^ carry;
-                    put<GH>(c, ((L & 1) ? c.dXs : c.dXf) + size_t(l - 1) * c.Y, xf, c.core);
+                    put(c, ((L & 1) ? c.dXs : c.dXf) + size_t(l - 1) * c.Y, xf, c.core, c.ghost_row);
                 }
             }
         }
         if (l == L) {
-            // sweep L has parity s (L even): X(s), Y(s) own; Y(f)[y] = B^{L-1}[y] ^ m^L[y-1]; X(f) via the carry
+            // sweep L has parity s (L even): X(s), Y(s) own; Y(f)[y+1] = C^L[y]; X(f) via the carry
             const uint32_t o = j * c.Y;
-            put<GH>(c, c.dXs + o, nA[li], c.core);
-            put<GH>(c, c.dYs + o, nB[li], c.core);
-            put<GH>(c, c.dYf + o, qB ^ shup(m), c.wyf);
-            if (!first) put<GH>(c, c.dXf + o, nR[li], c.core);
+            put(c, c.dXs + o, nA[li], c.core, c.ghost_row);
+            put(c, c.dYs + o, nB[li], c.core, c.ghost_row);
+            put(c, c.dYf1 + o, nC[li], c.core, c.ghost_row1);
+            if (!first) put(c, c.dXf + o, nR[li], c.core, c.ghost_row);
         }
     }
 #pragma unroll
@@ -328,12 +349,34 @@ __device__ __forceinline__ void deep_iter(DeepState<L, typename std::conditional
     }
 }
 
+// Ring stage `slot` <- word block b of the four source planes (one 3-D TMA box each), completing on full[slot].
+template <int L>
+__device__ __forceinline__ void deep_issue(uint64_t* ring, uint64_t* full, const CUtensorMap* tmK,
+                                           const CUtensorMap* tmK1, uint32_t blk_r0, int f, uint32_t pf,
+                                           uint32_t nblocks, uint32_t b, uint32_t slot) {
+    using ST = DeepStage<L>;
+    uint64_t* base = ring + size_t(slot) * ST::kWords;
+    const uint32_t kb = b * kKS, s_ = uint32_t(f ^ 1);
+    mbar_expect_tx(&full[slot], ST::kTx);
+    tma3d(base + ST::kXf, tmK, blk_r0, kb, uint32_t(f), &full[slot]);
+    tma3d(base + ST::kYf, tmK, blk_r0, kb, uint32_t(2 + f), &full[slot]);
+    tma3d(base + ST::kYs, tmK, blk_r0, kb, 2 + s_, &full[slot]);
+    tma3d(base + ST::kXs, tmK1, blk_r0, kb, s_, &full[slot]);
+    if (pf > 0 && b + pf < nblocks) {  // warm L2 pf stages ahead of the ring
+        const uint32_t kp = (b + pf) * kKS;
+        tma3d_prefetch(tmK, blk_r0, kp, uint32_t(f));
+        tma3d_prefetch(tmK, blk_r0, kp, uint32_t(2 + f));
+        tma3d_prefetch(tmK, blk_r0, kp, 2 + s_);
+        tma3d_prefetch(tmK1, blk_r0, kp, s_);
+    }
+}
+
 }  // namespace
 
 // CTR: xi from the opt-in counter-based streams (octgpu_set_rng): sweep l of the pass is global sweep
 // sigma0 + l - 1 of seed's streams; no stream state is loaded, parked or stored.
 template <int PM, int QM, int L, bool CTR>
-__global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
+__global__ void __launch_bounds__(32 * kDP, kDeepMinBlocks)
     k_mcs_deep(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, const uint64_t* __restrict__ rs,
                uint64_t* __restrict__ rd, int f, Geom g, ProbDev p, ProbDev q, const uint64_t* __restrict__ jtab, int S,
                const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmK1, uint64_t ctr_seed,
@@ -348,59 +391,30 @@ __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
     const uint32_t n = g.n;
     const int lane = threadIdx.x & 31;
     const int wib = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0);
-    const uint32_t rows = g.c1 - g.c0;
     const uint32_t blk_r0 = g.c0 - uint32_t(L - 1) + blockIdx.x * uint32_t(GEO::kRows);
-    const uint32_t left = rows - blockIdx.x * uint32_t(GEO::kRows);
-    const uint32_t nact = min(uint32_t(kDP), (left + GEO::kCore - 1) / GEO::kCore);
-    const uint32_t s_ = uint32_t(f ^ 1);
-
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
-    uint64_t* empty = full + kSMax;
     uint64_t* ring = reinterpret_cast<uint64_t*>(smem_raw + 128);
     uint64_t* slots = ring + S * ST::kWords;
+    uint64_t* xch = slots + SL::count() * kLanes;
     const uint32_t nblocks = (n + kKS - 1) / kKS;
 
+    // No producer warp: thread 0 refills a ring stage right after the exchange barrier that follows the
+    // word which consumed it (every warp has read the stage by then), so the ring needs only "full" barriers
+    // and the block is 8 warps: two blocks per SM leave 128 registers per thread. (The tensor maps are
+    // passed by address straight from the __grid_constant__ parameters: a copy in local memory is not a
+    // valid TMA descriptor.)
     if (threadIdx.x == 0) {
-        for (int i = 0; i < S; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], nact);
-        }
+        for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (uint32_t b = 0; b < uint32_t(S) && b < nblocks; ++b)
+            deep_issue<L>(ring, full, &tmK, &tmK1, blk_r0, f, g.pf, nblocks, b, b);
     }
     __syncthreads();
 
-    if (wib == kDP) {  // producer warp
-        if (lane == 0) {
-            uint32_t st = 0, ph = 0;
-            for (uint32_t b = 0; b < nblocks; ++b) {
-                if (b >= uint32_t(S)) mbar_wait(&empty[st], ph ^ 1u);
-                uint64_t* base = ring + size_t(st) * ST::kWords;
-                const uint32_t kb = b * kKS;
-                mbar_expect_tx(&full[st], ST::kTx);
-                tma3d(base + ST::kXf, &tmK, blk_r0, kb, uint32_t(f), &full[st]);
-                tma3d(base + ST::kYf, &tmK, blk_r0, kb, uint32_t(2 + f), &full[st]);
-                tma3d(base + ST::kYs, &tmK, blk_r0, kb, 2 + s_, &full[st]);
-                tma3d(base + ST::kXs, &tmK1, blk_r0, kb, s_, &full[st]);
-                if (g.pf > 0 && b + g.pf < nblocks) {  // warm L2 pf stages ahead of the ring
-                    const uint32_t kp = (b + g.pf) * kKS;
-                    tma3d_prefetch(&tmK, blk_r0, kp, uint32_t(f));
-                    tma3d_prefetch(&tmK, blk_r0, kp, uint32_t(2 + f));
-                    tma3d_prefetch(&tmK, blk_r0, kp, 2 + s_);
-                    tma3d_prefetch(&tmK1, blk_r0, kp, s_);
-                }
-                if (++st == uint32_t(S)) {
-                    st = 0;
-                    ph ^= 1u;
-                }
-            }
-        }
-        return;
-    }
-    if (uint32_t(wib) >= nact) return;
-    const uint32_t r0 = blk_r0 + uint32_t(GEO::kCore) * wib;
-    const int wrow = GEO::kCore * wib + lane;
-    const uint32_t v = r0 + lane;
+    const int t = int(threadIdx.x);  // block lane = row blk_r0 + t
+    const uint32_t v = blk_r0 + uint32_t(t);
     const uint32_t y = g.wrap ? v % g.wrap : v;
+    const uint32_t y1 = g.wrap ? (v + 1) % g.wrap : v + 1;
     const size_t PS = g.plane_stride;
     const int s = f ^ 1;
 
@@ -409,16 +423,18 @@ __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
     c.Y = g.Y;
     c.wrap = g.wrap;
     c.dXf = dst + size_t(0 + f) * PS + y;
-    c.dYf = dst + size_t(2 + f) * PS + y;
     c.dXs = dst + size_t(0 + s) * PS + y;
     c.dYs = dst + size_t(2 + s) * PS + y;
+    c.dYf1 = dst + size_t(2 + f) * PS + y1;
     c.sf1 = (uint32_t(f) ^ y ^ g.ypar) & 1u;
     c.sf2 = c.sf1 ^ 1u;
-    c.core = lane >= L - 1 && lane <= 32 - L && v < g.c1;
-    c.wyf = lane >= L && lane <= 33 - L && v - 1 < g.c1;
-    c.ghostw = g.ghost && (r0 + uint32_t(L - 1) < g.ghost || r0 + uint32_t(33 - L) >= g.wrap);
-    c.ghost_row = c.ghostw && y < g.ghost;
-    c.save = slots + threadIdx.x;
+    c.up = (lane + 31) & 31;
+    c.dn = (lane + 1) & 31;
+    c.core = t >= GEO::kFirst && t <= GEO::kLast && v < g.c1;
+    c.ghost_row = g.ghost && y < g.ghost;
+    c.ghost_row1 = g.ghost && y1 < g.ghost;
+    c.ghostw = __any_sync(0xffffffffu, c.core && (c.ghost_row || c.ghost_row1));
+    c.save = slots + t;
 
     DeepState<L, Src> R;
 #pragma unroll
@@ -469,34 +485,30 @@ __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
     uint32_t st = 0, ph = 0;
     for (uint32_t b = 0; b < nblocks; ++b) {
         mbar_wait(&full[st], ph);
-        const uint64_t* sb = ring + size_t(st) * ST::kWords + wrow;
+        const uint64_t* sb = ring + size_t(st) * ST::kWords + t;
         const uint32_t kb = b * kKS;
         if (b == 0) {
             R.cur = sb[ST::kXs];
             R.raw0 = R.cur;
         }
         if (kb >= uint32_t(2 * L) && kb + kKS < n) {  // i = n-1 is sweep 1's last word: generic
-#if OCTGPU_DEEP_GHOST_HOIST
-            if (c.ghostw) {
 #pragma unroll
-                for (int jj = 0; jj < kKS; ++jj) deep_iter<PM, QM, L, true, 1, CTR>(R, c, kb + jj, sb, jj, p, q);
-            } else {
-#pragma unroll
-                for (int jj = 0; jj < kKS; ++jj) deep_iter<PM, QM, L, true, 0, CTR>(R, c, kb + jj, sb, jj, p, q);
+            for (int jj = 0; jj < kKS; ++jj) {
+                deep_iter<PM, QM, L, true, CTR>(R, c, kb + jj, sb, jj, p, q);
+                edge_exchange<L>(R, xch, kb + jj, wib, lane);
             }
-#else
-#pragma unroll
-            for (int jj = 0; jj < kKS; ++jj) deep_iter<PM, QM, L, true, 2, CTR>(R, c, kb + jj, sb, jj, p, q);
-#endif
         } else {
 #pragma unroll 1
             for (int jj = 0; jj < kKS; ++jj) {
-                if (kb + jj >= n) break;
-                deep_iter<PM, QM, L, false, 2, CTR>(R, c, kb + jj, sb, jj, p, q);
+                if (kb + jj < n) {
+                    deep_iter<PM, QM, L, false, CTR>(R, c, kb + jj, sb, jj, p, q);
+                    edge_exchange<L>(R, xch, kb + jj, wib, lane);
+                }
             }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
+        // every warp is past this stage's last word (the exchange barrier): refill it
+        if (threadIdx.x == 0 && b + uint32_t(S) < nblocks)
+            deep_issue<L>(ring, full, &tmK, &tmK1, blk_r0, f, g.pf, nblocks, b + uint32_t(S), st);
         if (++st == uint32_t(S)) {
             st = 0;
             ph ^= 1u;
@@ -504,8 +516,10 @@ __global__ void __launch_bounds__(32 * (kDP + 1), kDeepMinBlocks)
     }
     // drain: sweeps 2..L finish their wrapped words
 #pragma unroll 1
-    for (uint32_t i = n; i < n + uint32_t(2 * L - 2); ++i)
-        deep_iter<PM, QM, L, false, 2, CTR>(R, c, i, nullptr, 0, p, q);
+    for (uint32_t i = n; i < n + uint32_t(2 * L - 2); ++i) {
+        deep_iter<PM, QM, L, false, CTR>(R, c, i, nullptr, 0, p, q);
+        edge_exchange<L>(R, xch, i, wib, lane);
+    }
 
     if constexpr (LIVE && !CTR) {
         Xo fin = R.rs[L - 1];
@@ -529,22 +543,9 @@ cudaError_t deep_go(const void* src, void* dst, const uint64_t* rs, uint64_t* rd
     auto kern = k_mcs_deep<PM, QM, L, CTR>;
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    kern<<<blocks, 32 * (kDP + 1), smem, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), rs,
+    kern<<<blocks, 32 * kDP, smem, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), rs,
                                                rd, f, g, p, q, jtab, S, *tmK, *tmK1, ctr_seed, sigma0);
     return cudaGetLastError();
-}
-
-template <int PM>
-cudaError_t deep_q(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
-                   const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK, const CUtensorMap* tmK1,
-                   cudaStream_t st) {
-    switch (q.mode) {
-    case M_ZERO: return deep_go<PM, M_ZERO, kDeepSweeps>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
-    case M_HALF: return deep_go<PM, M_HALF, kDeepSweeps>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
-    case M_DYADIC: return deep_go<PM, M_DYADIC, kDeepSweeps>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
-    case M_ONE: return deep_go<PM, M_ONE, kDeepSweeps>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
-    default: return cudaErrorInvalidValue;
-    }
 }
 
 template <int L>
@@ -552,57 +553,90 @@ size_t deep_smem_l(int pm, int qm, int S, bool ctr) {
     const bool pp = !(pm == M_ZERO || pm == M_ONE), pq = !(qm == M_ZERO || qm == M_ONE);
     const int parked = !ctr && (pp || pq) && L > kRegStreams ? L - kRegStreams : 0;
     const int slots = 5 * (L - 1) + 1 + (pp ? L * (L - 1) / 2 : 0) + (pq ? L * (L - 1) / 2 : 0) + 4 * parked;
-    return 128 + size_t(S) * DeepStage<L>::kWords * 8 + size_t(slots) * kLanes * 8;
+    const int xch = 2 * kDP * 2 * (L - 1);
+    return 128 + size_t(S) * DeepStage<L>::kWords * 8 + size_t(slots) * kLanes * 8 + size_t(xch) * 8;
 }
+
+constexpr bool cheap_mode(int m) { return m == M_ZERO || m == M_HALF || m == M_DYADIC || m == M_ONE; }
+constexpr bool const_mode(int m) { return m == M_ZERO || m == M_ONE; }
 
 }  // namespace
 
 bool mcs_deep_supported(int pm, int qm) {
-    auto cheap = [](int m) { return m == M_ZERO || m == M_HALF || m == M_DYADIC || m == M_ONE; };
-    const bool live = !((pm == M_ZERO || pm == M_ONE) && (qm == M_ZERO || qm == M_ONE));
+    const bool live = !(const_mode(pm) && const_mode(qm));
     // M_ONE next to a live stream still steps w draws per word: issue-bound, keep one MCS per pass
-    return cheap(pm) && cheap(qm) && !(live && (pm == M_ONE || qm == M_ONE));
+    return cheap_mode(pm) && cheap_mode(qm) && !(live && (pm == M_ONE || qm == M_ONE));
+}
+
+// L = 6 (3 MCS per pass) only without stream state: constant xi (xoshiro streams advance lazily) or the
+// counter-based streams; a live xoshiro pass keeps four 256-bit states per lane in registers at L = 4.
+bool mcs_deep_supported_l(int pm, int qm, int L, bool ctr) {
+    if (!mcs_deep_supported(pm, qm)) return false;
+    if (L == kDeepSweepsLive) return true;
+    if (L == kDeepSweepsConst) return const_mode(pm) && const_mode(qm);
+    return false;
 }
 
 size_t mcs_deep_smem(int pm, int qm, int L, int S, bool ctr) {
-    return L == kDeepSweeps ? deep_smem_l<kDeepSweeps>(pm, qm, S, ctr) : 0;
+    if (L == 4) return deep_smem_l<4>(pm, qm, S, ctr);
+    if (L == 6) return deep_smem_l<6>(pm, qm, S, ctr);
+    return 0;
 }
+
+namespace {
+
+template <int PM, int QM, bool CTR>
+cudaError_t deep_l(int L, const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g,
+                   const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK,
+                   const CUtensorMap* tmK1, cudaStream_t st, uint64_t seed, uint64_t sigma) {
+    if (L == 4) return deep_go<PM, QM, 4, CTR>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
+    if constexpr (const_mode(PM) && const_mode(QM)) {
+        if (L == 6) return deep_go<PM, QM, 6, CTR>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int PM, bool CTR>
+cudaError_t deep_q(int L, const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g,
+                   const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK,
+                   const CUtensorMap* tmK1, cudaStream_t st, uint64_t seed, uint64_t sigma) {
+    switch (q.mode) {
+    case M_ZERO: return deep_l<PM, M_ZERO, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
+    case M_HALF: return deep_l<PM, M_HALF, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
+    case M_DYADIC:
+        return deep_l<PM, M_DYADIC, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
+    case M_ONE: return deep_l<PM, M_ONE, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+template <bool CTR>
+cudaError_t deep_p(int L, const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g,
+                   const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK,
+                   const CUtensorMap* tmK1, cudaStream_t st, uint64_t seed, uint64_t sigma) {
+    if (S < 2 || S > kSMax || !mcs_deep_supported_l(p.mode, q.mode, L, CTR)) return cudaErrorInvalidValue;
+    switch (p.mode) {
+    case M_ZERO: return deep_q<M_ZERO, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
+    case M_HALF: return deep_q<M_HALF, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
+    case M_DYADIC: return deep_q<M_DYADIC, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
+    case M_ONE: return deep_q<M_ONE, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace
 
 cudaError_t launch_mcs_deep(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g,
-                            const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK,
-                            const CUtensorMap* tmK1, cudaStream_t st) {
-    if (S < 2 || S > kSMax) return cudaErrorInvalidValue;
-    switch (p.mode) {
-    case M_ZERO: return deep_q<M_ZERO>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
-    case M_HALF: return deep_q<M_HALF>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
-    case M_DYADIC: return deep_q<M_DYADIC>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
-    case M_ONE: return deep_q<M_ONE>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
-    default: return cudaErrorInvalidValue;
-    }
+                            const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int L, int S,
+                            const CUtensorMap* tmK, const CUtensorMap* tmK1, cudaStream_t st) {
+    return deep_p<false>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, 0, 0);
 }
 
-// counter-based streams (octgpu_set_rng): sweeps sigma .. sigma + kDeepSweeps - 1 of seed's streams
-#define OCT_CTR_ARGS src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, seed, sigma
-#define OCT_DQC(PM)                                                               \
-    switch (q.mode) {                                                             \
-    case M_ZERO: return deep_go<PM, M_ZERO, kDeepSweeps, true>(OCT_CTR_ARGS);     \
-    case M_HALF: return deep_go<PM, M_HALF, kDeepSweeps, true>(OCT_CTR_ARGS);     \
-    case M_DYADIC: return deep_go<PM, M_DYADIC, kDeepSweeps, true>(OCT_CTR_ARGS); \
-    case M_ONE: return deep_go<PM, M_ONE, kDeepSweeps, true>(OCT_CTR_ARGS);       \
-    default: return cudaErrorInvalidValue;                                        \
-    }
-
+// counter-based streams (octgpu_set_rng): sweeps sigma .. sigma + L - 1 of seed's streams
 cudaError_t launch_mcs_deep_ctr(const void* src, void* dst, int f, Geom g, const ProbDev& p, const ProbDev& q,
-                                uint64_t seed, uint64_t sigma, int S, const CUtensorMap* tmK, const CUtensorMap* tmK1,
-                                cudaStream_t st) {
-    if (S < 2 || S > kSMax) return cudaErrorInvalidValue;
-    switch (p.mode) {
-    case M_ZERO: OCT_DQC(M_ZERO)
-    case M_HALF: OCT_DQC(M_HALF)
-    case M_DYADIC: OCT_DQC(M_DYADIC)
-    case M_ONE: OCT_DQC(M_ONE)
-    default: return cudaErrorInvalidValue;
-    }
+                                uint64_t seed, uint64_t sigma, int L, int S, const CUtensorMap* tmK,
+                                const CUtensorMap* tmK1, cudaStream_t st) {
+    return deep_p<true>(L, src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, seed, sigma);
 }
 
 }  // namespace octgpu

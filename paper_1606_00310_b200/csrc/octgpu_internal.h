@@ -57,40 +57,47 @@ struct Geom {
 constexpr uint32_t kMcsConsumerWarps = OCTGPU_BULK_WARPS;  // k_mcs_bulk: compute warps per block (+1 producer)
 constexpr uint32_t kTmaBoxRows = 30 * kMcsConsumerWarps + 4;  // k_mcs_bulk window rows (124)
 
-// k_mcs_deep block shape (mcs_deep.cu): kDeepWarps compute warps + 1 producer.
+// k_mcs_deep block shape (mcs_deep.cu): kDeepWarps compute warps whose 32 * kDeepWarps lanes own that many
+// consecutive rows (the block's TMA window) + 1 producer warp. Warp-edge rows are exchanged through shared
+// memory every word, so only the block's own edges are halo rows: 256 - 2 L core rows for an L-sweep pass.
 #ifndef OCTGPU_DEEP_WARPS
-#define OCTGPU_DEEP_WARPS 9
+#define OCTGPU_DEEP_WARPS 8
 #endif
-#ifndef OCTGPU_DEEP_SWEEPS
-#define OCTGPU_DEEP_SWEEPS 4
-#endif
-// k_mcs_deep words per ring stage: 1 word x 5 stages beat 2 words x 3 stages (c2 0.1778 vs 0.1839 ms/MCS,
-// c2' 0.3105 vs 0.3234, c5 0.723 vs 0.725; tools/sweep_deep_ks*.sh)
+// k_mcs_deep words per ring stage: the two words of a stage are unrolled, so the sweeps' carried state
+// ping-pongs between two register sets instead of being copied every word. Block-wide kernel, ms/MCS at
+// KS = 1 / 2 / 4: c2 0.165 / 0.150 / 0.171, c2' 0.318 / 0.249 / 0.242 (tools/r2_deep_var2.sh; S = 2..5 within
+// 1%)
 #ifndef OCTGPU_DEEP_KS
-#define OCTGPU_DEEP_KS 1
+#define OCTGPU_DEEP_KS 2
 #endif
-constexpr int kDeepSweeps = OCTGPU_DEEP_SWEEPS;  // sweeps per k_mcs_deep pass (even)
 constexpr int kDeepKS = OCTGPU_DEEP_KS;          // k_mcs_deep words per ring stage
 constexpr int kDeepWarps = OCTGPU_DEEP_WARPS;
+constexpr int kDeepLanes = 32 * kDeepWarps;      // rows per block window (TMA box rows, <= 256)
+static_assert(kDeepLanes <= 256, "a TMA box dimension holds at most 256 rows");
 #ifndef OCTGPU_DEEP_MINB
-#define OCTGPU_DEEP_MINB (OCTGPU_DEEP_WARPS >= 8 ? 2 : 3)
+#define OCTGPU_DEEP_MINB 2
 #endif
 constexpr int kDeepMinBlocks = OCTGPU_DEEP_MINB;  // resident blocks per SM the register budget targets
-constexpr int deep_box_rows(int L) { return ((34 - 2 * L) * (kDeepWarps - 1) + 34) / 2 * 2; }
+// sweeps per k_mcs_deep pass (even): 6 (3 MCS) for constant xi on periodic lattices, 4 (2 MCS) for live
+// streams and for row stripes (whose halo rows are sized for 4)
+constexpr int kDeepSweepsConst = 6;
+constexpr int kDeepSweepsLive = 4;
+constexpr int kStripeSweeps = 4;
+constexpr int deep_box_rows() { return kDeepLanes; }
+constexpr int deep_core_rows(int L) { return kDeepLanes - 2 * L; }  // even: block windows start 16-B aligned
 
 constexpr int kGraphPasses = 16;  // passes per CUDA graph replayed by octgpu_step (even)
 
 // Row stripes: halo rows above / below the core rows (local rows 0..HA-1 and
 // HA+L..HA+L+HB-1): enough for k_mcs_deep's 2-MCS pass (3 rows of shrinking
 // lanes each side + stage 1's Y(s)[y+1]); the one-MCS kernels use 1 / 2 of them.
-constexpr uint32_t kStripeHA = uint32_t(kDeepSweeps) - 1;
-constexpr uint32_t kStripeHB = uint32_t(kDeepSweeps);
+constexpr uint32_t kStripeHA = uint32_t(kStripeSweeps) - 1;
+constexpr uint32_t kStripeHB = uint32_t(kStripeSweeps);
 
-// periodic lattices keep this many ghost rows (>= every TMA window) so windows never wrap
-constexpr uint32_t kGhostRows = deep_box_rows(kDeepSweeps) <= 192   ? 192
-                                : deep_box_rows(kDeepSweeps) <= 256 ? 256
-                                                                    : (uint32_t(deep_box_rows(kDeepSweeps)) + 63) / 64 * 64;
-static_assert(kTmaBoxRows <= kGhostRows && uint32_t(deep_box_rows(kDeepSweeps)) <= kGhostRows, "ghost rows");
+// periodic lattices keep this many ghost rows (>= every TMA window + the random tile-origin shift) so windows
+// never wrap
+constexpr uint32_t kGhostRows = 320;
+static_assert(kTmaBoxRows <= kGhostRows && uint32_t(deep_box_rows()) + 64 <= kGhostRows, "ghost rows");
 
 // Per-row RNG states are stored SoA: s[j * Y + y], j = 0..3.
 
@@ -130,20 +137,20 @@ cudaError_t launch_mcs_bulk_ctr(const void* src, void* dst, int f, Geom g, const
                                 cudaStream_t st);
 size_t mcs_bulk_smem(int ks, int S);  // dynamic smem of a block (kMcsConsumerWarps + 1 warps)
 
-// Temporally blocked variant (mcs_deep.cu): kDeepSweeps sweeps (kDeepSweeps/2
-// MCS, starting with parity f) in one pass, periodic lattices only. The
-// geometry's core rows must start at virtual row kDeepSweeps - 1 (see
-// engine.cu deep_geom). tmK / tmK1: tensor maps with boxes of
-// deep_box_rows(kDeepSweeps) rows x 2 and x 3 words.
+// Temporally blocked variant (mcs_deep.cu): L sweeps (L/2 MCS, starting with
+// parity f) in one pass, L in {4, 6} (6: constant xi only). The geometry's core
+// rows must start at virtual row L - 1 (see engine.cu deep_geom). tmK / tmK1:
+// tensor maps with boxes of deep_box_rows() rows x kDeepKS and x kDeepKS + 1 words.
 bool mcs_deep_supported(int p_mode, int q_mode);
+bool mcs_deep_supported_l(int p_mode, int q_mode, int L, bool ctr);
 size_t mcs_deep_smem(int p_mode, int q_mode, int L, int S, bool ctr = false);  // S ring stages
-// k_mcs_deep with counter-based xi: sweeps sigma .. sigma + kDeepSweeps - 1 of seed's streams (octgpu_set_rng)
+// k_mcs_deep with counter-based xi: sweeps sigma .. sigma + L - 1 of seed's streams (octgpu_set_rng)
 cudaError_t launch_mcs_deep_ctr(const void* src, void* dst, int f, Geom g, const ProbDev& p, const ProbDev& q,
-                                uint64_t seed, uint64_t sigma, int S, const CUtensorMap* tmK, const CUtensorMap* tmK1,
-                                cudaStream_t st);
+                                uint64_t seed, uint64_t sigma, int L, int S, const CUtensorMap* tmK,
+                                const CUtensorMap* tmK1, cudaStream_t st);
 cudaError_t launch_mcs_deep(const void* src, void* dst, const uint64_t* rng_src, uint64_t* rng_dst, int f, Geom g,
-                            const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK,
-                            const CUtensorMap* tmK1, cudaStream_t st);
+                            const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int L, int S,
+                            const CUtensorMap* tmK, const CUtensorMap* tmK1, cudaStream_t st);
 
 // s <- M s for every row state, M given as a 4-bit table (64 x 16 x 4 u64).
 cudaError_t launch_apply_jump(uint64_t* rng, uint32_t Y, const uint64_t* tab, cudaStream_t st);

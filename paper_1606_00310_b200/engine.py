@@ -203,6 +203,15 @@ class GpuEngine:
         k = int(lib().octgpu_get_rng(self._h))
         return {v: n for n, v in self.RNG_KINDS.items()}[k]
 
+    KERNELS = {0: "k_mcs", 1: "k_mcs_bulk", 2: "k_mcs_deep", 3: "k_sweep_ctr"}
+
+    def pass_plan(self, prm: UpdateParams) -> tuple[str, float]:
+        """(kernel, MCS per launch) of the passes step(prm) launches on this engine (octgpu_pass_plan)."""
+        c = prm.to_c()
+        k, sw = C.c_int(), C.c_int()
+        check(lib().octgpu_pass_plan(self._h, C.byref(c), C.byref(k), C.byref(sw)))
+        return self.KERNELS[k.value], sw.value / 2
+
     def set_stream(self, cuda_stream: int | None) -> None:
         check(lib().octgpu_set_stream(self._h, C.c_void_p(cuda_stream) if cuda_stream else None))
 

@@ -139,6 +139,14 @@ class StripeEngine:
     def set_stream(self, cuda_stream: int | None) -> None:
         check(lib().octgpu_set_stream(self._h, C.c_void_p(cuda_stream) if cuda_stream else None))
 
+    def pass_plan(self, prm) -> tuple[str, float]:
+        """(kernel, MCS per launch) of this stripe's passes for prm (octgpu_pass_plan)."""
+        from .engine import GpuEngine
+        c = prm.to_c()
+        k, sw = C.c_int(), C.c_int()
+        check(lib().octgpu_pass_plan(self._h, C.byref(c), C.byref(k), C.byref(sw)))
+        return GpuEngine.KERNELS[k.value], sw.value / 2
+
     def set_rng(self, kind: str) -> None:
         """GpuEngine.set_rng for this stripe: every stripe of a group must use the same kind (the counter
         streams are keyed by the master seed and the GLOBAL row, so a striped run equals the periodic one)."""

@@ -33,20 +33,3 @@ def test_from_flat_and_beyond_the_job():
     assert t0 == 0 and targets[-1] == 30 and sched == [t for t in SCHED if t <= 30]
     t0, sched, targets, desc = bench.timed_window(12_000, False, SCHED)
     assert t0 == 0 and targets[-1] == 12_000 and len(sched) == 33 and "2000 MCS more" in desc
-
-
-@pytest.mark.parametrize("pq,env,want", [
-    ((1.0, 0.0), "1", ("k_mcs_deep", 2)), ((0.5, 0.0), "1", ("k_mcs_deep", 2)),
-    ((0.5, 0.5), "1", ("k_mcs_bulk", 1)), ((0.98, 0.02), "1", ("k_mcs_bulk", 1)),
-    ((0.5, 0.5), "2", ("k_mcs_deep", 2)), ((1.0, 0.0), "0", ("k_mcs_bulk", 1))])
-def test_kernel_labels_at_configs(monkeypatch, pq, env, want):
-    monkeypatch.setenv("OCTGPU_DEEP", env)
-    assert bench._mcs_kernel(octgpu.UpdateParams.make(*pq), 65536, 512, 1) == want
-
-
-def test_counter_kernel_labels(monkeypatch):
-    monkeypatch.setenv("OCTGPU_DEEP", "1")
-    mk = octgpu.UpdateParams.make
-    assert bench._ctr_kernel(mk(0.5, 0.5), 65536, 512, 1) == ("k_mcs_deep", 2)
-    assert bench._ctr_kernel(mk(0.98, 0.02), 65536, 512, 1) == ("k_mcs_bulk", 1)
-    assert bench._ctr_kernel(mk(0.5, 0.0), 128, 4, 1) == ("k_sweep_ctr", 0.5)

@@ -623,6 +623,7 @@ int alloc_engine(octgpu_engine* e) {
     }
     trace_create("planes", false);
     CK(cudaMalloc(&e->scratch, measure_scratch_bytes(e->Y)));
+    CK(cudaMemset(e->scratch, 0, measure_scratch_bytes(e->Y)));  // k_col_scan's block ticket starts at 0
     CK(cudaMalloc(reinterpret_cast<void**>(&e->res_dev), sizeof(MeasureResult)));
     CK(cudaMallocHost(reinterpret_cast<void**>(&e->res_host), sizeof(MeasureResult)));
     trace_create("small", false);
@@ -1001,7 +1002,11 @@ bool deep_policy(const octgpu_engine* e, const ProbDev& p, const ProbDev& q, uin
     const bool live = !(is_const(p) && is_const(q));
     // 2-MCS passes with counter streams: no stream state to park, so every cheap mode qualifies from 2^28
     if (ctr || !live) return sites >= (uint64_t(1) << 28);
-    return D == 1 && sites >= (uint64_t(1) << 30);
+    // live xoshiro streams: one draw per word (p = 1/2, q = 0: 0.318 -> 0.249 ms/MCS at 2^16^2) and the
+    // half/half pair (p = q = 1/2, BASELINE configs[2]: 0.388 -> 0.347); a dyadic stream or three draws per
+    // word spill at the 128-register budget and stay on the one-MCS kernel (p = 3/4: 0.395 vs 0.521)
+    const bool cheap_live = D == 1 || (p.mode == M_HALF && q.mode == M_HALF);
+    return cheap_live && sites >= (uint64_t(1) << 30);
 }
 
 // One fused pass (k_mcs_deep: 2 or 3 MCS; else 1 MCS) from the current plane / rng set into the other,

@@ -9,41 +9,45 @@
 // h = G_y + u(x), G_y = H_y - sigma_x-(0,y), so S_k = sum_y sum_j C(k,j) G_y^(k-j) U_j(y)
 // with U_j(y) = sum_x u(x)^j.
 //
-// Kernels (one measurement = 2 launches):
-//   k_measure_rows  per block: 4 row groups of 31 rows (lane per row; lane 0 is the row above,
-//                   for the curl check) x 4 x-segments (one warp each). Word-parallel curl
-//                   check; U_j per segment from 16-site units read through two 8-site tables
-//                   (the second indexed by the first's net step, so a unit costs one combine);
-//                   segments and rows combined in int128 in a block-local column-0 gauge.
-//   k_measure_final one block: exclusive prefix of the blocks' column-0 increments, binomial
-//                   shift of each block's sums to the global gauge, reduction, closure data.
+// Kernels (one measurement = 3 launches):
+//   k_col_scan      one block: the column-0 prefix G_y = H_y - sigma_x-(0, y) of every core row (global
+//                   gauge), the column closure sum and sigma_y-(0, c0).
+//   k_measure_rows  persistent blocks of kSeg warps; a block takes a row group of 32 rows (lane per row)
+//                   and warp s the group's x-segment s. Word-parallel curl check; U_j per segment from
+//                   16-site units read through two 8-site tables (the second indexed by the first's net
+//                   step, so a unit costs one combine), unit sums accumulated in 32-bit registers relative
+//                   to a 4-word chunk and folded into the segment's sums once per chunk. Each thread then
+//                   shifts its own segment's sums by the segment's global start height (G_y plus the net
+//                   steps of the segments before it, exchanged through shared memory: one block barrier per
+//                   group) and keeps the block's sums in registers; one block reduction at the end.
+//   k_measure_final one block: sum of the blocks' partial sums, closure data.
 // Scan order = virtual rows c0 .. c1-1 (periodic: physical rows 1 .. Y-1, 0; a stripe: its core
 // rows); the gauge H is 0 at virtual row c0 - 1. For a periodic lattice that is the reference's
 // h(0,0) = 0 whenever the column closes (otherwise the measurement fails with the reference's
 // column error before the sums are used).
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "octgpu_internal.h"
 
 namespace octgpu {
 
-struct Partial {
-    __int128 S[4];                   // block sums in the block-local gauge (H = 0 before its first row)
+struct Partial {  // one row-pass block's sums
+    __int128 S[4];                   // sum h^k over the block's sites (global gauge)
     unsigned long long curl_count;
     unsigned long long curl_first;   // row_id * X + x, ~0 if none
-    long long row0;                  // sum_x sigma_x- of row_id 0 (the block holding it)
-    long long delta;                 // sum of sigma_y-(0, y) over the block's rows
-    long long sy_first;              // sigma_y-(0, c0) (block 0)
-    long long prefix;                // written by k_measure_final: H offset of the block
+    long long row0;                  // sum_x sigma_x- of row_id 0 (its share of the row's segments)
     unsigned long long n_sites;
-    long long pad;
 };
 
 namespace {
 
-constexpr int kRowsPerGroup = 31;  // lane 0 is the y-1 halo for the curl check
-constexpr int kSeg = 8;            // x-segments per row: one warp each; a block = one row group at a time
+constexpr int kRowsPerGroup = 32;  // lane per row; lane 0 reads the row above for the curl check
+#ifndef OCTGPU_MEAS_SEG
+#define OCTGPU_MEAS_SEG 16  // x-segments per row group: one warp each
+#endif
+constexpr int kSeg = OCTGPU_MEAS_SEG;
 constexpr int kMThreads = 32 * kSeg;
 
 __host__ __device__ inline uint32_t measure_groups(uint32_t rows) { return (rows + kRowsPerGroup - 1) / kRowsPerGroup; }
@@ -58,14 +62,16 @@ __device__ __forceinline__ __int128 shfl_down_i128(__int128 v, int off) {
 // ---- 8-site tables ---------------------------------------------------------------
 // A byte = 8 consecutive sites of a row: bits 0..3 the 4 even-x sites (one packed plane's nibble),
 // bits 4..7 the 4 odd-x sites; sites interleave e0 o0 e1 o1 ... (slope_field.hpp:15-53). For an
-// offset o (the height just before the byte, relative to the unit start) the entry holds
-// q_k = sum_i (o + p_i)^k over the byte's inclusive prefix values p_i, k = 1..4, and d = p_7.
-// T0 = offset 0 (first byte of a 16-site unit), T1[o + 8] = offsets -8..8 (second byte, indexed
-// by the first byte's d). Biased fields; the sum of a T0 and a T1 entry is the unit's, without
-// carries between fields:  lo = q3 + B3 (16 bits) | q1 + B1 << 16 (9 bits) | d + 8 << 25,
-// hi = q2 (11 bits) | q4 << 11 (18 bits); unit biases B1 = 136 (36 + 100), B3 = 18496 (1296 + 17200),
-// d: 16.
-constexpr int kUnitB1 = 136, kUnitB3 = 18496, kUnitD = 16;
+// offset o (the height just before the byte, relative to the 16-site unit start; o is even) the entry
+// holds q_k = sum_i (o + p_i)^k over the byte's inclusive prefix values p_i, k = 1..4, and d = p_8.
+// T0 = offset 0 (first byte of a unit), T1[(o + 8) * 256 + b] = offsets -8..8 (second byte, indexed by
+// the first byte's d + 8; odd rows unused). Since p_i = i (mod 2) and o is even, q1 is even, q2 = 0
+// (mod 4) and q4 = 4 (mod 16), so an entry packs into 64 bits with room for the sum of two:
+//   lo = q3 + B3 (16 bits) | q1 / 2 + B1 (8 bits) | d + 8 (8 bits)
+//   hi = q2 / 4 (9 bits) | (q4 - 4) / 16 (23 bits)
+// B3 = 1296 (T0) / 17200 (T1), B1 = 18 / 50. A unit (T0 + T1 entry) decodes as
+//   q3 = Q3 - 18496, q1 = 2 (Q1 - 68), d = D - 16, q2 = 4 Q2, q4 = 16 Q4 + 8.
+constexpr int kUnitB1 = 68, kUnitB3 = 18496;
 
 struct MeasTab {
     uint2 t0[256];
@@ -83,128 +89,161 @@ __host__ __device__ constexpr uint2 tab_entry(int b, int o, bool second) {
         q3 += v * v * v;
         q4 += v * v * v * v;
     }
-    const int b1 = second ? 100 : 36, b3 = second ? 17200 : 1296;
-    const uint32_t lo = uint32_t(q3 + b3) | (uint32_t(q1 + b1) << 16) | (uint32_t(p + 8) << 25);
-    const uint32_t hi = uint32_t(q2) | (uint32_t(q4) << 11);
+    const int b1 = second ? 50 : 18, b3 = second ? 17200 : 1296;
+    const uint32_t lo = uint32_t(q3 + b3) | (uint32_t(q1 / 2 + b1) << 16) | (uint32_t(p + 8) << 24);
+    const uint32_t hi = uint32_t(q2 / 4) | (uint32_t((q4 - 4) / 16) << 9);
     return uint2{lo, hi};
 }
 
 struct MeasTabInit : MeasTab {
     constexpr MeasTabInit() : MeasTab{} {
         for (int b = 0; b < 256; ++b) t0[b] = tab_entry(b, 0, false);
-        for (int o = -8; o <= 8; ++o)
+        for (int o = -8; o <= 8; o += 2)
             for (int b = 0; b < 256; ++b) t1[(o + 8) * 256 + b] = tab_entry(b, o, true);
     }
 };
 
 __device__ const MeasTab g_tab = MeasTabInit();
 
-// shared memory: T0 replicated x16 (entry b at [b][lane & 15]: every warp lookup conflict-free),
-// T1 once; reused for the cross-warp combine after the row pass
-#ifndef OCTGPU_MEAS_REP
-#define OCTGPU_MEAS_REP 16  // T0 replicas: 16 = every lookup conflict-free
-#endif
-#ifndef OCTGPU_MEAS_MINB
-#define OCTGPU_MEAS_MINB 2  // resident blocks per SM the register budget targets
-#endif
-constexpr int kRep = OCTGPU_MEAS_REP;
+// shared memory: T0 replicated x16 (entry b at [b][lane & 15]: every warp lookup conflict-free), T1 once,
+// then two buffers of the threads' segment net steps (groups alternate)
+constexpr int kRep = 16;
 constexpr int kT0Words = 256 * kRep;  // uint2
 constexpr int kT1Words = 17 * 256;
-struct SegOut {                      // one lane's segment result (int128 sums, delta, curl)
-    __int128 T[4];
-    long long D;
-    unsigned int rc, rfirst;
-};
-constexpr size_t kMeasSmem = sizeof(uint2) * (kT0Words + kT1Words) + sizeof(SegOut) * kMThreads;
+// Up to this many sites per segment (R <= 2^13) the segment sums T1..T3 and the per-chunk increment of T4
+// fit 64 bits (T3 <= 2^13 2^39; 4 R^3 C1 <= 2^59, R^4 ns <= 2^61 with C1 <= 2^18, ns = 512); T4 itself is
+// summed in 128. Wider segments (X > 2^17) form everything in 128 bits.
+constexpr uint32_t kNarrowSegSites = 8192;
+constexpr size_t kMeasSmem = sizeof(uint2) * (kT0Words + kT1Words) + 2 * sizeof(long long) * kMThreads +
+                             kSeg * sizeof(Partial);
 
 }  // namespace
 
+// device scratch of a measurement (engine.cu allocates measure_scratch_bytes and zeroes it once)
+struct MeasScratch {
+    long long* G;           // [Y] column-0 gauge G_y, relative to the row's 1024-row scan chunk
+    long long* col;         // [2] the column's total (closure), sigma_y-(0, c0)
+    unsigned int* ticket;   // k_col_scan: blocks done (the last one scans the chunk totals, resets it)
+    long long* tot;         // [chunks] chunk totals, then (in place) their exclusive prefix
+    Partial* part;          // [row-pass blocks]
+};
+constexpr uint32_t kColChunk = 1024;  // rows per k_col_scan block
+
+__host__ __device__ inline MeasScratch scratch_layout(void* base, uint32_t Y) {
+    MeasScratch m;
+    m.G = static_cast<long long*>(base);
+    m.col = m.G + Y;
+    m.ticket = reinterpret_cast<unsigned int*>(m.col + 2);
+    m.tot = m.col + 3;
+    const size_t chunks = Y / kColChunk + 2;
+    m.part = reinterpret_cast<Partial*>(m.tot + ((chunks + 1) & ~size_t(1)) + ((Y + 3) & 1));  // 16-B aligned
+    return m;
+}
+
 size_t measure_scratch_bytes(uint32_t Y) {
-    return size_t(Y + 2) * sizeof(long long) + size_t(measure_groups(Y + 1) + 1) * sizeof(Partial) + 64;
+    const MeasScratch m = scratch_layout(nullptr, Y);
+    return size_t(reinterpret_cast<char*>(m.part) - static_cast<char*>(nullptr)) +
+           size_t(measure_groups(Y + 1) + 1) * sizeof(Partial) + 64;
 }
 
 namespace {
 
-// signed 32 x 32 -> 64-bit multiply-add in one IMAD.WIDE (the compiler otherwise emits the unsigned form
-// plus a sign correction when it can prove one factor non-negative)
+// signed 32 x 32 -> 64-bit multiply-add in one IMAD.WIDE
 __device__ __forceinline__ long long madw(int a, int b, long long c) {
     long long d;
     asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
     return d;
 }
 
-// Unit accumulators since the last flush; heights relative to the segment base + u.
+// Unit accumulators of a chunk: r = height at the unit start relative to the chunk start (|r| <= 512),
+// Q* the biased unit fields (tab_entry); every sum stays in 32 bits over a 32-unit chunk except the three
+// held in 64 (sum r^3, sum r^4, sum r^3 Q1).
 struct UnitAcc {
-    int Au1, Au2, Aq1, Aq2, Aq3, X11, X12, units;
-    unsigned int Aq4;
-    long long Au3, Au4, X13, X21, X22, X31;
+    int ar, ar2, aq1, aq2, aq3, aq4, x11, x12, x13, x21;
+    unsigned int x22;
+    long long ar3, ar4, x31;
     __device__ __forceinline__ void clear() {
-        Au1 = Au2 = Aq1 = Aq2 = Aq3 = X11 = X12 = units = 0;
-        Aq4 = 0;
-        Au3 = Au4 = X13 = X21 = X22 = X31 = 0;
+        ar = ar2 = aq1 = aq2 = aq3 = aq4 = x11 = x12 = x13 = x21 = 0;
+        x22 = 0;
+        ar3 = ar4 = x31 = 0;
     }
 };
 
-// T_k += sum_j C(k,j) B^(k-j) t_j for the unit sums t_j of heights B + u (u = offset within the flush)
-__device__ __noinline__ void flush_units(UnitAcc& A, long long B, __int128* T) {
-    const long long K = A.units;
-    const long long t1 = 16ll * A.Au1 + A.Aq1 - kUnitB1 * K;
-    const long long t2 = 16ll * A.Au2 + 2ll * (A.X11 - (long long)kUnitB1 * A.Au1) + A.Aq2;
-    const long long t3 = 16ll * A.Au3 + 3ll * (A.X21 - (long long)kUnitB1 * A.Au2) + 3ll * A.X12 + A.Aq3 -
-                         (long long)kUnitB3 * K;
-    const long long t4 = 16ll * A.Au4 + 4ll * (A.X31 - (long long)kUnitB1 * A.Au3) + 6ll * A.X22 +
-                         4ll * (A.X13 - (long long)kUnitB3 * A.Au1) + (long long)A.Aq4;
-    const __int128 b = B, b2 = b * b, b3 = b2 * b, b4 = b2 * b2, t0 = 16 * K;
-    T[0] += b * t0 + t1;
-    T[1] += b2 * t0 + 2 * b * t1 + t2;
-    T[2] += b3 * t0 + 3 * b2 * t1 + 3 * b * t2 + t3;
-    T[3] += b4 * t0 + 4 * b3 * t1 + 6 * b2 * t2 + 4 * b * t3 + t4;
+// one 16-site unit: byte un of evn (first 8 sites), byte un of odd (next 8)
+__device__ __forceinline__ void unit(UnitAcc& A, int& r, uint32_t evn, uint32_t odd, uint32_t un, const uint2* t0l,
+                                     const uint2* t1) {
+    const uint2 e0 = t0l[__byte_perm(evn, 0, 0x4440 + un) * kRep];
+    const uint2 e1 = t1[__byte_perm(odd, e0.x >> 24, 0x5540 + un)];  // (d0 + 8) * 256 + byte
+    const uint32_t lo = e0.x + e1.x, hi = e0.y + e1.y;
+    const int q3 = int(lo & 0xffffu), q1 = int(__byte_perm(lo, 0, 0x4442)), q2 = int(hi & 0x1ffu), q4 = int(hi >> 9);
+    const int r2 = r * r, r3 = r2 * r;
+    A.ar += r;
+    A.ar2 += r2;
+    A.ar3 = madw(r2, r, A.ar3);
+    A.ar4 = madw(r2, r2, A.ar4);
+    A.aq1 += q1;
+    A.aq2 += q2;
+    A.aq3 += q3;
+    A.aq4 += q4;
+    A.x11 += r * q1;
+    A.x12 += r * q2;
+    A.x13 += r * q3;
+    A.x21 += r2 * q1;
+    A.x22 += uint32_t(r2) * uint32_t(q2);
+    A.x31 = madw(r3, q1, A.x31);
+    r += int(lo >> 24) - 16;
+}
+
+// Fold a chunk of K units (net step r, ns sites) into the segment sums T (relative to the segment start;
+// R = the chunk's start height there). The chunk's own sums C_k = sum (16 r^k + ... ) decode the biased
+// unit fields; then T_k += sum_j C(k, j) R^(k-j) C_j (C_0 = ns).
+template <typename TT>
+__device__ __forceinline__ void flush_chunk(UnitAcc& A, int K, int ns, long long R, TT& T1, TT& T2, TT& T3,
+                                            __int128& T4) {
+    const long long k = K;
+    const long long C1 = 16ll * A.ar + 2ll * A.aq1 - 2ll * kUnitB1 * k;
+    const long long C2 = 16ll * A.ar2 + 4ll * A.x11 - 4ll * kUnitB1 * A.ar + 4ll * A.aq2;
+    const long long C3 = 16ll * A.ar3 + 6ll * A.x21 - 6ll * kUnitB1 * A.ar2 + 12ll * A.x12 + A.aq3 - kUnitB3 * k;
+    const long long C4 = 16ll * A.ar4 + 8ll * A.x31 - 8ll * kUnitB1 * A.ar3 + 24ll * (long long)A.x22 +
+                         4ll * A.x13 - 4ll * kUnitB3 * A.ar + 16ll * A.aq4 + 8ll * k;
+    const TT r1 = R, r2 = r1 * r1, r3 = r2 * r1;
+    T1 += C1 + r1 * ns;
+    T2 += C2 + 2 * r1 * C1 + r2 * ns;
+    T3 += C3 + 3 * r1 * C2 + 3 * r2 * C1 + r3 * ns;
+    T4 += C4 + 4 * r1 * C3 + 6 * r2 * C2 + 4 * r3 * C1 + r2 * r2 * ns;  // 64-bit increment when narrow
     A.clear();
 }
 
-// one 16-site unit: byte b0 (first 8 sites) then b1 (next 8) of the row. t0b = this lane's replica of
-// T0 (entry b at t0b + 16 b), t1b = T1.
-__device__ __forceinline__ void unit(UnitAcc& A, int& u, uint32_t b0, uint32_t b1, const uint2* t0b,
-                                     const uint2* t1b) {
-    const uint2 e0 = t0b[b0 * kRep];
-    const uint2 e1 = t1b[(e0.x >> 25) * 256 + b1];
-    const uint32_t lo = e0.x + e1.x, hi = e0.y + e1.y;
-    const int q3b = int(lo & 0xffffu), q1b = int((lo >> 16) & 0x1ffu), Db = int(lo >> 25);
-    const int q2 = int(hi & 0x7ffu);
-    const unsigned int q4 = hi >> 11;
-    const int u2 = u * u, u3 = u2 * u;
-    A.Au1 += u;
-    A.Au2 += u2;
-    A.Au3 += (long long)u3;
-    A.Au4 = madw(u2, u2, A.Au4);
-    A.Aq1 += q1b;
-    A.Aq2 += q2;
-    A.Aq3 += q3b;
-    A.Aq4 += q4;
-    A.X11 += u * q1b;
-    A.X12 += u * q2;
-    A.X13 = madw(u, q3b, A.X13);
-    A.X21 = madw(u2, q1b, A.X21);
-    A.X22 = madw(u2, q2, A.X22);
-    A.X31 = madw(u3, q1b, A.X31);
-    u += Db - kUnitD;
-    ++A.units;
-}
+template <typename Word>
+struct Curl {  // word-parallel curl check of one word
+    static constexpr int W = int(sizeof(Word) * 8);
+    // parity ya (even-x sites, D rotated up one packed bit with the previous word's top bit) and parity !ya
+    // (odd-x sites, D aligned); bxa / bxb: the row above's X words
+    __device__ __forceinline__ static void eval(Word xa, Word xb, Word ca, Word cb, Word bxa, Word bxb, Word pcb,
+                                                Word& V1, Word& V2) {
+        const Word D1 = Word((cb << 1) | (pcb >> (W - 1)));
+        V1 = (xa ^ bxa ^ ca ^ D1) | ((xa ^ bxa) & (xa ^ ca));
+        V2 = (xb ^ bxb ^ cb ^ ca) | ((xb ^ bxb) & (xb ^ cb));
+    }
+};
 
 }  // namespace
 
 // ---- row pass -------------------------------------------------------------------------
-// Persistent blocks of kSeg warps walk the row groups (31 core rows each, lane 0 = the row above):
-// warp s handles x-segment s (words [s n / kSeg, (s+1) n / kSeg)) of the group's 32 rows, then warp 0
-// combines the segments of each row and the group's rows into one Partial (group-local gauge).
-template <typename Word>
-__global__ void __launch_bounds__(kMThreads, OCTGPU_MEAS_MINB) k_measure_rows(const Word* __restrict__ planes, Geom g, uint32_t X,
-                                                               long long* __restrict__ Gout, Partial* __restrict__ part) {
+// Persistent blocks of kSeg warps walk the row groups (32 rows each, lane per row): warp s handles
+// x-segment s (words [s n / kSeg, (s+1) n / kSeg)) of the group's rows and shifts its sums to the global
+// gauge (Gg: k_col_scan); part[blockIdx.x] = the block's sums.
+template <typename Word, bool WIDE>
+__global__ void __launch_bounds__(kMThreads, 2) k_measure_rows(const Word* __restrict__ planes, Geom g, uint32_t X,
+                                                               const long long* __restrict__ Gg,
+                                                               const long long* __restrict__ pre,
+                                                               Partial* __restrict__ part) {
     constexpr int W = int(sizeof(Word) * 8);
+    constexpr int kChunkWords = 256 / W;  // 32 units per chunk
     extern __shared__ __align__(16) unsigned char msm[];
     uint2* t0rep = reinterpret_cast<uint2*>(msm);
     uint2* t1 = t0rep + kT0Words;
-    SegOut* so = reinterpret_cast<SegOut*>(t1 + kT1Words);
+    long long* Dbuf = reinterpret_cast<long long*>(t1 + kT1Words);
     for (int i = threadIdx.x; i < kT0Words; i += kMThreads) t0rep[i] = g_tab.t0[i / kRep];
     {
         const uint4* src1 = reinterpret_cast<const uint4*>(g_tab.t1);
@@ -218,13 +257,21 @@ __global__ void __launch_bounds__(kMThreads, OCTGPU_MEAS_MINB) k_measure_rows(co
     const size_t PS = g.plane_stride;
     const uint32_t kbeg = uint32_t(seg) * n / kSeg, kend = uint32_t(seg + 1) * n / kSeg;
     const uint32_t ngroups = measure_groups(g.c1 - g.c0);
-    const uint2* t0b = t0rep + (lane % kRep);
+    const uint2* t0l = t0rep + (lane % kRep);
 
+    // the block's sums, one slot per warp (each warp adds its group shares; no contention)
+    Partial* wsum = reinterpret_cast<Partial*>(Dbuf + 2 * kMThreads);
+    if (lane == 0) {
+        Partial z{};
+        z.curl_first = ~0ull;
+        wsum[seg] = z;
+    }
+    uint32_t gen = 0;
     for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-        const uint32_t first = g.c0 + grp * uint32_t(kRowsPerGroup);  // the group's first core row
-        const uint32_t v = first - 1 + uint32_t(lane);                // lane 0: the row above
+        const uint32_t first = g.c0 + grp * uint32_t(kRowsPerGroup);  // the group's first row
+        const uint32_t v = first + uint32_t(lane);
         const uint32_t y = g.wrap ? v % g.wrap : v;
-        const bool core = lane >= 1 && v < g.c1;
+        const bool core = v < g.c1;
         const uint32_t row_id = g.wrap ? y : v - g.c0;
         const int ya = int((y ^ g.ypar) & 1u);
         // even-x sites of row y are in X(ya), odd-x in X(!ya); C = Y(ya), its partner Y(!ya)
@@ -232,41 +279,86 @@ __global__ void __launch_bounds__(kMThreads, OCTGPU_MEAS_MINB) k_measure_rows(co
         const Word* pXb = planes + size_t(ya ^ 1) * PS + y;
         const Word* pCa = planes + size_t(2 + ya) * PS + y;
         const Word* pCb = planes + size_t(3 - ya) * PS + y;
+        // lane 0: the row above (its X words, which the other lanes take from lane - 1); parity !ya
+        const uint32_t yu = g.wrap ? (v - 1) % g.wrap : v - 1;
+        const Word* pUa = planes + size_t(ya ^ 1) * PS + yu;
+        const Word* pUb = planes + size_t(ya) * PS + yu;
 
-        __int128 T[4] = {0, 0, 0, 0};
-        long long B = 0;
-        unsigned int rc = 0, rfirst = 0xffffffffu;
-        {
+        using TT = typename std::conditional<WIDE, __int128, long long>::type;
+        TT T1 = 0, T2 = 0, T3 = 0;
+        __int128 T4 = 0;
+        long long R = 0;
+        Word bad = 0;
+        if (kend > kbeg) {
             UnitAcc A;
             A.clear();
-            int u = 0;
-            Word pcb = 0, nxa = 0, nxb = 0, nca = 0, ncb = 0;
-            if (kend > kbeg) {
-                pcb = pCb[size_t(kbeg == 0 ? n - 1 : kbeg - 1) * Y];
-                const size_t o = size_t(kbeg) * Y;
-                nxa = pXa[o];
-                nxb = pXb[o];
-                nca = pCa[o];
-                ncb = pCb[o];
+            int r = 0;
+            Word pcb = pCb[size_t(kbeg == 0 ? n - 1 : kbeg - 1) * Y];
+            size_t o = size_t(kbeg) * Y;
+            Word nxa = pXa[o], nxb = pXb[o], nca = pCa[o], ncb = pCb[o], nua = 0, nub = 0;
+            if (lane == 0) {
+                nua = pUa[o];
+                nub = pUb[o];
             }
-            for (uint32_t k = kbeg; k < kend; ++k) {
-                const Word xa = nxa, xb = nxb, ca = nca, cb = ncb;
-                if (k + 1 < kend) {  // prefetch the next word (the loads were the top stall)
-                    const size_t o = size_t(k + 1) * Y;
-                    nxa = pXa[o];
-                    nxb = pXb[o];
-                    nca = pCa[o];
-                    ncb = pCb[o];
+            for (uint32_t kc = kbeg; kc < kend; kc += kChunkWords) {
+                const uint32_t kce = min(kend, kc + kChunkWords);
+                for (uint32_t k = kc; k < kce; ++k) {
+                    const Word xa = nxa, xb = nxb, ca = nca, cb = ncb, ua = nua, ub = nub;
+                    if (k + 1 < kend) {  // prefetch the next word
+                        o += Y;
+                        nxa = pXa[o];
+                        nxb = pXb[o];
+                        nca = pCa[o];
+                        ncb = pCb[o];
+                        if (lane == 0) {
+                            nua = pUa[o];
+                            nub = pUb[o];
+                        }
+                    }
+                    Word bxa = __shfl_up_sync(0xffffffffu, xa, 1);
+                    Word bxb = __shfl_up_sync(0xffffffffu, xb, 1);
+                    if (lane == 0) {
+                        bxa = ua;
+                        bxb = ub;
+                    }
+                    Word V1, V2;
+                    Curl<Word>::eval(xa, xb, ca, cb, bxa, bxb, pcb, V1, V2);
+                    bad |= V1 | V2;
+                    pcb = cb;
+#pragma unroll
+                    for (int half = 0; half < W / 32; ++half) {
+                        const uint32_t a32 = uint32_t(uint64_t(xa) >> (32 * half));
+                        const uint32_t b32 = uint32_t(uint64_t(xb) >> (32 * half));
+                        const uint32_t evn = (a32 & 0x0F0F0F0Fu) | ((b32 & 0x0F0F0F0Fu) << 4);  // chunks 0,2,4,6
+                        const uint32_t odd = ((a32 >> 4) & 0x0F0F0F0Fu) | (b32 & 0xF0F0F0F0u);  // chunks 1,3,5,7
+#pragma unroll
+                        for (uint32_t un = 0; un < 4; ++un) unit(A, r, evn, odd, un, t0l, t1);
+                    }
                 }
-                const Word bxa = __shfl_up_sync(0xffffffffu, xa, 1);
-                const Word bxb = __shfl_up_sync(0xffffffffu, xb, 1);
-                // curl check, word-parallel: parity ya (even-x sites, D rotated up one packed
-                // bit with the previous word's top bit) and parity !ya (odd-x sites, D aligned)
-                const Word D1 = Word((cb << 1) | (pcb >> (W - 1)));
-                const Word V1 = (xa ^ bxa ^ ca ^ D1) | ((xa ^ bxa) & (xa ^ ca));
-                const Word V2 = (xb ^ bxb ^ cb ^ ca) | ((xb ^ bxb) & (xb ^ cb));
+                const int words = int(kce - kc);
+                flush_chunk(A, words * (W / 8), words * 2 * W, R, T1, T2, T3, T4);
+                R += r;
+                r = 0;
+            }
+        }
+        unsigned int rc = 0, rfirst = 0xffffffffu;
+        if (!core) bad = 0;
+        if (__any_sync(0xffffffffu, bad != 0)) {
+            // rare: exact curl count and first plaquette of the segment (the reference's error message)
+            Word pcb = kend > kbeg ? pCb[size_t(kbeg == 0 ? n - 1 : kbeg - 1) * Y] : 0;
+            for (uint32_t k = kbeg; k < kend; ++k) {
+                const size_t o = size_t(k) * Y;
+                const Word xa = pXa[o], xb = pXb[o], ca = pCa[o], cb = pCb[o];
+                Word bxa = __shfl_up_sync(0xffffffffu, xa, 1);
+                Word bxb = __shfl_up_sync(0xffffffffu, xb, 1);
+                if (lane == 0) {
+                    bxa = pUa[o];
+                    bxb = pUb[o];
+                }
+                Word V1, V2;
+                Curl<Word>::eval(xa, xb, ca, cb, bxa, bxb, pcb, V1, V2);
                 pcb = cb;
-                if (V1 | V2) {
+                if (core && (V1 | V2)) {
                     rc += __popcll((unsigned long long)V1) + __popcll((unsigned long long)V2);
                     if (V1)
                         rfirst = min(rfirst, 2u * (k * W + uint32_t(__ffsll((long long)(unsigned long long)V1) - 1)));
@@ -274,155 +366,167 @@ __global__ void __launch_bounds__(kMThreads, OCTGPU_MEAS_MINB) k_measure_rows(co
                         rfirst = min(rfirst,
                                      2u * (k * W + uint32_t(__ffsll((long long)(unsigned long long)V2) - 1)) + 1u);
                 }
-                // rebase before the 32-bit unit accumulators could overflow: |u| <= 1024, <= 1024 units
-                if (u > 1024 - 2 * W || u < -(1024 - 2 * W) || A.units > 1024 - W / 4) {
-                    flush_units(A, B, T);
-                    B += u;
-                    u = 0;
-                }
-#pragma unroll
-                for (int half = 0; half < W / 32; ++half) {
-                    const uint32_t a32 = uint32_t(uint64_t(xa) >> (32 * half));
-                    const uint32_t b32 = uint32_t(uint64_t(xb) >> (32 * half));
-                    const uint32_t evn = (a32 & 0x0F0F0F0Fu) | ((b32 & 0x0F0F0F0Fu) << 4);  // chunks 0,2,4,6
-                    const uint32_t odd = ((a32 >> 4) & 0x0F0F0F0Fu) | (b32 & 0xF0F0F0F0u);  // chunks 1,3,5,7
-#pragma unroll
-                    for (int un = 0; un < 4; ++un)
-                        unit(A, u, __byte_perm(evn, 0, 0x4440 + un), __byte_perm(odd, 0, 0x4440 + un), t0b, t1);
-                }
             }
-            flush_units(A, B, T);
-            B += u;
         }
+        // this segment's start height: G_y + the net steps of the row's segments before it
+        long long* Dg = Dbuf + size_t(gen & 1u) * kMThreads;
+        Dg[threadIdx.x] = R;
+        __syncthreads();  // (the double-buffered D slots need no second barrier per group)
         {
-            SegOut& m = so[threadIdx.x];
-            for (int k = 0; k < 4; ++k) m.T[k] = T[k];
-            m.D = B;
-            m.rc = rc;
-            m.rfirst = rfirst;
-        }
-        __syncthreads();
-        if (seg == 0) {
-            // column 0 in the group gauge: inclusive prefix of sigma_y-(0, y) over the core rows
-            // sigma_y-(0, y) and sigma_x-(0, y): bit 0 of word 0 of Y(ya) and X(ya)
-            const int sy0 = (pCa[0] & 1) ? 1 : -1, sx0 = (pXa[0] & 1) ? 1 : -1;
-            long long incl = core ? sy0 : 0;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const long long t = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= off) incl += t;
-            }
             __int128 S[4] = {0, 0, 0, 0};
             unsigned long long ccount = 0, cfirst = ~0ull;
             long long row0 = 0;
             if (core) {
-                const long long G = incl - sx0;  // group-local G_y = H'_y - sigma_x-(0, y)
-                Gout[y] = G;
-                // the row's U_j: segments in order, each shifted by the net step of the segments before it
-                __int128 U[4] = {0, 0, 0, 0};
-                long long off = 0;
-                unsigned int crc = 0, cfst = 0xffffffffu;
-                for (int s2 = 0; s2 < kSeg; ++s2) {
-                    const SegOut& m = so[s2 * 32 + lane];
-                    const __int128 c = off, c2 = c * c, c3 = c2 * c, c4 = c2 * c2;
-                    const __int128 ns = (__int128)(uint32_t(s2 + 1) * n / kSeg - uint32_t(s2) * n / kSeg) * 2 * W;
-                    U[0] += c * ns + m.T[0];
-                    U[1] += c2 * ns + 2 * c * m.T[0] + m.T[1];
-                    U[2] += c3 * ns + 3 * c2 * m.T[0] + 3 * c * m.T[1] + m.T[2];
-                    U[3] += c4 * ns + 4 * c3 * m.T[0] + 6 * c2 * m.T[1] + 4 * c * m.T[2] + m.T[3];
-                    off += m.D;
-                    crc += m.rc;
-                    cfst = min(cfst, m.rfirst);
-                }
-                const __int128 Gq = G, g2 = Gq * Gq, g3 = g2 * Gq, g4 = g2 * g2, U0 = X;
-                S[0] = Gq * U0 + U[0];
-                S[1] = g2 * U0 + 2 * Gq * U[0] + U[1];
-                S[2] = g3 * U0 + 3 * g2 * U[0] + 3 * Gq * U[1] + U[2];
-                S[3] = g4 * U0 + 4 * g3 * U[0] + 6 * g2 * U[1] + 4 * Gq * U[2] + U[3];
-                ccount = crc;
-                if (cfst != 0xffffffffu) cfirst = (unsigned long long)row_id * X + cfst;
-                if (row_id == 0) row0 = off;  // sum_x sigma_x- of the row
+                long long off = Gg[y] + pre[(v - g.c0) / kColChunk];  // global gauge
+                for (int s2 = 0; s2 < seg; ++s2) off += Dg[s2 * 32 + lane];
+                // S_k = sum_j C(k, j) off^(k-j) T_j, T_0 = the segment's sites
+                const __int128 c = off, c2 = c * c, c3 = c2 * c, c4 = c2 * c2;
+                const __int128 ns = (__int128)(kend - kbeg) * 2 * W, t1 = T1, t2 = T2, t3 = T3;
+                S[0] = c * ns + t1;
+                S[1] = c2 * ns + 2 * c * t1 + t2;
+                S[2] = c3 * ns + 3 * c2 * t1 + 3 * c * t2 + t3;
+                S[3] = c4 * ns + 4 * c3 * t1 + 6 * c2 * t2 + 4 * c * t3 + T4;
+                ccount = rc;
+                if (rfirst != 0xffffffffu) cfirst = (unsigned long long)row_id * X + rfirst;
+                if (row_id == 0) row0 = R;  // sum_x sigma_x- of row 0 (over its segments)
             }
-            const long long delta = __shfl_sync(0xffffffffu, incl, 31);
-            const long long syf = __shfl_sync(0xffffffffu, (long long)sy0, 1);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                for (int off = 16; off > 0; off >>= 1) S[k] += shfl_down_i128(S[k], off);
-            for (int off = 16; off > 0; off >>= 1) {
-                ccount += __shfl_down_sync(0xffffffffu, ccount, off);
-                const unsigned long long o = __shfl_down_sync(0xffffffffu, cfirst, off);
-                cfirst = o < cfirst ? o : cfirst;
-                row0 += __shfl_down_sync(0xffffffffu, row0, off);
-            }
+                for (int o = 16; o > 0; o >>= 1) S[k] += shfl_down_i128(S[k], o);
+            const bool any_curl = __any_sync(0xffffffffu, ccount != 0), any_r0 = __any_sync(0xffffffffu, row0 != 0);
+            if (any_curl || any_r0)
+                for (int o = 16; o > 0; o >>= 1) {
+                    ccount += __shfl_down_sync(0xffffffffu, ccount, o);
+                    const unsigned long long f = __shfl_down_sync(0xffffffffu, cfirst, o);
+                    cfirst = f < cfirst ? f : cfirst;
+                    row0 += __shfl_down_sync(0xffffffffu, row0, o);
+                }
             if (lane == 0) {
-                Partial pr;
-                for (int k = 0; k < 4; ++k) pr.S[k] = S[k];
-                pr.curl_count = ccount;
-                pr.curl_first = cfirst;
-                pr.row0 = row0;
-                pr.delta = delta;
-                pr.sy_first = syf;
-                pr.prefix = 0;
-                pr.n_sites = (unsigned long long)min(uint32_t(kRowsPerGroup), g.c1 - first) * X;
-                pr.pad = 0;
-                part[grp] = pr;
+                Partial& pw = wsum[seg];
+                for (int k = 0; k < 4; ++k) pw.S[k] += S[k];
+                pw.curl_count += ccount;
+                pw.curl_first = cfirst < pw.curl_first ? cfirst : pw.curl_first;
+                pw.row0 += row0;
+                pw.n_sites += (unsigned long long)min(uint32_t(kRowsPerGroup), g.c1 - first) * (kend - kbeg) * 2 * W;
             }
         }
-        __syncthreads();  // the segment buffer is rewritten by the next group
+        ++gen;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Partial pr{};
+        pr.curl_first = ~0ull;
+        for (int w2 = 0; w2 < kSeg; ++w2) {
+            const Partial& pw = wsum[w2];
+            for (int k = 0; k < 4; ++k) pr.S[k] += pw.S[k];
+            pr.curl_count += pw.curl_count;
+            pr.curl_first = pw.curl_first < pr.curl_first ? pw.curl_first : pr.curl_first;
+            pr.row0 += pw.row0;
+            pr.n_sites += pw.n_sites;
+        }
+        part[blockIdx.x] = pr;
     }
 }
 
-__global__ void __launch_bounds__(1024) k_measure_final(Partial* __restrict__ part, uint32_t nb,
+// Column 0: G_y = H_y - sigma_x-(0, y) for the virtual rows c0 .. c1-1, H_y the inclusive prefix of
+// sigma_y-(0, y') from c0. Block b scans rows [1024 b, 1024 b + 1024) (coalesced: one row per thread) and
+// stores G relative to its chunk; the last block to finish turns the chunk totals into their exclusive
+// prefix (the global gauge is G_y + tot[i / 1024]) and writes the column's total and sigma_y-(0, c0).
+template <typename Word>
+__global__ void __launch_bounds__(1024) k_col_scan(const Word* __restrict__ planes, Geom g, MeasScratch m) {
+    __shared__ long long wt[32];
+    __shared__ bool last;
+    const uint32_t R = g.c1 - g.c0, t = threadIdx.x, lane = t & 31, wp = t >> 5;
+    const uint32_t i = blockIdx.x * kColChunk + t;
+    const size_t PS = g.plane_stride;
+    int sy = 0, sx = 0;
+    uint32_t y = 0;
+    if (i < R) {
+        const uint32_t v = g.c0 + i;
+        y = g.wrap ? v % g.wrap : v;
+        const int ya = int((y ^ g.ypar) & 1u);
+        sy = (planes[size_t(2 + ya) * PS + y] & 1) ? 1 : -1;
+        sx = (planes[size_t(ya) * PS + y] & 1) ? 1 : -1;
+    }
+    long long incl = sy;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= uint32_t(o)) incl += u;
+    }
+    if (lane == 31) wt[wp] = incl;
+    __syncthreads();
+    if (wp == 0) {
+        long long u = wt[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long z = __shfl_up_sync(0xffffffffu, u, o);
+            if (lane >= uint32_t(o)) u += z;
+        }
+        wt[lane] = u;
+    }
+    __syncthreads();
+    incl += wp > 0 ? wt[wp - 1] : 0;
+    if (i < R) m.G[y] = incl - sx;
+    if (i == 0) m.col[1] = sy;
+    if (t == 0) {
+        m.tot[blockIdx.x] = wt[31];
+        __threadfence();
+        last = atomicAdd(m.ticket, 1u) + 1u == gridDim.x;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // exclusive prefix of the chunk totals (gridDim.x <= 2^16 / ... chunks; a sequential pass per 1024)
+    long long carry = 0;
+    for (uint32_t b0 = 0; b0 < gridDim.x; b0 += 1024) {
+        const uint32_t b = b0 + t;
+        const long long v = b < gridDim.x ? ((volatile long long*)m.tot)[b] : 0;
+        long long c = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long z = __shfl_up_sync(0xffffffffu, c, o);
+            if (lane >= uint32_t(o)) c += z;
+        }
+        if (lane == 31) wt[wp] = c;
+        __syncthreads();
+        if (wp == 0) {
+            long long u = wt[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long z = __shfl_up_sync(0xffffffffu, u, o);
+                if (lane >= uint32_t(o)) u += z;
+            }
+            wt[lane] = u;
+        }
+        __syncthreads();
+        c += (wp > 0 ? wt[wp - 1] : 0) + carry;
+        if (b < gridDim.x) m.tot[b] = c - v;
+        carry += wt[31];
+        __syncthreads();
+    }
+    if (t == 0) {
+        m.col[0] = carry;
+        *m.ticket = 0;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_measure_final(const Partial* __restrict__ part, uint32_t nb,
+                                                        const long long* __restrict__ col,
                                                         MeasureResult* __restrict__ res) {
     __shared__ __int128 sh_s[4][32];
     __shared__ unsigned long long sh_cc[32], sh_cf[32];
-    __shared__ long long sh_r0[32], sh_tot[32];
-    __shared__ long long carry_sh;
+    __shared__ long long sh_r0[32];
     const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
-    if (t == 0) carry_sh = 0;
-    __syncthreads();
     __int128 S[4] = {0, 0, 0, 0};
     unsigned long long cc = 0, cf = ~0ull;
     long long r0 = 0;
-    for (uint32_t base = 0; base < nb; base += 1024) {
-        const uint32_t i = base + t;
-        Partial p{};
-        if (i < nb) p = part[i];
-        // exclusive prefix of the blocks' column-0 increments (block order = scan order)
-        long long incl = i < nb ? p.delta : 0;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const long long o = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= off) incl += o;
-        }
-        if (lane == 31) sh_tot[wp] = incl;
-        __syncthreads();
-        if (wp == 0) {
-            long long v = sh_tot[lane];
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const long long o = __shfl_up_sync(0xffffffffu, v, off);
-                if (lane >= off) v += o;
-            }
-            sh_tot[lane] = v;
-        }
-        __syncthreads();
-        const long long carry = carry_sh;
-        const long long pre = carry + incl - (i < nb ? p.delta : 0) + (wp > 0 ? sh_tot[wp - 1] : 0);
-        if (i < nb) {
-            part[i].prefix = pre;
-            const __int128 c = pre, c2 = c * c, c3 = c2 * c, c4 = c2 * c2, ns = (__int128)p.n_sites;
-            S[0] += c * ns + p.S[0];
-            S[1] += c2 * ns + 2 * c * p.S[0] + p.S[1];
-            S[2] += c3 * ns + 3 * c2 * p.S[0] + 3 * c * p.S[1] + p.S[2];
-            S[3] += c4 * ns + 4 * c3 * p.S[0] + 6 * c2 * p.S[1] + 4 * c * p.S[2] + p.S[3];
-            cc += p.curl_count;
-            cf = p.curl_first < cf ? p.curl_first : cf;
-            r0 += p.row0;
-        }
-        __syncthreads();
-        if (t == 1023) carry_sh = pre + (i < nb ? p.delta : 0);
-        __syncthreads();
+    for (uint32_t i = t; i < nb; i += 1024) {
+        const Partial& p = part[i];
+        for (int k = 0; k < 4; ++k) S[k] += p.S[k];
+        cc += p.curl_count;
+        cf = p.curl_first < cf ? p.curl_first : cf;
+        r0 += p.row0;
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -459,17 +563,17 @@ __global__ void __launch_bounds__(1024) k_measure_final(Partial* __restrict__ pa
         res->curl_count = tc;
         res->curl_first = tf;
         res->row0_sum = tr;
-        res->col0_sum = carry_sh;
-        res->sy_first = part[0].sy_first;
+        res->col0_sum = col[0];
+        res->sy_first = col[1];
         res->pad = 0;
     }
 }
 
 // Heights (reference HeightMap layout): one warp per row, lane l owns words
-// l, l+32, ...; h(x,y) = G_y + u(x) with G_y = block-local G + the block's prefix.
+// l, l+32, ...; h(x,y) = G_y + u(x) (G_y: k_col_scan of the last measurement).
 template <typename Word>
 __global__ void k_heights(const Word* __restrict__ planes, Geom g, uint32_t X, const long long* __restrict__ G,
-                          const Partial* __restrict__ part, int32_t* __restrict__ out) {
+                          const long long* __restrict__ pre, int32_t* __restrict__ out) {
     constexpr int W = int(sizeof(Word) * 8);
     const uint32_t Y = g.wrap, LD = g.Y, n = g.n;  // periodic only
     const uint32_t y = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -480,7 +584,7 @@ __global__ void k_heights(const Word* __restrict__ planes, Geom g, uint32_t X, c
     const Word* Xa = planes + size_t(ya) * PS + y;
     const Word* Xb = planes + size_t(ya ^ 1) * PS + y;
     const uint32_t vrow = y < g.c0 ? y + g.wrap : y;  // scan position of physical row y
-    long long carry = G[y] + part[(vrow - g.c0) / kRowsPerGroup].prefix;
+    long long carry = G[y] + pre[(vrow - g.c0) / kColChunk];  // global gauge (k_col_scan)
     int32_t* row = out + size_t(y) * X;
     for (uint32_t kb = 0; kb < n; kb += 32) {
         const uint32_t k = kb + lane;
@@ -605,9 +709,14 @@ cudaError_t launch_balances(int w, const void* planes, Geom g, uint32_t r0, uint
 
 cudaError_t launch_measure(int w, const void* planes, Geom g, uint32_t X, void* scratch, void* result_dev,
                            cudaStream_t st) {
-    long long* G = static_cast<long long*>(scratch);
-    Partial* part = reinterpret_cast<Partial*>(G + ((g.Y + 2) & ~1u));  // 16-B aligned (int128)
+    const MeasScratch m = scratch_layout(scratch, g.Y);
+    Partial* part = m.part;
     const uint32_t ngroups = measure_groups(g.c1 - g.c0);
+    const uint32_t cblocks = (g.c1 - g.c0 + kColChunk - 1) / kColChunk;
+    if (w == 64)
+        k_col_scan<uint64_t><<<cblocks, kColChunk, 0, st>>>(static_cast<const uint64_t*>(planes), g, m);
+    else
+        k_col_scan<uint32_t><<<cblocks, kColChunk, 0, st>>>(static_cast<const uint32_t*>(planes), g, m);
     // persistent grid: exactly the blocks that are resident at once (registers / shared memory)
     auto persistent = [&](auto kern, uint32_t& grid) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMeasSmem));
@@ -620,31 +729,36 @@ cudaError_t launch_measure(int w, const void* planes, Geom g, uint32_t X, void* 
         grid = std::max<uint32_t>(1, std::min<uint32_t>(ngroups, uint32_t(std::max(per_sm, 1) * sms)));
         return cudaSuccess;
     };
+    // segments of more than kNarrowSegSites sites (X > 2^17) keep all four segment sums in 128 bits
+    const bool wide = (X + kSeg - 1) / kSeg > kNarrowSegSites;
     uint32_t grid = 1;
+    auto go = [&](auto kern, const auto* pl) -> cudaError_t {
+        const cudaError_t e = persistent(kern, grid);
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kMThreads, kMeasSmem, st>>>(pl, g, X, m.G, m.tot, part);
+        return cudaSuccess;
+    };
+    cudaError_t e;
     if (w == 64) {
-        cudaError_t e = persistent(k_measure_rows<uint64_t>, grid);
-        if (e != cudaSuccess) return e;
-        k_measure_rows<uint64_t><<<grid, kMThreads, kMeasSmem, st>>>(static_cast<const uint64_t*>(planes), g, X, G,
-                                                                      part);
+        const uint64_t* pl = static_cast<const uint64_t*>(planes);
+        e = wide ? go(k_measure_rows<uint64_t, true>, pl) : go(k_measure_rows<uint64_t, false>, pl);
     } else {
-        cudaError_t e = persistent(k_measure_rows<uint32_t>, grid);
-        if (e != cudaSuccess) return e;
-        k_measure_rows<uint32_t><<<grid, kMThreads, kMeasSmem, st>>>(static_cast<const uint32_t*>(planes), g, X, G,
-                                                                      part);
+        const uint32_t* pl = static_cast<const uint32_t*>(planes);
+        e = wide ? go(k_measure_rows<uint32_t, true>, pl) : go(k_measure_rows<uint32_t, false>, pl);
     }
-    k_measure_final<<<1, 1024, 0, st>>>(part, ngroups, static_cast<MeasureResult*>(result_dev));
+    if (e != cudaSuccess) return e;
+    k_measure_final<<<1, 1024, 0, st>>>(part, grid, m.col, static_cast<MeasureResult*>(result_dev));
     return cudaGetLastError();
 }
 
 cudaError_t launch_heights(int w, const void* planes, Geom g, uint32_t X, const void* scratch, int32_t* out,
                            cudaStream_t st) {
-    const long long* G = static_cast<const long long*>(scratch);
-    const Partial* part = reinterpret_cast<const Partial*>(G + ((g.Y + 2) & ~1u));
+    const MeasScratch m = scratch_layout(const_cast<void*>(scratch), g.Y);
     const uint32_t threads = 128, blocks = (g.wrap * 32 + threads - 1) / threads;
     if (w == 64)
-        k_heights<uint64_t><<<blocks, threads, 0, st>>>(static_cast<const uint64_t*>(planes), g, X, G, part, out);
+        k_heights<uint64_t><<<blocks, threads, 0, st>>>(static_cast<const uint64_t*>(planes), g, X, m.G, m.tot, out);
     else
-        k_heights<uint32_t><<<blocks, threads, 0, st>>>(static_cast<const uint32_t*>(planes), g, X, G, part, out);
+        k_heights<uint32_t><<<blocks, threads, 0, st>>>(static_cast<const uint32_t*>(planes), g, X, m.G, m.tot, out);
     return cudaGetLastError();
 }
 

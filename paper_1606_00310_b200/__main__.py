@@ -67,7 +67,10 @@ def cmd_run(a) -> int:
 
 
 def cmd_bench(a) -> int:
-    """BenchReport (SPEC.md:399-420): engine,L,p,q,mode,workers,mcs,updates_per_ns,net_GBps,wall_s."""
+    """BenchReport (SPEC.md:399-432): engine,L,p,q,mode,workers,gpus,mcs,updates_per_ns,net_GBps,wall_s, the
+    median over --repeats timed runs after a 10% warm-up; runs shorter than 1 ms in total are
+    refused. The CPU reference column lives in bench.py (cpu_baseline / --impl reference): the
+    reference engine is test infrastructure and the package never loads it."""
     from .engine import GpuEngine
     from .params import LatticeConfig, UpdateParams
 
@@ -78,15 +81,24 @@ def cmd_bench(a) -> int:
     warm = max(1, a.mcs // 10)  # first 10% discarded
     eng.step(prm, warm)
     eng.sync()
-    t0 = time.perf_counter()
-    eng.step(prm, a.mcs)
-    eng.sync()
-    wall = time.perf_counter() - t0
+    walls = []
+    for _ in range(max(1, a.repeats)):
+        t0 = time.perf_counter()
+        eng.step(prm, a.mcs)
+        eng.sync()
+        walls.append(time.perf_counter() - t0)
+    wall = sorted(walls)[len(walls) // 2]
+    if wall < 1e-3:
+        print(f"error: {a.mcs} MCS of {X}x{Y} took {wall * 1e3:.3f} ms < 1 ms: too short to time "
+              f"(raise --mcs)", file=sys.stderr)
+        return 1
     ups = X * Y * a.mcs / (wall * 1e9)
+    kernel, mcs_per_launch = eng.pass_plan(prm)
     row = {"engine": "gpu" if a.rng == "xoshiro" else "gpu-counter-rng", "L": X if X == Y else f"{X}x{Y}",
            "p": a.p, "q": a.q,
-           "mode": f"{prm.p.mode.label}/{prm.q.mode.label}", "workers": a.workers, "mcs": a.mcs,
-           "updates_per_ns": ups, "net_GBps": ups * 1.0, "wall_s": wall}
+           "mode": f"{prm.p.mode.label}/{prm.q.mode.label}", "workers": a.workers, "gpus": 1, "mcs": a.mcs,
+           "updates_per_ns": ups, "net_GBps": ups * 1.0, "wall_s": wall, "repeats": len(walls),
+           "kernel": kernel, "mcs_per_launch": mcs_per_launch}
     if a.csv:
         print(",".join(row))
         print(",".join(str(v) for v in row.values()))
@@ -119,6 +131,7 @@ def main(argv=None) -> int:
     b = sub.add_parser("bench")
     _common(b)
     b.add_argument("--mcs", type=int, default=100)
+    b.add_argument("--repeats", type=int, default=3)
     b.add_argument("--csv", action="store_true")
     f = sub.add_parser("fit")
     f.add_argument("csv_path")

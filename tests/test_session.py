@@ -119,7 +119,7 @@ def test_cli_run_matches_reference_session(goldens, tmp_path, capsys):
                "--tmax", str(s["tmax"]), "--ppd", str(s["ppd"]), "--out", str(tmp_path)])
     assert rc == 0
     assert open(tmp_path / "measurements.csv").read() == s["csv"]
-    assert main(["bench", "--size", "4096", "--p", "0.5", "--mcs", "20"]) == 0
+    assert main(["bench", "--size", "4096", "--p", "0.5", "--mcs", "200"]) == 0
 
 
 @pytest.mark.gpu
@@ -139,4 +139,21 @@ def test_counter_rng_session_resume(tmp_path):
     assert meta["rng"]["generator"] == "splitmix64-counter"
     xo = run_session(RunConfig(t_max=200, out_dir=str(tmp_path / "xo"), **{**kw, "rng": "xoshiro"}))
     assert open(xo.snapshot_path, "rb").read() != open(whole.snapshot_path, "rb").read()
-    assert main(["bench", "--size", "4096", "--p", "0.5", "--mcs", "20", "--rng", "counter"]) == 0
+    assert main(["bench", "--size", "4096", "--p", "0.5", "--mcs", "200", "--rng", "counter"]) == 0
+
+
+@pytest.mark.gpu
+def test_cli_bench_report_fields(capsys):
+    """BenchReport: the x1 byte identity, gpus, the median of the repeats, the engine's own
+    kernel plan, and the refusal of runs too short to time (< 1 ms)."""
+    import json
+
+    from paper_1606_00310_b200.__main__ import main
+    capsys.readouterr()
+    assert main(["bench", "--size", "4096", "--p", "0.5", "--mcs", "300", "--repeats", "3"]) == 0
+    row = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert row["gpus"] == 1 and row["repeats"] == 3 and row["mcs"] == 300
+    assert row["net_GBps"] == row["updates_per_ns"] * 1.0
+    assert abs(row["updates_per_ns"] - 4096 * 4096 * 300 / (row["wall_s"] * 1e9)) < 1e-6 * row["updates_per_ns"]
+    assert row["kernel"] in ("k_mcs_bulk", "k_mcs_deep") and row["mcs_per_launch"] >= 1
+    assert main(["bench", "--size", "256", "--p", "0.5", "--mcs", "10", "--repeats", "1"]) == 1  # ~0.1 ms

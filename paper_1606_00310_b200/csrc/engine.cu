@@ -993,6 +993,17 @@ int deep_sweeps(const octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool
                : kDeepSweepsLive;
 }
 
+// k_mcs_deep does not mirror its plane stores into a periodic lattice's ghost rows: rows 0..ghost-1 of the
+// new plane set are copied there after the pass (every (plane, word) column holds its rows contiguously, so
+// one strided device copy of ghost x 8 bytes per column)
+cudaError_t mirror_ghost_planes(const octgpu_engine* e, void* planes) {
+    if (e->stripe || kGhostRows > e->L) return cudaSuccess;
+    char* base = static_cast<char*>(planes);
+    const size_t pitch = size_t(e->Y) * e->word_bytes();
+    return cudaMemcpy2DAsync(base + size_t(e->L) * e->word_bytes(), pitch, base, pitch, size_t(kGhostRows) * e->word_bytes(),
+                             size_t(4) * e->n, cudaMemcpyDeviceToDevice, e->stream);
+}
+
 // Periodic lattices: does octgpu_step run k_mcs_deep passes for these parameters? (D = draws per word of a
 // xoshiro sweep; ctr = the counter-based streams)
 bool deep_policy(const octgpu_engine* e, const ProbDev& p, const ProbDev& q, uint64_t D, bool ctr) {
@@ -1042,6 +1053,7 @@ int step_pass(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool live, i
         CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase,
                            shifted(e, e->deep_geom(ls), uint32_t(deep_box_rows())), p, q, jtab, ls,
                            deep_ring(e, p, q, ls), &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
+        CK(mirror_ghost_planes(e, e->planes[ps ^ 1]));
     } else if (e->mcs_impl == 2) {
         int rc = plan_bulk(e, p, q);
         if (rc) return rc;
@@ -1099,6 +1111,7 @@ int step_counter(octgpu_engine* e, const ProbDev& p, const ProbDev& q, uint64_t 
                                    shifted(e, e->deep_geom(ls), uint32_t(deep_box_rows())), p, q, e->master_seed,
                                    2 * e->t, ls, deep_ring(e, p, q, ls, true), &e->tmd[ps][0], &e->tmd[ps][1],
                                    e->stream));
+            CK(mirror_ghost_planes(e, e->planes[ps ^ 1]));
             ++e->launches;
             e->pcur ^= 1;
             e->t += mpp;

@@ -170,7 +170,7 @@ struct DeepCtx {
     uint32_t wrap;
     uint32_t sf1, sf2;   // x+ neighbour shifted by one packed bit in sweeps of parity f / s
     int up, dn;          // shuffle source lanes of rows y - 1 / y + 1 (rotating: see edge exchange)
-    bool core, ghostw, ghost_row, ghost_row1;
+    bool core, ghost_row;  // ghost_row: the row's stream state is mirrored into the ghost rows
     uint64_t* save;  // this lane's parking slots: save[slot * kLanes]
 };
 
@@ -182,12 +182,9 @@ struct DeepState {
     uint64_t cur, raw0;                   // sweep 1: original X(s)[y][j], X(s)[y][0]
 };
 
-// GH: the warp stores rows 0..ghost-1 of a periodic lattice and mirrors them into the ghost rows
-// (warp-uniform; 2 = decide at run time)
-__device__ __forceinline__ void put(const DeepCtx& c, uint64_t* ptr, uint64_t val, bool pred, bool ghost_row) {
-    st_pred(ptr, val, pred);
-    if (c.ghostw) st_pred(ptr + c.wrap, val, pred && ghost_row);
-}
+// plane stores of the last sweep (the host mirrors rows 0..ghost-1 into a periodic lattice's ghost rows after
+// the pass: one strided device copy instead of a branch per store here)
+__device__ __forceinline__ void put(uint64_t* ptr, uint64_t val, bool pred) { st_pred(ptr, val, pred); }
 
 // Edge exchange after every word: lane 31 of warp w publishes its rows' C outputs (row y+1's Y input of the
 // next sweep) and lane 0 its B outputs (row y-1's Y(s)[y+1] input); after the barrier lane 31 of warp w+1
@@ -325,17 +322,17 @@ __device__ __forceinline__ void deep_iter(DeepState<L, typename std::conditional
                     c.save[(sv + 3) * kLanes] ^= carry;
                 } else {
                     const uint64_t xf = c.save[sv * kLanes] ^ carry;
-                    put(c, ((L & 1) ? c.dXs : c.dXf) + size_t(l - 1) * c.Y, xf, c.core, c.ghost_row);
+                    put(((L & 1) ? c.dXs : c.dXf) + size_t(l - 1) * c.Y, xf, c.core);
                 }
             }
         }
         if (l == L) {
             // sweep L has parity s (L even): X(s), Y(s) own; Y(f)[y+1] = C^L[y]; X(f) via the carry
             const uint32_t o = j * c.Y;
-            put(c, c.dXs + o, nA[li], c.core, c.ghost_row);
-            put(c, c.dYs + o, nB[li], c.core, c.ghost_row);
-            put(c, c.dYf1 + o, nC[li], c.core, c.ghost_row1);
-            if (!first) put(c, c.dXf + o, nR[li], c.core, c.ghost_row);
+            put(c.dXs + o, nA[li], c.core);
+            put(c.dYs + o, nB[li], c.core);
+            put(c.dYf1 + o, nC[li], c.core);
+            if (!first) put(c.dXf + o, nR[li], c.core);
         }
     }
 #pragma unroll
@@ -432,8 +429,6 @@ __global__ void __launch_bounds__(32 * kDP, kDeepMinBlocks)
     c.dn = (lane + 1) & 31;
     c.core = t >= GEO::kFirst && t <= GEO::kLast && v < g.c1;
     c.ghost_row = g.ghost && y < g.ghost;
-    c.ghost_row1 = g.ghost && y1 < g.ghost;
-    c.ghostw = __any_sync(0xffffffffu, c.core && (c.ghost_row || c.ghost_row1));
     c.save = slots + t;
 
     DeepState<L, Src> R;

@@ -93,8 +93,8 @@ struct DeepSlots {
     __host__ __device__ static constexpr int st0() { return preQ0() + (kPreQ ? npre() : 0); }
     __host__ __device__ static constexpr int count() { return st0() + 4 * parked(); }
     __host__ __device__ static constexpr int pre(int l, int j) { return (l - 1) * (l - 2) / 2 + j; }
-    // edge exchange: [2 buffers][kDP warps][C of lane 31 | B of lane 0][L-1 sweeps] u64
-    __host__ __device__ static constexpr int xch_words() { return 2 * kDP * 2 * (L - 1); }
+    // edge exchange: [2 buffers][kDP warps][C of lane 31 | B of lane 0][L words, L-1 used] u64
+    __host__ __device__ static constexpr int xch_words() { return 2 * kDP * 2 * L; }
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -163,10 +163,8 @@ __device__ __forceinline__ void slot_store(uint64_t* save, int slot, const Xo& s
 // Lane context shared by every iteration.
 struct DeepCtx {
     uint32_t n, Y;
-    uint64_t* dXf;  // dst planes at this lane's physical row
-    uint64_t* dXs;
-    uint64_t* dYs;
-    uint64_t* dYf1;  // Y(f) of the row below (physical row y + 1)
+    uint64_t* d0;   // dst at this lane's physical row y
+    uint64_t* d1;   // dst at physical row y + 1 (Y(f) of the row below)
     uint32_t wrap;
     uint32_t sf1, sf2;   // x+ neighbour shifted by one packed bit in sweeps of parity f / s
     int up, dn;          // shuffle source lanes of rows y - 1 / y + 1 (rotating: see edge exchange)
@@ -191,26 +189,52 @@ __device__ __forceinline__ void put(uint64_t* ptr, uint64_t val, bool pred) { st
 // takes warp w's C and lane 0 of warp w-1 takes warp w's B. Lane 31's own C and lane 0's own B are consumed
 // only by the neighbouring warp, so they are overwritten in place and the rotating shuffles of the next word
 // (lane 0 <- lane 31, lane 31 <- lane 0) deliver the other warp's row.
+// predicated shared-memory accesses (no branch around the edge lanes' exchange)
+__device__ __forceinline__ void sts2_pred(uint64_t* p, uint64_t a, uint64_t b, bool pred) {
+    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %3, 0;\n@q st.shared.v2.u64 [%0], {%1, %2};\n}\n" ::"r"(smem_u32(p)),
+                 "l"(a), "l"(b), "r"(int(pred))
+                 : "memory");
+}
+__device__ __forceinline__ void sts1_pred(uint64_t* p, uint64_t a, bool pred) {
+    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.shared.u64 [%0], %1;\n}\n" ::"r"(smem_u32(p)), "l"(a),
+                 "r"(int(pred))
+                 : "memory");
+}
+__device__ __forceinline__ void lds2_pred(const uint64_t* p, uint64_t& a, uint64_t& b, bool pred) {
+    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %3, 0;\n@q ld.shared.v2.u64 {%0, %1}, [%2];\n}\n"
+                 : "+l"(a), "+l"(b)
+                 : "r"(smem_u32(p)), "r"(int(pred))
+                 : "memory");
+}
+__device__ __forceinline__ void lds1_pred(const uint64_t* p, uint64_t& a, bool pred) {
+    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q ld.shared.u64 %0, [%1];\n}\n"
+                 : "+l"(a)
+                 : "r"(smem_u32(p)), "r"(int(pred))
+                 : "memory");
+}
+// v[0..L-2] <-> a 16-B aligned row of L words
+template <int L>
+__device__ __forceinline__ void xrow_store(uint64_t* row, const uint64_t* v, bool pred) {
+#pragma unroll
+    for (int l = 0; l + 1 < L - 1; l += 2) sts2_pred(row + l, v[l], v[l + 1], pred);
+    if constexpr ((L - 1) % 2) sts1_pred(row + L - 2, v[L - 2], pred);
+}
+template <int L>
+__device__ __forceinline__ void xrow_load(const uint64_t* row, uint64_t* v, bool pred) {
+#pragma unroll
+    for (int l = 0; l + 1 < L - 1; l += 2) lds2_pred(row + l, v[l], v[l + 1], pred);
+    if constexpr ((L - 1) % 2) lds1_pred(row + L - 2, v[L - 2], pred);
+}
+
 template <int L, typename StateT>
 __device__ __forceinline__ void edge_exchange(StateT& S, uint64_t* xch, uint32_t i, int wib, int lane) {
-    uint64_t* buf = xch + size_t(i & 1u) * (kDP * 2 * (L - 1));
-    if (lane == 31) {
-#pragma unroll
-        for (int l = 0; l < L - 1; ++l) buf[(wib * 2 + 0) * (L - 1) + l] = S.pC[l];
-    }
-    if (lane == 0) {
-#pragma unroll
-        for (int l = 0; l < L - 1; ++l) buf[(wib * 2 + 1) * (L - 1) + l] = S.pB[l];
-    }
+    // buffer i&1: [kDP warps][C of lane 31 | B of lane 0][L words (L-1 used)]
+    uint64_t* buf = xch + size_t(i & 1u) * (kDP * 2 * L);
+    xrow_store<L>(buf + (wib * 2 + 0) * L, S.pC, lane == 31);
+    xrow_store<L>(buf + (wib * 2 + 1) * L, S.pB, lane == 0);
     xch_barrier();
-    if (lane == 31 && wib > 0) {
-#pragma unroll
-        for (int l = 0; l < L - 1; ++l) S.pC[l] = buf[((wib - 1) * 2 + 0) * (L - 1) + l];
-    }
-    if (lane == 0 && wib < kDP - 1) {
-#pragma unroll
-        for (int l = 0; l < L - 1; ++l) S.pB[l] = buf[((wib + 1) * 2 + 1) * (L - 1) + l];
-    }
+    xrow_load<L>(buf + ((wib - 1) * 2 + 0) * L, S.pC, lane == 31 && wib > 0);
+    xrow_load<L>(buf + ((wib + 1) * 2 + 1) * L, S.pB, lane == 0 && wib < kDP - 1);
 }
 
 // One iteration i: sweep l on word (i-(l-1)) mod n for every active l.
@@ -218,7 +242,10 @@ __device__ __forceinline__ void edge_exchange(StateT& S, uint64_t* xch, uint32_t
 template <int PM, int QM, int L, bool STEADY, bool CTR = false>
 __device__ __forceinline__ void deep_iter(DeepState<L, typename std::conditional<CTR, Ctr, Xo>::type>& S,
                                           const DeepCtx& c, uint32_t i, const uint64_t* sb, int jj,
-                                          const ProbDev& p, const ProbDev& q) {
+                                          const ProbDev& p, const ProbDev& q, const Geom& g, int f) {
+    // plane offsets of the last sweep's stores, formed from the kernel parameters (uniform, no registers)
+    const size_t oXf = size_t(f) * g.plane_stride, oXs = size_t(f ^ 1) * g.plane_stride;
+    const size_t oYf = size_t(2 + f) * g.plane_stride, oYs = size_t(3 - f) * g.plane_stride;
     using ST = DeepStage<L>;
     using SL = DeepSlots<L, PM, QM, CTR>;
     const uint32_t n = c.n;
@@ -322,17 +349,17 @@ __device__ __forceinline__ void deep_iter(DeepState<L, typename std::conditional
                     c.save[(sv + 3) * kLanes] ^= carry;
                 } else {
                     const uint64_t xf = c.save[sv * kLanes] ^ carry;
-                    put(((L & 1) ? c.dXs : c.dXf) + size_t(l - 1) * c.Y, xf, c.core);
+                    put(c.d0 + (((L & 1) ? oXs : oXf) + size_t(l - 1) * c.Y), xf, c.core);
                 }
             }
         }
         if (l == L) {
             // sweep L has parity s (L even): X(s), Y(s) own; Y(f)[y+1] = C^L[y]; X(f) via the carry
-            const uint32_t o = j * c.Y;
-            put(c.dXs + o, nA[li], c.core);
-            put(c.dYs + o, nB[li], c.core);
-            put(c.dYf1 + o, nC[li], c.core);
-            if (!first) put(c.dXf + o, nR[li], c.core);
+            const size_t o = size_t(j) * c.Y;
+            put(c.d0 + (oXs + o), nA[li], c.core);
+            put(c.d0 + (oYs + o), nB[li], c.core);
+            put(c.d1 + (oYf + o), nC[li], c.core);
+            if (!first) put(c.d0 + (oXf + o), nR[li], c.core);
         }
     }
 #pragma unroll
@@ -419,10 +446,8 @@ __global__ void __launch_bounds__(32 * kDP, kDeepMinBlocks)
     c.n = n;
     c.Y = g.Y;
     c.wrap = g.wrap;
-    c.dXf = dst + size_t(0 + f) * PS + y;
-    c.dXs = dst + size_t(0 + s) * PS + y;
-    c.dYs = dst + size_t(2 + s) * PS + y;
-    c.dYf1 = dst + size_t(2 + f) * PS + y1;
+    c.d0 = dst + y;
+    c.d1 = dst + y1;
     c.sf1 = (uint32_t(f) ^ y ^ g.ypar) & 1u;
     c.sf2 = c.sf1 ^ 1u;
     c.up = (lane + 31) & 31;
@@ -489,14 +514,14 @@ __global__ void __launch_bounds__(32 * kDP, kDeepMinBlocks)
         if (kb >= uint32_t(2 * L) && kb + kKS < n) {  // i = n-1 is sweep 1's last word: generic
 #pragma unroll
             for (int jj = 0; jj < kKS; ++jj) {
-                deep_iter<PM, QM, L, true, CTR>(R, c, kb + jj, sb, jj, p, q);
+                deep_iter<PM, QM, L, true, CTR>(R, c, kb + jj, sb, jj, p, q, g, f);
                 edge_exchange<L>(R, xch, kb + jj, wib, lane);
             }
         } else {
 #pragma unroll 1
             for (int jj = 0; jj < kKS; ++jj) {
                 if (kb + jj < n) {
-                    deep_iter<PM, QM, L, false, CTR>(R, c, kb + jj, sb, jj, p, q);
+                    deep_iter<PM, QM, L, false, CTR>(R, c, kb + jj, sb, jj, p, q, g, f);
                     edge_exchange<L>(R, xch, kb + jj, wib, lane);
                 }
             }
@@ -512,7 +537,7 @@ __global__ void __launch_bounds__(32 * kDP, kDeepMinBlocks)
     // drain: sweeps 2..L finish their wrapped words
 #pragma unroll 1
     for (uint32_t i = n; i < n + uint32_t(2 * L - 2); ++i) {
-        deep_iter<PM, QM, L, false, CTR>(R, c, i, nullptr, 0, p, q);
+        deep_iter<PM, QM, L, false, CTR>(R, c, i, nullptr, 0, p, q, g, f);
         edge_exchange<L>(R, xch, i, wib, lane);
     }
 
@@ -548,7 +573,7 @@ size_t deep_smem_l(int pm, int qm, int S, bool ctr) {
     const bool pp = !(pm == M_ZERO || pm == M_ONE), pq = !(qm == M_ZERO || qm == M_ONE);
     const int parked = !ctr && (pp || pq) && L > kRegStreams ? L - kRegStreams : 0;
     const int slots = 5 * (L - 1) + 1 + (pp ? L * (L - 1) / 2 : 0) + (pq ? L * (L - 1) / 2 : 0) + 4 * parked;
-    const int xch = 2 * kDP * 2 * (L - 1);
+    const int xch = 2 * kDP * 2 * L;
     return 128 + size_t(S) * DeepStage<L>::kWords * 8 + size_t(slots) * kLanes * 8 + size_t(xch) * 8;
 }
 

@@ -193,7 +193,7 @@ int octgpu_balances(octgpu_engine* e, int64_t* rows_out, int64_t* cols_out);
  * A stripe engine owns global rows [y0, y1) (at least 4) of an X x Y periodic
  * lattice (sublattice partition as the reference's SweepPlan row blocks,
  * params.hpp:107-127; results do not depend on the partition). One pass of
- * k = 1 MCS (or k = octgpu_stripe_max_mcs(), 2 for constant xi: the
+ * k = 1 MCS (or k = octgpu_stripe_max_mcs(), 3 for constant xi: the
  * temporally blocked kernel):
  *   octgpu_halo_pack -> exchange (to_prev -> rank-1, to_next -> rank+1) ->
  *   octgpu_halo_unpack -> octgpu_stripe_mcs_n(k) -> exchange boundary (-> rank+1) ->

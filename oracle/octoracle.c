@@ -563,13 +563,14 @@ uint32_t oo_log_schedule(uint64_t t_max, uint32_t ppd, uint64_t* out, uint32_t c
 /* k MCS (2k sweeps f, f^1, ...) of a row stripe held with halos, as the GPU
  * multi-stripe path organises it (not a reference function; built from
  * sweep_range, so it is exactly the reference's sweeps restricted to the rows
- * the stripe can complete): R = L + 7 buffer rows, 0..2 halo above, 3..L+2
- * own, L+3..L+6 halo below. Sweep i (1-based) runs on rows [i-1, R-i): each
- * sweep needs the previous one on rows y-1..y+1, so the valid band shrinks by
- * one row per side; sweep 2k <= 4 still covers rows 3..L+2. Afterwards rows
- * 3..L+2 are final except y-plane f of row 3 (completed by the previous
- * stripe's boundary row), and y-plane f of row L+3 is the boundary row for the
- * next stripe. yoff = global row of buffer row 0 (= y0 - 3 mod Y). */
+ * the stripe can complete): R = L + HA + HB buffer rows (HA = 5, HB = 6 on the
+ * GPU path), 0..HA-1 halo above, HA..HA+L-1 own, then the halo below. Sweep i
+ * (1-based) runs on rows [i-1, R-i): each sweep needs the previous one on rows
+ * y-1..y+1, so the valid band shrinks by one row per side; sweep 2k <= HA + 1
+ * still covers the own rows. Afterwards the own rows are final except y-plane f
+ * of row HA (completed by the previous stripe's boundary row), and y-plane f of
+ * row HA+L is the boundary row for the next stripe. yoff = global row of buffer
+ * row 0 (= y0 - HA mod Y). */
 void oo_mcs_stripe(uint32_t X, uint32_t w, uint32_t R, uint32_t nsweeps, uint32_t yoff, uint64_t* planes,
                    uint64_t* states, int f, const oo_prob* p, const oo_prob* q) {
     lat_t Lt = {X, R, w, X / (2 * w), 0, R, planes, NULL, yoff};

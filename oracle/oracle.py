@@ -356,10 +356,10 @@ class RefEngine:
 class OracleStripe:
     """CPU stand-in for paper_1606_00310_b200.stripes.StripeEngine (test infra):
     same pack/unpack/mcs/finish/measure_local contract and buffer layout
-    (3 halo rows above, 4 below, include/octgpu.h), computed by oo_mcs_stripe
-    (the reference's sweeps restricted to a stripe with halos)."""
+    (5 halo rows above, 6 below: engine.cu kStripeHA / kStripeHB), computed by
+    oo_mcs_stripe (the reference's sweeps restricted to a stripe with halos)."""
 
-    HA, HB = 3, 4
+    HA, HB = 5, 6
 
     def __init__(self, o: Oracle, X: int, Y: int, y0: int, y1: int, seed: int, w: int = 64):
         self.o, self.X, self.Y, self.w, self.y0, self.y1 = o, X, Y, w, y0, y1
@@ -401,7 +401,7 @@ class OracleStripe:
         self._scatter(self.HA + self.L, self.HB, from_next)
 
     def max_mcs(self, prm):
-        return 2  # the CPU stand-in runs the 2-MCS protocol for every mode
+        return 3  # the CPU stand-in runs the 3-MCS protocol for every mode
 
     def mcs(self, prm, boundary_out, n=1):
         o = self.o

@@ -339,6 +339,9 @@ struct octgpu_engine {
     CUtensorMap tmd[2][2];  // the same for k_mcs_deep (deep_box_rows rows x 2 / 3 words)
     bool tmd_ok = false;
     int deep = 1;  // temporally blocked passes (k_mcs_deep) where supported; OCTGPU_DEEP=0 disables
+    // multi-MCS peer-memory stripe passes fused with their halo exchange: -1 = when a neighbour is on another
+    // device (decided at connect), 0 / 1 = OCTGPU_FUSED_LINK
+    int fused_link = -1;
     int deep_l = kDeepSweepsConst;  // sweeps of a constant-xi deep pass (OCTGPU_DEEP_L = 4 keeps 2 MCS per pass)
     bool graphs = true;  // replay CUDA graphs for long step() calls (OCTGPU_GRAPH=0 disables)
     uint32_t prefetch = 0;  // TMA kernels: L2 prefetch distance in ring stages (OCTGPU_PREFETCH)
@@ -474,6 +477,7 @@ int plan_mcs(octgpu_engine* e) {
     if (const char* v = getenv("OCTGPU_P2P_TIMEOUT_MS")) e->p2p_timeout = std::max(1LL, atoll(v)) * 2'000'000LL;
     if (const char* v = getenv("OCTGPU_PREFETCH")) e->prefetch = uint32_t(std::max(0, std::min(64, atoi(v))));
     if (const char* v = getenv("OCTGPU_DEEP_S")) e->deep_S = std::max(2, std::min(8, atoi(v)));
+    if (const char* v = getenv("OCTGPU_FUSED_LINK")) e->fused_link = atoi(v) != 0 ? 1 : 0;
     if (const char* v = getenv("OCTGPU_DEEP_L")) e->deep_l = atoi(v) == kDeepSweepsLive ? kDeepSweepsLive : kDeepSweepsConst;
     return OCTGPU_OK;
 }
@@ -984,10 +988,9 @@ int deep_ring(octgpu_engine* e, const ProbDev& p, const ProbDev& q, int ls, bool
     return S;
 }
 
-// sweeps per k_mcs_deep pass: 6 (3 MCS) where the kernel takes it (constant xi on a periodic lattice), else 4;
-// row stripes always 4 (their halo rows are sized for kStripeSweeps)
+// sweeps per k_mcs_deep pass: 6 (3 MCS) where the kernel takes it (constant xi), else 4 (row stripes too: their
+// halo rows are sized for kStripeSweeps = 6)
 int deep_sweeps(const octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool ctr) {
-    if (e->stripe) return kStripeSweeps;
     return (e->deep_l == kDeepSweepsConst && mcs_deep_supported_l(p.mode, q.mode, kDeepSweepsConst, ctr))
                ? kDeepSweepsConst
                : kDeepSweepsLive;
@@ -1575,16 +1578,27 @@ bool stripe_deep_ok(const octgpu_engine* e, const ProbDev& p, const ProbDev& q) 
     return e->deep && size_ok && e->mcs_impl == 2 && mcs_deep_supported(p.mode, q.mode) && xi_ok;
 }
 
-// one fused stripe pass with counter-based xi (n_mcs = 1: k_mcs_bulk<CTR>, else k_mcs_deep<CTR>)
-int stripe_kernel_ctr(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool deep) {
+// sweeps of a stripe pass of n_mcs MCS: 0 = the one-MCS kernel; 4 / 6 = k_mcs_deep (2 MCS for cheap modes with
+// constant xi or counter streams, 3 where the kernel takes L = 6). -1: not a valid pass length.
+int stripe_pass_sweeps(const octgpu_engine* e, const ProbDev& p, const ProbDev& q, uint32_t n_mcs) {
+    if (n_mcs == 1) return 0;
+    if (!stripe_deep_ok(e, p, q)) return -1;
+    const bool ctr = e->rng_kind == OCTGPU_RNG_COUNTER;
+    if (n_mcs == 2) return kDeepSweepsLive;
+    if (n_mcs == 3 && deep_sweeps(e, p, q, ctr) == kDeepSweepsConst) return kDeepSweepsConst;
+    return -1;
+}
+
+// one fused stripe pass with counter-based xi (ls = 0: k_mcs_bulk<CTR>, else k_mcs_deep<CTR> of ls sweeps)
+int stripe_kernel_ctr(octgpu_engine* e, const ProbDev& p, const ProbDev& q, int ls) {
+    const bool deep = ls > 0;
     const Geom g = e->geom();
     const int ps = e->pcur;
     if (deep) {
         int rc = ensure_tmaps_deep(e);
         if (rc) return rc;
-        CK(launch_mcs_deep_ctr(e->planes[ps], e->planes[ps ^ 1], e->phase, g, p, q, e->master_seed, 2 * e->t,
-                               kStripeSweeps, deep_ring(e, p, q, kStripeSweeps, true), &e->tmd[ps][0],
-                               &e->tmd[ps][1], e->stream));
+        CK(launch_mcs_deep_ctr(e->planes[ps], e->planes[ps ^ 1], e->phase, g, p, q, e->master_seed, 2 * e->t, ls,
+                               deep_ring(e, p, q, ls, true), &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
     } else {
         int rc = plan_bulk(e, p, q);
         if (rc) return rc;
@@ -1606,7 +1620,7 @@ int octgpu_pass_plan(octgpu_engine* e, const octgpu_params* prm, int* kernel, in
     if (e->stripe) {
         if (stripe_deep_ok(e, p, q)) {
             k = OCTGPU_KERNEL_DEEP;
-            ls = kStripeSweeps;
+            ls = deep_sweeps(e, p, q, ctr);
         }
     } else {
         const uint64_t D = draws(prm->p, e->w) + (q.mode != M_ZERO ? draws(prm->q, e->w) : 0);
@@ -1630,7 +1644,7 @@ int octgpu_stripe_max_mcs(octgpu_engine* e, const octgpu_params* prm) {
     }
     ProbDev p, q;
     if (lower_params(prm, p, q)) return 0;
-    return stripe_deep_ok(e, p, q) ? kStripeSweeps / 2 : 1;
+    return stripe_deep_ok(e, p, q) ? deep_sweeps(e, p, q, e->rng_kind == OCTGPU_RNG_COUNTER) / 2 : 1;
 }
 
 int octgpu_stripe_mcs_n(octgpu_engine* e, const octgpu_params* prm, uint32_t n_mcs, void* boundary_out) {
@@ -1639,10 +1653,11 @@ int octgpu_stripe_mcs_n(octgpu_engine* e, const octgpu_params* prm, uint32_t n_m
     int rc = lower_params(prm, p, q);
     if (!rc) rc = use_device(e);
     if (rc) return rc;
-    const bool deep = n_mcs == uint32_t(kStripeSweeps / 2);
-    if (n_mcs != 1 && !(deep && stripe_deep_ok(e, p, q)))
-        return fail(OCTGPU_ERR_CONFIG, "a stripe pass covers 1 MCS, or " + std::to_string(kStripeSweeps / 2) +
-                                           " with constant xi (see octgpu_stripe_max_mcs)");
+    const int ls = stripe_pass_sweeps(e, p, q, n_mcs);
+    if (ls < 0)
+        return fail(OCTGPU_ERR_CONFIG, "a stripe pass covers 1 MCS, or up to octgpu_stripe_max_mcs() with constant "
+                                       "xi (2 or 3)");
+    const bool deep = ls > 0;
     const bool ctr = e->rng_kind == OCTGPU_RNG_COUNTER;
     const bool live = !ctr && !(is_const(p) && is_const(q));
     const uint64_t D = draws(prm->p, e->w) + (q.mode != M_ZERO ? draws(prm->q, e->w) : 0);
@@ -1656,14 +1671,13 @@ int octgpu_stripe_mcs_n(octgpu_engine* e, const octgpu_params* prm, uint32_t n_m
     const Geom g = e->geom();
     const int ps = e->pcur, rs = e->rcur;
     if (ctr) {
-        rc = stripe_kernel_ctr(e, p, q, deep);
+        rc = stripe_kernel_ctr(e, p, q, ls);
         if (rc) return rc;
     } else if (deep) {
         rc = ensure_tmaps_deep(e);
         if (rc) return rc;
-        CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
-                           kStripeSweeps, deep_ring(e, p, q, kStripeSweeps), &e->tmd[ps][0], &e->tmd[ps][1],
-                           e->stream));
+        CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab, ls,
+                           deep_ring(e, p, q, ls), &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
     } else if (e->mcs_impl == 2) {
         rc = plan_bulk(e, p, q);
         if (rc) return rc;
@@ -1826,6 +1840,11 @@ int octgpu_stripe_connect(octgpu_engine* e, const octgpu_peer* prev, const octgp
     e->prev = *prev;
     e->next = *next;
     e->p2p = true;
+    // Fused passes leave the boundary blocks waiting inside the MCS kernel: right when each stripe has its own
+    // GPU; stripes sharing one GPU (streams / processes time-sharing its SMs) would hold SM slots the awaited
+    // neighbour needs (measured on one B200: 3 launches +1.7 / +3.3 / +6.0% vs fused +21 / +21 / +18% per MCS
+    // over the periodic engine at 2 / 4 / 8 stripes, tools/stripe_overhead.py).
+    if (e->fused_link < 0) e->fused_link = (prev->device != e->device || next->device != e->device) ? 1 : 0;
     return p2p_pull(e, true);  // halo rows with their streams; later passes advance those streams locally
 }
 
@@ -1848,20 +1867,59 @@ int octgpu_stripe_pull(octgpu_engine* e) {
     return p2p_pull(e, false);
 }
 
+namespace {
+// One fused 2-MCS stripe pass (constant xi or counter streams: no stream state crosses the stripe boundary).
+int stripe_pass_fused(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool ctr, uint64_t per_sweep, int ls) {
+    const Geom g = e->geom();
+    const int ps = e->pcur;
+    StripeLink lk{};
+    lk.prev = peer_view(e, e->prev);
+    lk.next = peer_view(e, e->next);
+    lk.need = e->passes;
+    lk.err = e->p2p_err;
+    lk.done = e->done;
+    lk.ticket = reinterpret_cast<uint32_t*>(e->done + 1);
+    lk.value = e->passes + 1;
+    lk.next_planes = reinterpret_cast<void*>(e->next.planes[ps ^ 1]);
+    lk.next_Y = e->next.alloc_rows;
+    lk.push_plane = 2 + e->phase;
+    lk.active = 1;
+    int rc = ensure_tmaps_deep(e);
+    if (rc) return rc;
+    if (ctr) {
+        CK(launch_mcs_deep_ctr(e->planes[ps], e->planes[ps ^ 1], e->phase, g, p, q, e->master_seed, 2 * e->t, ls,
+                               deep_ring(e, p, q, ls, true), &e->tmd[ps][0], &e->tmd[ps][1], e->stream, &lk));
+    } else {
+        CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[e->rcur], e->rng[e->rcur ^ 1], e->phase, g, p,
+                           q, nullptr, ls, deep_ring(e, p, q, ls), &e->tmd[ps][0], &e->tmd[ps][1], e->stream, &lk));
+        e->pending += uint64_t(ls) * per_sweep;
+    }
+    ++e->launches;
+    e->pcur ^= 1;
+    e->t += uint64_t(ls / 2);
+    ++e->passes;
+    return OCTGPU_OK;
+}
+}  // namespace
+
 int octgpu_stripe_pass(octgpu_engine* e, const octgpu_params* prm, uint32_t n_mcs) {
     if (!e || !e->stripe || !e->p2p) return fail(OCTGPU_ERR_CONFIG, "not a connected row stripe");
     ProbDev p, q;
     int rc = lower_params(prm, p, q);
     if (!rc) rc = use_device(e);
     if (rc) return rc;
-    const bool deep = n_mcs == uint32_t(kStripeSweeps / 2);
-    if (n_mcs != 1 && !(deep && stripe_deep_ok(e, p, q)))
-        return fail(OCTGPU_ERR_CONFIG, "a stripe pass covers 1 MCS, or " + std::to_string(kStripeSweeps / 2) +
-                                           " with constant xi (see octgpu_stripe_max_mcs)");
+    const int ls = stripe_pass_sweeps(e, p, q, n_mcs);
+    if (ls < 0)
+        return fail(OCTGPU_ERR_CONFIG, "a stripe pass covers 1 MCS, or up to octgpu_stripe_max_mcs() with constant "
+                                       "xi (2 or 3)");
+    const bool deep = ls > 0;
     const bool ctr = e->rng_kind == OCTGPU_RNG_COUNTER;
     const bool live = !ctr && !(is_const(p) && is_const(q));
     const uint64_t D = draws(prm->p, e->w) + (q.mode != M_ZERO ? draws(prm->q, e->w) : 0);
     const uint64_t per_sweep = uint64_t(e->n) * D;
+    // multi-MCS passes (k_mcs_deep) run as ONE launch with the halo exchange fused in (stripe_link.cuh);
+    // one-MCS passes: pull, kernel, push + signal (p2p.cu)
+    if (deep && e->fused_link == 1) return stripe_pass_fused(e, p, q, ctr, per_sweep, ls);
     // 1. wait for the neighbours' previous pass, pull their boundary rows
     rc = p2p_pull(e, false);
     if (rc) return rc;
@@ -1876,14 +1934,13 @@ int octgpu_stripe_pass(octgpu_engine* e, const octgpu_params* prm, uint32_t n_mc
     const Geom g = e->geom();
     const int ps = e->pcur, rs = e->rcur;
     if (ctr) {
-        rc = stripe_kernel_ctr(e, p, q, deep);
+        rc = stripe_kernel_ctr(e, p, q, ls);
         if (rc) return rc;
     } else if (deep) {
         rc = ensure_tmaps_deep(e);
         if (rc) return rc;
-        CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
-                           kStripeSweeps, deep_ring(e, p, q, kStripeSweeps), &e->tmd[ps][0], &e->tmd[ps][1],
-                           e->stream));
+        CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab, ls,
+                           deep_ring(e, p, q, ls), &e->tmd[ps][0], &e->tmd[ps][1], e->stream));
     } else {
         rc = plan_bulk(e, p, q);
         if (rc) return rc;

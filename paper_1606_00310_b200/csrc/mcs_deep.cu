@@ -34,6 +34,7 @@
 
 #include "device_common.cuh"
 #include "octgpu_internal.h"
+#include "stripe_link.cuh"
 
 namespace octgpu {
 
@@ -404,7 +405,7 @@ __global__ void __launch_bounds__(32 * kDP, kDeepMinBlocks)
     k_mcs_deep(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, const uint64_t* __restrict__ rs,
                uint64_t* __restrict__ rd, int f, Geom g, ProbDev p, ProbDev q, const uint64_t* __restrict__ jtab, int S,
                const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmK1, uint64_t ctr_seed,
-               uint64_t sigma0) {
+               uint64_t sigma0, const __grid_constant__ StripeLink lk) {
     static_assert(L % 2 == 0 && L >= 2, "whole MCS only");
     using GEO = DeepGeo<L>;
     using ST = DeepStage<L>;
@@ -427,6 +428,22 @@ __global__ void __launch_bounds__(32 * kDP, kDeepMinBlocks)
     // and the block is 8 warps: two blocks per SM leave 128 registers per thread. (The tensor maps are
     // passed by address straight from the __grid_constant__ parameters: a copy in local memory is not a
     // valid TMA descriptor.)
+    // a row stripe's fused halo exchange: this block's roles (block-uniform)
+    bool sig = false, push = false;
+    uint32_t nsig = 0;
+    if (lk.active) {
+        const uint32_t c0 = g.c0, c1 = g.c1, nb = gridDim.x;
+        auto core_lo = [&](uint32_t b) { return max(c0, c0 + b * uint32_t(GEO::kRows)); };
+        auto core_hi = [&](uint32_t b) { return min(c1, c0 + (b + 1) * uint32_t(GEO::kRows)); };  // exclusive
+        auto signals = [&](uint32_t b) {  // writes what the neighbours pull: the first HB / last HA core rows
+            return core_lo(b) < c0 + kStripeHB || core_hi(b) > c1 - kStripeHA;
+        };
+        for (uint32_t b = 0; b < nb; ++b) nsig += signals(b) ? 1u : 0u;
+        sig = signals(blockIdx.x);
+        push = core_hi(blockIdx.x) == c1;
+        const bool above = blk_r0 < kStripeHA, below = blk_r0 + uint32_t(kLanes) > c1;
+        if ((above || below) && !link_pull(lk, const_cast<uint64_t*>(src), g, above, below)) return;
+    }
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -549,6 +566,7 @@ __global__ void __launch_bounds__(32 * kDP, kDeepMinBlocks)
             if (c.ghost_row) store_state(rd, g.Y, y + g.wrap, fin);
         }
     }
+    if (sig) link_signal(lk, dst, g, push, nsig);
 }
 
 namespace {
@@ -556,15 +574,17 @@ namespace {
 template <int PM, int QM, int L, bool CTR = false>
 cudaError_t deep_go(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
                     const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK, const CUtensorMap* tmK1,
-                    cudaStream_t st, uint64_t ctr_seed = 0, uint64_t sigma0 = 0) {
+                    cudaStream_t st, uint64_t ctr_seed, uint64_t sigma0, const StripeLink* link) {
     using GEO = DeepGeo<L>;
     const uint32_t blocks = (g.c1 - g.c0 + GEO::kRows - 1) / GEO::kRows;
     const size_t smem = mcs_deep_smem(p.mode, q.mode, L, S, CTR);
     auto kern = k_mcs_deep<PM, QM, L, CTR>;
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
+    StripeLink lk{};
+    if (link) lk = *link;
     kern<<<blocks, 32 * kDP, smem, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), rs,
-                                               rd, f, g, p, q, jtab, S, *tmK, *tmK1, ctr_seed, sigma0);
+                                               rd, f, g, p, q, jtab, S, *tmK, *tmK1, ctr_seed, sigma0, lk);
     return cudaGetLastError();
 }
 
@@ -608,10 +628,13 @@ namespace {
 template <int PM, int QM, bool CTR>
 cudaError_t deep_l(int L, const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g,
                    const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK,
-                   const CUtensorMap* tmK1, cudaStream_t st, uint64_t seed, uint64_t sigma) {
-    if (L == 4) return deep_go<PM, QM, 4, CTR>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
+                   const CUtensorMap* tmK1, cudaStream_t st, uint64_t seed, uint64_t sigma,
+                   const StripeLink* link) {
+    if (L == 4)
+        return deep_go<PM, QM, 4, CTR>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma, link);
     if constexpr (const_mode(PM) && const_mode(QM)) {
-        if (L == 6) return deep_go<PM, QM, 6, CTR>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
+        if (L == 6)
+            return deep_go<PM, QM, 6, CTR>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma, link);
     }
     return cudaErrorInvalidValue;
 }
@@ -619,13 +642,14 @@ cudaError_t deep_l(int L, const void* src, void* dst, const uint64_t* rs, uint64
 template <int PM, bool CTR>
 cudaError_t deep_q(int L, const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g,
                    const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK,
-                   const CUtensorMap* tmK1, cudaStream_t st, uint64_t seed, uint64_t sigma) {
+                   const CUtensorMap* tmK1, cudaStream_t st, uint64_t seed, uint64_t sigma,
+                   const StripeLink* link) {
     switch (q.mode) {
-    case M_ZERO: return deep_l<PM, M_ZERO, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
-    case M_HALF: return deep_l<PM, M_HALF, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
+    case M_ZERO: return deep_l<PM, M_ZERO, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma, link);
+    case M_HALF: return deep_l<PM, M_HALF, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma, link);
     case M_DYADIC:
-        return deep_l<PM, M_DYADIC, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
-    case M_ONE: return deep_l<PM, M_ONE, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
+        return deep_l<PM, M_DYADIC, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma, link);
+    case M_ONE: return deep_l<PM, M_ONE, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma, link);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -633,13 +657,14 @@ cudaError_t deep_q(int L, const void* src, void* dst, const uint64_t* rs, uint64
 template <bool CTR>
 cudaError_t deep_p(int L, const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g,
                    const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK,
-                   const CUtensorMap* tmK1, cudaStream_t st, uint64_t seed, uint64_t sigma) {
+                   const CUtensorMap* tmK1, cudaStream_t st, uint64_t seed, uint64_t sigma,
+                   const StripeLink* link) {
     if (S < 2 || S > kSMax || !mcs_deep_supported_l(p.mode, q.mode, L, CTR)) return cudaErrorInvalidValue;
     switch (p.mode) {
-    case M_ZERO: return deep_q<M_ZERO, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
-    case M_HALF: return deep_q<M_HALF, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
-    case M_DYADIC: return deep_q<M_DYADIC, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
-    case M_ONE: return deep_q<M_ONE, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma);
+    case M_ZERO: return deep_q<M_ZERO, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma, link);
+    case M_HALF: return deep_q<M_HALF, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma, link);
+    case M_DYADIC: return deep_q<M_DYADIC, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma, link);
+    case M_ONE: return deep_q<M_ONE, CTR>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma, link);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -648,15 +673,15 @@ cudaError_t deep_p(int L, const void* src, void* dst, const uint64_t* rs, uint64
 
 cudaError_t launch_mcs_deep(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g,
                             const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int L, int S,
-                            const CUtensorMap* tmK, const CUtensorMap* tmK1, cudaStream_t st) {
-    return deep_p<false>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, 0, 0);
+                            const CUtensorMap* tmK, const CUtensorMap* tmK1, cudaStream_t st, const StripeLink* link) {
+    return deep_p<false>(L, src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, 0, 0, link);
 }
 
 // counter-based streams (octgpu_set_rng): sweeps sigma .. sigma + L - 1 of seed's streams
 cudaError_t launch_mcs_deep_ctr(const void* src, void* dst, int f, Geom g, const ProbDev& p, const ProbDev& q,
                                 uint64_t seed, uint64_t sigma, int L, int S, const CUtensorMap* tmK,
-                                const CUtensorMap* tmK1, cudaStream_t st) {
-    return deep_p<true>(L, src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, seed, sigma);
+                                const CUtensorMap* tmK1, cudaStream_t st, const StripeLink* link) {
+    return deep_p<true>(L, src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, seed, sigma, link);
 }
 
 }  // namespace octgpu

@@ -78,19 +78,18 @@ static_assert(kDeepLanes <= 256, "a TMA box dimension holds at most 256 rows");
 #define OCTGPU_DEEP_MINB 2
 #endif
 constexpr int kDeepMinBlocks = OCTGPU_DEEP_MINB;  // resident blocks per SM the register budget targets
-// sweeps per k_mcs_deep pass (even): 6 (3 MCS) for constant xi on periodic lattices, 4 (2 MCS) for live
-// streams and for row stripes (whose halo rows are sized for 4)
+// sweeps per k_mcs_deep pass (even): 6 (3 MCS) for constant xi, 4 (2 MCS) for live streams
 constexpr int kDeepSweepsConst = 6;
 constexpr int kDeepSweepsLive = 4;
-constexpr int kStripeSweeps = 4;
+constexpr int kStripeSweeps = kDeepSweepsConst;  // the longest stripe pass (its halo rows are sized for it)
 constexpr int deep_box_rows() { return kDeepLanes; }
 constexpr int deep_core_rows(int L) { return kDeepLanes - 2 * L; }  // even: block windows start 16-B aligned
 
 constexpr int kGraphPasses = 16;  // passes per CUDA graph replayed by octgpu_step (even)
 
 // Row stripes: halo rows above / below the core rows (local rows 0..HA-1 and
-// HA+L..HA+L+HB-1): enough for k_mcs_deep's 2-MCS pass (3 rows of shrinking
-// lanes each side + stage 1's Y(s)[y+1]); the one-MCS kernels use 1 / 2 of them.
+// HA+L..HA+L+HB-1): enough for k_mcs_deep's 3-MCS pass (5 rows of shrinking
+// lanes each side + stage 1's Y(s)[y+1]); shorter passes use fewer of them.
 constexpr uint32_t kStripeHA = uint32_t(kStripeSweeps) - 1;
 constexpr uint32_t kStripeHB = uint32_t(kStripeSweeps);
 
@@ -100,6 +99,8 @@ constexpr uint32_t kGhostRows = 320;
 static_assert(kTmaBoxRows <= kGhostRows && uint32_t(deep_box_rows()) + 64 <= kGhostRows, "ghost rows");
 
 // Per-row RNG states are stored SoA: s[j * Y + y], j = 0..3.
+
+struct StripeLink;  // below
 
 // ---- launchers (return the launch error, never synchronise) ----
 // host layout [4][rows][n] (compact) <-> device rows 0..rows-1 of each plane
@@ -145,12 +146,14 @@ bool mcs_deep_supported(int p_mode, int q_mode);
 bool mcs_deep_supported_l(int p_mode, int q_mode, int L, bool ctr);
 size_t mcs_deep_smem(int p_mode, int q_mode, int L, int S, bool ctr = false);  // S ring stages
 // k_mcs_deep with counter-based xi: sweeps sigma .. sigma + L - 1 of seed's streams (octgpu_set_rng)
+// link: a row stripe's halo exchange fused into the pass (nullptr: none)
 cudaError_t launch_mcs_deep_ctr(const void* src, void* dst, int f, Geom g, const ProbDev& p, const ProbDev& q,
                                 uint64_t seed, uint64_t sigma, int L, int S, const CUtensorMap* tmK,
-                                const CUtensorMap* tmK1, cudaStream_t st);
+                                const CUtensorMap* tmK1, cudaStream_t st, const StripeLink* link = nullptr);
 cudaError_t launch_mcs_deep(const void* src, void* dst, const uint64_t* rng_src, uint64_t* rng_dst, int f, Geom g,
                             const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int L, int S,
-                            const CUtensorMap* tmK, const CUtensorMap* tmK1, cudaStream_t st);
+                            const CUtensorMap* tmK, const CUtensorMap* tmK1, cudaStream_t st,
+                            const StripeLink* link = nullptr);
 
 // s <- M s for every row state, M given as a 4-bit table (64 x 16 x 4 u64).
 cudaError_t launch_apply_jump(uint64_t* rng, uint32_t Y, const uint64_t* tab, cudaStream_t st);
@@ -183,6 +186,23 @@ struct PeerView {
     uint32_t Y;  // allocated rows (row stride)
     uint32_t L;  // core rows
     long long timeout;  // wait limit in SM clock cycles (the prev view's value is used)
+};
+// A stripe pass fused with its halo exchange (one launch; csrc/stripe_link.cuh): the blocks whose TMA window
+// covers halo rows wait for the neighbour(s) to report done >= need and copy their boundary core rows into the
+// local halo rows of the source set before their first TMA load; the blocks that write the boundary core rows
+// (and the one that completes Y(f) of the first halo row below, which it also pushes into the next stripe's new
+// set) publish done = value through a ticket once all of them are finished. active = 0: a periodic lattice.
+struct StripeLink {
+    PeerView prev, next;
+    uint64_t need;          // neighbours' passes done before ours may read their rows
+    uint32_t* err;          // wait timeout flag
+    uint64_t* done;         // ours: passes completed (read by the neighbours)
+    uint32_t* ticket;       // ours: signalling blocks finished in this pass
+    uint64_t value;         // done after this pass
+    void* next_planes;      // the next stripe's NEW plane set (the push target)
+    uint32_t next_Y;        // its allocated rows
+    int push_plane;         // Y(f) = 2 + f
+    int active;
 };
 constexpr long long kP2PTimeoutCycles = 20'000'000'000ll;  // default ~10 s at 2 GHz: a dead neighbour is an error, not a hang
 // wait for prev.done >= need && next.done >= need, then copy the neighbours' boundary core rows (+ states)

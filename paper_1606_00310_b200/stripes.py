@@ -2,18 +2,18 @@
 
 Partition: contiguous row blocks exactly as the reference's SweepPlan
 (params.hpp:107-127; the result is partition-independent, like the
-reference's worker count). Per pass of k MCS (k = 2 for constant-xi
-parameters: the temporally blocked kernel; else 1), stripe r (rows [y0, y1),
-at least 4):
+reference's worker count). Per pass of k MCS (k = 3 for constant-xi
+parameters: the temporally blocked kernel, 2 for a remainder of 2; else 1),
+stripe r (rows [y0, y1), at least 6):
 
-  1. pack      rows y0..y0+3 (+ rng states) -> to_prev; rows y1-3..y1-1 (+ states) -> to_next
+  1. pack      rows y0..y0+5 (+ rng states) -> to_prev; rows y1-5..y1-1 (+ states) -> to_next
   2. exchange  shift-up   (to_prev -> rank r-1, from_next <- rank r+1)
                shift-down (to_next -> rank r+1, from_prev <- rank r-1)
-  3. unpack    halo rows y0-3..y0-1 (from_prev) and y1..y1+3 (from_next)
+  3. unpack    halo rows y0-5..y0-1 (from_prev) and y1..y1+5 (from_next)
   4. mcs       k fused MCS over the stripe's rows (k_mcs_deep / k_mcs_bulk)
   5. boundary  y-plane f of row y1 -> rank r+1, which completes its row y0 (finish)
 
-The halo traffic is 7 x 4 plane-rows + one plane-row per stripe boundary
+The halo traffic is 11 x 4 plane-rows + one plane-row per stripe boundary
 per pass (X/16 bytes per plane-row), independent of the stripe height. Measurement: every stripe reduces its own rows in a local height
 gauge; the exact int128 power sums are shifted binomially by the column-0
 prefix of the stripes above and summed (``combine``).
@@ -23,12 +23,13 @@ stripes on one GPU — used to prove bit-exactness on one device) and
 ``DistTransport`` (one stripe per rank over torch.distributed: NCCL on GPUs,
 gloo on CPU for the protocol tests) run steps 1-5 from the host.
 ``PeerLocalTransport`` / ``PeerDistTransport`` replace them with the
-device-side exchange over peer memory (csrc/p2p.cu): each pass is one halo
-pull kernel that reads the neighbours' rows over NVLink (waiting on their
-"passes done" counters), the MCS kernel, and one kernel that writes the
-boundary plane-row into the next stripe and publishes the pass — no NCCL, no
-host synchronisation between passes. Peers are mapped with CUDA IPC across
-processes.
+device-side exchange over peer memory (csrc/p2p.cu, csrc/stripe_link.cuh): a
+multi-MCS pass between stripes on different GPUs is ONE kernel whose boundary
+blocks wait on the neighbours' "passes done" counters, read their rows over
+NVLink, and publish the pass; otherwise a pass is a halo pull kernel, the MCS
+kernel, and one kernel that writes the boundary plane-row into the next stripe
+and publishes the pass — no NCCL, no host synchronisation between passes. Peers
+are mapped with CUDA IPC across processes.
 """
 from __future__ import annotations
 

@@ -53,7 +53,7 @@ def _worker(rank, world, port, X, Y, seed, pq, mcs, out):
 @pytest.mark.parametrize("world,X,Y,pq,mcs", [
     (2, 256, 34, (0.5, 0.0), 6),
     (3, 384, 40, (0.75, 0.25), 5),
-    (2, 128, 8, (0.98, 0.02), 3),
+    (2, 128, 12, (0.98, 0.02), 3),
     (2, 256, 66, (1.0, 0.0), 4),
 ])
 def test_stripes_over_gloo_match_single_lattice(oracle, world, X, Y, pq, mcs):

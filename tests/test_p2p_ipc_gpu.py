@@ -27,13 +27,14 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, X, Y, seed, pq, mcs, out):
+def _worker(rank, world, port, X, Y, seed, pq, mcs, out, fused="1"):
     import sys
     if ROOT not in sys.path:
         sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    os.environ["OCTGPU_DEEP"] = "2"  # 2-MCS passes at test sizes (constant xi)
+    os.environ["OCTGPU_DEEP"] = "2"  # multi-MCS passes at test sizes (constant xi)
+    os.environ["OCTGPU_FUSED_LINK"] = fused  # the one-launch passes of separate GPUs, or the three launches
     import torch
     import torch.distributed as dist
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -59,13 +60,14 @@ def _worker(rank, world, port, X, Y, seed, pq, mcs, out):
 
 @pytest.mark.parametrize("world,X,Y,pq,mcs", [(2, 2048, 256, (1.0, 0.0), 7), (2, 1024, 200, (0.5, 0.0), 5),
                                               (3, 1024, 300, (0.75, 0.25), 4)])
-def test_peer_exchange_across_processes(world, X, Y, pq, mcs):
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_peer_exchange_across_processes(world, X, Y, pq, mcs, fused):
     import paper_1606_00310_b200 as octgpu
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, X, Y, 13, pq, mcs, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, X, Y, 13, pq, mcs, q, fused)) for r in range(world)]
     for p in procs:
         p.start()
     deadline = time.time() + 240

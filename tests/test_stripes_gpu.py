@@ -37,14 +37,17 @@ def _group(cfg, parts, seed, stream, transport="host"):
     return StripeGroup(LocalTransport(engines, alloc), cfg.X, cfg.Y), engines
 
 
-# (1024, 32, 8): 4-row stripes, the minimum (the 2-MCS pass reads 4 rows of the next stripe)
+# (1024, 48, 8): 6-row stripes, the minimum (the 3-MCS pass reads 6 rows of the next stripe)
 @pytest.mark.parametrize("X,Y,parts", [(1024, 128, 2), (1024, 130, 4), (2048, 96, 3), (256, 40, 2), (8192, 512, 8),
-                                       (1024, 32, 8)])
+                                       (1024, 48, 8)])
 @pytest.mark.parametrize("pq", [(0.5, 0.0), (0.98, 0.02), (1.0, 0.0), (0.75, 0.5), (0.0, 0.0)])
-@pytest.mark.parametrize("transport", ["host", "peer", "peer-streams"])
-def test_stripes_match_single_engine(X, Y, parts, pq, transport):
+@pytest.mark.parametrize("transport", ["host", "peer", "peer-streams", "peer-fused"])
+def test_stripes_match_single_engine(X, Y, parts, pq, transport, monkeypatch):
     if transport.startswith("peer") and X < 1024:
         pytest.skip("the peer-memory exchange runs the TMA kernels (X >= 1024)")
+    if transport == "peer-fused":  # the one-launch passes (default only when neighbours are on other GPUs)
+        monkeypatch.setenv("OCTGPU_FUSED_LINK", "1")
+        transport = "peer-streams"
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         cfg = octgpu.LatticeConfig(X, Y)
@@ -66,12 +69,15 @@ def test_stripes_match_single_engine(X, Y, parts, pq, transport):
         assert abs(rec.W2 - rref.W2) <= 2 ** -50 * rref.W2
 
 
-@pytest.mark.parametrize("X,Y,parts", [(1024, 128, 2), (1024, 130, 4), (2048, 96, 3), (8192, 512, 8), (1024, 32, 8)])
+@pytest.mark.parametrize("X,Y,parts", [(1024, 128, 2), (1024, 130, 4), (2048, 96, 3), (8192, 512, 8), (1024, 48, 8)])
 @pytest.mark.parametrize("pq", [(0.5, 0.0), (0.5, 0.5), (0.98, 0.02), (1.0, 0.0), (0.75, 0.25)])
-@pytest.mark.parametrize("transport", ["host", "peer"])
-def test_counter_rng_stripes_match_single_engine(X, Y, parts, pq, transport):
+@pytest.mark.parametrize("transport", ["host", "peer", "peer-fused"])
+def test_counter_rng_stripes_match_single_engine(X, Y, parts, pq, transport, monkeypatch):
     """Opt-in counter streams on row stripes (k_mcs_bulk<CTR> / k_mcs_deep<CTR> with local -> global rows):
     the striped run equals the periodic engine's (itself pinned to the oracle's oo_step_ctr)."""
+    if transport == "peer-fused":
+        monkeypatch.setenv("OCTGPU_FUSED_LINK", "1")
+        transport = "peer"
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         cfg = octgpu.LatticeConfig(X, Y)
@@ -128,12 +134,13 @@ def test_stripe_curl_violation_reported_globally():
 def test_stripe_pass_sizes():
     cfg = octgpu.LatticeConfig(1024, 64)
     e = StripeEngine(cfg, 0, 32, 3)
-    assert e.max_mcs(octgpu.UpdateParams.make(1.0, 0.0)) == 2  # constant xi: 2-MCS passes (k_mcs_deep)
+    assert e.max_mcs(octgpu.UpdateParams.make(1.0, 0.0)) == 3  # constant xi: 3-MCS passes (k_mcs_deep)
     assert e.max_mcs(octgpu.UpdateParams.make(0.5, 0.0)) == 1
+    assert e.pass_plan(octgpu.UpdateParams.make(1.0, 0.0)) == ("k_mcs_deep", 3.0)
     with pytest.raises(octgpu.ConfigError):
         e.mcs(octgpu.UpdateParams.make(0.5, 0.0), torch.zeros(e.boundary_bytes, dtype=torch.uint8, device="cuda"), 2)
     with pytest.raises(octgpu.ConfigError):
-        StripeEngine(cfg, 0, 3, 3)  # fewer rows than the halo a pass reads
+        StripeEngine(cfg, 0, 5, 3)  # fewer rows than the halo a pass reads (6)
 
 
 @pytest.mark.parametrize("transport", ["host", "peer-streams"])

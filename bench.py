@@ -316,7 +316,11 @@ def main():
         if one_gpu:
             dist.init_process_group("gloo")
         else:
+            # NCCL's communicator lines (ranks, devices, NVLink / NVLS paths) on stderr, for the run record
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
+            torch.distributed.barrier()  # create the communicator now (eagerly, so it is logged up front)
     stream = torch.cuda.Stream(dev)  # a real (non-default) stream shared by the engine and the timing events
     torch.cuda.set_stream(stream)
 

@@ -13,3 +13,6 @@ for c in c4; do timeout 400 ncu --set full --clock-control none --import-source 
 timeout 300 ncu --set full --clock-control none -k regex:k_measure_rows -c 1 -o gpurun_out/${TAG}_meas python bench.py --config c2 --steps 2 --warmup 3 --from-flat --no-cpu-baseline --no-e2e > /dev/null 2>&1; python tools/ncu_extract.py gpurun_out/${TAG}_meas.ncu-rep gpurun_out/${TAG}_ncu_k_measure_rows_c2.json --label "k_measure_rows c2 $TAG"
 ncu -i gpurun_out/${TAG}_deep_c2.ncu-rep --page source --csv > gpurun_out/${TAG}_deep_c2_source.csv 2>/dev/null
 rm -f gpurun_out/*.ncu-rep
+# the driver's own command line (K = 20, W = 5) and its reference arm
+timeout 600 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/${TAG}_bench_k20.json 2> gpurun_out/${TAG}_bench_k20.err; python -c "import json; d=json.load(open('gpurun_out/${TAG}_bench_k20.json')); print('k20', round(d['value']), round(d['ms_per_step'],4), round(d['e2e']['value']))"
+timeout 600 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > gpurun_out/${TAG}_bench_reference_k20.json 2>&1; tail -c 300 gpurun_out/${TAG}_bench_reference_k20.json

@@ -408,9 +408,17 @@ class PeerDistTransport:
         self.dist.barrier()
 
     def gather(self, parts: list[StripeMoments]) -> list[StripeMoments]:
-        out = [None] * self.size
-        self.dist.all_gather_object(out, parts[0].to_array().tolist())
-        return [StripeMoments.from_array(np.array(o, np.int64)) for o in out]
+        """One fixed-size all_gather of the 16-word moment records (device tensors on NCCL, host tensors on gloo;
+        no pickling: this sits inside every timed W^2 point of a multi-GPU run)."""
+        import torch
+
+        mine = torch.from_numpy(parts[0].to_array())
+        if self.dist.get_backend() == "nccl":
+            mine = mine.to(torch.device("cuda", torch.cuda.current_device()))
+        out = torch.empty(self.size * mine.numel(), dtype=mine.dtype, device=mine.device)
+        self.dist.all_gather_into_tensor(out, mine)
+        host = out.cpu().numpy().reshape(self.size, -1)
+        return [StripeMoments.from_array(host[r]) for r in range(self.size)]
 
 
 class StripeGroup:

@@ -448,6 +448,25 @@ cudaError_t launch_export(int w, const void* planes, void* out, Geom g, uint32_t
                    : transpose_w<uint32_t, false>(planes, out, g, rows, st);
 }
 
+// rows 0..ghost-1 -> rows wrap..wrap+ghost-1 of every (plane, word) column (word-major: a column's rows are
+// contiguous), 16 B per thread; requires ghost <= wrap and 16-B aligned columns (Y even, ghost even)
+__global__ void k_ghost_copy(uint64_t* __restrict__ planes, uint32_t Y, uint32_t wrap, uint32_t ghost, uint32_t cols) {
+    const uint32_t per = ghost / 2, total = per * cols;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const uint32_t c = i / per, r = (i - c * per) * 2;
+        uint64_t* col = planes + size_t(c) * Y;
+        *reinterpret_cast<ulonglong2*>(col + wrap + r) = *reinterpret_cast<const ulonglong2*>(col + r);
+    }
+}
+
+cudaError_t launch_ghost_copy(void* planes, uint32_t Y, uint32_t wrap, uint32_t ghost, uint32_t cols,
+                              cudaStream_t st) {
+    const uint32_t total = ghost / 2 * cols;
+    const uint32_t blocks = std::min<uint32_t>(1184, (total + 255) / 256);
+    k_ghost_copy<<<blocks, 256, 0, st>>>(static_cast<uint64_t*>(planes), Y, wrap, ghost, cols);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_refresh_ghosts(int w, void* planes, uint64_t* rng, Geom g, cudaStream_t st) {
     if (!g.ghost) return cudaSuccess;
     const uint32_t blocks = std::min<uint32_t>(256, (4 * g.ghost * g.n + 255) / 256);

@@ -106,6 +106,9 @@ struct StripeLink;  // below
 // host layout [4][rows][n] (compact) <-> device rows 0..rows-1 of each plane
 cudaError_t launch_import(int w, const void* host_layout_dev, void* planes, Geom g, uint32_t rows, cudaStream_t st);
 cudaError_t launch_export(int w, const void* planes, void* host_layout_dev, Geom g, uint32_t rows, cudaStream_t st);
+// w = 64 planes: rows 0..ghost-1 -> wrap..wrap+ghost-1 of each of the `cols` (plane, word) columns of Y rows
+cudaError_t launch_ghost_copy(void* planes, uint32_t Y, uint32_t wrap, uint32_t ghost, uint32_t cols,
+                              cudaStream_t st);
 // periodic lattices: rewrite the ghost rows (planes, and rng when non-null) from rows 0..ghost-1
 cudaError_t launch_refresh_ghosts(int w, void* planes, uint64_t* rng, Geom g, cudaStream_t st);
 

@@ -32,13 +32,14 @@ def _digest(oracle, states):
     return oracle.states_digest(np.ascontiguousarray(states, np.uint64))
 
 
-# (name, X, Y, p, q, MCS, expected passes): BASELINE configs 2' (p = 1/2, the paper's case), 3, 4, 2 and 5
+# (name, X, Y, p, q, MCS, expected kernel launches): BASELINE configs 2' (p = 1/2, the paper's case), 3, 4, 2
+# and 5; every k_mcs_deep pass is followed by the ghost-row copy kernel
 CASES = [
-    ("c2h", 1 << 16, 1 << 16, 0.5, 0.0, 20, 10),   # k_mcs_deep, live xoshiro (one draw per word)
-    ("c3", 1 << 16, 1 << 16, 0.5, 0.5, 10, 5),     # k_mcs_deep, live xoshiro (two half draws per word)
+    ("c2h", 1 << 16, 1 << 16, 0.5, 0.0, 20, 20),   # k_mcs_deep x 10, live xoshiro (one draw per word)
+    ("c3", 1 << 16, 1 << 16, 0.5, 0.5, 10, 10),    # k_mcs_deep x 5, live xoshiro (two half draws per word)
     ("c4", 1 << 16, 1 << 16, 0.98, 0.02, 2, 2),    # k_mcs_bulk, arbitrary (128 draws per word)
-    ("c2", 1 << 16, 1 << 16, 1.0, 0.0, 20, 7),     # k_mcs_deep, constant xi: 6 x 3 MCS + 1 x 2 MCS (lazy draws)
-    ("c5h", 1 << 17, 1 << 17, 0.5, 0.0, 4, 2),     # k_mcs_deep at 2^34 sites
+    ("c2", 1 << 16, 1 << 16, 1.0, 0.0, 20, 14),    # k_mcs_deep, constant xi: 6 x 3 MCS + 1 x 2 MCS (lazy draws)
+    ("c5h", 1 << 17, 1 << 17, 0.5, 0.0, 4, 4),     # k_mcs_deep x 2 at 2^34 sites
 ]
 
 

@@ -341,7 +341,7 @@ struct octgpu_engine {
     int deep = 1;  // temporally blocked passes (k_mcs_deep) where supported; OCTGPU_DEEP=0 disables
     // multi-MCS peer-memory stripe passes fused with their halo exchange: -1 = when a neighbour is on another
     // device (decided at connect), 0 / 1 = OCTGPU_FUSED_LINK
-    int fused_link = -1;
+    int fused_link = -1, fused_link_env = -1;
     bool ghost_kernel = true;  // deep passes' ghost-row mirror: a copy kernel (OCTGPU_GHOST=memcpy: cudaMemcpy2DAsync)
     int deep_l = kDeepSweepsConst;  // sweeps of a constant-xi deep pass (OCTGPU_DEEP_L = 4 keeps 2 MCS per pass)
     bool graphs = true;  // replay CUDA graphs for long step() calls (OCTGPU_GRAPH=0 disables)
@@ -478,7 +478,7 @@ int plan_mcs(octgpu_engine* e) {
     if (const char* v = getenv("OCTGPU_P2P_TIMEOUT_MS")) e->p2p_timeout = std::max(1LL, atoll(v)) * 2'000'000LL;
     if (const char* v = getenv("OCTGPU_PREFETCH")) e->prefetch = uint32_t(std::max(0, std::min(64, atoi(v))));
     if (const char* v = getenv("OCTGPU_DEEP_S")) e->deep_S = std::max(2, std::min(8, atoi(v)));
-    if (const char* v = getenv("OCTGPU_FUSED_LINK")) e->fused_link = atoi(v) != 0 ? 1 : 0;
+    if (const char* v = getenv("OCTGPU_FUSED_LINK")) e->fused_link = e->fused_link_env = atoi(v) != 0 ? 1 : 0;
     if (const char* v = getenv("OCTGPU_GHOST")) e->ghost_kernel = std::string(v) != "memcpy";
     if (const char* v = getenv("OCTGPU_DEEP_L")) e->deep_l = atoi(v) == kDeepSweepsLive ? kDeepSweepsLive : kDeepSweepsConst;
     return OCTGPU_OK;
@@ -1864,6 +1864,7 @@ int octgpu_stripe_disconnect(octgpu_engine* e) {
     e->ipc_opened.clear();
     e->p2p = false;
     e->prev = e->next = octgpu_peer{};
+    e->fused_link = e->fused_link_env;  // decided again at the next connect
     return OCTGPU_OK;
 }
 

@@ -540,11 +540,15 @@ def main():
             cpu = {"value": None, "unit": "updates/ns", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {ex}"}
 
-    def dram(kn: str, cname: str, lms: float):
-        """ncu DRAM bytes per launch (profiles/ncu_summary.json) over this run's event time per launch."""
+    def dram(kn: str, cname: str, lms: float, sites: int | None = None):
+        """ncu DRAM bytes per launch (profiles/ncu_summary.json, captured on one GPU on the config's whole lattice)
+        over this run's event time per launch; `sites` = this GPU's sites when it holds a stripe (the traffic
+        scales with the rows a launch processes: strong-scaled c5 stripes are 1/N of the profiled lattice)."""
         tr = _traffic(kn, cname)
         if not tr:
             return None, None, tr
+        if sites is not None:
+            tr = tr * sites / (CONFIGS[cname]["X"] * CONFIGS[cname]["Y"])
         gbs = tr / (lms * 1e-3) / 1e9
         return gbs, gbs / peak, tr
 
@@ -600,10 +604,13 @@ def main():
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": "u64", "data": "synthetic (flat start h=(x+y) mod 2, seed 1)", "config": config_key,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": _traffic(kname, args.config), "kernel": f"{kname} ({mcs_per_launch} MCS per launch)",
+                         "traffic": dram(kname, args.config, launch_ms, X * Y // ws)[2],
+                         "kernel": f"{kname} ({mcs_per_launch} MCS per launch)",
                          "alg_bytes_per_launch": alg_bytes, "launch_ms": launch_ms, "kernel_ms": kernel_ms,
-                         "peak_source": peak_src, "dram_gbs": dram(kname, args.config, launch_ms)[0],
-                         "dram_frac": dram(kname, args.config, launch_ms)[1],
+                         "peak_source": peak_src, "dram_gbs": dram(kname, args.config, launch_ms, X * Y // ws)[0],
+                         "dram_frac": dram(kname, args.config, launch_ms, X * Y // ws)[1],
+                         "dram_per_gpu": "traffic and dram_frac are per GPU (its stripe's share of the profiled "
+                                         "launch) when n_gpus > 1",
                          "note": "alg bytes = 1 B/site-update (2 slope bits x 2 reads + 2 writes per MCS); the fused "
                                  "kernels move ~0.5 B (k_mcs_bulk) / ~0.25 or ~0.17 B (k_mcs_deep, 2 or 3 MCS) of DRAM traffic per update, "
                                  "so frac exceeds 1; traffic = ncu dram bytes per launch (profiles/ncu_summary.json)"},

@@ -450,23 +450,33 @@ def main():
     final_checksum = engs[0].checksum() if ws == 1 else None
     # Correctness digest of the timed job (every N): the exact global power sums S_k = sum h^k at the
     # window's last W^2 point and each stripe's field_checksum (its own rows as a field; N = 1: the
-    # lattice's). Weak-scaled c2 from the flat start with p = 1 is deterministic and invariant under even
-    # row shifts, so every 2^16-row stripe at N GPUs must equal the N = 1 lattice (stripe checksum = the N = 1
-    # final_checksum) and S_k(N) = N * S_k(1).
+    # lattice's), with the exactly known expected values for p = 1 (below: `expected`, `verified`).
     job.sync()
     rec = records[-1] if records else job.measure()
-    mine = engs[0].checksum()
+    mine = final_checksum if final_checksum is not None else engs[0].checksum()
     allc = [hex(mine)]
     if ws > 1:
         allc = [None] * ws
         torch.distributed.all_gather_object(allc, hex(mine))
     digest = {"t": rec.t, "power_sums": [str(v) for v in rec.power_sums], "W2": rec.W2, "mean_h": rec.mean_h,
               "stripe_checksums": allc}
-    if ws > 1 and scaling == "weak" and cfg["p"] == 1.0 and cfg["q"] == 0.0:
-        digest["expected"] = ("p=1 from the flat start: every stripe checksum equals the N=1 c2 final_checksum; "
-                              "power_sums equal N x the N=1 power_sums")
     _close(job)
     del job, engs
+    if cfg["p"] == 1.0 and cfg["q"] == 0.0 and Y % ws == 0:
+        # p = 1 from the flat start is flat again after every MCS: the expected state is known
+        # exactly -- every GPU's rows are a flat X x Y/N field at the same t (its checksum, untimed) and the
+        # lattice's sums are the flat ones (heights (x + y) mod 2: S_k = the sites at height 1 = X Y / 2, every k)
+        rows = Y // ws
+        flat_planes = np.zeros((4, rows, X // 128), np.uint64)  # new_flat (slope_field.hpp:110-118)
+        flat_planes[1] = flat_planes[3] = np.iinfo(np.uint64).max
+        flat = octgpu.GpuEngine(octgpu.SlopeField(octgpu.LatticeConfig(X, rows, 64), flat_planes, t_start + K, 0),
+                                octgpu.RngStreamSet.derive(1, rows), device=local)
+        exp_sum = hex(flat.checksum())
+        del flat, flat_planes
+        exp_ps = [str(X * Y // 2)] * 4
+        digest["expected"] = {"power_sums": exp_ps, "stripe_checksum": exp_sum,
+                              "rule": "p=1 from the flat start: flat after every MCS"}
+        digest["verified"] = digest["power_sums"] == exp_ps and all(c == exp_sum for c in digest["stripe_checksums"])
 
     # ---- e2e through the C-ABI with host buffers ----
     e2e = None

@@ -1877,9 +1877,10 @@ int octgpu_stripe_pull(octgpu_engine* e) {
 
 namespace {
 // One fused 2-MCS stripe pass (constant xi or counter streams: no stream state crosses the stripe boundary).
-int stripe_pass_fused(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool ctr, uint64_t per_sweep, int ls) {
+int stripe_pass_fused(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool ctr, bool live,
+                      uint64_t per_sweep, int ls) {
     const Geom g = e->geom();
-    const int ps = e->pcur;
+    const int ps = e->pcur, rs = e->rcur;
     StripeLink lk{};
     lk.prev = peer_view(e, e->prev);
     lk.next = peer_view(e, e->next);
@@ -1892,19 +1893,41 @@ int stripe_pass_fused(octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool
     lk.next_Y = e->next.alloc_rows;
     lk.push_plane = 2 + e->phase;
     lk.active = 1;
-    int rc = ensure_tmaps_deep(e);
-    if (rc) return rc;
-    if (ctr) {
-        CK(launch_mcs_deep_ctr(e->planes[ps], e->planes[ps ^ 1], e->phase, g, p, q, e->master_seed, 2 * e->t, ls,
-                               deep_ring(e, p, q, ls, true), &e->tmd[ps][0], &e->tmd[ps][1], e->stream, &lk));
-    } else {
-        CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[e->rcur], e->rng[e->rcur ^ 1], e->phase, g, p,
-                           q, nullptr, ls, deep_ring(e, p, q, ls), &e->tmd[ps][0], &e->tmd[ps][1], e->stream, &lk));
-        e->pending += uint64_t(ls) * per_sweep;
+    uint64_t* jtab = nullptr;
+    if (live) {  // lazy stream advance: no neighbour reads our states after connect
+        int rc = materialize(e);
+        if (!rc) rc = get_table(e, per_sweep, &jtab);
+        if (rc) return rc;
     }
+    if (ls > 0) {  // k_mcs_deep, 2 or 3 MCS
+        int rc = ensure_tmaps_deep(e);
+        if (rc) return rc;
+        if (ctr)
+            CK(launch_mcs_deep_ctr(e->planes[ps], e->planes[ps ^ 1], e->phase, g, p, q, e->master_seed, 2 * e->t, ls,
+                                   deep_ring(e, p, q, ls, true), &e->tmd[ps][0], &e->tmd[ps][1], e->stream, &lk));
+        else
+            CK(launch_mcs_deep(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q,
+                               nullptr, ls, deep_ring(e, p, q, ls), &e->tmd[ps][0], &e->tmd[ps][1], e->stream, &lk));
+    } else {  // k_mcs_bulk, one MCS
+        int rc = plan_bulk(e, p, q);
+        if (rc) return rc;
+        if (ctr) {
+            if (e->bulk_ks != 2) return fail(OCTGPU_ERR_CONFIG, "the counter-based rng needs OCTGPU_MCS_KS=2");
+            CK(launch_mcs_bulk_ctr(e->planes[ps], e->planes[ps ^ 1], e->phase, g, p, q, e->master_seed, 2 * e->t,
+                                   e->bulk_S, &e->tm[ps][0], &e->tm[ps][1], e->stream, &lk));
+        } else {
+            CK(launch_mcs_bulk(e->planes[ps], e->planes[ps ^ 1], e->rng[rs], e->rng[rs ^ 1], e->phase, g, p, q, jtab,
+                               e->bulk_ks, e->bulk_S, &e->tm[ps][0], &e->tm[ps][1], e->stream, &lk));
+        }
+    }
+    const uint64_t mcs = ls > 0 ? uint64_t(ls / 2) : 1;
     ++e->launches;
     e->pcur ^= 1;
-    e->t += uint64_t(ls / 2);
+    if (live)
+        e->rcur ^= 1;
+    else if (!ctr)
+        e->pending += 2 * mcs * per_sweep;
+    e->t += mcs;
     ++e->passes;
     return OCTGPU_OK;
 }
@@ -1925,9 +1948,9 @@ int octgpu_stripe_pass(octgpu_engine* e, const octgpu_params* prm, uint32_t n_mc
     const bool live = !ctr && !(is_const(p) && is_const(q));
     const uint64_t D = draws(prm->p, e->w) + (q.mode != M_ZERO ? draws(prm->q, e->w) : 0);
     const uint64_t per_sweep = uint64_t(e->n) * D;
-    // multi-MCS passes (k_mcs_deep) run as ONE launch with the halo exchange fused in (stripe_link.cuh);
-    // one-MCS passes: pull, kernel, push + signal (p2p.cu)
-    if (deep && e->fused_link == 1) return stripe_pass_fused(e, p, q, ctr, per_sweep, ls);
+    // ONE launch with the halo exchange fused into the MCS kernel (stripe_link.cuh) when a neighbour is on another
+    // GPU; otherwise pull, kernel, push + signal (p2p.cu)
+    if (e->fused_link == 1 && e->mcs_impl == 2) return stripe_pass_fused(e, p, q, ctr, live, per_sweep, ls);
     // 1. wait for the neighbours' previous pass, pull their boundary rows
     rc = p2p_pull(e, false);
     if (rc) return rc;

@@ -23,6 +23,7 @@
 
 #include "device_common.cuh"
 #include "octgpu_internal.h"
+#include "stripe_link.cuh"
 
 namespace octgpu {
 
@@ -129,7 +130,8 @@ __global__ void __launch_bounds__(32 * (kP + 1), kP >= 8 ? 2 : 4) k_mcs_bulk(con
                                                             ProbDev q, const uint64_t* __restrict__ jtab, int S,
                                                             const __grid_constant__ CUtensorMap tmK,
                                                             const __grid_constant__ CUtensorMap tmK1,
-                                                            uint64_t ck1, uint64_t ck2) {
+                                                            uint64_t ck1, uint64_t ck2,
+                                                            const __grid_constant__ StripeLink lk) {
     using Word = uint64_t;
     using LY = StageLayout<KS>;
     constexpr bool LIVE = Plan<PM, QM>::live;
@@ -150,6 +152,20 @@ __global__ void __launch_bounds__(32 * (kP + 1), kP >= 8 ? 2 : 4) k_mcs_bulk(con
     Word* ring = reinterpret_cast<Word*>(smem_raw + kBarBytes);
     const uint32_t nblocks = (n + KS - 1) / KS;
 
+    // a row stripe's fused halo exchange (stripe_link.cuh): this block's roles (block-uniform)
+    bool sig = false, push = false;
+    uint32_t nsig = 0;
+    if (lk.active) {
+        const uint32_t c0 = g.c0, c1 = g.c1, nb = gridDim.x, K = 30u * kP;
+        auto core_lo = [&](uint32_t b) { return c0 + b * K; };
+        auto core_hi = [&](uint32_t b) { return min(c1, c0 + (b + 1) * K); };  // exclusive
+        auto signals = [&](uint32_t b) { return core_lo(b) < c0 + kStripeHB || core_hi(b) > c1 - kStripeHA; };
+        for (uint32_t b = 0; b < nb; ++b) nsig += signals(b) ? 1u : 0u;
+        sig = signals(blockIdx.x);
+        push = core_hi(blockIdx.x) == c1;
+        const bool above = blk_r0 < kStripeHA, below = blk_r0 + uint32_t(kWin) > c1;
+        if ((above || below) && !link_pull(lk, const_cast<uint64_t*>(src), g, above, below)) return;
+    }
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1);
@@ -162,6 +178,7 @@ __global__ void __launch_bounds__(32 * (kP + 1), kP >= 8 ? 2 : 4) k_mcs_bulk(con
     if (wib == kP) {
         // ---- producer warp: one lane streams the window, KS words per stage ----
         if (lane == 0) {
+            if (lk.active) asm volatile("fence.proxy.async.global;" ::: "memory");  // after a halo pull
             uint32_t st = 0, ph = 0;  // stage, and the parity of its fill round
             for (uint32_t b = 0; b < nblocks; ++b) {
                 if (b >= uint32_t(S)) mbar_wait(&empty[st], ph ^ 1u);
@@ -363,6 +380,7 @@ __global__ void __launch_bounds__(32 * (kP + 1), kP >= 8 ? 2 : 4) k_mcs_bulk(con
         if (core || halo_state) store_state(rd, Y, y, st2);
         if (core && ghost_row) store_state(rd, Y, y + g.wrap, st2);
     }
+    if (sig) link_signal(lk, dst, g, push, nsig, 32u * nact);  // the compute warps (producer / idle ones exited)
 }
 
 namespace {
@@ -370,37 +388,39 @@ namespace {
 template <int PM, int QM, int KS, bool CTR = false>
 cudaError_t bulk_go(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
                     const ProbDev& q, const uint64_t* jtab, int S, const CUtensorMap* tmK, const CUtensorMap* tmK1,
-                    cudaStream_t st, uint64_t ck1 = 0, uint64_t ck2 = 0) {
+                    cudaStream_t st, uint64_t ck1, uint64_t ck2, const StripeLink* link) {
     const uint32_t warps = (g.c1 - g.c0 + 29) / 30;
     const uint32_t threads = 32 * (kP + 1), blocks = (warps + kP - 1) / kP;
     const size_t smem = mcs_bulk_smem(KS, S);
     auto kern = k_mcs_bulk<PM, QM, KS, CTR>;
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
+    StripeLink lk{};
+    if (link) lk = *link;
     kern<<<blocks, threads, smem, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), rs, rd, f, g,
-                                        p, q, jtab, S, *tmK, *tmK1, ck1, ck2);
+                                        p, q, jtab, S, *tmK, *tmK1, ck1, ck2, lk);
     return cudaGetLastError();
 }
 
 template <int PM, int QM>
 cudaError_t bulk_pq(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g, const ProbDev& p,
                     const ProbDev& q, const uint64_t* jtab, int ks, int S, const CUtensorMap* tmK,
-                    const CUtensorMap* tmK1, cudaStream_t st) {
+                    const CUtensorMap* tmK1, cudaStream_t st, const StripeLink* link) {
     switch (ks) {
-    case 1: return bulk_go<PM, QM, 1>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
-    case 2: return bulk_go<PM, QM, 2>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
-    case 4: return bulk_go<PM, QM, 4>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st);
+    case 1: return bulk_go<PM, QM, 1>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, 0, 0, link);
+    case 2: return bulk_go<PM, QM, 2>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, 0, 0, link);
+    case 4: return bulk_go<PM, QM, 4>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, 0, 0, link);
     default: return cudaErrorInvalidValue;
     }
 }
 
 #define OCT_BQ(PM)                                                                              \
     switch (q.mode) {                                                                           \
-    case M_ZERO: return bulk_pq<PM, M_ZERO>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, tmK, tmK1, st);     \
-    case M_HALF: return bulk_pq<PM, M_HALF>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, tmK, tmK1, st);     \
-    case M_DYADIC: return bulk_pq<PM, M_DYADIC>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, tmK, tmK1, st); \
-    case M_ARB: return bulk_pq<PM, M_ARB>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, tmK, tmK1, st);       \
-    case M_ONE: return bulk_pq<PM, M_ONE>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, tmK, tmK1, st);       \
+    case M_ZERO: return bulk_pq<PM, M_ZERO>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, tmK, tmK1, st, link);     \
+    case M_HALF: return bulk_pq<PM, M_HALF>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, tmK, tmK1, st, link);     \
+    case M_DYADIC: return bulk_pq<PM, M_DYADIC>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, tmK, tmK1, st, link); \
+    case M_ARB: return bulk_pq<PM, M_ARB>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, tmK, tmK1, st, link);       \
+    case M_ONE: return bulk_pq<PM, M_ONE>(src, dst, rs, rd, f, g, p, q, jtab, ks, S, tmK, tmK1, st, link);       \
     default: return cudaErrorInvalidValue;                                                      \
     }
 
@@ -410,7 +430,7 @@ size_t mcs_bulk_smem(int ks, int S) { return kBarBytes + size_t(S) * mcs_bulk_st
 
 cudaError_t launch_mcs_bulk(const void* src, void* dst, const uint64_t* rs, uint64_t* rd, int f, Geom g,
                             const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int ks, int S,
-                            const CUtensorMap* tmK, const CUtensorMap* tmK1, cudaStream_t st) {
+                            const CUtensorMap* tmK, const CUtensorMap* tmK1, cudaStream_t st, const StripeLink* link) {
     switch (p.mode) {
     case M_ZERO: OCT_BQ(M_ZERO)
     case M_HALF: OCT_BQ(M_HALF)
@@ -422,7 +442,7 @@ cudaError_t launch_mcs_bulk(const void* src, void* dst, const uint64_t* rs, uint
 }
 
 // counter-based streams: KS = 2 only (the engine's plan)
-#define OCT_CTR_ARGS src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, k1, k2
+#define OCT_CTR_ARGS src, dst, nullptr, nullptr, f, g, p, q, nullptr, S, tmK, tmK1, st, k1, k2, link
 #define OCT_BQC(PM)                                                           \
     switch (q.mode) {                                                         \
     case M_ZERO: return bulk_go<PM, M_ZERO, 2, true>(OCT_CTR_ARGS);         \
@@ -435,7 +455,7 @@ cudaError_t launch_mcs_bulk(const void* src, void* dst, const uint64_t* rs, uint
 
 cudaError_t launch_mcs_bulk_ctr(const void* src, void* dst, int f, Geom g, const ProbDev& p, const ProbDev& q,
                                 uint64_t seed, uint64_t sigma, int S, const CUtensorMap* tmK, const CUtensorMap* tmK1,
-                                cudaStream_t st) {
+                                cudaStream_t st, const StripeLink* link) {
     const uint64_t k1 = ctr_sweep_key(seed, sigma), k2 = ctr_sweep_key(seed, sigma + 1);
     switch (p.mode) {
     case M_ZERO: OCT_BQC(M_ZERO)

@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(32 * kDP, kDeepMinBlocks)
             if (c.ghost_row) store_state(rd, g.Y, y + g.wrap, fin);
         }
     }
-    if (sig) link_signal(lk, dst, g, push, nsig);
+    if (sig) link_signal(lk, dst, g, push, nsig, kLanes);
 }
 
 namespace {

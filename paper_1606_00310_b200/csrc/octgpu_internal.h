@@ -133,12 +133,13 @@ cudaError_t launch_mcs(int w, const void* src, void* dst, const uint64_t* rng_sr
 // boxes of kTmaBoxRows rows x ks and x ks+1 words (see engine.cu ensure_tmaps).
 cudaError_t launch_mcs_bulk(const void* src, void* dst, const uint64_t* rng_src, uint64_t* rng_dst, int f, Geom g,
                             const ProbDev& p, const ProbDev& q, const uint64_t* jtab, int ks, int S,
-                            const CUtensorMap* tmK, const CUtensorMap* tmK1, cudaStream_t st);
+                            const CUtensorMap* tmK, const CUtensorMap* tmK1, cudaStream_t st,
+                            const StripeLink* link = nullptr);
 size_t mcs_bulk_stage_bytes(int ks);
 // k_mcs_bulk with counter-based xi (KS = 2 tensor maps): sweeps sigma (phase f) and sigma + 1 of seed's streams
 cudaError_t launch_mcs_bulk_ctr(const void* src, void* dst, int f, Geom g, const ProbDev& p, const ProbDev& q,
                                 uint64_t seed, uint64_t sigma, int S, const CUtensorMap* tmK, const CUtensorMap* tmK1,
-                                cudaStream_t st);
+                                cudaStream_t st, const StripeLink* link = nullptr);
 size_t mcs_bulk_smem(int ks, int S);  // dynamic smem of a block (kMcsConsumerWarps + 1 warps)
 
 // Temporally blocked variant (mcs_deep.cu): L sweeps (L/2 MCS, starting with

@@ -68,19 +68,24 @@ __device__ bool link_pull(const StripeLink& lk, Word* __restrict__ planes, const
     return true;
 }
 
-// Block-wide, at the end of a signalling block: push (if this block completed it) the Y(f) plane-row of the first
-// halo row below into the next stripe's new set, then take a ticket; the last of `nsig` blocks publishes done.
+__device__ __forceinline__ void link_bar(uint32_t nthreads) {
+    asm volatile("barrier.sync 2, %0;" ::"r"(nthreads) : "memory");
+}
+
+// At the end of a signalling block, by its threads 0..nthreads-1 (the compute warps; a multiple of 32): push (if
+// this block completed it) the Y(f) plane-row of the first halo row below into the next stripe's new set, then
+// take a ticket; the last of `nsig` blocks publishes done.
 template <typename Word>
 __device__ void link_signal(const StripeLink& lk, const Word* __restrict__ dst, const Geom& g, bool push,
-                            uint32_t nsig) {
-    __syncthreads();  // every store of this block issued
+                            uint32_t nsig, uint32_t nthreads) {
+    link_bar(nthreads);  // every store of these threads issued (named barrier 2: producers may have exited)
     if (push) {
         const uint32_t L = g.c1 - g.c0;
         Word* np = static_cast<Word*>(lk.next_planes);
-        for (uint32_t k = threadIdx.x; k < g.n; k += blockDim.x)
+        for (uint32_t k = threadIdx.x; k < g.n; k += nthreads)
             np[size_t(lk.push_plane) * size_t(g.n) * lk.next_Y + size_t(k) * lk.next_Y + kStripeHA] =
                 dst[size_t(lk.push_plane) * g.plane_stride + size_t(k) * g.Y + kStripeHA + L];
-        __syncthreads();
+        link_bar(nthreads);
     }
     if (threadIdx.x == 0) {
         __threadfence_system();

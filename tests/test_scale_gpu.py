@@ -70,6 +70,32 @@ def test_baseline_geometry_matches_reference(oracle, reflib, case):
     assert rec.mean_h == sums[0] / (X * Y)
 
 
+# (name, X, Y, [(p, q, MCS), ...]): mixed schedules through the default dispatch -- p = 1 on a ROUGH field runs
+# the 3-MCS constant-xi pass on non-trivial dynamics (from the flat start p = 1 returns to flat every MCS), and a
+# long p = 1/2 leg checks the 2-MCS live pass over 100 passes
+LEGS = [
+    ("c2rough", 1 << 16, 1 << 16, [(0.5, 0.0, 6), (1.0, 0.0, 21), (0.5, 0.5, 3), (0.0, 0.0, 3)]),
+    ("c2h200", 1 << 16, 1 << 16, [(0.5, 0.0, 200)]),
+]
+
+
+@pytest.mark.parametrize("case", LEGS, ids=[c[0] for c in LEGS])
+def test_mixed_schedules_match_reference(oracle, reflib, case):
+    from oracle import RefEngine
+
+    name, X, Y, legs = case
+    eng = octgpu.GpuEngine(octgpu.LatticeConfig(X, Y, 64), 3)
+    ref = RefEngine(reflib, X, Y, 3, workers=CORES)
+    for p, q, mcs in legs:
+        eng.step(octgpu.UpdateParams.make(p, q), mcs)
+        ref.step(p, q, mcs)
+    eng.sync()
+    assert eng.checksum() == ref.checksum()
+    assert _digest(oracle, eng.streams().states) == _digest(oracle, ref.states())
+    sums, err = oracle.measure_planes(ref.planes())
+    assert err is None and list(eng.measure().power_sums) == sums
+
+
 def test_eight_peer_stripes_match_periodic_engine_2p17(oracle):
     """BASELINE configs[4]: the 2^17 x 2^17 lattice as 8 row stripes (SweepPlan blocks, params.hpp:107-127)
     exchanging halos device-side over peer memory, against the periodic engine: p = 1 (2-MCS stripe passes)

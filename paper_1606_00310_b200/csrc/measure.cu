@@ -48,6 +48,9 @@ constexpr int kRowsPerGroup = 32;  // lane per row; lane 0 reads the row above f
 #define OCTGPU_MEAS_SEG 16  // x-segments per row group: one warp each
 #endif
 constexpr int kSeg = OCTGPU_MEAS_SEG;
+#ifndef OCTGPU_MEAS_MINB
+#define OCTGPU_MEAS_MINB 1  // resident blocks per SM the register budget targets: 1 x 16 warps, 128 registers
+#endif
 constexpr int kMThreads = 32 * kSeg;
 
 __host__ __device__ inline uint32_t measure_groups(uint32_t rows) { return (rows + kRowsPerGroup - 1) / kRowsPerGroup; }
@@ -234,7 +237,7 @@ struct Curl {  // word-parallel curl check of one word
 // x-segment s (words [s n / kSeg, (s+1) n / kSeg)) of the group's rows and shifts its sums to the global
 // gauge (Gg: k_col_scan); part[blockIdx.x] = the block's sums.
 template <typename Word, bool WIDE>
-__global__ void __launch_bounds__(kMThreads, 2) k_measure_rows(const Word* __restrict__ planes, Geom g, uint32_t X,
+__global__ void __launch_bounds__(kMThreads, OCTGPU_MEAS_MINB) k_measure_rows(const Word* __restrict__ planes, Geom g, uint32_t X,
                                                                const long long* __restrict__ Gg,
                                                                const long long* __restrict__ pre,
                                                                Partial* __restrict__ part) {

@@ -343,6 +343,7 @@ struct octgpu_engine {
     // device (decided at connect), 0 / 1 = OCTGPU_FUSED_LINK
     int fused_link = -1, fused_link_env = -1;
     bool ghost_kernel = true;  // deep passes' ghost-row mirror: a copy kernel (OCTGPU_GHOST=memcpy: cudaMemcpy2DAsync)
+    bool deep_long = true;  // 4-MCS passes for remainders of 3-MCS schedules (OCTGPU_DEEP_LONG=0: 2 / 1-MCS passes)
     int deep_l = kDeepSweepsConst;  // sweeps of a constant-xi deep pass (OCTGPU_DEEP_L = 4 keeps 2 MCS per pass)
     bool graphs = true;  // replay CUDA graphs for long step() calls (OCTGPU_GRAPH=0 disables)
     uint32_t prefetch = 0;  // TMA kernels: L2 prefetch distance in ring stages (OCTGPU_PREFETCH)
@@ -479,6 +480,7 @@ int plan_mcs(octgpu_engine* e) {
     if (const char* v = getenv("OCTGPU_PREFETCH")) e->prefetch = uint32_t(std::max(0, std::min(64, atoi(v))));
     if (const char* v = getenv("OCTGPU_DEEP_S")) e->deep_S = std::max(2, std::min(8, atoi(v)));
     if (const char* v = getenv("OCTGPU_FUSED_LINK")) e->fused_link = e->fused_link_env = atoi(v) != 0 ? 1 : 0;
+    if (const char* v = getenv("OCTGPU_DEEP_LONG")) e->deep_long = atoi(v) != 0;
     if (const char* v = getenv("OCTGPU_GHOST")) e->ghost_kernel = std::string(v) != "memcpy";
     if (const char* v = getenv("OCTGPU_DEEP_L")) e->deep_l = atoi(v) == kDeepSweepsLive ? kDeepSweepsLive : kDeepSweepsConst;
     return OCTGPU_OK;
@@ -1013,6 +1015,19 @@ cudaError_t mirror_ghost_planes(octgpu_engine* e, void* planes) {
                              size_t(4) * e->n, cudaMemcpyDeviceToDevice, e->stream);
 }
 
+// Sweeps of the next deep pass with `left` MCS to go: full-length passes (lsmax); in a 3-MCS schedule a remainder
+// of 1 or 2 is absorbed by one or two 4-MCS passes (L = 8 runs at the 3-MCS pass's cost per MCS, while a 2-MCS
+// pass costs ~1.6x per MCS and a one-MCS pass ~2.6x: 20 MCS = 4 x 3 + 2 x 4, not 6 x 3 + 2); then 2, then 0.
+int pass_sweeps(const octgpu_engine* e, const ProbDev& p, const ProbDev& q, bool ctr, int lsmax, uint64_t left) {
+    if (lsmax == kDeepSweepsConst && e->deep_long && !e->stripe &&
+        mcs_deep_supported_l(p.mode, q.mode, kDeepSweepsLong, ctr)) {
+        const uint64_t r = left % 3;
+        if ((r == 1 && left >= 4) || (r == 2 && left >= 8)) return kDeepSweepsLong;
+    }
+    if (left >= uint64_t(lsmax / 2)) return lsmax;
+    return left >= 2 ? kDeepSweepsLive : 0;
+}
+
 // Periodic lattices: does octgpu_step run k_mcs_deep passes for these parameters? (D = draws per word of a
 // xoshiro sweep; ctr = the counter-based streams)
 bool deep_policy(const octgpu_engine* e, const ProbDev& p, const ProbDev& q, uint64_t D, bool ctr) {
@@ -1113,7 +1128,7 @@ int step_counter(octgpu_engine* e, const ProbDev& p, const ProbDev& q, uint64_t 
         if (rc) return rc;
         const int lsmax = deep_sweeps(e, p, q, true);
         while (n_mcs >= 2) {  // full-length passes, then a 2-MCS pass for a remainder of 2
-            const int ls = n_mcs >= uint64_t(lsmax / 2) ? lsmax : kDeepSweepsLive;
+            const int ls = pass_sweeps(e, p, q, true, lsmax, n_mcs);
             const uint64_t mpp = uint64_t(ls / 2);
             const int ps = e->pcur;
             CK(launch_mcs_deep_ctr(e->planes[ps], e->planes[ps ^ 1], e->phase,
@@ -1237,7 +1252,7 @@ int octgpu_step(octgpu_engine* e, const octgpu_params* prm, uint64_t n_mcs) {
     }
     while (left > 0) {
         // full-length passes, then a 2-MCS pass for a remainder of 2 (of a 3-MCS schedule), then one MCS
-        const int ls = !deep ? 0 : left >= mpp ? lsmax : left >= 2 ? kDeepSweepsLive : 0;
+        const int ls = !deep ? 0 : pass_sweeps(e, p, q, false, lsmax, left);
         rc = step_pass(e, p, q, live, ls, jtab, per_sweep);
         if (rc) return rc;
         left -= ls ? uint64_t(ls / 2) : 1;

@@ -608,18 +608,19 @@ bool mcs_deep_supported(int pm, int qm) {
     return cheap_mode(pm) && cheap_mode(qm) && !(live && (pm == M_ONE || qm == M_ONE));
 }
 
-// L = 6 (3 MCS per pass) only without stream state: constant xi (xoshiro streams advance lazily) or the
-// counter-based streams; a live xoshiro pass keeps four 256-bit states per lane in registers at L = 4.
+// L = 6 / 8 (3 / 4 MCS per pass) only with constant xi (xoshiro streams advance lazily); a live pass keeps
+// four 256-bit states per lane in registers at L = 4 (8 with counter streams would spill).
 bool mcs_deep_supported_l(int pm, int qm, int L, bool ctr) {
     if (!mcs_deep_supported(pm, qm)) return false;
     if (L == kDeepSweepsLive) return true;
-    if (L == kDeepSweepsConst) return const_mode(pm) && const_mode(qm);
+    if (L == kDeepSweepsConst || L == kDeepSweepsLong) return const_mode(pm) && const_mode(qm);
     return false;
 }
 
 size_t mcs_deep_smem(int pm, int qm, int L, int S, bool ctr) {
     if (L == 4) return deep_smem_l<4>(pm, qm, S, ctr);
     if (L == 6) return deep_smem_l<6>(pm, qm, S, ctr);
+    if (L == 8) return deep_smem_l<8>(pm, qm, S, ctr);
     return 0;
 }
 
@@ -635,6 +636,8 @@ cudaError_t deep_l(int L, const void* src, void* dst, const uint64_t* rs, uint64
     if constexpr (const_mode(PM) && const_mode(QM)) {
         if (L == 6)
             return deep_go<PM, QM, 6, CTR>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma, link);
+        if (L == 8)
+            return deep_go<PM, QM, 8, CTR>(src, dst, rs, rd, f, g, p, q, jtab, S, tmK, tmK1, st, seed, sigma, link);
     }
     return cudaErrorInvalidValue;
 }

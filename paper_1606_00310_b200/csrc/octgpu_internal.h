@@ -81,6 +81,7 @@ constexpr int kDeepMinBlocks = OCTGPU_DEEP_MINB;  // resident blocks per SM the 
 // sweeps per k_mcs_deep pass (even): 6 (3 MCS) for constant xi, 4 (2 MCS) for live streams
 constexpr int kDeepSweepsConst = 6;
 constexpr int kDeepSweepsLive = 4;
+constexpr int kDeepSweepsLong = 8;  // 4-MCS constant-xi passes on periodic lattices: absorb remainders of 3-MCS schedules
 constexpr int kStripeSweeps = kDeepSweepsConst;  // the longest stripe pass (its halo rows are sized for it)
 constexpr int deep_box_rows() { return kDeepLanes; }
 constexpr int deep_core_rows(int L) { return kDeepLanes - 2 * L; }  // even: block windows start 16-B aligned

@@ -38,7 +38,7 @@ CASES = [
     ("c2h", 1 << 16, 1 << 16, 0.5, 0.0, 20, 20),   # k_mcs_deep x 10, live xoshiro (one draw per word)
     ("c3", 1 << 16, 1 << 16, 0.5, 0.5, 10, 10),    # k_mcs_deep x 5, live xoshiro (two half draws per word)
     ("c4", 1 << 16, 1 << 16, 0.98, 0.02, 2, 2),    # k_mcs_bulk, arbitrary (128 draws per word)
-    ("c2", 1 << 16, 1 << 16, 1.0, 0.0, 20, 14),    # k_mcs_deep, constant xi: 6 x 3 MCS + 1 x 2 MCS (lazy draws)
+    ("c2", 1 << 16, 1 << 16, 1.0, 0.0, 20, 12),    # k_mcs_deep, constant xi: 2 x 4 MCS + 4 x 3 MCS (lazy draws)
     ("c5h", 1 << 17, 1 << 17, 0.5, 0.0, 4, 4),     # k_mcs_deep x 2 at 2^34 sites
 ]
 

@@ -431,12 +431,17 @@ void trace_create(const char* what, bool start);
 // Apply owed draws to every row stream (lazy advance of constant-xi sweeps). The table of T^pending is
 // not cached (every pending count is different): it goes through one engine-owned pinned + device buffer
 // pair, reused once the previous jump that read it has completed (pend_ev).
+int dev_alloc(octgpu_engine* e, void** out, size_t bytes);
+cudaError_t host_pinned(void** out, size_t bytes);
+constexpr size_t kPendTabBytes = size_t(64) * 16 * 4 * sizeof(uint64_t);
+
 int materialize(octgpu_engine* e) {
     if (!e->pending) return OCTGPU_OK;
-    const size_t bytes = size_t(64) * 16 * 4 * sizeof(uint64_t);
+    const size_t bytes = kPendTabBytes;
     if (!e->pend_tab) {
-        CK(cudaMalloc(reinterpret_cast<void**>(&e->pend_tab), bytes));
-        CK(cudaMallocHost(reinterpret_cast<void**>(&e->pend_host), bytes));
+        int rc = dev_alloc(e, reinterpret_cast<void**>(&e->pend_tab), bytes);
+        if (rc) return rc;
+        CK(host_pinned(reinterpret_cast<void**>(&e->pend_host), bytes));
         CK(cudaEventCreateWithFlags(&e->pend_ev, cudaEventDisableTiming));
     } else {
         CK(cudaEventSynchronize(e->pend_ev));
@@ -596,6 +601,59 @@ int engine_pool(int device, cudaMemPool_t* out) {
     return OCTGPU_OK;
 }
 
+// Device buffers of an engine: from the library pool on the engine's stream when the engine is pooled
+// (periodic), else cudaMalloc (stripes export theirs over CUDA IPC).
+int dev_alloc(octgpu_engine* e, void** out, size_t bytes) {
+    if (!e->pooled) {
+        CK(cudaMalloc(out, bytes));
+        return OCTGPU_OK;
+    }
+    cudaMemPool_t pool = nullptr;
+    int rc = engine_pool(e->device, &pool);
+    if (rc) return rc;
+    cudaError_t ae = cudaMallocFromPoolAsync(out, bytes, pool, e->stream);
+    if (ae == cudaErrorMemoryAllocation) {  // trim what earlier engines left and retry once
+        cudaGetLastError();
+        CK(cudaStreamSynchronize(e->stream));
+        CK(cudaMemPoolTrimTo(pool, 0));
+        ae = cudaMallocFromPoolAsync(out, bytes, pool, e->stream);
+    }
+    CK(ae);
+    return OCTGPU_OK;
+}
+
+void dev_free(octgpu_engine* e, void* ptr) {
+    if (!ptr) return;
+    if (e->pooled)  // on the engine's own stream: a user stream may already be gone
+        cudaFreeAsync(ptr, e->own_stream);
+    else
+        cudaFree(ptr);
+}
+
+// Small pinned host buffers (measure results, jump tables) are recycled process-wide: cudaMallocHost
+// costs ~1 ms per call, paid again by every engine otherwise.
+std::mutex g_pinned_mu;
+std::multimap<size_t, void*> g_pinned_free;
+
+cudaError_t host_pinned(void** out, size_t bytes) {
+    {
+        std::lock_guard<std::mutex> lk(g_pinned_mu);
+        auto it = g_pinned_free.find(bytes);
+        if (it != g_pinned_free.end()) {
+            *out = it->second;
+            g_pinned_free.erase(it);
+            return cudaSuccess;
+        }
+    }
+    return cudaMallocHost(out, bytes);
+}
+
+void host_pinned_release(void* ptr, size_t bytes) {
+    if (!ptr) return;
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    g_pinned_free.emplace(bytes, ptr);
+}
+
 int alloc_engine(octgpu_engine* e) {
     CK(cudaSetDevice(e->device));
     CK(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
@@ -610,30 +668,19 @@ int alloc_engine(octgpu_engine* e) {
     // engine leaves in it is returned with octgpu_release_pool(device), and automatically when a later
     // plane-set allocation of this library would otherwise fail.
     e->pooled = !e->stripe;
-    cudaMemPool_t pool = nullptr;
-    if (e->pooled) {
-        int rc = engine_pool(e->device, &pool);
+    for (int i = 0; i < 2; ++i) {
+        int rc = dev_alloc(e, &e->planes[i], e->set_bytes());
+        if (!rc) rc = dev_alloc(e, reinterpret_cast<void**>(&e->rng[i]), e->rng_bytes());
         if (rc) return rc;
     }
-    for (int i = 0; i < 2; ++i) {
-        if (e->pooled) {
-            cudaError_t ae = cudaMallocFromPoolAsync(&e->planes[i], e->set_bytes(), pool, e->stream);
-            if (ae == cudaErrorMemoryAllocation) {  // trim what earlier engines left and retry once
-                cudaGetLastError();
-                CK(cudaStreamSynchronize(e->stream));
-                CK(cudaMemPoolTrimTo(pool, 0));
-                ae = cudaMallocFromPoolAsync(&e->planes[i], e->set_bytes(), pool, e->stream);
-            }
-            CK(ae);
-        } else
-            CK(cudaMalloc(&e->planes[i], e->set_bytes()));
-        CK(cudaMalloc(reinterpret_cast<void**>(&e->rng[i]), e->rng_bytes()));
-    }
     trace_create("planes", false);
-    CK(cudaMalloc(&e->scratch, measure_scratch_bytes(e->Y)));
-    CK(cudaMemset(e->scratch, 0, measure_scratch_bytes(e->Y)));  // k_col_scan's block ticket starts at 0
-    CK(cudaMalloc(reinterpret_cast<void**>(&e->res_dev), sizeof(MeasureResult)));
-    CK(cudaMallocHost(reinterpret_cast<void**>(&e->res_host), sizeof(MeasureResult)));
+    // the small buffers too: a synchronous cudaMalloc / cudaMemset / cudaMallocHost each cost 0.5-1.5 ms
+    // of an engine re-created inside a timed region
+    int rc = dev_alloc(e, &e->scratch, measure_scratch_bytes(e->Y));
+    if (!rc) rc = dev_alloc(e, reinterpret_cast<void**>(&e->res_dev), sizeof(MeasureResult));
+    if (rc) return rc;
+    CK(cudaMemsetAsync(e->scratch, 0, measure_scratch_bytes(e->Y), e->stream));  // k_col_scan's ticket starts at 0
+    CK(host_pinned(reinterpret_cast<void**>(&e->res_host), sizeof(MeasureResult)));
     trace_create("small", false);
     return plan_mcs(e);
 }
@@ -915,26 +962,21 @@ void octgpu_destroy(octgpu_engine* e) {
     cudaSetDevice(e->device);
     if (e->stream) cudaStreamSynchronize(e->stream);
     for (int i = 0; i < 2; ++i) {
-        if (e->planes[i]) {
-            if (e->pooled)  // on the engine's own stream: a user stream may already be gone
-                cudaFreeAsync(e->planes[i], e->own_stream);
-            else
-                cudaFree(e->planes[i]);
-        }
-        if (e->rng[i]) cudaFree(e->rng[i]);
+        dev_free(e, e->planes[i]);
+        dev_free(e, e->rng[i]);
     }
     for (auto& kv : e->graph_cache) cudaGraphExecDestroy(kv.second.first);
     for (auto& kv : e->jtabs) cudaFree(kv.second);
-    if (e->pend_tab) cudaFree(e->pend_tab);
-    if (e->pend_host) cudaFreeHost(e->pend_host);
+    dev_free(e, e->pend_tab);
+    host_pinned_release(e->pend_host, kPendTabBytes);
     if (e->pend_ev) cudaEventDestroy(e->pend_ev);
     for (void* ptr : e->ipc_opened) cudaIpcCloseMemHandle(ptr);
     if (e->done) cudaFree(e->done);
     if (e->p2p_err) cudaFree(e->p2p_err);
     if (e->stage) cudaFree(e->stage);
-    if (e->scratch) cudaFree(e->scratch);
-    if (e->res_dev) cudaFree(e->res_dev);
-    if (e->res_host) cudaFreeHost(e->res_host);
+    dev_free(e, e->scratch);
+    dev_free(e, e->res_dev);
+    host_pinned_release(e->res_host, sizeof(MeasureResult));
     if (e->own_stream) {
         cudaStreamSynchronize(e->own_stream);
         cudaStreamDestroy(e->own_stream);

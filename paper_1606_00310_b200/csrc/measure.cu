@@ -13,10 +13,11 @@
 //   k_col_scan      one block: the column-0 prefix G_y = H_y - sigma_x-(0, y) of every core row (global
 //                   gauge), the column closure sum and sigma_y-(0, c0).
 //   k_measure_rows  persistent blocks of kSeg warps; a block takes a row group of 32 rows (lane per row)
-//                   and warp s the group's x-segment s. Word-parallel curl check; U_j per segment from
-//                   16-site units read through two 8-site tables (the second indexed by the first's net
-//                   step, so a unit costs one combine), unit sums accumulated in 32-bit registers relative
-//                   to a 4-word chunk and folded into the segment's sums once per chunk. Each thread then
+//                   and warp s the group's x-segment s (plane-major coalesced loads). Word-parallel curl
+//                   check; U_j per segment from 32-site units read through four chained 8-site tables (each
+//                   indexed by the partial net step of the ones before, entries summed as packed 64-bit
+//                   words), unit sums accumulated in 32-bit registers relative to a 4-word chunk and folded
+//                   into the segment's sums once per chunk (16-site units: OCTGPU_MEAS_UNIT=16). Each thread then
 //                   shifts its own segment's sums by the segment's global start height (G_y plus the net
 //                   steps of the segments before it, exchanged through shared memory: one block barrier per
 //                   group) and keeps the block's sums in registers; one block reduction at the end.
@@ -108,11 +109,106 @@ struct MeasTabInit : MeasTab {
 
 __device__ const MeasTab g_tab = MeasTabInit();
 
-// shared memory: T0 replicated x16 (entry b at [b][lane & 15]: every warp lookup conflict-free), T1 once,
-// then two buffers of the threads' segment net steps (groups alternate)
+#ifndef OCTGPU_MEAS_UNIT
+#define OCTGPU_MEAS_UNIT 32  // sites per unit: 32 (four chained 8-site tables) or 16 (two)
+#endif
+constexpr int kUnit = OCTGPU_MEAS_UNIT;
+static_assert(kUnit == 16 || kUnit == 32, "OCTGPU_MEAS_UNIT must be 16 or 32");
+
+// ---- 32-site units: four chained 8-site tables -----------------------------------------
+// Byte j of a unit (j = 0..3) is read at offset o in -8j..8j (even): T0 (o = 0) and Tj (o = 2 (f - 4j),
+// f = 0..8j the partial step field of the entries so far). An entry is one 64-bit word of five fields,
+// each sized for the SUM of a unit's four entries (no carries between fields):
+//   bits  0..16  F3 = (q3 - q1) / 6 + B3_j   (v^3 - v is divisible by 6)
+//   bits 17..28  F2 = q2 / 4
+//   bits 29..38  F1 = q1 / 2 + B1_j
+//   bits 39..57  F4 = (q4 - 4) / 16
+//   bits 58..63  FD = d / 2 + 4 = popcount(byte)   (the unit's partial sum indexes the next table)
+// B1_j, B3_j = minus the field's minimum over Tj (the all-down byte at o = -8j), so a unit decodes as
+//   q1 = 2 (F1 - B1), q2 = 4 F2, q3 = 6 (F3 - B3) + q1, q4 = 16 F4 + 16, d = 2 (FD - 16).
+// Unit ranges: |q1| <= 528, q2 <= 11440, |q3 - q1| / 6 <= 46376, q4 <= 7246096, |d| <= 32.
+constexpr int kTRows = 9 + 17 + 25;           // T1, T2, T3 (even offsets only)
+__host__ __device__ constexpr int tab_base(int j) { return j <= 1 ? 0 : j == 2 ? 9 : 26; }  // Tj's first row
+struct TabQ {
+    long long q1, q2, q3, q4;
+    int pc;
+};
+__host__ __device__ constexpr TabQ tab_q(int b, int o) {
+    TabQ t{0, 0, 0, 0, 0};
+    int p = 0;
+    for (int i = 0; i < 8; ++i) {
+        const int bit = (i & 1) ? (b >> (4 + (i >> 1))) & 1 : (b >> (i >> 1)) & 1;
+        p += bit ? 1 : -1;
+        t.pc += bit;
+        const long long v = o + p, v2 = v * v;
+        t.q1 += v;
+        t.q2 += v2;
+        t.q3 += v2 * v;
+        t.q4 += v2 * v2;
+    }
+    return t;
+}
+__host__ __device__ constexpr long long tab_b1(int j) { return -tab_q(0, -8 * j).q1 / 2; }
+__host__ __device__ constexpr long long tab_b3(int j) { return -(tab_q(0, -8 * j).q3 - tab_q(0, -8 * j).q1) / 6; }
+constexpr long long kU32B1 = tab_b1(0) + tab_b1(1) + tab_b1(2) + tab_b1(3);
+constexpr long long kU32B3 = tab_b3(0) + tab_b3(1) + tab_b3(2) + tab_b3(3);
+static_assert(kU32B1 == 264 && kU32B3 == 46376, "unit biases");
+
+__host__ __device__ constexpr unsigned long long tab32_entry(int b, int o, long long b1, long long b3) {
+    const TabQ t = tab_q(b, o);
+    return (unsigned long long)((t.q3 - t.q1) / 6 + b3) | ((unsigned long long)(t.q2 / 4) << 17) |
+           ((unsigned long long)(t.q1 / 2 + b1) << 29) | ((unsigned long long)((t.q4 - 4) / 16) << 39) |
+           ((unsigned long long)t.pc << 58);
+}
+
+struct MeasTab32 {
+    unsigned long long t0[256];
+    unsigned long long tj[kTRows * 256];
+};
+struct MeasTab32Init : MeasTab32 {
+    constexpr MeasTab32Init() : MeasTab32{} {
+        for (int b = 0; b < 256; ++b) t0[b] = tab32_entry(b, 0, tab_b1(0), tab_b3(0));
+        for (int j = 1; j < 4; ++j) {
+            const long long b1 = tab_b1(j), b3 = tab_b3(j);
+            for (int f = 0; f <= 8 * j; ++f)
+                for (int b = 0; b < 256; ++b) tj[(tab_base(j) + f) * 256 + b] = tab32_entry(b, 2 * (f - 4 * j), b1, b3);
+        }
+    }
+};
+__device__ const MeasTab32 g_tab32 = MeasTab32Init();
+
+// shared memory: T0 replicated x16 (entry b at [b][lane & 15]: every warp lookup conflict-free), the
+// chained tables once, then two buffers of the threads' segment net steps (groups alternate)
 constexpr int kRep = 16;
-constexpr int kT0Words = 256 * kRep;  // uint2
-constexpr int kT1Words = 17 * 256;
+// 32-site units: table j is replicated R_j times, entry b of copy c at [b][c] and lane l reads copy l % R_j.
+// A 64-bit entry spans a bank pair and a warp's LDS.64 is served per half-warp: the wavefronts of one lookup
+// are the sum over the two half-warps of the fullest pair. Entry b of copy c sits in pair (R_j b + c) mod 16,
+// so a half-warp splits into R_j lane groups with disjoint pairs. Measured wavefronts per lookup (random
+// bytes, ncu source page): R = 1: 6.9, 2: 6.4, 4: 5.5, 8: 4.0, 16: 2.0 (conflict-free). Default T0 x 16
+// (32 KB), T1 x 4 (72 KB), T2, T3 once (34 + 50 KB): larger copies shrink the L1 the plane loads stream
+// through and measured slower (tools/r2_u32rep.sh, tools/r2_u32load.sh).
+#ifndef OCTGPU_MEAS_R0
+#define OCTGPU_MEAS_R0 16
+#endif
+#ifndef OCTGPU_MEAS_R1
+#define OCTGPU_MEAS_R1 4
+#endif
+#ifndef OCTGPU_MEAS_R2
+#define OCTGPU_MEAS_R2 1
+#endif
+#ifndef OCTGPU_MEAS_R3
+#define OCTGPU_MEAS_R3 1
+#endif
+__host__ __device__ constexpr int tab_rep(int j) {
+    return j == 0 ? OCTGPU_MEAS_R0 : j == 1 ? OCTGPU_MEAS_R1 : j == 2 ? OCTGPU_MEAS_R2 : OCTGPU_MEAS_R3;
+}
+__host__ __device__ constexpr int tab_rows(int j) { return j == 0 ? 1 : 8 * j + 1; }
+// first entry of table j's copies in shared memory
+__host__ __device__ constexpr int tab_off(int j) {
+    return j == 0 ? 0 : tab_off(j - 1) + 256 * tab_rows(j - 1) * tab_rep(j - 1);
+}
+constexpr int kT0Words = kUnit == 32 ? 0 : 256 * kRep;  // 8-byte entries
+constexpr int kT1Words = kUnit == 32 ? tab_off(4) : 17 * 256;
 // Up to this many sites per segment (R <= 2^13) the segment sums T1..T3 and the per-chunk increment of T4
 // fit 64 bits (T3 <= 2^13 2^39; 4 R^3 C1 <= 2^59, R^4 ns <= 2^61 with C1 <= 2^18, ns = 512); T4 itself is
 // summed in 128. Wider segments (X > 2^17) form everything in 128 bits.
@@ -217,6 +313,89 @@ __device__ __forceinline__ void flush_chunk(UnitAcc& A, int K, int ns, long long
     A.clear();
 }
 
+// Unit accumulators of a chunk of 32-site units: s = r / 2, r = the height at the unit start relative to
+// the chunk start (|s| <= 240 over 16 units); F* the biased unit fields. 32-bit sums except s^4 and s^3 F1.
+struct UnitAcc32 {
+    int as, as2, as3, f1, f2, f3, f4, sf1, sf2, sf3, s2f1, s2f2;
+    long long as4, s3f1;
+    __device__ __forceinline__ void clear() {
+        as = as2 = as3 = f1 = f2 = f3 = f4 = sf1 = sf2 = sf3 = s2f1 = s2f2 = 0;
+        as4 = s3f1 = 0;
+    }
+};
+
+// a lane's copies of the four tables (tab_off / tab_rep)
+struct TabLanes {
+    const unsigned long long *t0, *t1, *t2, *t3;
+};
+
+// one 32-site unit v of a 64-site half: bytes 2v (evn), 2v (odd), 2v + 1 (evn), 2v + 1 (odd)
+__device__ __forceinline__ void unit32(UnitAcc32& A, int& s, uint32_t evn, uint32_t odd, uint32_t v,
+                                       const TabLanes& T) {
+    const uint32_t k0 = 2 * v, k1 = 2 * v + 1;
+    unsigned long long e = T.t0[__byte_perm(evn, 0, 0x4440 + k0) * tab_rep(0)];
+    e += T.t1[__byte_perm(odd, uint32_t(e >> 58), 0x5540 + k0) * tab_rep(1)];
+    e += T.t2[__byte_perm(evn, uint32_t(e >> 58), 0x5540 + k1) * tab_rep(2)];
+    e += T.t3[__byte_perm(odd, uint32_t(e >> 58), 0x5540 + k1) * tab_rep(3)];
+    const uint32_t lo = uint32_t(e), hi = uint32_t(e >> 32);
+    const int F3 = int(lo & 0x1ffffu), F2 = int((lo >> 17) & 0xfffu), F1 = int(__funnelshift_r(lo, hi, 29) & 0x3ffu),
+              F4 = int((hi >> 7) & 0x7ffffu), FD = int(hi >> 26);
+    const int s2 = s * s, s3 = s2 * s;
+    A.as += s;
+    A.as2 += s2;
+    A.as3 += s3;
+    A.as4 = madw(s2, s2, A.as4);
+    A.f1 += F1;
+    A.f2 += F2;
+    A.f3 += F3;
+    A.f4 += F4;
+    A.sf1 += s * F1;
+    A.sf2 += s * F2;
+    A.sf3 += s * F3;
+    A.s2f1 += s2 * F1;
+    A.s2f2 += s2 * F2;
+    A.s3f1 = madw(s3, F1, A.s3f1);
+    s += FD - 16;
+}
+
+// Fold a chunk of K 32-site units (ns sites) into the segment sums; with r = 2 s and the unit decode above,
+// C_k = sum over units of sum_j C(k, j) r^(k-j) q_j (q_0 = 32), then T_k += sum_j C(k, j) R^(k-j) C_j.
+template <typename TT>
+__device__ __forceinline__ void flush_chunk32(UnitAcc32& A, int K, int ns, long long R, TT& T1, TT& T2, TT& T3,
+                                              __int128& T4) {
+    const long long k = K, B1 = kU32B1, B3 = kU32B3;
+    const long long as = A.as, as2 = A.as2, as3 = A.as3, f1 = A.f1;
+    const long long C1 = 64 * as + 2 * f1 - 2 * B1 * k;
+    const long long C2 = 128 * as2 + 8ll * A.sf1 - 8 * B1 * as + 4ll * A.f2;
+    const long long C3 = 256 * as3 + 24ll * A.s2f1 - 24 * B1 * as2 + 24ll * A.sf2 + 6ll * A.f3 - 6 * B3 * k + 2 * f1 -
+                         2 * B1 * k;
+    const long long C4 = 512 * A.as4 + 64 * A.s3f1 - 64 * B1 * as3 + 96ll * A.s2f2 + 48ll * A.sf3 - 48 * B3 * as +
+                         16ll * A.sf1 - 16 * B1 * as + 16ll * A.f4 + 16 * k;
+    const TT r1 = R, r2 = r1 * r1, r3 = r2 * r1;
+    T1 += C1 + r1 * ns;
+    T2 += C2 + 2 * r1 * C1 + r2 * ns;
+    T3 += C3 + 3 * r1 * C2 + 3 * r2 * C1 + r3 * ns;
+    T4 += C4 + 4 * r1 * C3 + 6 * r2 * C2 + 4 * r3 * C1 + r2 * r2 * ns;
+    A.clear();
+}
+
+// base[o] through one 32 x 32 -> 64-bit address multiply-add (keeps the per-word address arithmetic at one
+// instruction per plane)
+template <typename Word>
+__device__ __forceinline__ Word ldg_word(const Word* base, uint32_t o) {
+    if constexpr (sizeof(Word) == 8) {
+        unsigned long long v;
+        asm("{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %2, 8, %1;\n\tld.global.nc.u64 %0, [a];\n\t}"
+            : "=l"(v) : "l"(base), "r"(o));
+        return Word(v);
+    } else {
+        unsigned int v;
+        asm("{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %2, 4, %1;\n\tld.global.nc.u32 %0, [a];\n\t}"
+            : "=r"(v) : "l"(base), "r"(o));
+        return Word(v);
+    }
+}
+
 template <typename Word>
 struct Curl {  // word-parallel curl check of one word
     static constexpr int W = int(sizeof(Word) * 8);
@@ -242,13 +421,22 @@ __global__ void __launch_bounds__(kMThreads, OCTGPU_MEAS_MINB) k_measure_rows(co
                                                                const long long* __restrict__ pre,
                                                                Partial* __restrict__ part) {
     constexpr int W = int(sizeof(Word) * 8);
-    constexpr int kChunkWords = 256 / W;  // 32 units per chunk
+    constexpr int kChunkWords = 256 / W;  // 512 sites per chunk
+    constexpr bool kU32 = kUnit == 32 && W > 0;  // (dependent: the other unit's branch is discarded)
     extern __shared__ __align__(16) unsigned char msm[];
     uint2* t0rep = reinterpret_cast<uint2*>(msm);
     uint2* t1 = t0rep + kT0Words;
     long long* Dbuf = reinterpret_cast<long long*>(t1 + kT1Words);
-    for (int i = threadIdx.x; i < kT0Words; i += kMThreads) t0rep[i] = g_tab.t0[i / kRep];
-    {
+    if constexpr (kU32) {  // the replicated copies of T0..T3
+        unsigned long long* tq = reinterpret_cast<unsigned long long*>(msm);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const unsigned long long* src = j == 0 ? g_tab32.t0 : g_tab32.tj + tab_base(j) * 256;
+            const int n = 256 * tab_rows(j) * tab_rep(j);
+            for (int i = threadIdx.x; i < n; i += kMThreads) tq[tab_off(j) + i] = src[i / tab_rep(j)];
+        }
+    } else {
+        for (int i = threadIdx.x; i < kT0Words; i += kMThreads) t0rep[i] = g_tab.t0[i / kRep];
         const uint4* src1 = reinterpret_cast<const uint4*>(g_tab.t1);
         uint4* dst1 = reinterpret_cast<uint4*>(t1);
         for (int i = threadIdx.x; i < kT1Words / 2; i += kMThreads) dst1[i] = src1[i];
@@ -261,6 +449,12 @@ __global__ void __launch_bounds__(kMThreads, OCTGPU_MEAS_MINB) k_measure_rows(co
     const uint32_t kbeg = uint32_t(seg) * n / kSeg, kend = uint32_t(seg + 1) * n / kSeg;
     const uint32_t ngroups = measure_groups(g.c1 - g.c0);
     const uint2* t0l = t0rep + (lane % kRep);
+    TabLanes TL{};
+    if constexpr (kU32) {
+        const unsigned long long* tq = reinterpret_cast<const unsigned long long*>(msm);
+        TL = TabLanes{tq + tab_off(0) + lane % tab_rep(0), tq + tab_off(1) + lane % tab_rep(1),
+                      tq + tab_off(2) + lane % tab_rep(2), tq + tab_off(3) + lane % tab_rep(3)};
+    }
 
     // the block's sums, one slot per warp (each warp adds its group shares; no contention)
     Partial* wsum = reinterpret_cast<Partial*>(Dbuf + 2 * kMThreads);
@@ -293,30 +487,42 @@ __global__ void __launch_bounds__(kMThreads, OCTGPU_MEAS_MINB) k_measure_rows(co
         long long R = 0;
         Word bad = 0;
         if (kend > kbeg) {
-            UnitAcc A;
+            typename std::conditional<kU32, UnitAcc32, UnitAcc>::type A;
             A.clear();
             int r = 0;
             Word pcb = pCb[size_t(kbeg == 0 ? n - 1 : kbeg - 1) * Y];
-            size_t o = size_t(kbeg) * Y;
-            Word nxa = pXa[o], nxb = pXb[o], nca = pCa[o], ncb = pCb[o], nua = 0, nub = 0;
+            uint32_t o = kbeg * Y;  // word offset within a plane (n Y < 2^32: launch_measure)
+            // plane-major loads (a warp's 32 rows of one plane: one contiguous 256-B segment), the parity
+            // selects at use: lane l reads X(ya) / X(!ya) / Y(ya) / Y(!ya) of its row from planes 0..3
+            const Word* P0 = planes + y;
+            const Word* P1 = planes + PS + y;
+            const Word* P2 = planes + 2 * PS + y;
+            const Word* P3 = planes + 3 * PS + y;
+            const Word* U0 = planes + yu;
+            const Word* U1 = planes + PS + yu;
+            Word nw0 = ldg_word(P0, o), nw1 = ldg_word(P1, o), nw2 = ldg_word(P2, o), nw3 = ldg_word(P3, o), nu0 = 0,
+                 nu1 = 0;
             if (lane == 0) {
-                nua = pUa[o];
-                nub = pUb[o];
+                nu0 = ldg_word(U0, o);
+                nu1 = ldg_word(U1, o);
             }
             for (uint32_t kc = kbeg; kc < kend; kc += kChunkWords) {
                 const uint32_t kce = min(kend, kc + kChunkWords);
-                for (uint32_t k = kc; k < kce; ++k) {
-                    const Word xa = nxa, xb = nxb, ca = nca, cb = ncb, ua = nua, ub = nub;
-                    if (k + 1 < kend) {  // prefetch the next word
-                        o += Y;
-                        nxa = pXa[o];
-                        nxb = pXb[o];
-                        nca = pCa[o];
-                        ncb = pCb[o];
-                        if (lane == 0) {
-                            nua = pUa[o];
-                            nub = pUb[o];
-                        }
+#pragma unroll
+                for (uint32_t i = 0; i < uint32_t(kChunkWords); ++i) {  // unrolled: the prefetch rotates by renaming
+                    const uint32_t k = kc + i;
+                    if (k >= kce) break;
+                    const Word xa = ya ? nw1 : nw0, xb = ya ? nw0 : nw1, ca = ya ? nw3 : nw2, cb = ya ? nw2 : nw3;
+                    const Word ua = ya ? nu0 : nu1, ub = ya ? nu1 : nu0;
+                    // prefetch the next word (the segment's last word re-reads itself: no branch, no copies)
+                    o += k + 1 < kend ? Y : 0u;
+                    nw0 = ldg_word(P0, o);
+                    nw1 = ldg_word(P1, o);
+                    nw2 = ldg_word(P2, o);
+                    nw3 = ldg_word(P3, o);
+                    if (lane == 0) {
+                        nu0 = ldg_word(U0, o);
+                        nu1 = ldg_word(U1, o);
                     }
                     Word bxa = __shfl_up_sync(0xffffffffu, xa, 1);
                     Word bxb = __shfl_up_sync(0xffffffffu, xb, 1);
@@ -334,13 +540,23 @@ __global__ void __launch_bounds__(kMThreads, OCTGPU_MEAS_MINB) k_measure_rows(co
                         const uint32_t b32 = uint32_t(uint64_t(xb) >> (32 * half));
                         const uint32_t evn = (a32 & 0x0F0F0F0Fu) | ((b32 & 0x0F0F0F0Fu) << 4);  // chunks 0,2,4,6
                         const uint32_t odd = ((a32 >> 4) & 0x0F0F0F0Fu) | (b32 & 0xF0F0F0F0u);  // chunks 1,3,5,7
+                        if constexpr (kU32) {
+                            unit32(A, r, evn, odd, 0, TL);
+                            unit32(A, r, evn, odd, 1, TL);
+                        } else {
 #pragma unroll
-                        for (uint32_t un = 0; un < 4; ++un) unit(A, r, evn, odd, un, t0l, t1);
+                            for (uint32_t un = 0; un < 4; ++un) unit(A, r, evn, odd, un, t0l, t1);
+                        }
                     }
                 }
                 const int words = int(kce - kc);
-                flush_chunk(A, words * (W / 8), words * 2 * W, R, T1, T2, T3, T4);
-                R += r;
+                if constexpr (kU32) {
+                    flush_chunk32(A, words * (W / 16), words * 2 * W, R, T1, T2, T3, T4);
+                    R += 2 * r;  // r holds s = (height step) / 2
+                } else {
+                    flush_chunk(A, words * (W / 8), words * 2 * W, R, T1, T2, T3, T4);
+                    R += r;
+                }
                 r = 0;
             }
         }
@@ -734,6 +950,7 @@ cudaError_t launch_measure(int w, const void* planes, Geom g, uint32_t X, void* 
     };
     // segments of more than kNarrowSegSites sites (X > 2^17) keep all four segment sums in 128 bits
     const bool wide = (X + kSeg - 1) / kSeg > kNarrowSegSites;
+    if (uint64_t(g.n) * g.Y >= (uint64_t(1) << 32)) return cudaErrorInvalidValue;  // 32-bit word offsets
     uint32_t grid = 1;
     auto go = [&](auto kern, const auto* pl) -> cudaError_t {
         const cudaError_t e = persistent(kern, grid);

@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(32 * (kP + 1), kP >= 8 ? 2 : 4) k_mcs_bulk(con
         if (core || halo_state) store_state(rd, Y, y, st2);
         if (core && ghost_row) store_state(rd, Y, y + g.wrap, st2);
     }
-    if (sig) link_signal(lk, dst, g, push, nsig, 32u * nact);  // the compute warps (producer / idle ones exited)
+    if (sig) link_signal<false>(lk, dst, g, push, nsig, 32u * nact);  // the compute warps (producer / idle ones exited)
 }
 
 namespace {

@@ -50,6 +50,7 @@ constexpr int kLanes = kDeepLanes;  // rows per block = compute lanes = parking-
 #define OCTGPU_DEEP_REG_STREAMS 4
 #endif
 constexpr int kRegStreams = OCTGPU_DEEP_REG_STREAMS;
+
 constexpr int kXchBar = 1;  // named barrier of the compute warps' edge exchange (0 = __syncthreads)
 
 template <int L>
@@ -566,7 +567,7 @@ __global__ void __launch_bounds__(32 * kDP, kDeepMinBlocks)
             if (c.ghost_row) store_state(rd, g.Y, y + g.wrap, fin);
         }
     }
-    if (sig) link_signal(lk, dst, g, push, nsig, kLanes);
+    if (sig) link_signal<true>(lk, dst, g, push, nsig, kLanes);
 }
 
 namespace {

@@ -74,18 +74,28 @@ __device__ __forceinline__ void link_bar(uint32_t nthreads) {
 
 // At the end of a signalling block, by its threads 0..nthreads-1 (the compute warps; a multiple of 32): push (if
 // this block completed it) the Y(f) plane-row of the first halo row below into the next stripe's new set, then
-// take a ticket; the last of `nsig` blocks publishes done.
-template <typename Word>
+// take a ticket; the last of `nsig` blocks publishes done. WHOLE: every thread of the block takes part
+// (k_mcs_deep: __syncthreads; a named barrier with a runtime count there cost the live 2-MCS pass a register
+// spill in its main loop, 0.249 -> 0.291 ms/MCS)
+template <bool WHOLE, typename Word>
 __device__ void link_signal(const StripeLink& lk, const Word* __restrict__ dst, const Geom& g, bool push,
                             uint32_t nsig, uint32_t nthreads) {
-    link_bar(nthreads);  // every store of these threads issued (named barrier 2: producers may have exited)
+    if constexpr (WHOLE) {
+        nthreads = blockDim.x;
+        __syncthreads();
+    } else {
+        link_bar(nthreads);  // every store of these threads issued (named barrier 2: producers may have exited)
+    }
     if (push) {
         const uint32_t L = g.c1 - g.c0;
         Word* np = static_cast<Word*>(lk.next_planes);
         for (uint32_t k = threadIdx.x; k < g.n; k += nthreads)
             np[size_t(lk.push_plane) * size_t(g.n) * lk.next_Y + size_t(k) * lk.next_Y + kStripeHA] =
                 dst[size_t(lk.push_plane) * g.plane_stride + size_t(k) * g.Y + kStripeHA + L];
-        link_bar(nthreads);
+        if constexpr (WHOLE)
+            __syncthreads();
+        else
+            link_bar(nthreads);
     }
     if (threadIdx.x == 0) {
         __threadfence_system();

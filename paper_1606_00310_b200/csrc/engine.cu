@@ -446,7 +446,9 @@ int materialize(octgpu_engine* e) {
     } else {
         CK(cudaEventSynchronize(e->pend_ev));
     }
+    trace_create("mat-alloc", false);
     const std::vector<uint64_t> tab = power_table(e->pending);
+    trace_create("mat-power", false);
     std::memcpy(e->pend_host, tab.data(), bytes);
     CK(cudaMemcpyAsync(e->pend_tab, e->pend_host, bytes, cudaMemcpyHostToDevice, e->stream));
     CK(launch_apply_jump(e->rng[e->rcur], e->Y, e->pend_tab, e->stream));
@@ -1376,8 +1378,10 @@ int octgpu_get_planes(octgpu_engine* e, void* out) {
     CK(launch_export(e->w, e->planes[e->pcur], stage, e->geom(), e->host_rows(), e->stream));
     ++e->launches;
     if (!e->stripe) {
+        trace_create("planes", true);
         CK(cudaMemcpyAsync(out, stage, e->host_bytes(), cudaMemcpyDeviceToHost, e->stream));
         CK(cudaStreamSynchronize(e->stream));
+        trace_create("planes-d2h", false);
         return OCTGPU_OK;
     }
     // a stripe's core rows of each plane are contiguous in the staged reference layout: one copy per plane
@@ -1393,15 +1397,18 @@ int octgpu_get_planes(octgpu_engine* e, void* out) {
 
 int octgpu_get_states(octgpu_engine* e, uint64_t* out) {
     if (!e || !out) return fail(OCTGPU_ERR_CONFIG, "null argument");
+    trace_create("states", true);
     int rc = use_device(e);
     if (!rc) rc = materialize(e);
     if (rc) return rc;
     std::vector<uint64_t> soa(4 * size_t(e->Y));
     CK(cudaMemcpyAsync(soa.data(), e->rng[e->rcur], e->rng_bytes(), cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
+    trace_create("states-d2h", false);
     const uint32_t r0 = e->first_row();
     for (uint32_t y = 0; y < e->core_rows(); ++y)
         for (int j = 0; j < 4; ++j) out[4 * size_t(y) + j] = soa[size_t(j) * e->Y + r0 + y];
+    trace_create("states-aos", false);
     return OCTGPU_OK;
 }
 

@@ -21,14 +21,16 @@ for rep in range(3):
     eng = octgpu.GpuEngine(octgpu.SlopeField(lat, hp), octgpu.RngStreamSet(1, hs))
     eng.sync()
     t1 = time.perf_counter()
-    eng.step(prm, 100)
+    eng.step(prm, int(os.environ.get('MCS', 100)))
     eng.sync()
     t2 = time.perf_counter()
     eng.measure()
     t3 = time.perf_counter()
     eng.planes(out=pp)
+    t35 = time.perf_counter()
     eng.streams(out=ps)
     t4 = time.perf_counter()
+    print(f"planes {t35 - t3:.4f}  streams {t4 - t35:.4f}")
     del eng
     torch.cuda.synchronize()
     t5 = time.perf_counter()

@@ -835,8 +835,13 @@ int load_planes(octgpu_engine* e, const void* planes) {
     ++e->launches;
     rc = refresh_ghosts(e);
     if (rc) return rc;
-    CK(cudaStreamSynchronize(e->stream));
-    trace_create("import", false);
+    // no host sync here: every caller follows with upload_states, which transposes the states on the host
+    // while the planes are still in flight and then synchronises the stream (the caller's buffer is read
+    // until then)
+    if (getenv("OCTGPU_TRACE_CREATE")) {
+        CK(cudaStreamSynchronize(e->stream));
+        trace_create("import", false);
+    }
     return OCTGPU_OK;
 }
 
@@ -950,10 +955,14 @@ int octgpu_set_state(octgpu_engine* e, uint64_t t_mcs, int phase, const void* pl
     if (n_states < e->core_rows()) return fail(OCTGPU_ERR_INVARIANT, "stream set smaller than row count");
     int rc = use_device(e);
     if (!rc) rc = load_planes(e, planes);
-    if (rc) return rc;
-    e->pending = 0;
-    rc = upload_states(e, states);
-    if (rc) return rc;
+    if (!rc) {
+        e->pending = 0;
+        rc = upload_states(e, states);
+    }
+    if (rc) {
+        cudaStreamSynchronize(e->stream);  // no copy may still read the caller's buffers after we return
+        return rc;
+    }
     e->t = t_mcs;
     e->phase = phase;
     return OCTGPU_OK;

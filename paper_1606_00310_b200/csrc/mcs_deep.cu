@@ -239,22 +239,50 @@ __device__ __forceinline__ void edge_exchange(StateT& S, uint64_t* xch, uint32_t
     xrow_load<L>(buf + ((wib + 1) * 2 + 1) * L, S.pB, lane == 0 && wib < kDP - 1);
 }
 
+// Split-phase edge exchange (the one-draw live passes): publish (store the edge rows of iteration i, then one
+// arrive per warp on the iteration's mbarrier) and collect (wait for every warp's publish of iteration i, then
+// load the neighbours' rows). Between them a warp runs the next word's first sweep, which needs no neighbour
+// values, instead of idling at the block barrier. Iteration i uses buffer / mbarrier i & 1, phase (i >> 1) & 1;
+// a warp can publish iteration i + 2 into the same buffer only after collecting i + 1, i.e. after every warp has
+// collected i. Measured: c2' 0.249 -> 0.243 ms/MCS; the constant-xi and two-draw passes are faster with the
+// barrier (the release-arrive also orders the sweep's global stores), so they keep it.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+template <int L, typename StateT>
+__device__ __forceinline__ void xch_publish(StateT& S, uint64_t* xch, uint64_t* xbar, uint32_t i, int wib, int lane) {
+    uint64_t* buf = xch + size_t(i & 1u) * (kDP * 2 * L);
+    xrow_store<L>(buf + (wib * 2 + 0) * L, S.pC, lane == 31);
+    xrow_store<L>(buf + (wib * 2 + 1) * L, S.pB, lane == 0);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&xbar[i & 1u]);
+}
+template <int L, typename StateT>
+__device__ __forceinline__ void xch_collect(StateT& S, const uint64_t* xch, uint64_t* xbar, uint32_t i, int wib,
+                                            int lane) {
+    mbar_wait(&xbar[i & 1u], (i >> 1) & 1u);
+    const uint64_t* buf = xch + size_t(i & 1u) * (kDP * 2 * L);
+    xrow_load<L>(buf + ((wib - 1) * 2 + 0) * L, S.pC, lane == 31 && wib > 0);
+    xrow_load<L>(buf + ((wib + 1) * 2 + 1) * L, S.pB, lane == 0 && wib < kDP - 1);
+}
+
 // One iteration i: sweep l on word (i-(l-1)) mod n for every active l.
 // STEADY: all sweeps active, no first/second/last words, no wrap (i in [2L, n-1]).
-template <int PM, int QM, int L, bool STEADY, bool CTR = false>
-__device__ __forceinline__ void deep_iter(DeepState<L, typename std::conditional<CTR, Ctr, Xo>::type>& S,
-                                          const DeepCtx& c, uint32_t i, const uint64_t* sb, int jj,
-                                          const ProbDev& p, const ProbDev& q, const Geom& g, int f) {
+// (sweeps LO..HI into nA..nR; every sweep reads the state of iteration i - 1: deep_commit after the last range)
+template <int PM, int QM, int L, bool STEADY, bool CTR, int LO, int HI>
+__device__ __forceinline__ void deep_sweeps(DeepState<L, typename std::conditional<CTR, Ctr, Xo>::type>& S,
+                                            const DeepCtx& c, uint32_t i, const uint64_t* sb, int jj,
+                                            const ProbDev& p, const ProbDev& q, const Geom& g, int f,
+                                            uint64_t (&nA)[L], uint64_t (&nB)[L], uint64_t (&nC)[L],
+                                            uint64_t (&nR)[L], bool (&act)[L]) {
     // plane offsets of the last sweep's stores, formed from the kernel parameters (uniform, no registers)
     const size_t oXf = size_t(f) * g.plane_stride, oXs = size_t(f ^ 1) * g.plane_stride;
     const size_t oYf = size_t(2 + f) * g.plane_stride, oYs = size_t(3 - f) * g.plane_stride;
     using ST = DeepStage<L>;
     using SL = DeepSlots<L, PM, QM, CTR>;
     const uint32_t n = c.n;
-    uint64_t nA[L] = {}, nB[L] = {}, nC[L] = {}, nR[L] = {};
-    bool act[L];
 #pragma unroll
-    for (int l = 1; l <= L; ++l) {
+    for (int l = LO; l <= HI; ++l) {
         const int li = l - 1;
         uint32_t j = i - uint32_t(l - 1);
         bool active = true;
@@ -364,6 +392,11 @@ __device__ __forceinline__ void deep_iter(DeepState<L, typename std::conditional
             if (!first) put(c.d0 + (oXf + o), nR[li], c.core);
         }
     }
+}
+
+template <int L, typename StateT>
+__device__ __forceinline__ void deep_commit(StateT& S, const uint64_t (&nA)[L], const uint64_t (&nB)[L],
+                                            const uint64_t (&nC)[L], const uint64_t (&nR)[L], const bool (&act)[L]) {
 #pragma unroll
     for (int l = 0; l < L; ++l) {
         if (act[l]) {
@@ -373,6 +406,34 @@ __device__ __forceinline__ void deep_iter(DeepState<L, typename std::conditional
             S.pR[l] = nR[l];
         }
     }
+}
+
+// One iteration: every sweep, then commit (the block-barrier exchange follows in the caller)
+template <int PM, int QM, int L, bool STEADY, bool CTR = false>
+__device__ __forceinline__ void deep_iter(DeepState<L, typename std::conditional<CTR, Ctr, Xo>::type>& S,
+                                          const DeepCtx& c, uint32_t i, const uint64_t* sb, int jj,
+                                          const ProbDev& p, const ProbDev& q, const Geom& g, int f) {
+    uint64_t nA[L] = {}, nB[L] = {}, nC[L] = {}, nR[L] = {};
+    bool act[L];
+    deep_sweeps<PM, QM, L, STEADY, CTR, 1, L>(S, c, i, sb, jj, p, q, g, f, nA, nB, nC, nR, act);
+    deep_commit<L>(S, nA, nB, nC, nR, act);
+}
+
+// One iteration with the split-phase exchange: sweep 1 of word i, collect iteration i - 1, `refill` (thread 0's
+// ring refill), sweeps 2..L, commit, publish iteration i.
+template <int PM, int QM, int L, bool STEADY, bool CTR, typename Refill>
+__device__ __forceinline__ void deep_iter_split(DeepState<L, typename std::conditional<CTR, Ctr, Xo>::type>& S,
+                                                const DeepCtx& c, uint32_t i, const uint64_t* sb, int jj,
+                                                const ProbDev& p, const ProbDev& q, const Geom& g, int f,
+                                                uint64_t* xch, uint64_t* xbar, int wib, int lane, Refill&& refill) {
+    uint64_t nA[L] = {}, nB[L] = {}, nC[L] = {}, nR[L] = {};
+    bool act[L];
+    deep_sweeps<PM, QM, L, STEADY, CTR, 1, 1>(S, c, i, sb, jj, p, q, g, f, nA, nB, nC, nR, act);
+    if (STEADY || i > 0) xch_collect<L>(S, xch, xbar, i - 1, wib, lane);
+    refill();
+    deep_sweeps<PM, QM, L, STEADY, CTR, 2, L>(S, c, i, sb, jj, p, q, g, f, nA, nB, nC, nR, act);
+    deep_commit<L>(S, nA, nB, nC, nR, act);
+    xch_publish<L>(S, xch, xbar, i, wib, lane);
 }
 
 // Ring stage `slot` <- word block b of the four source planes (one 3-D TMA box each), completing on full[slot].
@@ -445,8 +506,15 @@ __global__ void __launch_bounds__(32 * kDP, kDeepMinBlocks)
         const bool above = blk_r0 < kStripeHA, below = blk_r0 + uint32_t(kLanes) > c1;
         if ((above || below) && !link_pull(lk, const_cast<uint64_t*>(src), g, above, below)) return;
     }
+    // one-draw live passes: the split-phase exchange (xch_publish / xch_collect)
+    constexpr bool kSplit = !CTR && ((PM == M_HALF && QM == M_ZERO) || (PM == M_ZERO && QM == M_HALF));
+    uint64_t* xbar = full + kSMax;
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+        if constexpr (kSplit) {
+            mbar_init(&xbar[0], kDP);
+            mbar_init(&xbar[1], kDP);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (uint32_t b = 0; b < uint32_t(S) && b < nblocks; ++b)
             deep_issue<L>(ring, full, &tmK, &tmK1, blk_r0, f, g.pf, nblocks, b, b);
@@ -529,6 +597,32 @@ __global__ void __launch_bounds__(32 * kDP, kDeepMinBlocks)
             R.cur = sb[ST::kXs];
             R.raw0 = R.cur;
         }
+        if constexpr (kSplit) {
+            // the previous stage is refilled once every warp has published its last word (the collect of this
+            // block's first word): by then every warp has read it
+            const uint32_t pst = st == 0 ? uint32_t(S) - 1 : st - 1;
+            auto refill = [&](int jj) {
+                if (jj == 0 && threadIdx.x == 0 && b > 0 && b - 1 + uint32_t(S) < nblocks)
+                    deep_issue<L>(ring, full, &tmK, &tmK1, blk_r0, f, g.pf, nblocks, b - 1 + uint32_t(S), pst);
+            };
+            if (kb >= uint32_t(2 * L) && kb + kKS < n) {
+#pragma unroll
+                for (int jj = 0; jj < kKS; ++jj)
+                    deep_iter_split<PM, QM, L, true, CTR>(R, c, kb + jj, sb, jj, p, q, g, f, xch, xbar, wib, lane,
+                                                          [&] { refill(jj); });
+            } else {
+#pragma unroll 1
+                for (int jj = 0; jj < kKS; ++jj)
+                    if (kb + jj < n)
+                        deep_iter_split<PM, QM, L, false, CTR>(R, c, kb + jj, sb, jj, p, q, g, f, xch, xbar, wib,
+                                                               lane, [&] { refill(jj); });
+            }
+            if (++st == uint32_t(S)) {
+                st = 0;
+                ph ^= 1u;
+            }
+            continue;
+        }
         if (kb >= uint32_t(2 * L) && kb + kKS < n) {  // i = n-1 is sweep 1's last word: generic
 #pragma unroll
             for (int jj = 0; jj < kKS; ++jj) {
@@ -555,8 +649,12 @@ __global__ void __launch_bounds__(32 * kDP, kDeepMinBlocks)
     // drain: sweeps 2..L finish their wrapped words
 #pragma unroll 1
     for (uint32_t i = n; i < n + uint32_t(2 * L - 2); ++i) {
-        deep_iter<PM, QM, L, false, CTR>(R, c, i, nullptr, 0, p, q, g, f);
-        edge_exchange<L>(R, xch, i, wib, lane);
+        if constexpr (kSplit) {
+            deep_iter_split<PM, QM, L, false, CTR>(R, c, i, nullptr, 0, p, q, g, f, xch, xbar, wib, lane, [] {});
+        } else {
+            deep_iter<PM, QM, L, false, CTR>(R, c, i, nullptr, 0, p, q, g, f);
+            edge_exchange<L>(R, xch, i, wib, lane);
+        }
     }
 
     if constexpr (LIVE && !CTR) {

@@ -14,10 +14,10 @@ CSRC = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
 KERNELS = [
     ("mcs_deep", "_ZN6octgpu10k_mcs_deepILi4ELi0ELi6ELb0E", 0),  # c2 / c5: p = 1, 3-MCS pass
     ("mcs_deep", "_ZN6octgpu10k_mcs_deepILi4ELi0ELi8ELb0E", 0),  # c2: 4-MCS remainder pass
-    # c2' / c5': p = 1/2, live 2-MCS pass with the split-phase exchange (16 B outside the main loop; measured
+    # c2' / c5': p = 1/2, live 2-MCS pass with the split-phase exchange (16 B of spills, and still faster:
     # 0.243 vs 0.248 ms/MCS for the spill-free barrier version)
     ("mcs_deep", "_ZN6octgpu10k_mcs_deepILi1ELi0ELi4ELb0E", 16),
-    ("mcs_deep", "_ZN6octgpu10k_mcs_deepILi1ELi1ELi4ELb0E", 8),  # c3: p = q = 1/2 (8 B outside the loop)
+    ("mcs_deep", "_ZN6octgpu10k_mcs_deepILi1ELi1ELi4ELb0E", 8),  # c3: p = q = 1/2 (8 B)
     ("measure", "_ZN6octgpu14k_measure_rowsImLb0EEEv", 0),       # W^2 row pass, 64-bit words
 ]
 

@@ -1041,7 +1041,7 @@ int deep_ring(octgpu_engine* e, const ProbDev& p, const ProbDev& q, int ls, bool
     if (cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, e->device) != cudaSuccess)
         return 2;
     int S = e->deep_S;
-    while (S > 2 && 2 * (mcs_deep_smem(p.mode, q.mode, ls, S, ctr) + 1024) > size_t(smem_sm)) --S;
+    while (S > 2 && size_t(kDeepMinBlocks) * (mcs_deep_smem(p.mode, q.mode, ls, S, ctr) + 1024) > size_t(smem_sm)) --S;
     return S;
 }
 
